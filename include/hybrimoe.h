@@ -1,0 +1,333 @@
+/*
+ * hybrimoe.h -- C ABI of the B200-native HybriMoE MoE-layer hot path.
+ *
+ * The reference (`moesim`, /root/reference/pkg/src/moesim) is a pure-Python
+ * function API with no FFI; every entry point below replaces one reference
+ * function (cited as file:line) and is bound from Python with ctypes by
+ * paper_2504_05897_b200/_lib.py.  Conventions:
+ *
+ *   - every function returns an int status: HM_OK or one of HM_E*;
+ *     the message of the last failure on the calling thread is available
+ *     through hm_last_error();
+ *   - caller-owned flat arrays, opaque handles, no C++ exceptions cross the
+ *     ABI, no hidden device synchronisation;
+ *   - an ExpertRef (core.py:27-36) is packed as uint32 (layer << 16 | expert)
+ *     so that integer order equals the reference's lexicographic tuple order;
+ *   - all decision arithmetic is IEEE fp64 evaluated in the reference's
+ *     expression order (the library is built with -ffp-contract=off);
+ *   - device entry points take a cudaStream_t (passed as void*).
+ */
+#ifndef HYBRIMOE_H_
+#define HYBRIMOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: map 1:1 onto the reference's exception types ---------- */
+#define HM_OK 0
+#define HM_EVALUE 1        /* ValueError            (costs.py:70, scheduling.py:169, caching.py:115, prefetch.py:130) */
+#define HM_EEVICTION 2     /* EvictionError         (caching.py:26, 96-99) */
+#define HM_EPLAN 3         /* PlanInvariantError    (scheduling.py:76-124) */
+#define HM_ERUNTIME 4      /* RuntimeError          (scheduling.py:233-234, "scheduler stalled") */
+#define HM_ECALIBRATION 5  /* CalibrationError      (costs.py:98) */
+#define HM_EASSERT 6       /* AssertionError        (engine.py:373-381, validate replan) */
+#define HM_ECUDA 7         /* CUDA runtime failure (no reference counterpart) */
+
+/* devices / kinds / assignments (scheduling.py:33-45) */
+#define HM_DEV_CPU 0
+#define HM_DEV_GPU 1
+#define HM_DEV_PCIE 2
+#define HM_KIND_COMPUTE 0
+#define HM_KIND_TRANSFER 1
+#define HM_ASSIGN_CPU 0
+#define HM_ASSIGN_GPU_CACHED 1
+#define HM_ASSIGN_GPU_TRANSFER 2
+
+/* cache policies (caching.py:20-23) */
+#define HM_POLICY_MRS 0
+#define HM_POLICY_LRU 1
+#define HM_POLICY_LFU 2
+
+/* scheduling policies (engine.py:66-70) */
+#define HM_SCHED_HYBRID 0
+#define HM_SCHED_STATIC_SPLIT 1
+#define HM_SCHED_FIXED_MAP 2
+#define HM_SCHED_GPU_ONDEMAND 3
+
+/* HardwareProfile (costs.py:33-65), field for field. */
+typedef struct hm_profile {
+  double gpu_time_per_expert;
+  double cpu_slope;
+  double transfer_bandwidth;
+  double transfer_latency;
+  int64_t gpu_saturation_load;
+  double gpu_slope;
+  double cpu_first_expert_penalty;
+  double shared_expert_time;
+  double non_expert_time;
+} hm_profile;
+
+/* ExpertTask (scheduling.py:48-50) */
+typedef struct hm_task {
+  uint32_t ref;
+  int32_t _pad;
+  int64_t load;
+} hm_task;
+
+/* TimelineEvent (scheduling.py:53-58) */
+typedef struct hm_event {
+  int32_t device;
+  int32_t kind;
+  uint32_t ref;
+  int32_t _pad;
+  double start;
+  double end;
+} hm_event;
+
+/* one SchedulePlan.assignment entry (scheduling.py:62-67) */
+typedef struct hm_assign {
+  uint32_t ref;
+  int32_t how;
+} hm_assign;
+
+/* PrefetchCandidate (prefetch.py:45-51) */
+typedef struct hm_candidate {
+  uint32_t ref;
+  int32_t layer_distance;
+  int64_t predicted_load;
+  double gain;
+  double cost;
+} hm_candidate;
+
+typedef struct hm_cache hm_cache;         /* CacheState (core.py:235-265) + HBM slot map */
+typedef struct hm_mrs hm_mrs;             /* MrsState (caching.py:30-55) */
+typedef struct hm_evaluator hm_evaluator; /* MakespanEvaluator (scheduling.py:433-465) */
+typedef struct hm_engine hm_engine;       /* run_pass state machine (engine.py:255-398) */
+
+/* Message of the last failing call on this thread; returns its length. */
+int hm_last_error(char *buf, size_t n);
+/* Library version string. */
+const char *hm_version(void);
+
+/* ---- cost model (costs.py:68-95) ------------------------------------------ */
+int hm_profile_check(const hm_profile *p);                                    /* costs.py:47-65 */
+int hm_gpu_time(const hm_profile *p, int64_t load, double *out);              /* costs.py:68-74 */
+int hm_cpu_time(const hm_profile *p, int64_t load, int64_t pos, double *out); /* costs.py:77-88 */
+int hm_transfer_time(const hm_profile *p, double expert_bytes, double *out);  /* costs.py:91-95 */
+
+/* ---- intra-layer scheduler (scheduling.py) -------------------------------- */
+/* Output buffers: events[2*n], assign[n]; n = total task count. */
+int hm_simulate_schedule(const hm_task *gpu_q, int n_gpu, const hm_task *cpu_q, int n_cpu,
+                         const hm_profile *p, double expert_bytes, hm_event *events,
+                         int *n_events, hm_assign *assign, int *n_assign,
+                         double *makespan); /* scheduling.py:160-270 */
+int hm_plan_all_cpu(const hm_task *tasks, int n, const hm_profile *p, hm_event *events,
+                    int *n_events, hm_assign *assign, int *n_assign,
+                    double *makespan); /* scheduling.py:273-284 */
+int hm_plan_all_gpu(const hm_task *cached, int n_cached, const hm_task *uncached,
+                    int n_uncached, const hm_profile *p, double expert_bytes,
+                    hm_event *events, int *n_events, hm_assign *assign, int *n_assign,
+                    double *makespan); /* scheduling.py:287-317 */
+int hm_select_plan_tasks(const hm_task *cached, int n_cached, const hm_task *uncached,
+                         int n_uncached, const hm_profile *p, double expert_bytes,
+                         hm_event *events, int *n_events, hm_assign *assign,
+                         int *n_assign, double *makespan); /* scheduling.py:320-335 */
+/* select_plan against a native cache: build_queues + _select_plan_tasks. */
+int hm_select_plan(const hm_cache *c, int layer, const int64_t *loads, int n,
+                   const hm_profile *p, double expert_bytes, hm_event *events,
+                   int *n_events, hm_assign *assign, int *n_assign,
+                   double *makespan); /* scheduling.py:135-147, 338-350 */
+int hm_check_plan(const hm_event *events, int n_events, const hm_assign *assign,
+                  int n_assign, double makespan); /* scheduling.py:80-124 */
+int hm_pcie_idle_budget(const hm_event *events, int n_events, double makespan,
+                        double *out); /* scheduling.py:405-412 */
+int hm_oracle_optimal(const hm_task *tasks, int n, const uint8_t *cached,
+                      const hm_profile *p, double expert_bytes, int limit,
+                      double *out); /* scheduling.py:356-402 */
+
+/* ---- memoised makespans (scheduling.py:433-465) --------------------------- */
+int hm_evaluator_create(const hm_profile *p, double expert_bytes, hm_evaluator **out);
+void hm_evaluator_destroy(hm_evaluator *e);
+int hm_evaluator_makespan(hm_evaluator *e, const int64_t *cached_loads, int n_cached,
+                          const int64_t *uncached_loads, int n_uncached, double *out);
+int hm_evaluator_size(const hm_evaluator *e, int64_t *out);
+
+/* ---- cache container + policies (core.py:235-265, caching.py:79-128) ------ */
+int hm_cache_create(int64_t capacity, hm_cache **out);
+void hm_cache_destroy(hm_cache *c);
+int hm_cache_capacity(const hm_cache *c, int64_t *out);
+int hm_cache_lookup(hm_cache *c, uint32_t ref, int policy, int *hit); /* caching.py:79-91 */
+int hm_cache_insert(hm_cache *c, uint32_t ref, int policy, const hm_mrs *mrs,
+                    uint32_t *victim, int *has_victim); /* caching.py:111-128 */
+int hm_cache_victim(const hm_cache *c, int policy, const hm_mrs *mrs,
+                    uint32_t *victim); /* caching.py:94-108 */
+int hm_cache_is_resident(const hm_cache *c, uint32_t ref, int *out);
+int hm_cache_is_pinned(const hm_cache *c, uint32_t ref, int *out);
+int hm_cache_pin(hm_cache *c, uint32_t ref);
+int hm_cache_unpin(hm_cache *c, uint32_t ref);
+int hm_cache_clear_pinned(hm_cache *c);
+int hm_cache_add_resident(hm_cache *c, uint32_t ref);  /* set-like add, no policy metadata */
+int hm_cache_remove_resident(hm_cache *c, uint32_t ref);
+int hm_cache_clear_resident(hm_cache *c);
+int hm_cache_counts(const hm_cache *c, int64_t *n_resident, int64_t *n_pinned);
+/* Copy out members (unordered); *n receives the total even if cap is short. */
+int hm_cache_resident(const hm_cache *c, uint32_t *out, int64_t cap, int64_t *n);
+int hm_cache_pinned(const hm_cache *c, uint32_t *out, int64_t cap, int64_t *n);
+/* LRU tick / LFU frequency metadata (core.py:253-259); has=0 when absent. */
+int hm_cache_last_access(const hm_cache *c, uint32_t ref, int64_t *out, int *has);
+int hm_cache_frequency(const hm_cache *c, uint32_t ref, int64_t *out, int *has);
+int hm_cache_set_last_access(hm_cache *c, uint32_t ref, int64_t v);
+int hm_cache_set_frequency(hm_cache *c, uint32_t ref, int64_t v);
+int hm_cache_tick(const hm_cache *c, int64_t *out);
+int hm_cache_next_tick(hm_cache *c, int64_t *out);
+/* HBM slot of a resident expert (runtime extension: which slot its weights occupy). */
+int hm_cache_slot(const hm_cache *c, uint32_t ref, int64_t *slot);
+
+/* ---- MRS score table (caching.py:30-76) ----------------------------------- */
+int hm_mrs_create(int num_layers, int num_routed, double alpha, int p, hm_mrs **out);
+void hm_mrs_destroy(hm_mrs *m);
+int hm_mrs_update(hm_mrs *m, int layer, const double *scores, int n); /* caching.py:65-76 */
+int hm_mrs_get(const hm_mrs *m, uint32_t ref, double *out);
+int hm_mrs_set(hm_mrs *m, uint32_t ref, double v);
+int hm_mrs_table(const hm_mrs *m, double *out); /* L*N fp64, row-major by layer */
+int hm_mrs_params(const hm_mrs *m, double *alpha, int *p, int *num_layers, int *num_routed);
+int hm_top_p_filter(const double *scores, int n, int p, double *out); /* caching.py:58-62 */
+
+/* ---- prefetch (prefetch.py:104-143) --------------------------------------- */
+/* gain of making `candidate` resident for the predicted layer request. */
+int hm_evaluate_gain(uint32_t candidate, int pred_layer, const int64_t *pred_loads, int n,
+                     const hm_cache *c, hm_evaluator *ev, double *gain);
+int hm_select_prefetches(const hm_candidate *cands, int n, double idle_budget,
+                         uint32_t *chosen, int *n_chosen);
+
+/* ---- the per-layer engine step (engine.py:255-398, 401-486) --------------- */
+typedef struct hm_engine_config {
+  int32_t num_layers;
+  int32_t num_routed;
+  int32_t num_activated;
+  int32_t scheduling;   /* HM_SCHED_* */
+  int32_t cache_policy; /* HM_POLICY_* */
+  int32_t prefetch;     /* bool */
+  int32_t validate;     /* bool */
+  int32_t split_point;  /* static_layer_split */
+  int64_t capacity;     /* cache slots = floor(ratio * L * N) */
+  double expert_bytes;  /* core.py:84-91 */
+  int32_t collect;      /* keep the per-layer decision record */
+  int32_t _pad;
+} hm_engine_config;
+
+/* PassResult (engine.py:159-168) plus the prefetch counters. */
+typedef struct hm_pass_result {
+  double latency;
+  double busy[3]; /* indexed by HM_DEV_* */
+  int64_t lookups, hits, inserts, evictions;
+  int64_t prefetch_issued, prefetch_hits, prefetch_expired;
+} hm_pass_result;
+
+/* The engine borrows the run's cache, MRS state (may be NULL, as in the
+ * reference) and evaluator, which must outlive it (engine.py:255-265). */
+int hm_engine_create(const hm_engine_config *cfg, const hm_profile *p, hm_cache *cache,
+                     hm_mrs *mrs, hm_evaluator *ev, hm_engine **out);
+void hm_engine_destroy(hm_engine *e);
+/* fixed_frequency_map GPU set (engine.py:195-231); residency is the caller's. */
+int hm_engine_set_fixed_pinned(hm_engine *e, const uint32_t *refs, int n);
+int hm_engine_begin_pass(hm_engine *e);
+/* One layer of run_pass in the exact engine.py:288-389 order.  `pred_*` are
+ * the predicted future LayerRequests (prefetch.py:54-101), concatenated:
+ * pred_layers[n_pred], pred_loads[n_pred*N]; ignored unless prefetch is on. */
+int hm_engine_run_layer(hm_engine *e, int layer, const int64_t *loads, const double *scores,
+                        int n, const int32_t *pred_layers, const int64_t *pred_loads,
+                        int n_pred);
+/* End-of-pass expiry (engine.py:392-395) and PassResult. */
+int hm_engine_end_pass(hm_engine *e, hm_pass_result *out);
+/* Makespan of every layer run in the current pass. */
+int hm_engine_layer_makespans(const hm_engine *e, double *out, int cap, int *n);
+
+/* Decision record of the last run layer (valid when cfg.collect or always for
+ * the plan).  Sizes first, then the arrays. */
+typedef struct hm_layer_record_sizes {
+  int32_t n_lookups;
+  int32_t n_events;
+  int32_t n_assign;
+  int32_t n_demand;
+  int32_t n_candidates;
+  int32_t n_chosen;
+  int32_t expired;
+  int32_t _pad;
+  double makespan;
+  double budget;
+} hm_layer_record_sizes;
+int hm_engine_record_sizes(const hm_engine *e, hm_layer_record_sizes *out);
+int hm_engine_record(const hm_engine *e, uint32_t *lookup_refs, uint8_t *lookup_hits,
+                     hm_event *events, hm_assign *assign, uint32_t *demand_refs,
+                     uint32_t *demand_victims, uint8_t *demand_has_victim,
+                     hm_candidate *candidates, uint32_t *chosen_refs,
+                     uint32_t *chosen_victims, uint8_t *chosen_has_victim);
+
+/* ======================================================================= */
+/* Device side (CUDA, sm_100a).  Pointers are device pointers unless noted. */
+/* ======================================================================= */
+
+/* Router (tracegen.py:137-152 semantics; transformers mixtral/deepseek_v2/
+ * qwen2_moe routers): fp32 logits [T, N] -> per token top-K expert indices
+ * (value desc, index asc), combine weights (softmax over all N, optionally
+ * renormalised over the top-K), per-expert loads (bincount) and the fp64
+ * token-sum of the softmax (LayerRequest.scores before normalisation). */
+int hm_router_topk(const float *logits, int T, int N, int K, int renormalize,
+                   int32_t *topk_idx, float *topk_w, int32_t *loads, double *score_sum,
+                   void *stream);
+
+/* Router gate GEMV/GEMM: logits[T, N] = x[T, H] (bf16) . Wg[N, H]^T (bf16), fp32 accumulate. */
+int hm_router_logits(const uint16_t *x, const uint16_t *wg, int T, int H, int N,
+                     float *logits, void *stream);
+
+/* Permute tokens into expert-contiguous rows.  Given topk_idx [T, K] and the
+ * expert row offsets (exclusive prefix of loads, offsets[N+1]), writes
+ * row_token[T*K] (source token of each permuted row), row_weight[T*K] and
+ * pos[T*K] (permuted row of each (t,k)), and gathers xp[T*K, H] = x[row_token].
+ * Rows inside an expert are in token order (stable). */
+int hm_permute(const uint16_t *x, const int32_t *topk_idx, const float *topk_w, int T, int K,
+               int H, int N, const int32_t *offsets, int32_t *row_token, float *row_weight,
+               int32_t *pos, uint16_t *xp, void *stream);
+
+/* Exclusive scan of loads -> offsets[N+1] on device. */
+int hm_offsets(const int32_t *loads, int N, int32_t *offsets, void *stream);
+
+/* A batch of expert FFNs over permuted rows.  Each group g computes
+ *   out[rows of g] = down_g( silu(gate_g x) * (up_g x) )
+ * with weights at w13[g] ([2I, H] gate/up interleaved in 64-row blocks) and
+ * w2[g] ([H, I]), for rows row_begin[g] .. row_begin[g]+row_count[g].
+ * h is an [rows, I] bf16 scratch; out is [rows, H] fp32. */
+typedef struct hm_group {
+  const uint16_t *w13;
+  const uint16_t *w2;
+  int32_t row_begin;
+  int32_t row_count;
+} hm_group;
+
+/* Weight-streaming decode path: rows per group small (<= 8). */
+int hm_expert_gemv(const hm_group *groups_dev, int n_groups, int H, int I,
+                   const uint16_t *xp, uint16_t *h, float *out, void *stream);
+/* tcgen05/TMEM/TMA grouped GEMM path for prefill-sized groups. */
+int hm_expert_gemm(const hm_group *groups_host, int n_groups, int H, int I,
+                   const uint16_t *xp, int total_rows, uint16_t *h, float *out,
+                   void *stream);
+
+/* Combine: y[t] = sum_k w[t,k] * out[pos[t,k]] (+ residual x[t] when given). */
+int hm_combine(const float *out, const int32_t *pos, const float *topk_w, int T, int K,
+               int H, const uint16_t *residual, uint16_t *y, void *stream);
+
+/* GPU-side MRS update (caching.py:58-76): S[layer] <- a*TopP(s) + (1-a)*S[layer],
+ * fp64 with explicit round-to-nearest mul/add (no contraction). */
+int hm_mrs_update_dev(double *S, const double *scores, int layer, int N, int p,
+                      double alpha, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HYBRIMOE_H_ */

@@ -1,0 +1,226 @@
+"""ctypes binding of libhybrimoe.so (include/hybrimoe.h).
+
+This is the only place that touches the native library.  Status codes map
+1:1 onto the reference's exception types; there is no Python
+fallback for anything the library implements -- if the library cannot be
+loaded, importing the package fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+from .errors import CalibrationError, EvictionError, PlanInvariantError
+
+_LIB_PATH = Path(__file__).resolve().parent / "libhybrimoe.so"
+
+HM_OK, HM_EVALUE, HM_EEVICTION, HM_EPLAN, HM_ERUNTIME, HM_ECALIBRATION, HM_EASSERT, HM_ECUDA = range(8)
+DEV_CPU, DEV_GPU, DEV_PCIE = 0, 1, 2
+KIND_COMPUTE, KIND_TRANSFER = 0, 1
+ASSIGN_CPU, ASSIGN_GPU_CACHED, ASSIGN_GPU_TRANSFER = 0, 1, 2
+
+
+class Profile(C.Structure):
+    _fields_ = [
+        ("gpu_time_per_expert", C.c_double),
+        ("cpu_slope", C.c_double),
+        ("transfer_bandwidth", C.c_double),
+        ("transfer_latency", C.c_double),
+        ("gpu_saturation_load", C.c_int64),
+        ("gpu_slope", C.c_double),
+        ("cpu_first_expert_penalty", C.c_double),
+        ("shared_expert_time", C.c_double),
+        ("non_expert_time", C.c_double),
+    ]
+
+
+class Task(C.Structure):
+    _fields_ = [("ref", C.c_uint32), ("_pad", C.c_int32), ("load", C.c_int64)]
+
+
+class Event(C.Structure):
+    _fields_ = [("device", C.c_int32), ("kind", C.c_int32), ("ref", C.c_uint32), ("_pad", C.c_int32),
+                ("start", C.c_double), ("end", C.c_double)]
+
+
+class Assign(C.Structure):
+    _fields_ = [("ref", C.c_uint32), ("how", C.c_int32)]
+
+
+class Candidate(C.Structure):
+    _fields_ = [("ref", C.c_uint32), ("layer_distance", C.c_int32), ("predicted_load", C.c_int64),
+                ("gain", C.c_double), ("cost", C.c_double)]
+
+
+class EngineConfig(C.Structure):
+    _fields_ = [
+        ("num_layers", C.c_int32), ("num_routed", C.c_int32), ("num_activated", C.c_int32),
+        ("scheduling", C.c_int32), ("cache_policy", C.c_int32), ("prefetch", C.c_int32),
+        ("validate", C.c_int32), ("split_point", C.c_int32), ("capacity", C.c_int64),
+        ("expert_bytes", C.c_double), ("collect", C.c_int32), ("_pad", C.c_int32),
+    ]
+
+
+class PassResult(C.Structure):
+    _fields_ = [("latency", C.c_double), ("busy", C.c_double * 3), ("lookups", C.c_int64),
+                ("hits", C.c_int64), ("inserts", C.c_int64), ("evictions", C.c_int64),
+                ("prefetch_issued", C.c_int64), ("prefetch_hits", C.c_int64),
+                ("prefetch_expired", C.c_int64)]
+
+
+class RecordSizes(C.Structure):
+    _fields_ = [("n_lookups", C.c_int32), ("n_events", C.c_int32), ("n_assign", C.c_int32),
+                ("n_demand", C.c_int32), ("n_candidates", C.c_int32), ("n_chosen", C.c_int32),
+                ("expired", C.c_int32), ("_pad", C.c_int32), ("makespan", C.c_double),
+                ("budget", C.c_double)]
+
+
+class Group(C.Structure):
+    _fields_ = [("w13", C.c_void_p), ("w2", C.c_void_p), ("row_begin", C.c_int32),
+                ("row_count", C.c_int32)]
+
+
+def _load():
+    if not _LIB_PATH.exists():
+        raise ImportError(
+            f"{_LIB_PATH} is missing: build it with `python -m paper_2504_05897_b200._build` "
+            "(or __graft_entry__.build()); there is no Python fallback")
+    return C.CDLL(str(_LIB_PATH), mode=os.RTLD_NOW | os.RTLD_GLOBAL)
+
+
+lib = _load()
+
+P = C.POINTER
+vp = C.c_void_p
+i32, i64, u32, f64, u8 = C.c_int32, C.c_int64, C.c_uint32, C.c_double, C.c_uint8
+_SIGS = {
+    "hm_last_error": ([C.c_char_p, C.c_size_t], C.c_int),
+    "hm_version": ([], C.c_char_p),
+    "hm_profile_check": ([P(Profile)], C.c_int),
+    "hm_gpu_time": ([P(Profile), i64, P(f64)], C.c_int),
+    "hm_cpu_time": ([P(Profile), i64, i64, P(f64)], C.c_int),
+    "hm_transfer_time": ([P(Profile), f64, P(f64)], C.c_int),
+    "hm_simulate_schedule": ([P(Task), C.c_int, P(Task), C.c_int, P(Profile), f64, P(Event), P(C.c_int),
+                              P(Assign), P(C.c_int), P(f64)], C.c_int),
+    "hm_plan_all_cpu": ([P(Task), C.c_int, P(Profile), P(Event), P(C.c_int), P(Assign), P(C.c_int), P(f64)],
+                        C.c_int),
+    "hm_plan_all_gpu": ([P(Task), C.c_int, P(Task), C.c_int, P(Profile), f64, P(Event), P(C.c_int),
+                         P(Assign), P(C.c_int), P(f64)], C.c_int),
+    "hm_select_plan_tasks": ([P(Task), C.c_int, P(Task), C.c_int, P(Profile), f64, P(Event), P(C.c_int),
+                              P(Assign), P(C.c_int), P(f64)], C.c_int),
+    "hm_select_plan": ([vp, C.c_int, P(i64), C.c_int, P(Profile), f64, P(Event), P(C.c_int), P(Assign),
+                        P(C.c_int), P(f64)], C.c_int),
+    "hm_check_plan": ([P(Event), C.c_int, P(Assign), C.c_int, f64], C.c_int),
+    "hm_pcie_idle_budget": ([P(Event), C.c_int, f64, P(f64)], C.c_int),
+    "hm_oracle_optimal": ([P(Task), C.c_int, P(u8), P(Profile), f64, C.c_int, P(f64)], C.c_int),
+    "hm_evaluator_create": ([P(Profile), f64, P(vp)], C.c_int),
+    "hm_evaluator_destroy": ([vp], None),
+    "hm_evaluator_makespan": ([vp, P(i64), C.c_int, P(i64), C.c_int, P(f64)], C.c_int),
+    "hm_evaluator_size": ([vp, P(i64)], C.c_int),
+    "hm_cache_create": ([i64, P(vp)], C.c_int),
+    "hm_cache_destroy": ([vp], None),
+    "hm_cache_capacity": ([vp, P(i64)], C.c_int),
+    "hm_cache_lookup": ([vp, u32, C.c_int, P(C.c_int)], C.c_int),
+    "hm_cache_insert": ([vp, u32, C.c_int, vp, P(u32), P(C.c_int)], C.c_int),
+    "hm_cache_victim": ([vp, C.c_int, vp, P(u32)], C.c_int),
+    "hm_cache_is_resident": ([vp, u32, P(C.c_int)], C.c_int),
+    "hm_cache_is_pinned": ([vp, u32, P(C.c_int)], C.c_int),
+    "hm_cache_pin": ([vp, u32], C.c_int),
+    "hm_cache_unpin": ([vp, u32], C.c_int),
+    "hm_cache_clear_pinned": ([vp], C.c_int),
+    "hm_cache_add_resident": ([vp, u32], C.c_int),
+    "hm_cache_remove_resident": ([vp, u32], C.c_int),
+    "hm_cache_clear_resident": ([vp], C.c_int),
+    "hm_cache_counts": ([vp, P(i64), P(i64)], C.c_int),
+    "hm_cache_resident": ([vp, P(u32), i64, P(i64)], C.c_int),
+    "hm_cache_pinned": ([vp, P(u32), i64, P(i64)], C.c_int),
+    "hm_cache_last_access": ([vp, u32, P(i64), P(C.c_int)], C.c_int),
+    "hm_cache_frequency": ([vp, u32, P(i64), P(C.c_int)], C.c_int),
+    "hm_cache_set_last_access": ([vp, u32, i64], C.c_int),
+    "hm_cache_set_frequency": ([vp, u32, i64], C.c_int),
+    "hm_cache_tick": ([vp, P(i64)], C.c_int),
+    "hm_cache_next_tick": ([vp, P(i64)], C.c_int),
+    "hm_cache_slot": ([vp, u32, P(i64)], C.c_int),
+    "hm_mrs_create": ([C.c_int, C.c_int, f64, C.c_int, P(vp)], C.c_int),
+    "hm_mrs_destroy": ([vp], None),
+    "hm_mrs_update": ([vp, C.c_int, P(f64), C.c_int], C.c_int),
+    "hm_mrs_get": ([vp, u32, P(f64)], C.c_int),
+    "hm_mrs_set": ([vp, u32, f64], C.c_int),
+    "hm_mrs_table": ([vp, P(f64)], C.c_int),
+    "hm_mrs_params": ([vp, P(f64), P(C.c_int), P(C.c_int), P(C.c_int)], C.c_int),
+    "hm_top_p_filter": ([P(f64), C.c_int, C.c_int, P(f64)], C.c_int),
+    "hm_evaluate_gain": ([u32, C.c_int, P(i64), C.c_int, vp, vp, P(f64)], C.c_int),
+    "hm_select_prefetches": ([P(Candidate), C.c_int, f64, P(u32), P(C.c_int)], C.c_int),
+    "hm_engine_create": ([P(EngineConfig), P(Profile), vp, vp, vp, P(vp)], C.c_int),
+    "hm_engine_destroy": ([vp], None),
+    "hm_engine_set_fixed_pinned": ([vp, P(u32), C.c_int], C.c_int),
+    "hm_engine_begin_pass": ([vp], C.c_int),
+    "hm_engine_run_layer": ([vp, C.c_int, P(i64), P(f64), C.c_int, P(i32), P(i64), C.c_int], C.c_int),
+    "hm_engine_end_pass": ([vp, P(PassResult)], C.c_int),
+    "hm_engine_layer_makespans": ([vp, P(f64), C.c_int, P(C.c_int)], C.c_int),
+    "hm_engine_record_sizes": ([vp, P(RecordSizes)], C.c_int),
+    "hm_engine_record": ([vp, P(u32), P(u8), P(Event), P(Assign), P(u32), P(u32), P(u8), P(Candidate), P(u32),
+                          P(u32), P(u8)], C.c_int),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+
+def last_error() -> str:
+    buf = C.create_string_buffer(4096)
+    lib.hm_last_error(buf, len(buf))
+    return buf.value.decode(errors="replace")
+
+
+def check(status: int) -> None:
+    """Raise the reference's exception type for a non-zero status."""
+    if status == HM_OK:
+        return
+    msg = last_error()
+    if status == HM_EVALUE:
+        raise ValueError(msg)
+    if status == HM_EEVICTION:
+        raise EvictionError(msg)
+    if status == HM_EPLAN:
+        raise PlanInvariantError(msg)
+    if status == HM_ECALIBRATION:
+        raise CalibrationError(msg)
+    if status == HM_EASSERT:
+        raise AssertionError(msg)
+    raise RuntimeError(msg)
+
+
+def pack(layer: int, expert: int) -> int:
+    if not (0 <= layer < 65536 and 0 <= expert < 65536):
+        raise ValueError(f"ExpertRef({layer}, {expert}) outside the packed 16-bit range")
+    return (layer << 16) | expert
+
+
+def unpack(r: int) -> tuple[int, int]:
+    return r >> 16, r & 0xFFFF
+
+
+def i64_array(values) -> np.ndarray:
+    return np.ascontiguousarray(values, dtype=np.int64)
+
+
+def f64_array(values) -> np.ndarray:
+    return np.ascontiguousarray(values, dtype=np.float64)
+
+
+def ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(P(ctype))
+
+
+def symbols_declared() -> list[str]:
+    """Every function name declared in include/hybrimoe.h."""
+    import re
+
+    hdr = (Path(__file__).resolve().parent.parent / "include" / "hybrimoe.h").read_text()
+    body = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    return sorted(set(re.findall(r"\b(hm_[a-z0-9_]+)\s*\(", body)))
