@@ -257,6 +257,8 @@ typedef struct hm_layer_record_sizes {
   int32_t n_candidates;
   int32_t n_chosen;
   int32_t expired;
+  int32_t n_selected;           /* select_prefetches output length */
+  int32_t prefetch_evict_error; /* a prefetch insert raised EvictionError */
   int32_t _pad;
   double makespan;
   double budget;
@@ -266,7 +268,8 @@ int hm_engine_record(const hm_engine *e, uint32_t *lookup_refs, uint8_t *lookup_
                      hm_event *events, hm_assign *assign, uint32_t *demand_refs,
                      uint32_t *demand_victims, uint8_t *demand_has_victim,
                      hm_candidate *candidates, uint32_t *chosen_refs,
-                     uint32_t *chosen_victims, uint8_t *chosen_has_victim);
+                     uint32_t *chosen_victims, uint8_t *chosen_has_victim,
+                     uint32_t *selected_refs);
 
 /* ======================================================================= */
 /* Device side (CUDA, sm_100a).  Pointers are device pointers unless noted. */

@@ -74,7 +74,8 @@ class PassResult(C.Structure):
 class RecordSizes(C.Structure):
     _fields_ = [("n_lookups", C.c_int32), ("n_events", C.c_int32), ("n_assign", C.c_int32),
                 ("n_demand", C.c_int32), ("n_candidates", C.c_int32), ("n_chosen", C.c_int32),
-                ("expired", C.c_int32), ("_pad", C.c_int32), ("makespan", C.c_double),
+                ("expired", C.c_int32), ("n_selected", C.c_int32), ("prefetch_evict_error", C.c_int32),
+                ("_pad", C.c_int32), ("makespan", C.c_double),
                 ("budget", C.c_double)]
 
 
@@ -163,7 +164,7 @@ _SIGS = {
     "hm_engine_layer_makespans": ([vp, P(f64), C.c_int, P(C.c_int)], C.c_int),
     "hm_engine_record_sizes": ([vp, P(RecordSizes)], C.c_int),
     "hm_engine_record": ([vp, P(u32), P(u8), P(Event), P(Assign), P(u32), P(u32), P(u8), P(Candidate), P(u32),
-                          P(u32), P(u8)], C.c_int),
+                          P(u32), P(u8), P(u32)], C.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(lib, _name)

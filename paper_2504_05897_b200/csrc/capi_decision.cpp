@@ -436,7 +436,8 @@ int hm_engine_record_sizes(const hm_engine *e, hm_layer_record_sizes *o) {
   o->n_candidates = static_cast<int32_t>(r.candidates.size());
   o->n_chosen = static_cast<int32_t>(r.chosen.size());
   o->expired = r.expired;
-  o->_pad = 0;
+  o->n_selected = static_cast<int32_t>(r.selected.size());
+  o->prefetch_evict_error = r.prefetch_evict_error;
   o->makespan = r.plan.makespan;
   o->budget = r.budget;
   HM_API_END
@@ -444,9 +445,11 @@ int hm_engine_record_sizes(const hm_engine *e, hm_layer_record_sizes *o) {
 int hm_engine_record(const hm_engine *e, uint32_t *lookup_refs, uint8_t *lookup_hits, hm_event *events,
                      hm_assign *assign, uint32_t *demand_refs, uint32_t *demand_victims,
                      uint8_t *demand_has_victim, hm_candidate *candidates, uint32_t *chosen_refs,
-                     uint32_t *chosen_victims, uint8_t *chosen_has_victim) {
+                     uint32_t *chosen_victims, uint8_t *chosen_has_victim, uint32_t *selected_refs) {
   HM_API_BEGIN
   const hm::LayerRecord &r = E(e)->rec;
+  for (size_t i = 0; i < r.selected.size(); ++i)
+    if (selected_refs) selected_refs[i] = r.selected[i];
   for (size_t i = 0; i < r.lookups.size(); ++i) {
     if (lookup_refs) lookup_refs[i] = r.lookups[i].first;
     if (lookup_hits) lookup_hits[i] = r.lookups[i].second;

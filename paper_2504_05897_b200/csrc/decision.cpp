@@ -684,6 +684,8 @@ void Engine::run_layer(int layer, const int64_t *loads, const double *scores, in
   rec.demand.clear();
   rec.candidates.clear();
   rec.chosen.clear();
+  rec.selected.clear();
+  rec.prefetch_evict_error = 0;
   rec.budget = 0.0;
   rec.expired = 0;
 
@@ -808,6 +810,7 @@ void Engine::run_layer(int layer, const int64_t *loads, const double *scores, in
       spent += c->cost;
       chosen.push_back(c->ref);
     }
+    rec.selected = chosen;
     for (uint32_t r : chosen) {
       if (cache.is_resident(r)) continue;
       uint32_t v = 0;
@@ -815,7 +818,10 @@ void Engine::run_layer(int layer, const int64_t *loads, const double *scores, in
       try {
         has = cache.insert(r, policy, mrs_, &v);
       } catch (const Error &err) {
-        if (err.code == HM_EEVICTION) break;  // prefetch is opportunistic
+        if (err.code == HM_EEVICTION) {  // prefetch is opportunistic
+          rec.prefetch_evict_error = 1;
+          break;
+        }
         throw;
       }
       ++res.inserts;

@@ -111,7 +111,9 @@ struct LayerRecord {
   Plan plan;
   std::vector<std::pair<uint32_t, int64_t>> demand;  // (ref, victim or -1)
   std::vector<hm_candidate> candidates;
-  std::vector<std::pair<uint32_t, int64_t>> chosen;  // (ref, victim or -1)
+  std::vector<uint32_t> selected;                   // select_prefetches output
+  std::vector<std::pair<uint32_t, int64_t>> chosen;  // inserted: (ref, victim or -1)
+  int prefetch_evict_error = 0;                     // an insert hit EvictionError (engine.py:360-363)
   double budget = 0.0;
   int expired = 0;
 };

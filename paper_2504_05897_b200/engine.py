@@ -241,7 +241,7 @@ class _NativeEngine:
         s = self._sizes()
         ev = (_lib.Event * max(1, s.n_events))()
         asg = (_lib.Assign * max(1, s.n_assign))()
-        check(lib.hm_engine_record(self._h, None, None, ev, asg, None, None, None, None, None, None, None))
+        check(lib.hm_engine_record(self._h, None, None, ev, asg, None, None, None, None, None, None, None, None))
         return plan_from_native(ev, s.n_events, asg, s.n_assign, s.makespan)
 
     def record(self) -> dict:
@@ -258,7 +258,8 @@ class _NativeEngine:
         cr = (C.c_uint32 * max(1, s.n_chosen))()
         cv = (C.c_uint32 * max(1, s.n_chosen))()
         ch = (C.c_uint8 * max(1, s.n_chosen))()
-        check(lib.hm_engine_record(self._h, lr, lh, ev, asg, dr, dv, dh, cd, cr, cv, ch))
+        sl = (C.c_uint32 * max(1, s.n_selected))()
+        check(lib.hm_engine_record(self._h, lr, lh, ev, asg, dr, dv, dh, cd, cr, cv, ch, sl))
         plan = plan_from_native(ev, s.n_events, asg, s.n_assign, s.makespan)
         return {
             "lookups": [(_ref_of(lr[i]), bool(lh[i])) for i in range(s.n_lookups)],
@@ -267,7 +268,9 @@ class _NativeEngine:
             "candidates": [(_ref_of(cd[i].ref), cd[i].predicted_load, cd[i].gain, cd[i].layer_distance)
                            for i in range(s.n_candidates)],
             "budget": s.budget if self.policy.prefetch else None,
+            "selected": [_ref_of(sl[i]) for i in range(s.n_selected)],
             "chosen": [(_ref_of(cr[i]), _ref_of(cv[i]) if ch[i] else None) for i in range(s.n_chosen)],
+            "prefetch_evict_error": bool(s.prefetch_evict_error),
             "expired": s.expired,
         }
 
