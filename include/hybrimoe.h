@@ -272,60 +272,61 @@ int hm_engine_record(const hm_engine *e, uint32_t *lookup_refs, uint8_t *lookup_
                      uint32_t *selected_refs);
 
 /* ======================================================================= */
-/* Device side (CUDA, sm_100a).  Pointers are device pointers unless noted. */
+/* Device side (CUDA, sm_100a).  Pointers are device pointers unless noted; */
+/* `stream` is a cudaStream_t.  No entry point synchronises the device.      */
 /* ======================================================================= */
 
-/* Router (tracegen.py:137-152 semantics; transformers mixtral/deepseek_v2/
- * qwen2_moe routers): fp32 logits [T, N] -> per token top-K expert indices
- * (value desc, index asc), combine weights (softmax over all N, optionally
- * renormalised over the top-K), per-expert loads (bincount) and the fp64
- * token-sum of the softmax (LayerRequest.scores before normalisation). */
-int hm_router_topk(const float *logits, int T, int N, int K, int renormalize,
-                   int32_t *topk_idx, float *topk_w, int32_t *loads, double *score_sum,
-                   void *stream);
-
-/* Router gate GEMV/GEMM: logits[T, N] = x[T, H] (bf16) . Wg[N, H]^T (bf16), fp32 accumulate. */
+/* Router (Eq. 1; tracegen.py:137-152; transformers mixtral /
+ * deepseek_v2 / qwen2_moe routers).  logits [T, ld] fp32, routed experts in
+ * columns [0, N).  Per token: softmax over the N routed logits, top-K by
+ * (logit desc, expert index asc) -- the reference's tie rule (core.py:94-97)
+ * -- combine weight = probability, renormalised over the K when `renormalize`.
+ * Shared experts are appended as always-selected columns N..N+n_shared-1
+ * with weight 1, or sigmoid(logits[t, shared_gate_col]) when that is >= 0.
+ * Outputs: sel/w [T, K+n_shared], probs [T, N] (routed softmax),
+ * counts [N+n_shared] (bincount, tracegen.py:148; zeroed here). */
+int hm_router_topk(const float *logits, int T, int N, int ld, int K, int renormalize,
+                   int n_shared, int shared_gate_col, int32_t *sel, float *w, float *probs,
+                   int32_t *counts, void *stream);
+/* score_sum[e] = sum_t probs[t, e] in fp64, fixed reduction order; the
+ * LayerRequest scores are score_sum normalised (tracegen.py:149-150). */
+int hm_score_sums(const float *probs, int T, int N, double *score_sum, void *stream);
+/* Gate GEMV/GEMM: logits[T, N] = x[T, H] . wg[N, H]^T (bf16 in, fp32 out). */
 int hm_router_logits(const uint16_t *x, const uint16_t *wg, int T, int H, int N,
                      float *logits, void *stream);
+/* Exclusive scan: offsets[E+1] from counts[E]. */
+int hm_offsets(const int32_t *counts, int E, int32_t *offsets, void *stream);
+/* Expert-contiguous permutation of the T*Kp selections (token order inside
+ * an expert): pos[t*Kp+k] = permuted row, row_src[row] = t*Kp+k. */
+int hm_permute(const int32_t *sel, int T, int Kp, int E, const int32_t *offsets,
+               int32_t *pos, int32_t *row_src, void *stream);
+/* xp[r, :] = x[row_src[r] / Kp, :] */
+int hm_gather_rows(const uint16_t *x, const int32_t *row_src, int rows, int Kp, int H,
+                   uint16_t *xp, void *stream);
 
-/* Permute tokens into expert-contiguous rows.  Given topk_idx [T, K] and the
- * expert row offsets (exclusive prefix of loads, offsets[N+1]), writes
- * row_token[T*K] (source token of each permuted row), row_weight[T*K] and
- * pos[T*K] (permuted row of each (t,k)), and gathers xp[T*K, H] = x[row_token].
- * Rows inside an expert are in token order (stable). */
-int hm_permute(const uint16_t *x, const int32_t *topk_idx, const float *topk_w, int T, int K,
-               int H, int N, const int32_t *offsets, int32_t *row_token, float *row_weight,
-               int32_t *pos, uint16_t *xp, void *stream);
-
-/* Exclusive scan of loads -> offsets[N+1] on device. */
-int hm_offsets(const int32_t *loads, int N, int32_t *offsets, void *stream);
-
-/* A batch of expert FFNs over permuted rows.  Each group g computes
- *   out[rows of g] = down_g( silu(gate_g x) * (up_g x) )
- * with weights at w13[g] ([2I, H] gate/up interleaved in 64-row blocks) and
- * w2[g] ([H, I]), for rows row_begin[g] .. row_begin[g]+row_count[g].
- * h is an [rows, I] bf16 scratch; out is [rows, H] fp32. */
+/* Expert weight pool: n_slots expert images of 3*H*I bf16 each --
+ *   [0, 2IH)   W13: gate/up rows interleaved in 128-row blocks,
+ *   [2IH, 3IH) W2 [H, I] row-major.
+ * One group = one expert applied to a contiguous range of permuted rows. */
 typedef struct hm_group {
-  const uint16_t *w13;
-  const uint16_t *w2;
+  int32_t slot;
   int32_t row_begin;
   int32_t row_count;
+  int32_t _pad;
 } hm_group;
-
-/* Weight-streaming decode path: rows per group small (<= 8). */
-int hm_expert_gemv(const hm_group *groups_dev, int n_groups, int H, int I,
-                   const uint16_t *xp, uint16_t *h, float *out, void *stream);
-/* tcgen05/TMEM/TMA grouped GEMM path for prefill-sized groups. */
-int hm_expert_gemm(const hm_group *groups_host, int n_groups, int H, int I,
-                   const uint16_t *xp, int total_rows, uint16_t *h, float *out,
-                   void *stream);
-
-/* Combine: y[t] = sum_k w[t,k] * out[pos[t,k]] (+ residual x[t] when given). */
-int hm_combine(const float *out, const int32_t *pos, const float *topk_w, int T, int K,
-               int H, const uint16_t *residual, uint16_t *y, void *stream);
-
+#define HM_FFN_AUTO 0 /* <= 4 rows: weight-streaming GEMV; larger: tcgen05 GEMM */
+#define HM_FFN_GEMV 1
+#define HM_FFN_GEMM 2
+/* out[rows of g] = W2_g (silu(Wg_g x) * (Wu_g x)) for every group (groups is
+ * a HOST array).  h [total_rows, I] bf16 scratch, out [total_rows, H] fp32. */
+int hm_expert_ffn(const uint16_t *pool, int n_slots, int H, int I, const hm_group *groups,
+                  int n_groups, const uint16_t *xp, int total_rows, uint16_t *h, float *out,
+                  int path, void *stream);
+/* y[t] = residual[t] (optional) + sum_k w[t,k] * out[pos[t,k]]  (Eq. 1 combine). */
+int hm_combine(const float *out, const int32_t *pos, const float *w, int T, int Kp, int H,
+               const uint16_t *residual, uint16_t *y, void *stream);
 /* GPU-side MRS update (caching.py:58-76): S[layer] <- a*TopP(s) + (1-a)*S[layer],
- * fp64 with explicit round-to-nearest mul/add (no contraction). */
+ * fp64 with explicit round-to-nearest mul/add (bit-identical to the host core). */
 int hm_mrs_update_dev(double *S, const double *scores, int layer, int N, int p,
                       double alpha, void *stream);
 

@@ -225,3 +225,27 @@ def symbols_declared() -> list[str]:
     hdr = (Path(__file__).resolve().parent.parent / "include" / "hybrimoe.h").read_text()
     body = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
     return sorted(set(re.findall(r"\b(hm_[a-z0-9_]+)\s*\(", body)))
+
+
+class HmGroup(C.Structure):
+    _fields_ = [("slot", C.c_int32), ("row_begin", C.c_int32), ("row_count", C.c_int32), ("_pad", C.c_int32)]
+
+
+_DEV_SIGS = {
+    "hm_router_topk": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp],
+                       C.c_int),
+    "hm_score_sums": ([vp, C.c_int, C.c_int, vp, vp], C.c_int),
+    "hm_router_logits": ([vp, vp, C.c_int, C.c_int, C.c_int, vp, vp], C.c_int),
+    "hm_offsets": ([vp, C.c_int, vp, vp], C.c_int),
+    "hm_permute": ([vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp], C.c_int),
+    "hm_gather_rows": ([vp, vp, C.c_int, C.c_int, C.c_int, vp, vp], C.c_int),
+    "hm_expert_ffn": ([vp, C.c_int, C.c_int, C.c_int, P(HmGroup), C.c_int, vp, C.c_int, vp, vp, C.c_int, vp],
+                      C.c_int),
+    "hm_combine": ([vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp, vp], C.c_int),
+    "hm_mrs_update_dev": ([vp, vp, C.c_int, C.c_int, C.c_int, f64, vp], C.c_int),
+}
+for _name, (_args, _res) in _DEV_SIGS.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+FFN_AUTO, FFN_GEMV, FFN_GEMM = 0, 1, 2

@@ -1,0 +1,222 @@
+// Host worker: executes the experts the schedule assigns to the CPU
+// (the CPU timeline of scheduling.py:257-268).  bf16 expert
+// images are read straight from the pinned host master store in the slot
+// layout (include/hybrimoe.h, hm_group); arithmetic is AVX-512 BF16
+// (vdpbf16ps: bf16 pairs, fp32 accumulate), the intermediate h is rounded to
+// bf16 exactly like the GPU path, outputs are fp32 rows in permuted order.
+// Decode (1 token) is a DRAM-bandwidth-bound GEMV split over all threads;
+// prefill blocks 16 weight rows x 4 tokens so weights are reused from L2.
+#include <immintrin.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <condition_variable>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "host_worker.hpp"
+
+namespace hm {
+
+// ------------------------------------------------------------ thread pool
+ThreadPool::ThreadPool(int n) : n_(std::max(1, n)) {
+  for (int t = 1; t < n_; ++t) threads_.emplace_back([this, t] { loop(t); });
+}
+
+ThreadPool::~ThreadPool() {
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    stop_ = true;
+    ++gen_;
+  }
+  cv_.notify_all();
+  for (auto &th : threads_) th.join();
+}
+
+void ThreadPool::loop(int tid) {
+  uint64_t seen = 0;
+  for (;;) {
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      if (stop_) return;
+    }
+    job_(tid, n_);
+    if (pending_.fetch_sub(1, std::memory_order_acq_rel) == 1) {
+      std::lock_guard<std::mutex> g(mu_);
+      done_cv_.notify_all();
+    }
+  }
+}
+
+void ThreadPool::run(const std::function<void(int, int)> &fn) {
+  if (n_ == 1) {
+    fn(0, 1);
+    return;
+  }
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    job_ = fn;
+    pending_.store(n_ - 1, std::memory_order_release);
+    ++gen_;
+  }
+  cv_.notify_all();
+  fn(0, n_);
+  std::unique_lock<std::mutex> lk(mu_);
+  done_cv_.wait(lk, [&] { return pending_.load(std::memory_order_acquire) == 0; });
+}
+
+// ------------------------------------------------------------ kernels
+namespace {
+
+constexpr int kIlv = 128;
+
+inline float bf2f(uint16_t v) {
+  uint32_t u = static_cast<uint32_t>(v) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+inline uint16_t f2bf(float f) {  // round to nearest even
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+inline __m512bh ldbh(const uint16_t *p) { return (__m512bh)_mm512_loadu_si512(p); }
+
+// acc[r][t] = sum_k W[r][k] * X[t][k] for R rows and TT tokens (K % 32 == 0).
+template <int R, int TT>
+inline void dot_tile(const uint16_t *const *w, const uint16_t *const *x, int K, float (&out)[R][TT]) {
+  __m512 acc[R][TT];
+#pragma GCC unroll 4
+  for (int r = 0; r < R; ++r)
+#pragma GCC unroll 4
+    for (int t = 0; t < TT; ++t) acc[r][t] = _mm512_setzero_ps();
+  for (int k = 0; k < K; k += 32) {
+    __m512bh xv[TT];
+#pragma GCC unroll 4
+    for (int t = 0; t < TT; ++t) xv[t] = ldbh(x[t] + k);
+#pragma GCC unroll 4
+    for (int r = 0; r < R; ++r) {
+      const __m512bh wv = ldbh(w[r] + k);
+#pragma GCC unroll 4
+      for (int t = 0; t < TT; ++t) acc[r][t] = _mm512_dpbf16_ps(acc[r][t], wv, xv[t]);
+    }
+  }
+  for (int r = 0; r < R; ++r)
+    for (int t = 0; t < TT; ++t) out[r][t] = _mm512_reduce_add_ps(acc[r][t]);
+}
+
+inline float silu(float g) { return g / (1.0f + std::exp(-g)); }
+
+// W13 phase for pairs [i0, i1): h[t][i] = bf16(silu(g.x_t) * (u.x_t))
+void phase1(const uint16_t *img, int H, int I, const uint16_t *x, int M, uint16_t *h, int i0, int i1) {
+  for (int tb = 0; tb < M; tb += 4) {
+    const int tt = std::min(4, M - tb);
+    const uint16_t *xp[4];
+    for (int t = 0; t < 4; ++t) xp[t] = x + static_cast<size_t>(tb + std::min(t, tt - 1)) * H;
+    for (int i = i0; i < i1; i += 2) {
+      const int npair = std::min(2, i1 - i);
+      const uint16_t *w[4];
+      for (int q = 0; q < 2; ++q) {
+        const int ii = i + std::min(q, npair - 1);
+        const size_t grow = static_cast<size_t>((ii / kIlv) * 2 * kIlv + ii % kIlv);
+        w[2 * q] = img + grow * H;
+        w[2 * q + 1] = img + (grow + kIlv) * H;
+      }
+      float o[4][4];
+      if (tt == 1) {
+        float o1[4][1];
+        dot_tile<4, 1>(w, xp, H, o1);
+        for (int r = 0; r < 4; ++r) o[r][0] = o1[r][0];
+      } else {
+        dot_tile<4, 4>(w, xp, H, o);
+      }
+      for (int q = 0; q < npair; ++q)
+        for (int t = 0; t < tt; ++t)
+          h[static_cast<size_t>(tb + t) * I + i + q] = f2bf(silu(o[2 * q][t]) * o[2 * q + 1][t]);
+    }
+  }
+}
+
+// W2 phase for output rows [j0, j1): out[t][j] = W2[j] . h[t]
+void phase2(const uint16_t *img, int H, int I, const uint16_t *h, int M, float *out, int j0, int j1) {
+  const uint16_t *w2 = img + static_cast<size_t>(2) * I * H;
+  constexpr int RB = 16;  // weight rows kept hot across token blocks
+  for (int jb = j0; jb < j1; jb += RB) {
+    const int je = std::min(j1, jb + RB);
+    for (int tb = 0; tb < M; tb += 4) {
+      const int tt = std::min(4, M - tb);
+      const uint16_t *hp[4];
+      for (int t = 0; t < 4; ++t) hp[t] = h + static_cast<size_t>(tb + std::min(t, tt - 1)) * I;
+      for (int j = jb; j < je; j += 4) {
+        const int nr = std::min(4, je - j);
+        const uint16_t *w[4];
+        for (int r = 0; r < 4; ++r) w[r] = w2 + static_cast<size_t>(j + std::min(r, nr - 1)) * I;
+        float o[4][4];
+        if (tt == 1) {
+          float o1[4][1];
+          dot_tile<4, 1>(w, hp, I, o1);
+          for (int r = 0; r < 4; ++r) o[r][0] = o1[r][0];
+        } else {
+          dot_tile<4, 4>(w, hp, I, o);
+        }
+        for (int r = 0; r < nr; ++r)
+          for (int t = 0; t < tt; ++t) out[static_cast<size_t>(tb + t) * H + j + r] = o[r][t];
+      }
+    }
+  }
+}
+
+}  // namespace
+
+void cpu_expert(ThreadPool &pool, const uint16_t *img, int H, int I, const uint16_t *x, int M, float *out,
+                std::vector<uint16_t> &hbuf) {
+  HM_REQUIRE(H % 32 == 0 && I % kIlv == 0, HM_EVALUE, "host worker needs H % 32 == 0 and I % 128 == 0");
+  if (M <= 0) return;
+  hbuf.resize(static_cast<size_t>(M) * I);
+  uint16_t *h = hbuf.data();
+  pool.run([&](int tid, int nt) {
+    // pairs in multiples of 16 per thread keep each thread on contiguous rows
+    const int per = ((I + nt - 1) / nt + 15) / 16 * 16;
+    const int i0 = std::min(I, tid * per), i1 = std::min(I, i0 + per);
+    if (i0 < i1) phase1(img, H, I, x, M, h, i0, i1);
+  });
+  pool.run([&](int tid, int nt) {
+    const int per = ((H + nt - 1) / nt + 3) / 4 * 4;
+    const int j0 = std::min(H, tid * per), j1 = std::min(H, j0 + per);
+    if (j0 < j1) phase2(img, H, I, h, M, out, j0, j1);
+  });
+}
+
+}  // namespace hm
+
+extern "C" {
+
+struct hm_cpu_pool;
+
+int hm_cpu_pool_create(int nthreads, hm_cpu_pool **out) {
+  HM_API_BEGIN
+  if (nthreads <= 0) nthreads = static_cast<int>(std::thread::hardware_concurrency());
+  *out = reinterpret_cast<hm_cpu_pool *>(new hm::ThreadPool(nthreads));
+  HM_API_END
+}
+
+void hm_cpu_pool_destroy(hm_cpu_pool *p) { delete reinterpret_cast<hm::ThreadPool *>(p); }
+
+int hm_cpu_expert(hm_cpu_pool *pool, const uint16_t *img, int H, int I, const uint16_t *x, int M, float *out) {
+  HM_API_BEGIN
+  std::vector<uint16_t> hbuf;
+  hm::cpu_expert(*reinterpret_cast<hm::ThreadPool *>(pool), img, H, I, x, M, out, hbuf);
+  HM_API_END
+}
+
+int hm_cpu_has_avx512bf16(void) { return __builtin_cpu_supports("avx512bf16") ? 1 : 0; }
+
+}  // extern "C"

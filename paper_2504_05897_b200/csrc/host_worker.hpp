@@ -1,0 +1,40 @@
+// Host worker thread pool and CPU expert kernel (see host_worker.cpp).
+#pragma once
+
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "common.hpp"
+
+namespace hm {
+
+// Fixed pool; run(fn) executes fn(tid, n) on every thread (the caller is tid 0).
+class ThreadPool {
+ public:
+  explicit ThreadPool(int n);
+  ~ThreadPool();
+  int size() const { return n_; }
+  void run(const std::function<void(int, int)> &fn);
+
+ private:
+  void loop(int tid);
+  int n_;
+  std::vector<std::thread> threads_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  std::function<void(int, int)> job_;
+  std::atomic<int> pending_{0};
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+// out[M, H] fp32 = W2 (silu(Wg x) * (Wu x)) for one expert image (slot layout).
+void cpu_expert(ThreadPool &pool, const uint16_t *img, int H, int I, const uint16_t *x, int M, float *out,
+                std::vector<uint16_t> &hbuf);
+
+}  // namespace hm

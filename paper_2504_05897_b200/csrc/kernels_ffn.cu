@@ -1,0 +1,526 @@
+// Expert FFN kernels for the HybriMoE layer on sm_100a:
+//   E(x) = W2 ( silu(Wg x) * (Wu x) )            (Eq. 1; SwiGLU experts)
+//
+// Weights live in an HBM slot pool: slot s is one expert image of 3*H*I bf16
+//   [0, 2IH)   W13 = gate/up rows interleaved in 128-row blocks
+//              (rows 256b..256b+127 = gate rows 128b.., the next 128 = up rows)
+//   [2IH, 3IH) W2  = [H, I] row-major
+// so one H2D copy moves an expert and one 256-row W13 tile carries matching
+// gate and up columns for a fused SwiGLU epilogue.
+//
+// Two paths, chosen per token group by size:
+//   * decode (<= 4 rows): weight-streaming warp GEMV, 16-byte L1-bypassing
+//     loads, activations staged in shared memory; HBM-bound.
+//   * prefill: persistent grouped GEMM, TMA (SWIZZLE_128B) -> 4-stage smem
+//     ring -> tcgen05.mma (M=128, N=256, fp32 accumulators in TMEM, double
+//     buffered) -> tcgen05.ld epilogue (SwiGLU for W13, fp32 store for W2).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+#include "device.cuh"
+
+namespace hm {
+namespace {
+
+constexpr int kMaxGroups = 96;
+constexpr int kGemvMaxRows = 4;
+constexpr int kIlv = 128;  // gate/up interleave block
+
+struct GemvParams {
+  const uint16_t *pool;
+  size_t slot_elems;
+  int H, I;
+  int n_groups;
+  int bpg;    // blocks per group
+  int chunk;  // pairs (ffn1) or rows (ffn2) per block
+  const uint16_t *xp;
+  uint16_t *h;
+  float *out;
+  int32_t slot[kMaxGroups];
+  int32_t row_begin[kMaxGroups];
+  int32_t row_count[kMaxGroups];
+};
+
+// h[r, i] = silu(gate_i . x_r) * (up_i . x_r) for the rows of one group.
+template <int MR>
+__global__ void __launch_bounds__(256) ffn1_gemv_kernel(const __grid_constant__ GemvParams p) {
+  extern __shared__ __align__(16) uint16_t xs[];  // [MR][H]
+  const int g = blockIdx.x / p.bpg, cid = blockIdx.x % p.bpg;
+  const int M = p.row_count[g], rb = p.row_begin[g], H = p.H, I = p.I;
+  for (int v = threadIdx.x; v < M * H / 8; v += blockDim.x)
+    reinterpret_cast<uint4 *>(xs)[v] = reinterpret_cast<const uint4 *>(p.xp + static_cast<size_t>(rb) * H)[v];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint16_t *w13 = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_elems;
+  const int i_end = min(I, (cid + 1) * p.chunk);
+  for (int i = cid * p.chunk + wid; i < i_end; i += nw) {
+    const size_t grow = static_cast<size_t>((i / kIlv) * 2 * kIlv + (i % kIlv));
+    const uint16_t *wg = w13 + grow * H;
+    const uint16_t *wu = wg + static_cast<size_t>(kIlv) * H;
+    float ag[MR], au[MR];
+#pragma unroll
+    for (int m = 0; m < MR; ++m) ag[m] = au[m] = 0.f;
+    constexpr int U = 4;
+    for (int c0 = lane * 8; c0 < H; c0 += 256 * U) {
+      uint4 gv[U], uv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + u * 256;
+        if (c < H) {
+          gv[u] = dev::ld_stream(wg + c);
+          uv[u] = dev::ld_stream(wu + c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + u * 256;
+        if (c < H) {
+#pragma unroll
+          for (int m = 0; m < MR; ++m) {
+            if (m < M) {
+              const uint4 xv = *reinterpret_cast<const uint4 *>(xs + m * H + c);
+              ag[m] += dev::dot8(gv[u], xv);
+              au[m] += dev::dot8(uv[u], xv);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MR; ++m) {
+      if (m < M) {
+        const float gs = dev::warp_sum(ag[m]), us = dev::warp_sum(au[m]);
+        if (lane == 0) p.h[static_cast<size_t>(rb + m) * I + i] = dev::f2bf(dev::silu(gs) * us);
+      }
+    }
+  }
+}
+
+// out[r, j] = W2[j, :] . h[r, :]
+template <int MR>
+__global__ void __launch_bounds__(256) ffn2_gemv_kernel(const __grid_constant__ GemvParams p) {
+  extern __shared__ __align__(16) uint16_t hs[];  // [MR][I]
+  const int g = blockIdx.x / p.bpg, cid = blockIdx.x % p.bpg;
+  const int M = p.row_count[g], rb = p.row_begin[g], H = p.H, I = p.I;
+  for (int v = threadIdx.x; v < M * I / 8; v += blockDim.x)
+    reinterpret_cast<uint4 *>(hs)[v] = reinterpret_cast<const uint4 *>(p.h + static_cast<size_t>(rb) * I)[v];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint16_t *w2 = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_elems + static_cast<size_t>(2) * I * H;
+  const int j_end = min(H, (cid + 1) * p.chunk);
+  for (int j = cid * p.chunk + wid; j < j_end; j += nw) {
+    const uint16_t *wr = w2 + static_cast<size_t>(j) * I;
+    float acc[MR];
+#pragma unroll
+    for (int m = 0; m < MR; ++m) acc[m] = 0.f;
+    constexpr int U = 4;
+    for (int c0 = lane * 8; c0 < I; c0 += 256 * U) {
+      uint4 wv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + u * 256;
+        if (c < I) wv[u] = dev::ld_stream(wr + c);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + u * 256;
+        if (c < I) {
+#pragma unroll
+          for (int m = 0; m < MR; ++m)
+            if (m < M) acc[m] += dev::dot8(wv[u], *reinterpret_cast<const uint4 *>(hs + m * I + c));
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MR; ++m) {
+      if (m < M) {
+        const float s = dev::warp_sum(acc[m]);
+        if (lane == 0) p.out[static_cast<size_t>(rb + m) * H + j] = s;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ tcgen05 GEMM
+constexpr int BM = 128, BK = 64, STAGES = 4;
+
+struct GemmParams {
+  int n_groups, n_tiles, K, n_blocks, ldo;
+  uint16_t *h;
+  float *out;
+  int32_t tile_start[kMaxGroups + 1];
+  int32_t row_begin[kMaxGroups];
+  int32_t row_count[kMaxGroups];
+  int32_t b_row_base[kMaxGroups];
+};
+
+template <int BN>
+constexpr int gemm_smem_bytes() {
+  return STAGES * (BM + BN) * BK * 2 + 1024 /*align*/ + 256 /*barriers*/;
+}
+
+// MODE 0: A = xp [rows, H], B = W13 view, epilogue SwiGLU -> h (bf16, ldo = I)
+// MODE 1: A = h  [rows, I], B = W2 view,  epilogue fp32 -> out (ldo = H)
+template <int BN, int MODE>
+__global__ void __launch_bounds__(256, 1)
+    expert_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                       const __grid_constant__ GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = dev::smem_u32(smem_raw);
+  uint8_t *smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint8_t *sA = smem;                                    // STAGES x BM x BK bf16
+  uint8_t *sB = smem + STAGES * BM * BK * 2;             // STAGES x BN x BK bf16
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sB + STAGES * BN * BK * 2);
+  uint64_t *full = bars, *empty = bars + STAGES, *tfull = bars + 2 * STAGES, *tempty = bars + 2 * STAGES + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&tmA);
+    dev::tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      dev::mbar_init(&full[s], 1);
+      dev::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      dev::mbar_init(&tfull[a], 1);
+      dev::mbar_init(&tempty[a], 4);
+    }
+    dev::fence_barrier_init();
+  }
+  if (warp == 2) dev::tmem_alloc<512>(tmem_slot);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto decode = [&](int t, int &g, int &mb, int &nb) {
+    g = 0;
+    while (g + 1 < p.n_groups && p.tile_start[g + 1] <= t) ++g;
+    const int local = t - p.tile_start[g];
+    const int mblocks = (p.row_count[g] + BM - 1) / BM;
+    nb = local / mblocks;
+    mb = local % mblocks;
+  };
+  const int nkb = p.K / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+        int g, mb, nb;
+        decode(t, g, mb, nb);
+        const int a_row = p.row_begin[g] + mb * BM;
+        const int b_row = p.b_row_base[g] + nb * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          dev::mbar_wait(&empty[stage], phase ^ 1u);
+          dev::mbar_arrive_expect_tx(&full[stage], (BM + BN) * BK * 2);
+          dev::tma_load_2d(sA + stage * BM * BK * 2, &tmA, &full[stage], kb * BK, a_row);
+          dev::tma_load_2d(sB + stage * BN * BK * 2, &tmB, &full[stage], kb * BK, b_row);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer (single thread)
+      constexpr uint32_t idesc = dev::umma_idesc_bf16(BM, BN);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0;
+      for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+        dev::mbar_wait(&tempty[acc], aphase ^ 1u);
+        dev::tc_fence_after();
+        const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < nkb; ++kb) {
+          dev::mbar_wait(&full[stage], phase);
+          dev::tc_fence_after();
+          const uint32_t a0 = dev::smem_u32(sA + stage * BM * BK * 2);
+          const uint32_t b0 = dev::smem_u32(sB + stage * BN * BK * 2);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            dev::umma_bf16(d, dev::umma_desc_sw128(a0 + k * 32), dev::umma_desc_sw128(b0 + k * 32), idesc,
+                           (kb | k) != 0 ? 1u : 0u);
+          dev::umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        dev::umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1u;
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {  // ---------------- epilogue: TMEM -> registers -> global
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+      int g, mb, nb;
+      decode(t, g, mb, nb);
+      dev::mbar_wait(&tfull[acc], aphase);
+      dev::tc_fence_after();
+      const int lrow = mb * BM + q * 32 + lane;
+      const bool live = lrow < p.row_count[g];
+      const size_t row = static_cast<size_t>(p.row_begin[g] + lrow);
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
+      if constexpr (MODE == 0) {
+#pragma unroll 1
+        for (int c = 0; c < BN / 2; c += 32) {
+          uint32_t gr[32], ur[32];
+          dev::tmem_ld_32x32b_x32(tbase + c, gr);
+          dev::tmem_ld_32x32b_x32(tbase + BN / 2 + c, ur);
+          dev::tmem_ld_wait();
+          if (live) {
+            uint4 *dst = reinterpret_cast<uint4 *>(p.h + row * p.ldo + nb * (BN / 2) + c);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint32_t w[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int j = v * 8 + e * 2;
+                const float h0 = dev::silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]);
+                const float h1 = dev::silu(__uint_as_float(gr[j + 1])) * __uint_as_float(ur[j + 1]);
+                w[e] = dev::pack_bf2(h0, h1);
+              }
+              dst[v] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          dev::tmem_ld_32x32b_x32(tbase + c, r);
+          dev::tmem_ld_wait();
+          if (live) {
+            float4 *dst = reinterpret_cast<float4 *>(p.out + row * p.ldo + nb * BN + c);
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+              dst[v] = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                   __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+          }
+        }
+      }
+      dev::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) dev::mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1u;
+    }
+  }
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  if (warp == 2) dev::tmem_dealloc<512>(tmem_base);
+}
+
+// ------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void *f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  if (!fn) raise(HM_ECUDA, "cuTensorMapEncodeTiled is unavailable");
+  return fn;
+}
+
+// 2D bf16 tensor [outer, inner] with a (64 x box_rows) box and 128-byte swizzle.
+CUtensorMap make_map(const void *base, uint64_t inner, uint64_t outer, uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise(HM_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+  return m;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <typename K>
+void set_smem(K kernel, int bytes) {
+  HM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
+void launch_gemv(const uint16_t *pool, size_t slot_elems, int H, int I, const std::vector<hm_group> &gs,
+                 const uint16_t *xp, uint16_t *h, float *out, cudaStream_t st) {
+  if (gs.empty()) return;
+  HM_REQUIRE(static_cast<int>(gs.size()) <= kMaxGroups, HM_EVALUE, "too many expert groups in one launch");
+  HM_REQUIRE(H % 8 == 0 && I % 8 == 0 && I % kIlv == 0, HM_EVALUE, "GEMV needs H % 8 == 0 and I % 128 == 0");
+  GemvParams p{};
+  p.pool = pool;
+  p.slot_elems = slot_elems;
+  p.H = H;
+  p.I = I;
+  p.n_groups = static_cast<int>(gs.size());
+  p.xp = xp;
+  p.h = h;
+  p.out = out;
+  int mr = 1;
+  for (size_t g = 0; g < gs.size(); ++g) {
+    p.slot[g] = gs[g].slot;
+    p.row_begin[g] = gs[g].row_begin;
+    p.row_count[g] = gs[g].row_count;
+    mr = std::max(mr, gs[g].row_count);
+  }
+  const int target = num_sms() * 4;
+  const int G = p.n_groups;
+  // ffn1: pairs of (gate, up) rows
+  int chunk = static_cast<int>((static_cast<long>(G) * I + target - 1) / target);
+  chunk = std::max(8, (chunk + 7) / 8 * 8);
+  p.chunk = chunk;
+  p.bpg = (I + chunk - 1) / chunk;
+  int smem = mr * H * 2;
+  HM_REQUIRE(smem <= 200 * 1024, HM_EVALUE, "decode rows do not fit shared memory");
+  switch (mr) {
+    case 1: set_smem(ffn1_gemv_kernel<1>, smem); ffn1_gemv_kernel<1><<<G * p.bpg, 256, smem, st>>>(p); break;
+    case 2: set_smem(ffn1_gemv_kernel<2>, smem); ffn1_gemv_kernel<2><<<G * p.bpg, 256, smem, st>>>(p); break;
+    default: set_smem(ffn1_gemv_kernel<4>, smem); ffn1_gemv_kernel<4><<<G * p.bpg, 256, smem, st>>>(p); break;
+  }
+  HM_LAUNCH_CHECK();
+  chunk = static_cast<int>((static_cast<long>(G) * H + target - 1) / target);
+  chunk = std::max(8, (chunk + 7) / 8 * 8);
+  p.chunk = chunk;
+  p.bpg = (H + chunk - 1) / chunk;
+  smem = mr * I * 2;
+  HM_REQUIRE(smem <= 200 * 1024, HM_EVALUE, "decode rows do not fit shared memory");
+  switch (mr) {
+    case 1: set_smem(ffn2_gemv_kernel<1>, smem); ffn2_gemv_kernel<1><<<G * p.bpg, 256, smem, st>>>(p); break;
+    case 2: set_smem(ffn2_gemv_kernel<2>, smem); ffn2_gemv_kernel<2><<<G * p.bpg, 256, smem, st>>>(p); break;
+    default: set_smem(ffn2_gemv_kernel<4>, smem); ffn2_gemv_kernel<4><<<G * p.bpg, 256, smem, st>>>(p); break;
+  }
+  HM_LAUNCH_CHECK();
+}
+
+template <int BN, int MODE>
+void launch_gemm_one(const CUtensorMap &ta, const CUtensorMap &tb, GemmParams &p, cudaStream_t st) {
+  if (p.n_tiles == 0) return;
+  constexpr int smem = gemm_smem_bytes<BN>();
+  set_smem(expert_gemm_kernel<BN, MODE>, smem);
+  const int grid = std::min(p.n_tiles, num_sms());
+  expert_gemm_kernel<BN, MODE><<<grid, 256, smem, st>>>(ta, tb, p);
+  HM_LAUNCH_CHECK();
+}
+
+void launch_gemm(const uint16_t *pool, int n_slots, int H, int I, const std::vector<hm_group> &gs,
+                 const uint16_t *xp, int total_rows, uint16_t *h, float *out, cudaStream_t st) {
+  if (gs.empty()) return;
+  HM_REQUIRE(static_cast<int>(gs.size()) <= kMaxGroups, HM_EVALUE, "too many expert groups in one launch");
+  HM_REQUIRE(H % 128 == 0 && I % 128 == 0, HM_EVALUE, "GEMM path needs H % 128 == 0 and I % 128 == 0");
+  const uint64_t rows = static_cast<uint64_t>(std::max(total_rows, 1));
+  // ffn1: [rows, H] x W13^T -> h[rows, I]   (B view: pool as [n_slots*3I, H])
+  {
+    CUtensorMap ta = make_map(xp, H, rows, BM);
+    CUtensorMap tb = make_map(pool, H, static_cast<uint64_t>(n_slots) * 3 * I, 256);
+    GemmParams p{};
+    p.n_groups = static_cast<int>(gs.size());
+    p.K = H;
+    p.n_blocks = 2 * I / 256;
+    p.ldo = I;
+    p.h = h;
+    int t = 0;
+    for (size_t g = 0; g < gs.size(); ++g) {
+      p.tile_start[g] = t;
+      p.row_begin[g] = gs[g].row_begin;
+      p.row_count[g] = gs[g].row_count;
+      p.b_row_base[g] = gs[g].slot * 3 * I;
+      t += ((gs[g].row_count + BM - 1) / BM) * p.n_blocks;
+    }
+    p.tile_start[gs.size()] = t;
+    p.n_tiles = t;
+    launch_gemm_one<256, 0>(ta, tb, p, st);
+  }
+  // ffn2: h[rows, I] x W2^T -> out[rows, H]   (B view: pool as [n_slots*3H, I])
+  {
+    CUtensorMap ta = make_map(h, I, rows, BM);
+    const bool wide = H % 256 == 0;
+    CUtensorMap tb = make_map(pool, I, static_cast<uint64_t>(n_slots) * 3 * H, wide ? 256 : 128);
+    GemmParams p{};
+    p.n_groups = static_cast<int>(gs.size());
+    p.K = I;
+    p.n_blocks = H / (wide ? 256 : 128);
+    p.ldo = H;
+    p.out = out;
+    int t = 0;
+    for (size_t g = 0; g < gs.size(); ++g) {
+      p.tile_start[g] = t;
+      p.row_begin[g] = gs[g].row_begin;
+      p.row_count[g] = gs[g].row_count;
+      p.b_row_base[g] = gs[g].slot * 3 * H + 2 * H;
+      t += ((gs[g].row_count + BM - 1) / BM) * p.n_blocks;
+    }
+    p.tile_start[gs.size()] = t;
+    p.n_tiles = t;
+    if (wide)
+      launch_gemm_one<256, 1>(ta, tb, p, st);
+    else
+      launch_gemm_one<128, 1>(ta, tb, p, st);
+  }
+}
+
+}  // namespace
+}  // namespace hm
+
+extern "C" {
+
+int hm_expert_ffn(const uint16_t *pool, int n_slots, int H, int I, const hm_group *groups, int n_groups,
+                  const uint16_t *xp, int total_rows, uint16_t *h, float *out, int path, void *stream) {
+  HM_API_BEGIN
+  HM_REQUIRE(n_groups >= 0 && (n_groups == 0 || groups), HM_EVALUE, "bad group table");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::vector<hm_group> small, big;
+  for (int g = 0; g < n_groups; ++g) {
+    const hm_group &gr = groups[g];
+    HM_REQUIRE(gr.slot >= 0 && gr.slot < n_slots && gr.row_begin >= 0 && gr.row_count >= 0 &&
+                   gr.row_begin + gr.row_count <= total_rows,
+               HM_EVALUE, "expert group outside the pool or the row range");
+    if (gr.row_count == 0) continue;
+    const bool gemv = path == HM_FFN_GEMV || (path == HM_FFN_AUTO && gr.row_count <= hm::kGemvMaxRows);
+    if (gemv) {
+      HM_REQUIRE(gr.row_count <= hm::kGemvMaxRows, HM_EVALUE, "GEMV path takes at most 4 rows per expert");
+      small.push_back(gr);
+    } else {
+      big.push_back(gr);
+    }
+  }
+  const size_t slot_elems = static_cast<size_t>(3) * H * I;
+  for (size_t b = 0; b < small.size(); b += hm::kMaxGroups) {
+    std::vector<hm_group> part(small.begin() + b, small.begin() + std::min(small.size(), b + hm::kMaxGroups));
+    hm::launch_gemv(pool, slot_elems, H, I, part, xp, h, out, st);
+  }
+  for (size_t b = 0; b < big.size(); b += hm::kMaxGroups) {
+    std::vector<hm_group> part(big.begin() + b, big.begin() + std::min(big.size(), b + hm::kMaxGroups));
+    hm::launch_gemm(pool, n_slots, H, I, part, xp, total_rows, h, out, st);
+  }
+  HM_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,321 @@
+// Router, token permutation, combine and the GPU MRS update (sm_100a).
+//
+// Router semantics (Eq. 1; transformers mixtral / deepseek_v2 /
+// qwen2_moe routers): softmax over the N routed logits in fp32, top-K by
+// (logit desc, expert index asc) -- the reference's documented tie rule
+// (core.py:94-97, tracegen.py:139-141) -- combine weight = softmax probability,
+// optionally renormalised over the selected K (Mixtral).  Shared experts are
+// appended as always-selected columns N..N+S-1 with weight 1 or, for the
+// Qwen2 shared expert, sigmoid of a gate logit.  Per-expert loads are the
+// bincount of the selection (tracegen.py:148); score sums are the fp64
+// token-sum of the routed softmax (tracegen.py:149) reduced in a fixed order.
+#include <cfloat>
+
+#include "device.cuh"
+
+namespace hm {
+namespace {
+
+constexpr int kMaxPerLane = 8;  // N <= 256 routed experts
+
+__global__ void router_topk_kernel(const float *__restrict__ logits, int T, int N, int ld, int K, int renorm,
+                                   int n_shared, int shared_gate_col, int32_t *__restrict__ sel,
+                                   float *__restrict__ w, float *__restrict__ probs, int32_t *__restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (blockIdx.x == 0 && threadIdx.x < n_shared) counts[N + threadIdx.x] = T;
+  if (t >= T) return;
+  const float *row = logits + static_cast<size_t>(t) * ld;
+  float v[kMaxPerLane];
+  float m = -FLT_MAX;
+#pragma unroll
+  for (int j = 0; j < kMaxPerLane; ++j) {
+    int e = lane + 32 * j;
+    v[j] = e < N ? row[e] : -FLT_MAX;
+    m = fmaxf(m, v[j]);
+  }
+  m = dev::warp_max(m);
+  float ex[kMaxPerLane];
+  float s = 0.0f;
+#pragma unroll
+  for (int j = 0; j < kMaxPerLane; ++j) {
+    int e = lane + 32 * j;
+    ex[j] = e < N ? expf(v[j] - m) : 0.0f;
+    s += ex[j];
+  }
+  s = dev::warp_sum(s);
+  const float inv = 1.0f / s;
+#pragma unroll
+  for (int j = 0; j < kMaxPerLane; ++j) {
+    int e = lane + 32 * j;
+    if (e < N) probs[static_cast<size_t>(t) * N + e] = ex[j] * inv;
+  }
+  // top-K: repeated warp arg-max with (value desc, index asc)
+  const int Kp = K + n_shared;
+  uint32_t taken = 0;
+  float psel[8];
+  float psum = 0.0f;
+  for (int k = 0; k < K; ++k) {
+    float bv = -FLT_MAX;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int j = 0; j < kMaxPerLane; ++j) {
+      int e = lane + 32 * j;
+      if (e < N && !((taken >> j) & 1u) && (v[j] > bv || (v[j] == bv && e < bi))) {
+        bv = v[j];
+        bi = e;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+    float p = expf(bv - m) * inv;
+    psel[k] = p;
+    psum += p;
+    if (lane == 0) {
+      sel[static_cast<size_t>(t) * Kp + k] = bi;
+      atomicAdd(&counts[bi], 1);
+    }
+  }
+  if (lane == 0) {
+    for (int k = 0; k < K; ++k) w[static_cast<size_t>(t) * Kp + k] = renorm ? psel[k] / psum : psel[k];
+    float g = 1.0f;
+    if (shared_gate_col >= 0) g = 1.0f / (1.0f + expf(-row[shared_gate_col]));
+    for (int s2 = 0; s2 < n_shared; ++s2) {
+      sel[static_cast<size_t>(t) * Kp + K + s2] = N + s2;
+      w[static_cast<size_t>(t) * Kp + K + s2] = g;
+    }
+  }
+}
+
+// score_sum[e] = sum_t probs[t, e] in fp64, fixed reduction order.
+__global__ void score_sum_kernel(const float *__restrict__ probs, int T, int N, double *__restrict__ out) {
+  __shared__ double red[256];
+  const int e = blockIdx.x;
+  double acc = 0.0;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) acc += static_cast<double>(probs[static_cast<size_t>(t) * N + e]);
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[e] = red[0];
+}
+
+// logits[t, n] = x[t, :] . wg[n, :]  (bf16 in, fp32 accumulate); one warp per (t, n).
+__global__ void router_logits_kernel(const uint16_t *__restrict__ x, const uint16_t *__restrict__ wg, int T, int H,
+                                     int N, float *__restrict__ logits) {
+  const int lane = threadIdx.x & 31;
+  const long item = static_cast<long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (item >= static_cast<long>(T) * N) return;
+  const int t = static_cast<int>(item / N), n = static_cast<int>(item % N);
+  const uint16_t *xr = x + static_cast<size_t>(t) * H;
+  const uint16_t *wr = wg + static_cast<size_t>(n) * H;
+  float acc = 0.0f;
+  for (int c = lane * 8; c < H; c += 256) acc += dev::dot8(dev::ld_stream(wr + c), *reinterpret_cast<const uint4 *>(xr + c));
+  acc = dev::warp_sum(acc);
+  if (lane == 0) logits[item] = acc;
+}
+
+__global__ void offsets_kernel(const int32_t *__restrict__ counts, int E, int32_t *__restrict__ offsets) {
+  if (threadIdx.x == 0) {
+    int32_t run = 0;
+    for (int e = 0; e < E; ++e) {
+      offsets[e] = run;
+      run += counts[e];
+    }
+    offsets[E] = run;
+  }
+}
+
+// One block per expert: rows of expert e in (token, slot) order.
+__global__ void permute_kernel(const int32_t *__restrict__ sel, int TK, const int32_t *__restrict__ offsets,
+                               int32_t *__restrict__ pos, int32_t *__restrict__ row_src) {
+  __shared__ int32_t warp_tot[32];
+  __shared__ int32_t base;
+  const int e = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) base = offsets[e];
+  __syncthreads();
+  for (int j0 = 0; j0 < TK; j0 += blockDim.x) {
+    const int j = j0 + threadIdx.x;
+    const bool hit = j < TK && sel[j] == e;
+    const uint32_t ballot = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) warp_tot[wid] = __popc(ballot);
+    __syncthreads();
+    int before = 0;
+    for (int w2 = 0; w2 < wid; ++w2) before += warp_tot[w2];
+    if (hit) {
+      const int p = base + before + __popc(ballot & ((1u << lane) - 1u));
+      pos[j] = p;
+      row_src[p] = j;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int w2 = 0; w2 < nw; ++w2) tot += warp_tot[w2];
+      base += tot;
+    }
+    __syncthreads();
+  }
+}
+
+// xp[r, :] = x[row_src[r] / Kp, :]
+__global__ void gather_kernel(const uint16_t *__restrict__ x, const int32_t *__restrict__ row_src, int rows, int Kp,
+                              int H, uint16_t *__restrict__ xp) {
+  const int r = blockIdx.x;
+  if (r >= rows) return;
+  const int t = row_src[r] / Kp;
+  const uint4 *src = reinterpret_cast<const uint4 *>(x + static_cast<size_t>(t) * H);
+  uint4 *dst = reinterpret_cast<uint4 *>(xp + static_cast<size_t>(r) * H);
+  for (int c = threadIdx.x; c < H / 8; c += blockDim.x) dst[c] = src[c];
+}
+
+// y[t, :] = residual[t, :] + sum_k w[t, k] * out[pos[t, k], :]   (k in order)
+__global__ void combine_kernel(const float *__restrict__ out, const int32_t *__restrict__ pos,
+                               const float *__restrict__ w, int Kp, int H, const uint16_t *__restrict__ residual,
+                               uint16_t *__restrict__ y) {
+  const int t = blockIdx.x;
+  for (int c = threadIdx.x * 4; c < H; c += blockDim.x * 4) {
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    for (int k = 0; k < Kp; ++k) {
+      const float wk = w[static_cast<size_t>(t) * Kp + k];
+      const float4 o = *reinterpret_cast<const float4 *>(out + static_cast<size_t>(pos[static_cast<size_t>(t) * Kp + k]) * H + c);
+      a0 = fmaf(wk, o.x, a0);
+      a1 = fmaf(wk, o.y, a1);
+      a2 = fmaf(wk, o.z, a2);
+      a3 = fmaf(wk, o.w, a3);
+    }
+    if (residual) {
+      const uint2 rv = *reinterpret_cast<const uint2 *>(residual + static_cast<size_t>(t) * H + c);
+      a0 += dev::bf_lo(rv.x);
+      a1 += dev::bf_hi(rv.x);
+      a2 += dev::bf_lo(rv.y);
+      a3 += dev::bf_hi(rv.y);
+    }
+    uint2 o2;
+    o2.x = dev::pack_bf2(a0, a1);
+    o2.y = dev::pack_bf2(a2, a3);
+    *reinterpret_cast<uint2 *>(y + static_cast<size_t>(t) * H + c) = o2;
+  }
+}
+
+// S[layer, i] <- a * TopP(s)[i] + (1 - a) * S[layer, i]   (caching.py:58-76)
+// Round-to-nearest intrinsics keep every operation a separate IEEE rounding,
+// exactly like the host core (no FMA contraction).
+__global__ void mrs_update_kernel(double *__restrict__ S, const double *__restrict__ s, int layer, int N, int p,
+                                  double a) {
+  const int i = threadIdx.x;
+  if (i >= N) return;
+  const double si = s[i];
+  int rank = 0;
+  for (int j = 0; j < N; ++j) {
+    const double sj = s[j];
+    rank += (sj > si || (sj == si && j < i)) ? 1 : 0;
+  }
+  const double t = rank < p ? si : 0.0;
+  const double keep = __dsub_rn(1.0, a);
+  double *row = S + static_cast<size_t>(layer) * N;
+  row[i] = __dadd_rn(__dmul_rn(a, t), __dmul_rn(keep, row[i]));
+}
+
+}  // namespace
+}  // namespace hm
+
+using hm::raise;
+
+extern "C" {
+
+int hm_router_topk(const float *logits, int T, int N, int ld, int K, int renormalize, int n_shared,
+                   int shared_gate_col, int32_t *sel, float *w, float *probs, int32_t *counts, void *stream) {
+  HM_API_BEGIN
+  HM_REQUIRE(N >= 1 && N <= 256 && K >= 1 && K <= 8 && K <= N && ld >= N, HM_EVALUE, "router shape out of range");
+  HM_REQUIRE(n_shared >= 0 && n_shared <= 32, HM_EVALUE, "too many shared expert columns");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  HM_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (N + n_shared), st));
+  if (T > 0) {
+    const int warps = 8;
+    hm::router_topk_kernel<<<(T + warps - 1) / warps, 32 * warps, 0, st>>>(logits, T, N, ld, K, renormalize, n_shared,
+                                                                          shared_gate_col, sel, w, probs, counts);
+    HM_LAUNCH_CHECK();
+  } else if (n_shared > 0) {
+    HM_CUDA(cudaMemsetAsync(counts + N, 0, sizeof(int32_t) * n_shared, st));
+  }
+  HM_API_END
+}
+
+int hm_score_sums(const float *probs, int T, int N, double *score_sum, void *stream) {
+  HM_API_BEGIN
+  hm::score_sum_kernel<<<N, 256, 0, static_cast<cudaStream_t>(stream)>>>(probs, T, N, score_sum);
+  HM_LAUNCH_CHECK();
+  HM_API_END
+}
+
+int hm_router_logits(const uint16_t *x, const uint16_t *wg, int T, int H, int N, float *logits, void *stream) {
+  HM_API_BEGIN
+  HM_REQUIRE(H % 8 == 0, HM_EVALUE, "hidden size must be a multiple of 8");
+  const long items = static_cast<long>(T) * N;
+  if (items > 0) {
+    hm::router_logits_kernel<<<static_cast<unsigned>((items + 7) / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        x, wg, T, H, N, logits);
+    HM_LAUNCH_CHECK();
+  }
+  HM_API_END
+}
+
+int hm_offsets(const int32_t *counts, int E, int32_t *offsets, void *stream) {
+  HM_API_BEGIN
+  hm::offsets_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(counts, E, offsets);
+  HM_LAUNCH_CHECK();
+  HM_API_END
+}
+
+int hm_permute(const int32_t *sel, int T, int Kp, int E, const int32_t *offsets, int32_t *pos, int32_t *row_src,
+               void *stream) {
+  HM_API_BEGIN
+  if (T > 0) {
+    hm::permute_kernel<<<E, 256, 0, static_cast<cudaStream_t>(stream)>>>(sel, T * Kp, offsets, pos, row_src);
+    HM_LAUNCH_CHECK();
+  }
+  HM_API_END
+}
+
+int hm_gather_rows(const uint16_t *x, const int32_t *row_src, int rows, int Kp, int H, uint16_t *xp, void *stream) {
+  HM_API_BEGIN
+  HM_REQUIRE(H % 8 == 0, HM_EVALUE, "hidden size must be a multiple of 8");
+  if (rows > 0) {
+    hm::gather_kernel<<<rows, 128, 0, static_cast<cudaStream_t>(stream)>>>(x, row_src, rows, Kp, H, xp);
+    HM_LAUNCH_CHECK();
+  }
+  HM_API_END
+}
+
+int hm_combine(const float *out, const int32_t *pos, const float *w, int T, int Kp, int H, const uint16_t *residual,
+               uint16_t *y, void *stream) {
+  HM_API_BEGIN
+  HM_REQUIRE(H % 4 == 0, HM_EVALUE, "hidden size must be a multiple of 4");
+  if (T > 0) {
+    hm::combine_kernel<<<T, 256, 0, static_cast<cudaStream_t>(stream)>>>(out, pos, w, Kp, H, residual, y);
+    HM_LAUNCH_CHECK();
+  }
+  HM_API_END
+}
+
+int hm_mrs_update_dev(double *S, const double *scores, int layer, int N, int p, double alpha, void *stream) {
+  HM_API_BEGIN
+  HM_REQUIRE(N >= 1 && N <= 1024, HM_EVALUE, "MRS row too wide");
+  hm::mrs_update_kernel<<<1, ((N + 31) / 32) * 32, 0, static_cast<cudaStream_t>(stream)>>>(S, scores, layer, N, p,
+                                                                                          alpha);
+  HM_LAUNCH_CHECK();
+  HM_API_END
+}
+
+}  // extern "C"

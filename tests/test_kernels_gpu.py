@@ -1,0 +1,186 @@
+"""sm_100a kernel parity against the fp32 CPU oracle (oracle/moe_ref.py).
+
+Tolerances: router indices / loads / permutation bit-exact; router weights and
+probabilities rtol 1e-5 (fp32 expf vs numpy exp); expert outputs
+max|gpu - ref| / max|ref| <= 1e-2 (BASELINE.json north_star: bf16 weights and
+activations, fp32 accumulation, h rounded to bf16); MRS update bit-exact.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import moe_ref as ref
+
+import paper_2504_05897_b200.caching as mc
+from paper_2504_05897_b200 import _lib, kernels as K
+from paper_2504_05897_b200.weights import pack_expert
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-2
+
+
+def rel_err(got: np.ndarray, want: np.ndarray) -> float:
+    return float(np.abs(got - want).max() / max(np.abs(want).max(), 1e-30))
+
+
+def make_pool(n_slots: int, H: int, I: int, seed: int):
+    """Random N(0, 0.02^2) bf16 experts packed into a slot pool; returns (pool_gpu, experts fp32)."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    pool = torch.empty((n_slots, 3 * H * I), dtype=torch.bfloat16, device="cuda")
+    experts = []
+    for s in range(n_slots):
+        gate = (torch.randn((I, H), generator=g, device="cuda") * 0.02).to(torch.bfloat16)
+        up = (torch.randn((I, H), generator=g, device="cuda") * 0.02).to(torch.bfloat16)
+        down = (torch.randn((H, I), generator=g, device="cuda") * 0.02).to(torch.bfloat16)
+        gn, un, dn = (t.view(torch.int16).cpu().numpy().view(np.uint16) for t in (gate, up, down))
+        img = pack_expert(gn, un, dn)
+        pool[s].copy_(torch.from_numpy(img.view(np.int16)).view(torch.bfloat16).to("cuda"))
+        experts.append((ref.bf16_to_f32(gn), ref.bf16_to_f32(un), ref.bf16_to_f32(dn)))
+    return pool.view(-1), experts
+
+
+def bf16_numpy(t: torch.Tensor) -> np.ndarray:
+    return ref.bf16_to_f32(t.view(torch.int16).cpu().numpy().view(np.uint16))
+
+
+@pytest.mark.parametrize("T,N,Kk,renorm,S,gate", [(1, 8, 2, True, 0, -1), (1024, 8, 2, True, 0, -1),
+                                                  (1024, 64, 6, False, 2, -1), (1024, 64, 8, False, 8, 64),
+                                                  (7, 256, 8, True, 0, -1), (0, 8, 2, True, 1, -1)])
+def test_router_parity(T, N, Kk, renorm, S, gate):
+    rng = np.random.default_rng(T * 1000 + N)
+    ld = N + (1 if gate >= 0 else 0)
+    logits = rng.standard_normal((T, ld)).astype(np.float32)
+    if T > 2:
+        logits[1] = 0.5                     # an all-tied row
+        logits[2, : N // 2] = logits[2, N // 2: 2 * (N // 2)]  # pairwise ties
+    sel, w, probs, counts = K.router_topk(torch.from_numpy(logits).cuda(), N, Kk, renorm, S, gate)
+    ssum = K.score_sums(probs) if T > 0 else None
+    torch.cuda.synchronize()
+    r_sel, r_w, r_probs, r_counts, r_ssum = ref.router(logits, N, Kk, renorm, S, gate)
+    assert np.array_equal(sel.cpu().numpy(), r_sel)
+    assert np.array_equal(counts.cpu().numpy(), r_counts)
+    if T > 0:
+        np.testing.assert_allclose(w.cpu().numpy(), r_w, rtol=1e-5, atol=1e-7)
+        np.testing.assert_allclose(probs.cpu().numpy(), r_probs, rtol=1e-5, atol=1e-7)
+        np.testing.assert_allclose(ssum.cpu().numpy(), r_ssum, rtol=1e-5)
+
+
+def test_permute_gather_combine():
+    T, N, Kk, S, H = 300, 16, 4, 1, 256
+    rng = np.random.default_rng(3)
+    logits = torch.from_numpy(rng.standard_normal((T, N)).astype(np.float32)).cuda()
+    sel, w, probs, counts = K.router_topk(logits, N, Kk, False, S)
+    offs = K.offsets(counts)
+    pos, row_src = K.permute(sel, offs, N + S)
+    x = torch.randn((T, H), device="cuda").to(torch.bfloat16)
+    xp = K.gather_rows(x, row_src, Kk + S)
+    torch.cuda.synchronize()
+    sel_flat = sel.cpu().numpy().ravel()
+    want = np.concatenate([np.nonzero(sel_flat == e)[0] for e in range(N + S)])
+    assert np.array_equal(row_src.cpu().numpy(), want)
+    assert np.array_equal(pos.cpu().numpy().ravel()[want], np.arange(T * (Kk + S)))
+    assert torch.equal(xp, x[torch.from_numpy(want // (Kk + S)).cuda()])
+    out = torch.randn((T * (Kk + S), H), device="cuda")
+    y = K.combine(out, pos, w, residual=x)
+    torch.cuda.synchronize()
+    o, pn, wn = out.cpu().numpy(), pos.cpu().numpy(), w.cpu().numpy()
+    exp = bf16_numpy(x) + np.einsum("tk,tkh->th", wn, o[pn])
+    assert rel_err(bf16_numpy(y), exp) < 1e-2
+
+
+def _ffn_case(H, I, counts, path, seed=0):
+    n_slots = len(counts) + 1
+    pool, experts = make_pool(n_slots, H, I, seed)
+    rows = sum(counts)
+    x = (torch.randn((rows, H), device="cuda")).to(torch.bfloat16)
+    h = torch.empty((rows, I), dtype=torch.bfloat16, device="cuda")
+    out = torch.full((rows, H), float("nan"), device="cuda")
+    groups, rb = [], 0
+    for g, c in enumerate(counts):
+        groups.append(((g * 3 + 1) % n_slots, rb, c))   # slots out of order
+        rb += c
+    K.expert_ffn(pool, n_slots, H, I, groups, x, h, out, path)
+    torch.cuda.synchronize()
+    xn, on = bf16_numpy(x), out.cpu().numpy()
+    for slot, b, c in groups:
+        want = ref.expert(xn[b:b + c], *experts[slot])
+        assert rel_err(on[b:b + c], want) <= TOL, (slot, b, c)
+
+
+@pytest.mark.parametrize("counts", [[1], [1, 2, 3, 4], [4, 4, 1]])
+def test_expert_ffn_gemv(counts):
+    _ffn_case(512, 384, counts, _lib.FFN_GEMV)
+
+
+@pytest.mark.parametrize("counts", [[1], [5], [128], [130, 7, 300], [256, 256]])
+def test_expert_ffn_gemm(counts):
+    _ffn_case(512, 384, counts, _lib.FFN_GEMM)
+
+
+def test_expert_ffn_gemm_narrow_hidden():
+    _ffn_case(128, 256, [3, 200], _lib.FFN_GEMM)     # H % 256 != 0 -> BN=128 down-projection
+
+
+def test_expert_ffn_auto_mixed():
+    _ffn_case(256, 256, [1, 300, 2, 64], _lib.FFN_AUTO)
+
+
+@pytest.mark.parametrize("rows,path", [(1, _lib.FFN_GEMV), (256, _lib.FFN_GEMM)])
+def test_expert_ffn_mixtral_shape(rows, path):
+    H, I = 4096, 14336
+    pool, experts = make_pool(1, H, I, 11)
+    x = torch.randn((rows, H), device="cuda").to(torch.bfloat16)
+    h = torch.empty((rows, I), dtype=torch.bfloat16, device="cuda")
+    out = torch.empty((rows, H), device="cuda")
+    K.expert_ffn(pool, 1, H, I, [(0, 0, rows)], x, h, out, path)
+    torch.cuda.synchronize()
+    pick = np.arange(rows)[:: max(1, rows // 16)]
+    want = ref.expert(bf16_numpy(x)[pick], *experts[0])
+    assert rel_err(out.cpu().numpy()[pick], want) <= TOL
+
+
+def test_mrs_update_dev_bit_exact():
+    L, N, p, a = 3, 64, 12, 0.5
+    rng = np.random.default_rng(5)
+    host = mc.MrsState(None, alpha=a, p=p, num_layers=L, num_routed=N)
+    S = torch.full((L, N), 1.0 / N, dtype=torch.float64, device="cuda")
+    for step in range(20):
+        s = rng.random(N)
+        if step % 3 == 0:
+            s[:8] = s[8]                     # ties
+        s /= s.sum()
+        layer = step % L
+        mc.mrs_update(host, layer, s)
+        K.mrs_update_dev(S, torch.from_numpy(s).cuda(), layer, p, a)
+    torch.cuda.synchronize()
+    assert np.array_equal(S.cpu().numpy().view(np.uint64), host.table().view(np.uint64))
+
+
+@pytest.mark.parametrize("T,N,Kk,S,renorm,gate", [(64, 8, 2, 0, True, -1), (200, 16, 4, 2, False, -1),
+                                                  (1, 16, 4, 2, False, 16), (96, 16, 8, 2, False, 16)])
+def test_moe_layer_end_to_end(T, N, Kk, S, renorm, gate):
+    H, I = 256, 256
+    pool, experts = make_pool(N + S, H, I, 7)
+    rng = np.random.default_rng(T)
+    ld = N + (1 if gate >= 0 else 0)
+    logits = rng.standard_normal((T, ld)).astype(np.float32)
+    x = torch.randn((T, H), device="cuda").to(torch.bfloat16)
+    sel, w, probs, counts = K.router_topk(torch.from_numpy(logits).cuda(), N, Kk, renorm, S, gate)
+    offs = K.offsets(counts)
+    pos, row_src = K.permute(sel, offs, N + S)
+    xp = K.gather_rows(x, row_src, Kk + S)
+    rows = T * (Kk + S)
+    h = torch.empty((rows, I), dtype=torch.bfloat16, device="cuda")
+    out = torch.empty((rows, H), device="cuda")
+    o = offs.cpu().numpy()
+    groups = [(e, int(o[e]), int(o[e + 1] - o[e])) for e in range(N + S)]
+    K.expert_ffn(pool, N + S, H, I, groups, xp, h, out)
+    y = K.combine(out, pos, w, residual=x)
+    torch.cuda.synchronize()
+    want = ref.moe_layer(bf16_numpy(x), logits, experts, N, Kk, renorm, S, gate, residual=True)
+    assert rel_err(bf16_numpy(y), want) <= TOL
+
