@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""HybriMoE MoE-layer hot path on B200: decode tok/s and 1k-token prefill latency
+at a 25% expert-cache budget (BASELINE.json metric), one JSON line on rank 0.
+
+  python bench.py [--gpus 1] [--steps 8] [--warmup 3] [--shape mixtral] [--impl ours|reference]
+
+A "step" is one decode pass: one token through all L MoE layers of the named
+shape (random-init bf16 weights, synthetic routing from the reference's trace
+generator), executed under the HybriMoE schedule -- GPU experts from the HBM
+cache, demand copies over PCIe, CPU experts on the host worker -- with the
+decision core planning every layer from a profile calibrated on this box.
+The prefill pass (1024 tokens, cold cache) runs first and is reported as
+``prefill.ms``.  ``--impl reference`` times the CPU oracle port of the path
+(oracle/: the reference's decisions + fp32 numpy experts, all on the CPU).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def peaks() -> tuple[dict, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text()), "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int = 0) -> None:
+        self.gpu, self.rows, self._stop = gpu, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self) -> None:
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                self.rows.append([v.strip() for v in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self) -> dict:
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i - 3] for r in self.rows if len(r) >= 7 for i in range(3, 7)
+                          if r[i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- reference arm / cpu baseline
+def cpu_oracle_decode(shape: str, n_layers_sample: int, n_distinct: int = 2, seed: int = 0, threads: int | None = None):
+    """The reference's CPU path, ported: per layer the oracle's plan (all experts
+    uncached -> the decision restatement) + fp32 numpy SwiGLU experts on the CPU
+    (plan_all_cpu semantics, scheduling.py:273-284) for one decode token.
+    Returns (seconds per token scaled to all L layers, sample description)."""
+    from oracle import decisions as od
+    from oracle import moe_ref as ref
+    from paper_2504_05897_b200.moe import SHAPES, FAMILIES, shared_chunks
+    from paper_2504_05897_b200.tracegen import GenParams, generate_router_logits
+
+    cfg = SHAPES[shape]
+    fam = FAMILIES[shape]
+    H, I = cfg.routed_expert_dims
+    S = shared_chunks(cfg)
+    rng = np.random.default_rng(seed)
+    experts = [tuple((rng.standard_normal(sh, dtype=np.float32) * 0.02) for sh in ((I, H), (I, H), (H, I)))
+               for _ in range(n_distinct)]
+    _, logits = generate_router_logits(cfg, GenParams(seed=seed), 0, 1)
+    prof = dict(gpu_time_per_expert=1.0, cpu_slope=1.0, transfer_bandwidth=1e9, transfer_latency=0.0,
+                gpu_saturation_load=256, gpu_slope=0.0, cpu_first_expert_penalty=1.0, shared_expert_time=0.0,
+                non_expert_time=0.0)
+    x = rng.standard_normal((1, H), dtype=np.float32)
+    L = min(n_layers_sample, cfg.num_layers)
+    t0 = time.perf_counter()
+    for l in range(L):
+        lg = logits[0][l].astype(np.float32)
+        if fam.shared_gate:
+            lg = np.concatenate([lg, np.zeros((1, 1), np.float32)], axis=1)
+        sel, w, _, counts, _ = ref.router(lg, cfg.num_routed, cfg.num_activated, fam.renormalize, S,
+                                          cfg.num_routed if fam.shared_gate else -1)
+        tasks = [((l, e), int(counts[e])) for e in range(cfg.num_routed) if counts[e] > 0]
+        od.best_plan([], tasks, prof, 3.0 * H * I * 2)
+        y = np.zeros_like(x)
+        for k in range(sel.shape[1]):
+            e = int(sel[0, k])
+            y += w[0, k] * ref.expert(x, *experts[(l * 7 + e) % n_distinct])
+        x = x + y
+    dt = time.perf_counter() - t0
+    per_token = dt * cfg.num_layers / L
+    return per_token, f"{L} of {cfg.num_layers} layers of one decode token, fp32 numpy experts " \
+                      f"({n_distinct} distinct weight sets aliased), scaled to {cfg.num_layers} layers"
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count()
+    times = []
+    sample = ""
+    for i in range(args.warmup + args.steps):
+        dt, sample = cpu_oracle_decode(args.shape, args.ref_layers, seed=i)
+        if i >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * statistics.mean(times)
+    tok_s = 1e3 / ms * args.gpus
+    line = {"impl": "reference", "metric": "decode tok/s at 25% expert-cache budget", "value": tok_s,
+            "unit": "tok/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (reference trace generator routing, random-init weights)",
+            "config": {"workload": f"{args.shape}-shaped MoE decode, batch 1, CPU oracle port", "shape": args.shape},
+            "cpu_baseline": {"value": tok_s, "unit": "tok/s", "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": tok_s, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+def run_ours(args) -> None:
+    import torch
+
+    from paper_2504_05897_b200 import _lib
+    from paper_2504_05897_b200.calibration import calibrate_shape
+    from paper_2504_05897_b200.engine import EnginePolicy
+    from paper_2504_05897_b200.moe import FAMILIES, SHAPES, HybridMoE, with_shared_time
+    from paper_2504_05897_b200.prefetch import predict_layers
+    from paper_2504_05897_b200.tracegen import GenParams, generate_router_logits
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    cfg = SHAPES[args.shape]
+    H, I = cfg.routed_expert_dims
+    pk, pk_kind = peaks()
+    t_setup = time.time()
+    cal, _samples = calibrate_shape(H, I)
+    prof = with_shared_time(cal.profile, cfg)
+    policy = EnginePolicy(cache_policy=args.policy, prefetch=args.prefetch)
+    total_bytes = cfg.num_layers * cfg.num_routed * 3 * H * I * 2
+    host_images = args.host_images
+    if host_images is None:
+        try:
+            import psutil
+            avail = psutil.virtual_memory().available
+        except Exception:
+            avail = 0
+        host_images = None if avail > 1.3 * total_bytes else max(16, int(0.5 * avail / (3 * H * I * 2)))
+    moe = HybridMoE(cfg, args.shape, policy, args.ratio, prof, host_images=host_images,
+                    max_tokens=max(args.prefill, 1), cpu_threads=args.cpu_threads)
+    moe.init_random_weights(seed=args.seed + rank)
+    n_dec = args.warmup + args.steps
+    trace, logits = generate_router_logits(cfg, GenParams(seed=args.seed + rank), args.prefill, 2 * n_dec + 1)
+    dev_logits = []
+    for p in range(len(trace.passes)):
+        layer_logits = []
+        for l in range(cfg.num_layers):
+            lg = logits[p][l].astype(np.float32)
+            if moe.family.shared_gate:
+                lg = np.concatenate([lg, np.zeros((lg.shape[0], 1), np.float32)], axis=1)
+            layer_logits.append(torch.from_numpy(np.ascontiguousarray(lg)).cuda())
+        dev_logits.append(layer_logits)
+    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    xs = [torch.randn((f.token_count, H), generator=g, device="cuda").to(torch.bfloat16) for f in trace.passes]
+    torch.cuda.synchronize()
+    setup_s = time.time() - t_setup
+
+    def predictor(p):
+        fwd = trace.passes[p]
+        return lambda l: predict_layers(fwd.layers, cfg.num_layers, p, l, policy.prediction, args.seed)
+
+    st = torch.cuda.current_stream()
+    # ---- prefill: 1k tokens, cold cache (the reference's TTFT, engine.py:465-466)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(st)
+    _, pinfo = moe.forward_pass(xs[0], dev_logits[0], predict=predictor(0))
+    ev1.record(st)
+    ev1.synchronize()
+    prefill_ms = ev0.elapsed_time(ev1)
+    pst = pinfo["stats"]
+
+    # ---- decode: W warm-up passes, then K timed passes
+    for p in range(1, 1 + args.warmup):
+        moe.forward_pass(xs[p], dev_logits[p], predict=predictor(p))
+    torch.cuda.synchronize()
+    lib = _lib.lib
+    lib.hm_runtime_set_kernel_timing(moe._rt, 1)
+    launches0 = lib.hm_launch_count()
+    stats_all = []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(st)
+        for k in range(args.steps):
+            p = 1 + args.warmup + k
+            _, info = moe.forward_pass(xs[p], dev_logits[p], predict=predictor(p))
+            stats_all.extend(info["stats"])
+        t1.record(st)
+        t1.synchronize()
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = lib.hm_launch_count() - launches0
+    ms_total = t0.elapsed_time(t1)
+    import ctypes as C
+    kms, kbytes, kn, kmax = C.c_double(), C.c_int64(), C.c_int64(), C.c_double()
+    lib.hm_runtime_kernel_times(moe._rt, C.byref(kms), C.byref(kbytes), C.byref(kn), C.byref(kmax))
+    lib.hm_runtime_set_kernel_timing(moe._rt, 0)
+    if dist:
+        t = torch.tensor([ms_total], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    tok_s = world * 1e3 / ms_step
+
+    # ---- e2e: host buffers through the public API, copies inside the timed region
+    e2e_passes = range(1 + n_dec, 1 + 2 * n_dec)
+    host_x = [xs[p].cpu().pin_memory() for p in e2e_passes]
+    host_lg = [torch.stack([t.cpu() for t in dev_logits[p]]).pin_memory() for p in e2e_passes]
+    y_host = torch.empty((1, H), dtype=torch.bfloat16).pin_memory()
+    dx = torch.empty((1, H), dtype=torch.bfloat16, device="cuda")
+    dlg = torch.empty_like(host_lg[0], device="cuda")
+    for i in range(args.warmup):
+        p = list(e2e_passes)[i]
+        dx.copy_(host_x[i], non_blocking=True)
+        dlg.copy_(host_lg[i], non_blocking=True)
+        y, _ = moe.forward_pass(dx, list(dlg), predict=predictor(p))
+        y_host.copy_(y, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for i in range(args.warmup, n_dec):
+        p = list(e2e_passes)[i]
+        dx.copy_(host_x[i], non_blocking=True)
+        dlg.copy_(host_lg[i], non_blocking=True)
+        y, _ = moe.forward_pass(dx, list(dlg), predict=predictor(p))
+        y_host.copy_(y, non_blocking=True)
+    e1.record(st)
+    e1.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    h2d = H * 2 + host_lg[0].numel() * 4
+    d2h = H * 2
+
+    # ---- roofline of the dominant GPU kernel (decode expert FFN, HBM-bound)
+    achieved_gbs = kbytes.value / (kms.value / 1e3) / 1e9 if kms.value > 0 else 0.0
+    hbm_peak = float(pk["hbm_gbs"])
+    roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved_gbs / hbm_peak, "traffic": None,
+                "kernel": "decode expert FFN (ffn1_gemv + ffn2_gemv, weights streamed once)",
+                "launches": kn.value, "avg_launch_us": 1e3 * kms.value / max(1, kn.value),
+                "bytes_per_launch": kbytes.value / max(1, kn.value), "peak_kind": pk_kind}
+    # plan-conditional roofline of the whole step: max(B_gpu/BW_hbm, B_cpu/BW_host, B_h2d/BW_pcie) per layer
+    bw_host = args.host_bw_gbs * 1e9
+    bw_pcie = cal.profile.transfer_bandwidth  # bytes / s, fitted at warm-up
+    bound_s = sum(max(s.bytes_gpu / (hbm_peak * 1e9), s.bytes_cpu / bw_host, s.bytes_h2d / bw_pcie)
+                  for s in stats_all)
+    n_cpu = sum(s.n_cpu for s in stats_all) / args.steps
+    n_gpu = sum(s.n_gpu for s in stats_all) / args.steps
+    n_xfer = sum(s.n_transfer for s in stats_all) / args.steps
+
+    # ---- CPU baseline: the oracle port on this host, bounded sample
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        per_tok, sample = cpu_oracle_decode(args.shape, args.ref_layers)
+        cpu = {"value": 1.0 / per_tok, "unit": "tok/s", "cores": os.cpu_count(), "kind": "port", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": "decode tok/s at 25% expert-cache budget", "value": tok_s, "unit": "tok/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (reference trace-generator routing GenParams(1.0,0.85,0.6), random-init N(0,0.02^2) bf16 weights)",
+            "config": {"workload": f"{args.shape}-shaped MoE decode, batch 1, {args.ratio:.0%} expert-cache budget",
+                       "shape": args.shape, "layers": cfg.num_layers, "experts": cfg.num_routed,
+                       "top_k": cfg.num_activated, "hidden": H, "inter": I, "cache_slots": moe.capacity,
+                       "host_images": moe.host_images, "policy": args.policy, "prefetch": args.prefetch,
+                       "l2": "each step streams >= 2 x 352 MB of expert weights (> 126 MB L2); no flush needed",
+                       "parallelism": "ep" if world > 1 else "single"},
+            "prefill": {"tokens": args.prefill, "ms": prefill_ms, "cold_cache": True,
+                        "gpu_experts": sum(s.n_gpu for s in pst), "cpu_experts": sum(s.n_cpu for s in pst),
+                        "transfers": sum(s.n_transfer for s in pst)},
+            "e2e": {"value": world * 1e3 / e2e_ms, "unit": "tok/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "roofline": roofline,
+            "step_roofline": {"bound": "plan-conditional max(B_gpu/HBM, B_cpu/host DRAM, B_h2d/PCIe)",
+                              "bound_ms_per_step": 1e3 * bound_s / args.steps,
+                              "frac": (1e3 * bound_s / args.steps) / ms_step, "host_bw_gbs": args.host_bw_gbs,
+                              "pcie_gbs": bw_pcie / 1e9},
+            "per_step": {"gpu_experts": n_gpu, "cpu_experts": n_cpu, "transfers": n_xfer,
+                         "host_decide_us_per_layer": statistics.mean(s.t_decide_us for s in stats_all),
+                         "cpu_worker_ms": sum(s.t_cpu_us for s in stats_all) / 1e3 / args.steps},
+            "profile": {k: getattr(cal.profile, k) for k in ("gpu_time_per_expert", "cpu_slope", "transfer_bandwidth",
+                                                              "transfer_latency", "gpu_slope",
+                                                              "cpu_first_expert_penalty")},
+            "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks.summary(),
+            "setup_s": setup_s,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--shape", default="mixtral", choices=["tiny", "mixtral", "deepseek", "qwen2"])
+    ap.add_argument("--ratio", type=float, default=0.25)
+    ap.add_argument("--prefill", type=int, default=1024)
+    ap.add_argument("--policy", default="mrs", choices=["mrs", "lru", "lfu"])
+    ap.add_argument("--prefetch", action="store_true")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--host-images", type=int, default=None)
+    ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--host-bw-gbs", type=float, default=100.0)
+    ap.add_argument("--ref-layers", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -325,10 +325,77 @@ int hm_expert_ffn(const uint16_t *pool, int n_slots, int H, int I, const hm_grou
 /* y[t] = residual[t] (optional) + sum_k w[t,k] * out[pos[t,k]]  (Eq. 1 combine). */
 int hm_combine(const float *out, const int32_t *pos, const float *w, int T, int Kp, int H,
                const uint16_t *residual, uint16_t *y, void *stream);
+/* Number of kernels this library has launched so far (process-wide). */
+long long hm_launch_count(void);
 /* GPU-side MRS update (caching.py:58-76): S[layer] <- a*TopP(s) + (1-a)*S[layer],
  * fp64 with explicit round-to-nearest mul/add (bit-identical to the host core). */
 int hm_mrs_update_dev(double *S, const double *scores, int layer, int N, int p,
                       double alpha, void *stream);
+
+/* ======================================================================= */
+/* Host worker (AVX-512 BF16) and the layer executor.                        */
+/* ======================================================================= */
+typedef struct hm_cpu_pool hm_cpu_pool;
+int hm_cpu_pool_create(int nthreads, hm_cpu_pool **out); /* nthreads <= 0: all cores */
+void hm_cpu_pool_destroy(hm_cpu_pool *p);
+/* out[M, H] fp32 = expert(img)(x[M, H] bf16) on the host; img in slot layout (HOST pointers). */
+int hm_cpu_expert(hm_cpu_pool *pool, const uint16_t *img, int H, int I, const uint16_t *x, int M,
+                  float *out);
+int hm_cpu_has_avx512bf16(void);
+
+typedef struct hm_runtime hm_runtime;
+typedef struct hm_runtime_config {
+  int32_t num_layers;
+  int32_t num_routed;
+  int32_t num_activated;
+  int32_t hidden;
+  int32_t inter;
+  int32_t n_shared;        /* always-resident shared-expert chunks per layer (routed dims) */
+  int32_t renormalize;     /* renormalise the top-K weights (Mixtral) */
+  int32_t shared_gate_col; /* logits column of the Qwen2 shared-expert gate, -1 if none */
+  int64_t capacity;        /* routed-expert HBM cache slots = floor(ratio * L * N) */
+  int64_t host_images;     /* distinct expert images in the pinned master store */
+  int32_t cpu_threads;     /* host worker threads (<= 0: all cores) */
+  int32_t max_tokens;      /* largest T of one forward_layer call */
+  int32_t gpu_mrs;         /* keep the GPU copy of S updated with hm_mrs_update_dev */
+  int32_t residual;        /* y = x + MoE(x) (1) or y = MoE(x) (0) */
+} hm_runtime_config;
+
+typedef struct hm_layer_stats {
+  double makespan_planned; /* the plan's makespan (profile units) */
+  double t_wait_router_us; /* host wait for the router's LayerRequest */
+  double t_decide_us;      /* decision core time */
+  double t_cpu_us;         /* host worker time */
+  int32_t n_gpu, n_cpu, n_transfer, n_prefetch;
+  int64_t bytes_gpu, bytes_cpu, bytes_h2d; /* expert weight bytes per resource */
+} hm_layer_stats;
+
+/* The runtime drives `engine` (created with the same shape and capacity); it
+ * owns the HBM slot pool (capacity + L*n_shared slots), the pinned master
+ * store (host_images expert images; expert (l, e) uses image (l*N+e) mod
+ * host_images), a copy stream, per-slot events and the host worker pool. */
+int hm_runtime_create(const hm_runtime_config *cfg, hm_engine *engine, hm_runtime **out);
+void hm_runtime_destroy(hm_runtime *rt);
+int hm_runtime_buffers(hm_runtime *rt, void **pool, void **host_store, size_t *slot_bytes,
+                       int64_t *n_slots);
+int hm_runtime_image_of(const hm_runtime *rt, int layer, int expert, int64_t *image);
+int hm_runtime_shared_slot(const hm_runtime *rt, int layer, int chunk, int64_t *slot);
+/* One MoE layer: y[T, H] = x + sum_k w E_k(x) for router logits [T, ld],
+ * executing the decision core's plan for this layer (engine.py:288-389). */
+int hm_runtime_forward_layer(hm_runtime *rt, int layer, const uint16_t *x, const float *logits,
+                             int T, int ld, uint16_t *y, const int32_t *pred_layers,
+                             const int64_t *pred_loads, int n_pred, void *stream,
+                             hm_layer_stats *stats);
+/* The LayerRequest (loads, normalised scores) the router produced last. */
+int hm_runtime_last_request(const hm_runtime *rt, int64_t *loads, double *scores);
+/* GPU copy of the MRS table S [L, N] (synchronises the device). */
+int hm_runtime_device_mrs(hm_runtime *rt, double *host_out);
+int hm_runtime_sync(hm_runtime *rt);
+/* CUDA-event timing of every expert-FFN launch (bench roofline): enable, then
+ * read and reset the accumulated launch time / algorithmic bytes. */
+int hm_runtime_set_kernel_timing(hm_runtime *rt, int on);
+int hm_runtime_kernel_times(hm_runtime *rt, double *total_ms, int64_t *total_bytes, int64_t *n,
+                            double *max_ms);
 
 #ifdef __cplusplus
 }

@@ -249,3 +249,56 @@ for _name, (_args, _res) in _DEV_SIGS.items():
     _f.argtypes = _args
     _f.restype = _res
 FFN_AUTO, FFN_GEMV, FFN_GEMM = 0, 1, 2
+
+_HOST_SIGS = {
+    "hm_cpu_pool_create": ([C.c_int, P(vp)], C.c_int),
+    "hm_cpu_pool_destroy": ([vp], None),
+    "hm_cpu_expert": ([vp, vp, C.c_int, C.c_int, vp, C.c_int, vp], C.c_int),
+    "hm_cpu_has_avx512bf16": ([], C.c_int),
+}
+for _name, (_args, _res) in _HOST_SIGS.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+
+class RuntimeConfig(C.Structure):
+    _fields_ = [("num_layers", C.c_int32), ("num_routed", C.c_int32), ("num_activated", C.c_int32),
+                ("hidden", C.c_int32), ("inter", C.c_int32), ("n_shared", C.c_int32), ("renormalize", C.c_int32),
+                ("shared_gate_col", C.c_int32), ("capacity", C.c_int64), ("host_images", C.c_int64),
+                ("cpu_threads", C.c_int32), ("max_tokens", C.c_int32), ("gpu_mrs", C.c_int32),
+                ("residual", C.c_int32)]
+
+
+class LayerStats(C.Structure):
+    _fields_ = [("makespan_planned", C.c_double), ("t_wait_router_us", C.c_double), ("t_decide_us", C.c_double),
+                ("t_cpu_us", C.c_double), ("n_gpu", C.c_int32), ("n_cpu", C.c_int32), ("n_transfer", C.c_int32),
+                ("n_prefetch", C.c_int32), ("bytes_gpu", C.c_int64), ("bytes_cpu", C.c_int64),
+                ("bytes_h2d", C.c_int64)]
+
+
+_RT_SIGS = {
+    "hm_runtime_create": ([P(RuntimeConfig), vp, P(vp)], C.c_int),
+    "hm_runtime_destroy": ([vp], None),
+    "hm_runtime_buffers": ([vp, P(vp), P(vp), P(C.c_size_t), P(i64)], C.c_int),
+    "hm_runtime_image_of": ([vp, C.c_int, C.c_int, P(i64)], C.c_int),
+    "hm_runtime_shared_slot": ([vp, C.c_int, C.c_int, P(i64)], C.c_int),
+    "hm_runtime_forward_layer": ([vp, C.c_int, vp, vp, C.c_int, C.c_int, vp, P(i32), P(i64), C.c_int, vp,
+                                  P(LayerStats)], C.c_int),
+    "hm_runtime_last_request": ([vp, P(i64), P(f64)], C.c_int),
+    "hm_runtime_device_mrs": ([vp, P(f64)], C.c_int),
+    "hm_runtime_sync": ([vp], C.c_int),
+}
+for _name, (_args, _res) in _RT_SIGS.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+for _name, (_args, _res) in {
+    "hm_runtime_set_kernel_timing": ([vp, C.c_int], C.c_int),
+    "hm_runtime_kernel_times": ([vp, P(f64), P(i64), P(i64), P(f64)], C.c_int),
+    "hm_launch_count": ([], C.c_longlong),
+}.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res

@@ -1,0 +1,90 @@
+"""Warm-up calibration on the B200 box (§IV-A).
+
+Measures the three resources the decision core plans with and fits a
+``HardwareProfile`` with ``costs.calibrate`` (the reference's fits,
+costs.py:134-219), all in seconds, for one expert of shape (H, I):
+
+  gpu   one expert through ``hm_expert_ffn`` at loads 1..512 tokens (CUDA events)
+  cpu   one expert on the AVX-512 host worker at decode loads 1..4, in bursts of
+        three after an idle gap: position 0 is the cold first expert of a
+        burst (the reference's first-expert penalty, Fig. 3e)
+  pcie  pinned H2D copies of 1/4, 1/2 and 1 expert image (CUDA events)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+
+import numpy as np
+import torch
+
+from ._lib import check, lib
+from .costs import CalibrationSample, calibrate
+
+
+def _events():
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+def measure_samples(H: int, I: int, gpu_loads=(1, 2, 4, 8, 32, 128, 256, 384, 512), cpu_loads=(1, 2, 3, 4),
+                    reps: int = 3, cpu_bursts: int = 2, n_images: int = 4, cpu_threads: int = 0,
+                    seed: int = 0) -> list[CalibrationSample]:
+    from .kernels import expert_ffn
+
+    slot_elems = 3 * H * I
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    pool = (torch.randn((1, slot_elems), generator=g, device="cuda") * 0.02).to(torch.bfloat16)
+    host = torch.empty((n_images, slot_elems), dtype=torch.bfloat16).pin_memory()
+    for i in range(n_images):
+        host[i].copy_((torch.randn(slot_elems, generator=g, device="cuda") * 0.02).to(torch.bfloat16))
+    samples: list[CalibrationSample] = []
+    st = torch.cuda.current_stream()
+    maxm = max(gpu_loads)
+    x = torch.randn((maxm, H), generator=g, device="cuda").to(torch.bfloat16)
+    h = torch.empty((maxm, I), dtype=torch.bfloat16, device="cuda")
+    out = torch.empty((maxm, H), device="cuda")
+    flat = pool.view(-1)
+    for m in gpu_loads:
+        expert_ffn(flat, 1, H, I, [(0, 0, m)], x, h, out)
+        a, b = _events()
+        a.record(st)
+        for _ in range(reps):
+            expert_ffn(flat, 1, H, I, [(0, 0, m)], x, h, out)
+        b.record(st)
+        b.synchronize()
+        samples.append(CalibrationSample("gpu", float(m), 0, a.elapsed_time(b) / 1e3 / reps))
+
+    cpool = C.c_void_p()
+    check(lib.hm_cpu_pool_create(int(cpu_threads), C.byref(cpool)))
+    try:
+        xs = np.ascontiguousarray(x[: max(cpu_loads)].view(torch.int16).cpu().numpy().view(np.uint16))
+        outs = np.empty((max(cpu_loads), H), dtype=np.float32)
+        for m in cpu_loads:
+            for burst in range(cpu_bursts):
+                time.sleep(0.02)
+                for pos in range(3):
+                    img = host[(burst * 3 + pos) % n_images]
+                    t0 = time.perf_counter()
+                    check(lib.hm_cpu_expert(cpool, img.data_ptr(), H, I, xs.ctypes.data, m, outs.ctypes.data))
+                    samples.append(CalibrationSample("cpu", float(m), pos, time.perf_counter() - t0))
+    finally:
+        lib.hm_cpu_pool_destroy(cpool)
+
+    for frac in (4, 2, 1):
+        n = slot_elems // frac
+        flat[:n].copy_(host[0, :n], non_blocking=True)
+        for r in range(reps):
+            a, b = _events()
+            a.record(st)
+            flat[:n].copy_(host[1 + r % (n_images - 1), :n], non_blocking=True)
+            b.record(st)
+            b.synchronize()
+            samples.append(CalibrationSample("pcie", float(n * 2), 0, a.elapsed_time(b) / 1e3))
+    torch.cuda.synchronize()
+    return samples
+
+
+def calibrate_shape(H: int, I: int, gpu_saturation_load: int = 256, **kw):
+    """Measure and fit; returns (CalibrationResult, samples)."""
+    samples = measure_samples(H, I, **kw)
+    return calibrate(samples, gpu_saturation_load=gpu_saturation_load), samples

@@ -682,6 +682,8 @@ void Engine::run_layer(int layer, const int64_t *loads, const double *scores, in
   const int policy = cfg.cache_policy;
   rec.lookups.clear();
   rec.demand.clear();
+  rec.demand_slots.clear();
+  rec.chosen_slots.clear();
   rec.candidates.clear();
   rec.chosen.clear();
   rec.selected.clear();
@@ -744,6 +746,7 @@ void Engine::run_layer(int layer, const int64_t *loads, const double *scores, in
         if (k >= 0) prefetch_pins.erase(prefetch_pins.begin() + k);
       }
       rec.demand.emplace_back(e->ref, has ? static_cast<int64_t>(v) : -1);
+      rec.demand_slots.push_back(cache.resident.at(e->ref).slot);
     }
   }
 
@@ -835,6 +838,7 @@ void Engine::run_layer(int layer, const int64_t *loads, const double *scores, in
       cache.pinned.insert(r);
       if (find_prefetch_pin(r) < 0) prefetch_pins.emplace_back(r, false);
       rec.chosen.emplace_back(r, has ? static_cast<int64_t>(v) : -1);
+      rec.chosen_slots.push_back(cache.resident.at(r).slot);
     }
     if (cfg.validate) {
       Plan replan = build_plan(layer, loads, n);

@@ -110,6 +110,8 @@ struct LayerRecord {
   std::vector<std::pair<uint32_t, uint8_t>> lookups;
   Plan plan;
   std::vector<std::pair<uint32_t, int64_t>> demand;  // (ref, victim or -1)
+  std::vector<int64_t> demand_slots;                 // HBM slot each demand insert landed in
+  std::vector<int64_t> chosen_slots;                 // HBM slot of each prefetch insert
   std::vector<hm_candidate> candidates;
   std::vector<uint32_t> selected;                   // select_prefetches output
   std::vector<std::pair<uint32_t, int64_t>> chosen;  // inserted: (ref, victim or -1)

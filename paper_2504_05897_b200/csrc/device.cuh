@@ -19,9 +19,16 @@
       hm::raise(HM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(err_));             \
   } while (0)
 
-#define HM_LAUNCH_CHECK() HM_CUDA(cudaGetLastError())
+// Every kernel launch site ends with HM_LAUNCH_CHECK(), which also counts
+// the launch (hm_launch_count(): the bench's gpu_launches evidence).
+#define HM_LAUNCH_CHECK()            \
+  do {                               \
+    HM_CUDA(cudaGetLastError());     \
+    hm::count_launch();              \
+  } while (0)
 
 namespace hm {
+void count_launch();
 namespace dev {
 
 __device__ __forceinline__ float bf2f(uint16_t v) { return __uint_as_float(static_cast<uint32_t>(v) << 16); }

@@ -232,7 +232,15 @@ __global__ void mrs_update_kernel(double *__restrict__ S, const double *__restri
 
 using hm::raise;
 
+#include <atomic>
+namespace hm {
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace hm
+
 extern "C" {
+
+long long hm_launch_count(void) { return hm::g_launches.load(); }
 
 int hm_router_topk(const float *logits, int T, int N, int ld, int K, int renormalize, int n_shared,
                    int shared_gate_col, int32_t *sel, float *w, float *probs, int32_t *counts, void *stream) {

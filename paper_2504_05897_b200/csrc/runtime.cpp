@@ -1,0 +1,423 @@
+// The HybriMoE layer executor on one B200: turns the decision core's per-layer
+// record into real work (engine.py:288-389 step order).
+//
+//   compute stream : router -> score sums -> offsets -> permute/gather
+//                    -> [host decides] -> GPU experts (cached batch, then each
+//                    transferred expert after its copy) -> combine (+ residual)
+//   copy stream    : demand H2D copies in plan transfer order, then prefetches,
+//                    each from the pinned master store into its HBM slot
+//   host worker    : CPU-assigned experts in plan CPU order, from the pinned
+//                    master store, results H2D'd into the permuted output rows
+//
+// Slot reuse is event-guarded: a copy into a slot waits for the last kernel
+// that read it (a demand insert may evict an expert inserted earlier in the
+// same layer, engine.py:318-330), and a kernel waits for its slot's copy.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "decision.hpp"
+#include "host_worker.hpp"
+
+extern "C" {
+int hm_router_topk(const float *, int, int, int, int, int, int, int, int32_t *, float *, float *, int32_t *, void *);
+int hm_score_sums(const float *, int, int, double *, void *);
+int hm_offsets(const int32_t *, int, int32_t *, void *);
+int hm_permute(const int32_t *, int, int, int, const int32_t *, int32_t *, int32_t *, void *);
+int hm_gather_rows(const uint16_t *, const int32_t *, int, int, int, uint16_t *, void *);
+int hm_expert_ffn(const uint16_t *, int, int, int, const hm_group *, int, const uint16_t *, int, uint16_t *, float *,
+                  int, void *);
+int hm_combine(const float *, const int32_t *, const float *, int, int, int, const uint16_t *, uint16_t *, void *);
+int hm_mrs_update_dev(double *, const double *, int, int, int, double, void *);
+}
+
+namespace hm {
+namespace {
+
+#define RT_CUDA(call)                                                                          \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess) hm::raise(HM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+inline void ok(int status) {
+  if (status != HM_OK) raise(status, last_error());
+}
+
+double now_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+struct Runtime {
+  hm_runtime_config cfg;
+  Engine *engine;
+  int N, K, S, E, Kp, H, I, L;
+  size_t slot_elems, slot_bytes;
+  int64_t n_slots;
+  uint16_t *pool = nullptr;        // device: [n_slots][slot_elems]
+  uint16_t *store = nullptr;       // pinned host: [host_images][slot_elems]
+  cudaStream_t copy = nullptr;
+  std::vector<cudaEvent_t> ready, last_use;
+  cudaEvent_t ev_req = nullptr, ev_rows = nullptr;
+  // device scratch
+  int32_t *sel = nullptr, *counts = nullptr, *offsets = nullptr, *pos = nullptr, *row_src = nullptr;
+  float *w = nullptr, *probs = nullptr, *out = nullptr;
+  double *score_sum = nullptr, *S_dev = nullptr, *scores_dev = nullptr;
+  uint16_t *xp = nullptr, *h = nullptr;
+  // pinned host staging
+  int32_t *h_counts = nullptr, *h_offsets = nullptr;
+  double *h_score_sum = nullptr, *h_scores = nullptr;
+  uint16_t *h_x = nullptr;
+  float *h_out = nullptr;
+  std::unique_ptr<ThreadPool> workers;
+  std::vector<uint16_t> hbuf;
+  std::vector<int64_t> loads;
+  // optional CUDA-event timing of every expert-FFN launch (the bench's roofline)
+  bool time_kernels = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev;
+  std::vector<int64_t> kbytes;
+  size_t kused = 0;
+
+  void ffn(const hm_group *g, int n, int rows, cudaStream_t st) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (time_kernels) {
+      if (kused == kev.size()) {
+        cudaEvent_t e0, e1;
+        RT_CUDA(cudaEventCreate(&e0));
+        RT_CUDA(cudaEventCreate(&e1));
+        kev.emplace_back(e0, e1);
+        kbytes.push_back(0);
+      }
+      a = kev[kused].first;
+      b = kev[kused].second;
+      RT_CUDA(cudaEventRecord(a, st));
+    }
+    ok(hm_expert_ffn(pool, static_cast<int>(n_slots), H, I, g, n, xp, rows, h, out, HM_FFN_AUTO,
+                     static_cast<void *>(st)));
+    if (time_kernels) {
+      RT_CUDA(cudaEventRecord(b, st));
+      int64_t by = 0;
+      for (int i = 0; i < n; ++i)  // weights streamed + activations in/out
+        by += static_cast<int64_t>(slot_bytes) + static_cast<int64_t>(g[i].row_count) * (2LL * H + 2LL * I * 2 + 4LL * H);
+      kbytes[kused++] = by;
+    }
+  }
+  std::vector<double> scores;
+
+  Runtime(const hm_runtime_config &c, Engine *eng) : cfg(c), engine(eng) {
+    L = c.num_layers;
+    N = c.num_routed;
+    K = c.num_activated;
+    S = c.n_shared;
+    E = N + S;
+    Kp = K + S;
+    H = c.hidden;
+    I = c.inter;
+    HM_REQUIRE(L >= 1 && N >= 1 && K >= 1 && K <= N && S >= 0 && H > 0 && I > 0, HM_EVALUE, "bad runtime shape");
+    HM_REQUIRE(engine->cfg.num_layers == L && engine->cfg.num_routed == N && engine->cache.capacity == c.capacity,
+               HM_EVALUE, "engine and runtime disagree on the model shape or cache capacity");
+    HM_REQUIRE(c.host_images >= 1 && c.max_tokens >= 1, HM_EVALUE, "bad runtime sizes");
+    slot_elems = static_cast<size_t>(3) * H * I;
+    slot_bytes = slot_elems * 2;
+    n_slots = c.capacity + static_cast<int64_t>(L) * S;
+    if (n_slots > 0) RT_CUDA(cudaMalloc(&pool, static_cast<size_t>(n_slots) * slot_bytes));
+    RT_CUDA(cudaHostAlloc(&store, static_cast<size_t>(c.host_images) * slot_bytes, cudaHostAllocPortable));
+    RT_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+    ready.resize(static_cast<size_t>(n_slots));
+    last_use.resize(static_cast<size_t>(n_slots));
+    for (int64_t s = 0; s < n_slots; ++s) {
+      RT_CUDA(cudaEventCreateWithFlags(&ready[s], cudaEventDisableTiming));
+      RT_CUDA(cudaEventCreateWithFlags(&last_use[s], cudaEventDisableTiming));
+    }
+    RT_CUDA(cudaEventCreateWithFlags(&ev_req, cudaEventDisableTiming));
+    RT_CUDA(cudaEventCreateWithFlags(&ev_rows, cudaEventDisableTiming));
+    const size_t T = static_cast<size_t>(c.max_tokens);
+    const size_t rows = T * Kp;
+    RT_CUDA(cudaMalloc(&sel, rows * 4));
+    RT_CUDA(cudaMalloc(&w, rows * 4));
+    RT_CUDA(cudaMalloc(&probs, T * N * 4));
+    RT_CUDA(cudaMalloc(&counts, E * 4));
+    RT_CUDA(cudaMalloc(&offsets, (E + 1) * 4));
+    RT_CUDA(cudaMalloc(&pos, rows * 4));
+    RT_CUDA(cudaMalloc(&row_src, rows * 4));
+    RT_CUDA(cudaMalloc(&xp, rows * H * 2));
+    RT_CUDA(cudaMalloc(&h, rows * I * 2));
+    RT_CUDA(cudaMalloc(&out, rows * H * 4));
+    RT_CUDA(cudaMalloc(&score_sum, N * 8));
+    RT_CUDA(cudaMalloc(&scores_dev, N * 8));
+    RT_CUDA(cudaMalloc(&S_dev, static_cast<size_t>(L) * N * 8));
+    std::vector<double> prior(static_cast<size_t>(L) * N, 1.0 / static_cast<double>(N));
+    RT_CUDA(cudaMemcpy(S_dev, prior.data(), prior.size() * 8, cudaMemcpyHostToDevice));
+    RT_CUDA(cudaHostAlloc(&h_counts, E * 4, 0));
+    RT_CUDA(cudaHostAlloc(&h_offsets, (E + 1) * 4, 0));
+    RT_CUDA(cudaHostAlloc(&h_score_sum, N * 8, 0));
+    RT_CUDA(cudaHostAlloc(&h_scores, N * 8, 0));
+    RT_CUDA(cudaHostAlloc(&h_x, rows * H * 2, 0));
+    RT_CUDA(cudaHostAlloc(&h_out, rows * H * 4, 0));
+    workers.reset(new ThreadPool(c.cpu_threads > 0 ? c.cpu_threads
+                                                   : static_cast<int>(std::thread::hardware_concurrency())));
+    loads.assign(N, 0);
+    scores.assign(N, 0.0);
+  }
+
+  ~Runtime() {
+    if (copy) cudaStreamSynchronize(copy);
+    for (auto e : ready) cudaEventDestroy(e);
+    for (auto e : last_use) cudaEventDestroy(e);
+    if (ev_req) cudaEventDestroy(ev_req);
+    if (ev_rows) cudaEventDestroy(ev_rows);
+    if (copy) cudaStreamDestroy(copy);
+    for (void *p : {static_cast<void *>(pool), static_cast<void *>(sel), static_cast<void *>(w),
+                    static_cast<void *>(probs), static_cast<void *>(counts), static_cast<void *>(offsets),
+                    static_cast<void *>(pos), static_cast<void *>(row_src), static_cast<void *>(xp),
+                    static_cast<void *>(h), static_cast<void *>(out), static_cast<void *>(score_sum),
+                    static_cast<void *>(scores_dev), static_cast<void *>(S_dev)})
+      if (p) cudaFree(p);
+    for (void *p : {static_cast<void *>(store), static_cast<void *>(h_counts), static_cast<void *>(h_offsets),
+                    static_cast<void *>(h_score_sum), static_cast<void *>(h_scores), static_cast<void *>(h_x),
+                    static_cast<void *>(h_out)})
+      if (p) cudaFreeHost(p);
+  }
+
+  int64_t image_of(int layer, int expert) const {
+    return (static_cast<int64_t>(layer) * N + expert) % cfg.host_images;
+  }
+  int64_t shared_slot(int layer, int chunk) const { return cfg.capacity + static_cast<int64_t>(layer) * S + chunk; }
+  uint16_t *slot_ptr(int64_t s) const { return pool + static_cast<size_t>(s) * slot_elems; }
+  const uint16_t *image_ptr(uint32_t ref) const {
+    return store + static_cast<size_t>(image_of(ref_layer(ref), ref_expert(ref))) * slot_elems;
+  }
+
+  void issue_copy(uint32_t ref, int64_t slot, cudaStream_t /*compute*/) {
+    RT_CUDA(cudaStreamWaitEvent(copy, last_use[slot], 0));
+    RT_CUDA(cudaMemcpyAsync(slot_ptr(slot), image_ptr(ref), slot_bytes, cudaMemcpyHostToDevice, copy));
+    RT_CUDA(cudaEventRecord(ready[slot], copy));
+  }
+
+  void forward_layer(int layer, const uint16_t *x, const float *logits, int T, int ld, uint16_t *y,
+                     const int32_t *pred_layers, const int64_t *pred_loads, int n_pred, cudaStream_t st,
+                     hm_layer_stats *stats) {
+    HM_REQUIRE(layer >= 0 && layer < L, HM_EVALUE, "layer out of range");
+    HM_REQUIRE(T >= 1 && T <= cfg.max_tokens, HM_EVALUE, "token count exceeds the runtime's max_tokens");
+    hm_layer_stats s{};
+    void *vs = static_cast<void *>(st);
+    const int rows = T * Kp;
+    // (0) router, LayerRequest, permutation -- all on the compute stream
+    ok(hm_router_topk(logits, T, N, ld, K, cfg.renormalize, S, cfg.shared_gate_col, sel, w, probs, counts, vs));
+    ok(hm_score_sums(probs, T, N, score_sum, vs));
+    ok(hm_offsets(counts, E, offsets, vs));
+    RT_CUDA(cudaMemcpyAsync(h_counts, counts, E * 4, cudaMemcpyDeviceToHost, st));
+    RT_CUDA(cudaMemcpyAsync(h_offsets, offsets, (E + 1) * 4, cudaMemcpyDeviceToHost, st));
+    RT_CUDA(cudaMemcpyAsync(h_score_sum, score_sum, N * 8, cudaMemcpyDeviceToHost, st));
+    RT_CUDA(cudaEventRecord(ev_req, st));
+    ok(hm_permute(sel, T, Kp, E, offsets, pos, row_src, vs));
+    ok(hm_gather_rows(x, row_src, rows, Kp, H, xp, vs));
+    double t0 = now_us();
+    RT_CUDA(cudaEventSynchronize(ev_req));
+    double t1 = now_us();
+    s.t_wait_router_us = t1 - t0;
+
+    // (1)-(7) the decision core, engine.py:288-389
+    double tot = 0.0;
+    for (int e = 0; e < N; ++e) tot += h_score_sum[e];
+    for (int e = 0; e < N; ++e) {
+      loads[e] = h_counts[e];
+      scores[e] = tot > 0.0 ? h_score_sum[e] / tot : 0.0;
+      h_scores[e] = scores[e];
+    }
+    engine->run_layer(layer, loads.data(), scores.data(), N, pred_layers, pred_loads, n_pred);
+    const LayerRecord &rec = engine->rec;
+    s.makespan_planned = rec.plan.makespan;
+    double t2 = now_us();
+    s.t_decide_us = t2 - t1;
+
+    // CPU rows to host first so the worker can start while the GPU computes
+    std::vector<uint32_t> cpu_refs;
+    for (const Event &ev : rec.plan.events)
+      if (ev.device == HM_DEV_CPU) cpu_refs.push_back(ev.ref);
+    for (uint32_t r : cpu_refs) {
+      const int e = ref_expert(r);
+      const size_t rb = h_offsets[e], rc = h_counts[e];
+      RT_CUDA(cudaMemcpyAsync(h_x + rb * H, xp + rb * H, rc * H * 2, cudaMemcpyDeviceToHost, st));
+    }
+    if (!cpu_refs.empty()) RT_CUDA(cudaEventRecord(ev_rows, st));
+
+    auto assign_of = [&](uint32_t ref) {
+      for (auto &a : rec.plan.assign)
+        if (a.first == ref) return a.second;
+      return -1;
+    };
+    // GPU experts already resident (and the layer's shared chunks): one launch
+    std::vector<hm_group> batch;
+    for (const Event &ev : rec.plan.events) {
+      if (ev.device != HM_DEV_GPU || assign_of(ev.ref) != HM_ASSIGN_GPU_CACHED) continue;
+      const int e = ref_expert(ev.ref);
+      const int64_t slot = engine->cache.resident.at(ev.ref).slot;
+      RT_CUDA(cudaStreamWaitEvent(st, ready[slot], 0));  // a prefetch may still be in flight
+      batch.push_back(hm_group{static_cast<int32_t>(slot), h_offsets[e], h_counts[e], 0});
+    }
+    s.n_gpu = static_cast<int32_t>(batch.size());
+    for (int c = 0; c < S; ++c)
+      batch.push_back(hm_group{static_cast<int32_t>(shared_slot(layer, c)), h_offsets[N + c], h_counts[N + c], 0});
+    s.bytes_gpu = static_cast<int64_t>(batch.size()) * static_cast<int64_t>(slot_bytes);
+    if (!batch.empty()) {
+      ffn(batch.data(), static_cast<int>(batch.size()), rows, st);
+      for (auto &g : batch) RT_CUDA(cudaEventRecord(last_use[g.slot], st));
+    }
+    // Copies in plan transfer order (== insert order), then prefetches; an
+    // expert the plan computes on the GPU is launched right after its copy so
+    // that a later copy into the same slot (same-layer eviction) waits for it.
+    auto copy_and_maybe_compute = [&](uint32_t ref, int64_t slot, bool demand) {
+      issue_copy(ref, slot, st);
+      s.bytes_h2d += static_cast<int64_t>(slot_bytes);
+      if (demand && assign_of(ref) == HM_ASSIGN_GPU_TRANSFER) {
+        const int e = ref_expert(ref);
+        RT_CUDA(cudaStreamWaitEvent(st, ready[slot], 0));
+        hm_group g{static_cast<int32_t>(slot), h_offsets[e], h_counts[e], 0};
+        ffn(&g, 1, rows, st);
+        RT_CUDA(cudaEventRecord(last_use[slot], st));
+        ++s.n_gpu;
+        s.bytes_gpu += static_cast<int64_t>(slot_bytes);
+      }
+    };
+    for (size_t i = 0; i < rec.demand.size(); ++i) {
+      copy_and_maybe_compute(rec.demand[i].first, rec.demand_slots[i], true);
+      ++s.n_transfer;
+    }
+    for (size_t i = 0; i < rec.chosen.size(); ++i) {
+      copy_and_maybe_compute(rec.chosen[i].first, rec.chosen_slots[i], false);
+      ++s.n_prefetch;
+    }
+
+    // CPU experts in plan CPU order (scheduling.py:257-268)
+    if (!cpu_refs.empty()) {
+      RT_CUDA(cudaEventSynchronize(ev_rows));
+      const double c0 = now_us();
+      for (uint32_t r : cpu_refs) {
+        const int e = ref_expert(r);
+        const size_t rb = h_offsets[e];
+        cpu_expert(*workers, image_ptr(r), H, I, h_x + rb * H, h_counts[e], h_out + rb * H, hbuf);
+        s.bytes_cpu += static_cast<int64_t>(slot_bytes);
+        ++s.n_cpu;
+      }
+      s.t_cpu_us = now_us() - c0;
+      for (uint32_t r : cpu_refs) {
+        const int e = ref_expert(r);
+        const size_t rb = h_offsets[e], rc = h_counts[e];
+        RT_CUDA(cudaMemcpyAsync(out + rb * H, h_out + rb * H, rc * H * 4, cudaMemcpyHostToDevice, st));
+      }
+    }
+    // combine (Eq. 1) with the residual stream, then the GPU copy of S
+    ok(hm_combine(out, pos, w, T, Kp, H, cfg.residual ? x : nullptr, y, vs));
+    if (cfg.gpu_mrs && engine->cfg.cache_policy == HM_POLICY_MRS && engine->mrs_) {
+      RT_CUDA(cudaMemcpyAsync(scores_dev, h_scores, N * 8, cudaMemcpyHostToDevice, st));
+      ok(hm_mrs_update_dev(S_dev, scores_dev, layer, N, engine->mrs_->p, engine->mrs_->alpha, vs));
+    }
+    if (stats) *stats = s;
+  }
+};
+
+}  // namespace hm
+
+extern "C" {
+
+int hm_runtime_create(const hm_runtime_config *cfg, hm_engine *engine, hm_runtime **out) {
+  HM_API_BEGIN
+  HM_REQUIRE(cfg && engine && out, HM_EVALUE, "null argument");
+  *out = reinterpret_cast<hm_runtime *>(new hm::Runtime(*cfg, reinterpret_cast<hm::Engine *>(engine)));
+  HM_API_END
+}
+
+void hm_runtime_destroy(hm_runtime *rt) { delete reinterpret_cast<hm::Runtime *>(rt); }
+
+int hm_runtime_buffers(hm_runtime *rt, void **pool, void **host_store, size_t *slot_bytes, int64_t *n_slots) {
+  HM_API_BEGIN
+  auto *r = reinterpret_cast<hm::Runtime *>(rt);
+  if (pool) *pool = r->pool;
+  if (host_store) *host_store = r->store;
+  if (slot_bytes) *slot_bytes = r->slot_bytes;
+  if (n_slots) *n_slots = r->n_slots;
+  HM_API_END
+}
+
+int hm_runtime_image_of(const hm_runtime *rt, int layer, int expert, int64_t *image) {
+  HM_API_BEGIN
+  *image = reinterpret_cast<const hm::Runtime *>(rt)->image_of(layer, expert);
+  HM_API_END
+}
+
+int hm_runtime_shared_slot(const hm_runtime *rt, int layer, int chunk, int64_t *slot) {
+  HM_API_BEGIN
+  *slot = reinterpret_cast<const hm::Runtime *>(rt)->shared_slot(layer, chunk);
+  HM_API_END
+}
+
+int hm_runtime_forward_layer(hm_runtime *rt, int layer, const uint16_t *x, const float *logits, int T, int ld,
+                             uint16_t *y, const int32_t *pred_layers, const int64_t *pred_loads, int n_pred,
+                             void *stream, hm_layer_stats *stats) {
+  HM_API_BEGIN
+  reinterpret_cast<hm::Runtime *>(rt)->forward_layer(layer, x, logits, T, ld, y, pred_layers, pred_loads, n_pred,
+                                                    static_cast<cudaStream_t>(stream), stats);
+  HM_API_END
+}
+
+int hm_runtime_last_request(const hm_runtime *rt, int64_t *loads, double *scores) {
+  HM_API_BEGIN
+  auto *r = reinterpret_cast<const hm::Runtime *>(rt);
+  for (int e = 0; e < r->N; ++e) {
+    if (loads) loads[e] = r->loads[e];
+    if (scores) scores[e] = r->scores[e];
+  }
+  HM_API_END
+}
+
+int hm_runtime_device_mrs(hm_runtime *rt, double *host_out) {
+  HM_API_BEGIN
+  auto *r = reinterpret_cast<hm::Runtime *>(rt);
+  RT_CUDA(cudaDeviceSynchronize());
+  RT_CUDA(cudaMemcpy(host_out, r->S_dev, static_cast<size_t>(r->L) * r->N * 8, cudaMemcpyDeviceToHost));
+  HM_API_END
+}
+
+int hm_runtime_set_kernel_timing(hm_runtime *rt, int on) {
+  HM_API_BEGIN
+  auto *r = reinterpret_cast<hm::Runtime *>(rt);
+  r->time_kernels = on != 0;
+  r->kused = 0;
+  HM_API_END
+}
+
+int hm_runtime_kernel_times(hm_runtime *rt, double *total_ms, int64_t *total_bytes, int64_t *n, double *max_ms) {
+  HM_API_BEGIN
+  auto *r = reinterpret_cast<hm::Runtime *>(rt);
+  double tot = 0.0, mx = 0.0;
+  int64_t by = 0;
+  for (size_t i = 0; i < r->kused; ++i) {
+    RT_CUDA(cudaEventSynchronize(r->kev[i].second));
+    float ms = 0.f;
+    RT_CUDA(cudaEventElapsedTime(&ms, r->kev[i].first, r->kev[i].second));
+    tot += ms;
+    mx = ms > mx ? ms : mx;
+    by += r->kbytes[i];
+  }
+  if (total_ms) *total_ms = tot;
+  if (total_bytes) *total_bytes = by;
+  if (n) *n = static_cast<int64_t>(r->kused);
+  if (max_ms) *max_ms = mx;
+  r->kused = 0;
+  HM_API_END
+}
+
+int hm_runtime_sync(hm_runtime *rt) {
+  HM_API_BEGIN
+  auto *r = reinterpret_cast<hm::Runtime *>(rt);
+  RT_CUDA(cudaStreamSynchronize(r->copy));
+  HM_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,269 @@
+"""The real HybriMoE MoE layer stack on one B200 (``MoELayer.forward`` of SURVEY.md §8b).
+
+``HybridMoE`` owns one native runtime (include/hybrimoe.h ``hm_runtime_*``):
+an HBM slot pool capped at ``floor(ratio * L * N)`` routed experts (+ the
+always-resident shared-expert chunks), a pinned host master store, a copy
+stream, and the AVX-512 host worker -- and one native decision engine bound
+to this package's ``CacheState`` / ``MrsState`` / ``MakespanEvaluator``.
+Each layer the GPU router produces the ``LayerRequest`` (loads, scores), the
+decision core plans it exactly as the reference's ``run_pass`` would
+(engine.py:288-389), and the runtime executes the plan: cached experts on the
+GPU, demand copies on the side stream, CPU experts on the host worker.
+
+Routing inputs come either from the reference's synthetic router
+(``tracegen.generate_router_logits``; "trace mode") or from the model's own
+gate weights applied to the hidden state ("model mode").
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, replace
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, lib
+from .caching import MrsState, make_mrs_state
+from .core import CacheState, ModelConfig, expert_bytes
+from .costs import HardwareProfile
+from .engine import EnginePolicy, _NativeEngine, cache_capacity
+from .scheduling import MakespanEvaluator
+
+
+@dataclass(frozen=True)
+class Family:
+    """Router conventions of a model family (see oracle/moe_ref.py for citations)."""
+
+    renormalize: bool
+    shared_gate: bool  # Qwen2: shared expert scaled by sigmoid(x . w_sg)
+
+
+FAMILIES = {
+    "tiny": Family(renormalize=True, shared_gate=False),
+    "mixtral": Family(renormalize=True, shared_gate=False),
+    "deepseek": Family(renormalize=False, shared_gate=False),
+    "qwen2": Family(renormalize=False, shared_gate=True),
+}
+
+# SURVEY.md §8 configs (bf16 weights: bytes_per_weight = 2; Qwen2 uses the
+# released moe_intermediate_size).
+SHAPES = {
+    "tiny": ModelConfig(num_layers=4, num_routed=8, num_shared=0, num_activated=2, routed_expert_dims=(256, 256),
+                        bytes_per_weight=2),
+    "mixtral": ModelConfig(num_layers=32, num_routed=8, num_shared=0, num_activated=2,
+                           routed_expert_dims=(4096, 14336), bytes_per_weight=2),
+    "deepseek": ModelConfig(num_layers=26, num_routed=64, num_shared=2, num_activated=6,
+                            routed_expert_dims=(2048, 1408), shared_expert_dims=(2048, 1408), bytes_per_weight=2),
+    "qwen2": ModelConfig(num_layers=28, num_routed=64, num_shared=1, num_activated=8,
+                         routed_expert_dims=(3584, 2560), shared_expert_dims=(3584, 20480), bytes_per_weight=2),
+}
+
+
+def shared_chunks(cfg: ModelConfig) -> int:
+    """Shared experts as always-resident chunks of the routed shape: SwiGLU is
+    separable along the intermediate dimension, so one (H, k*I) shared expert
+    is exactly the sum of k (H, I) experts."""
+    if not cfg.num_shared or cfg.shared_expert_dims is None:
+        return 0
+    H, I = cfg.routed_expert_dims
+    sh, si = cfg.shared_expert_dims
+    if sh != H or si % I:
+        raise ValueError(f"shared expert dims {cfg.shared_expert_dims} are not whole chunks of {cfg.routed_expert_dims}")
+    return cfg.num_shared * (si // I)
+
+
+class _Raw:
+    """__cuda_array_interface__ / __array_interface__ shim to view native buffers as tensors."""
+
+    def __init__(self, ptr: int, n: int, cuda: bool) -> None:
+        typestr = "<i2" if cuda else "<u2"
+        iface = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3}
+        if cuda:
+            iface["strides"] = None
+            self.__cuda_array_interface__ = iface
+        else:
+            self.__array_interface__ = iface
+
+
+@dataclass
+class LayerStats:
+    makespan_planned: float
+    t_wait_router_us: float
+    t_decide_us: float
+    t_cpu_us: float
+    n_gpu: int
+    n_cpu: int
+    n_transfer: int
+    n_prefetch: int
+    bytes_gpu: int
+    bytes_cpu: int
+    bytes_h2d: int
+
+
+class HybridMoE:
+    """L MoE layers (router + experts + combine, residual stream) under the HybriMoE schedule."""
+
+    def __init__(self, config: ModelConfig, family: str, policy: EnginePolicy, capacity_ratio: float,
+                 profile: HardwareProfile, *, host_images: int | None = None, max_tokens: int = 1024,
+                 cpu_threads: int = 0, gpu_mrs: bool = True, residual: bool = True) -> None:
+        if not torch.cuda.is_available():
+            raise RuntimeError("HybridMoE executes on a CUDA device; no CPU fallback exists")
+        self.config = config
+        self.family = FAMILIES[family]
+        self.policy = policy
+        self.profile = profile
+        H, I = config.routed_expert_dims
+        self.H, self.I = H, I
+        self.L, self.N, self.K = config.num_layers, config.num_routed, config.num_activated
+        self.S = shared_chunks(config)
+        self.capacity = cache_capacity(config, capacity_ratio)
+        self.cache = CacheState(self.capacity)
+        self.mrs: MrsState = make_mrs_state(config, alpha=policy.mrs_alpha, p=policy.mrs_p)
+        self.evaluator = MakespanEvaluator(profile, expert_bytes(config))
+        split = policy.static_split_point
+        if split is None:
+            split = math.floor(capacity_ratio * config.num_layers)
+        self.engine = _NativeEngine(config, policy, self.cache, self.mrs, self.evaluator, profile, split,
+                                    frozenset(), collect=True)
+        total = self.L * self.N
+        self.host_images = total if host_images is None else max(1, min(int(host_images), total))
+        self.gate_col = self.N if self.family.shared_gate else -1
+        self.ld = self.N + (1 if self.family.shared_gate else 0)
+        rc = _lib.RuntimeConfig(num_layers=self.L, num_routed=self.N, num_activated=self.K, hidden=H, inter=I,
+                                n_shared=self.S, renormalize=int(self.family.renormalize),
+                                shared_gate_col=self.gate_col, capacity=self.capacity,
+                                host_images=self.host_images, cpu_threads=int(cpu_threads),
+                                max_tokens=int(max_tokens), gpu_mrs=int(gpu_mrs), residual=int(residual))
+        h = C.c_void_p()
+        check(lib.hm_runtime_create(C.byref(rc), self.engine._h, C.byref(h)))
+        self._rt = h.value
+        pool, store, sb, ns = C.c_void_p(), C.c_void_p(), C.c_size_t(), C.c_int64()
+        check(lib.hm_runtime_buffers(self._rt, C.byref(pool), C.byref(store), C.byref(sb), C.byref(ns)))
+        self.slot_bytes, self.n_slots = sb.value, ns.value
+        self.slot_elems = self.slot_bytes // 2
+        self.pool = (torch.as_tensor(_Raw(pool.value, self.n_slots * self.slot_elems, True), device="cuda")
+                     .view(torch.bfloat16).view(self.n_slots, self.slot_elems) if self.n_slots else None)
+        self.store = np.asarray(_Raw(store.value, self.host_images * self.slot_elems, False)).reshape(
+            self.host_images, self.slot_elems)
+        self.store_t = torch.from_numpy(self.store.view(np.int16)).view(torch.bfloat16)
+        self.gate_w: torch.Tensor | None = None
+        self.max_tokens = max_tokens
+        self._bufs: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
+
+    def __del__(self) -> None:
+        if getattr(self, "_rt", None):
+            torch.cuda.synchronize()
+            lib.hm_runtime_destroy(self._rt)
+            self._rt = None
+
+    # -------------------------------------------------------------- weights
+    def init_random_weights(self, seed: int = 0, chunk_images: int = 8) -> None:
+        """Random-init N(0, 0.02^2) bf16 experts, generated on the
+        GPU and written to the pinned master store / shared slots; router gate
+        weights N(0, 1/H) for model mode."""
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        n = self.slot_elems
+        for i0 in range(0, self.host_images, chunk_images):
+            k = min(chunk_images, self.host_images - i0)
+            buf = (torch.randn((k, n), generator=g, device="cuda", dtype=torch.float32) * 0.02).to(torch.bfloat16)
+            self.store_t[i0:i0 + k].copy_(buf)
+        for l in range(self.L):
+            for c in range(self.S):
+                s = self.shared_slot(l, c)
+                self.pool[s].copy_((torch.randn(n, generator=g, device="cuda") * 0.02).to(torch.bfloat16))
+        self.gate_w = (torch.randn((self.L, self.ld, self.H), generator=g, device="cuda") / math.sqrt(self.H)).to(
+            torch.bfloat16)
+        torch.cuda.synchronize()
+
+    def image_of(self, layer: int, expert: int) -> int:
+        v = C.c_int64()
+        check(lib.hm_runtime_image_of(self._rt, layer, expert, C.byref(v)))
+        return v.value
+
+    def shared_slot(self, layer: int, chunk: int) -> int:
+        v = C.c_int64()
+        check(lib.hm_runtime_shared_slot(self._rt, layer, chunk, C.byref(v)))
+        return v.value
+
+    def expert_image(self, layer: int, expert: int) -> np.ndarray:
+        """Host bytes of routed expert (layer, expert) in slot layout (uint16 bf16 bits)."""
+        return self.store[self.image_of(layer, expert)]
+
+    def shared_image(self, layer: int, chunk: int) -> np.ndarray:
+        return self.pool[self.shared_slot(layer, chunk)].view(torch.int16).cpu().numpy().view(np.uint16)
+
+    # -------------------------------------------------------------- forward
+    def _ping_pong(self, T: int) -> tuple[torch.Tensor, torch.Tensor]:
+        if T not in self._bufs:
+            self._bufs[T] = tuple(torch.empty((T, self.H), dtype=torch.bfloat16, device="cuda") for _ in range(2))
+        return self._bufs[T]
+
+    def forward_pass(self, x: torch.Tensor, logits=None, predict=None, decision_log: bool = False,
+                     keep_layers: bool = False, stream=None):
+        """Run all L layers on x [T, H] bf16.
+
+        logits: per-layer [T, ld] fp32 CUDA tensors (trace mode) or None (model
+        mode: x_l . W_g,l).  predict(layer) -> list of predicted LayerRequests
+        for the prefetch decision (prefetch.py:54-101).  Returns (y, info)."""
+        T = x.shape[0]
+        if T > self.max_tokens:
+            raise ValueError(f"T={T} exceeds max_tokens={self.max_tokens}")
+        st = stream if stream is not None else torch.cuda.current_stream()
+        a, b = self._ping_pong(T)
+        cur = x
+        stats, records, layers_io, requests = [], [], [], []
+        ls = _lib.LayerStats()
+        loads = np.zeros(self.N, dtype=np.int64)
+        scores = np.zeros(self.N, dtype=np.float64)
+        self.engine.begin_pass()
+        for l in range(self.L):
+            lg = logits[l] if logits is not None else self._model_logits(cur, l, st)
+            preds = predict(l) if (predict is not None and self.policy.prefetch) else []
+            pl = np.array([p.layer for p in preds], dtype=np.int32)
+            pload = np.zeros((max(1, len(preds)), self.N), dtype=np.int64)
+            for d, p in enumerate(preds):
+                for i in p.activated:
+                    pload[d, i] = p.loads[i]
+            out = a if (l % 2 == 0) else b
+            check(lib.hm_runtime_forward_layer(self._rt, l, cur.data_ptr(), lg.data_ptr(), T, lg.shape[1],
+                                               out.data_ptr(), _lib.ptr(pl, C.c_int32), _lib.ptr(pload, C.c_int64),
+                                               len(preds), st.cuda_stream, C.byref(ls)))
+            stats.append(LayerStats(*[getattr(ls, f) for f, _ in _lib.LayerStats._fields_]))
+            if decision_log:
+                rec = self.engine.record()
+                rec["mrs_row"] = self.mrs.table()[l].copy()
+                records.append(rec)
+                check(lib.hm_runtime_last_request(self._rt, _lib.ptr(loads, C.c_int64), _lib.ptr(scores, C.c_double)))
+                requests.append((loads.copy(), scores.copy()))
+            if keep_layers:
+                layers_io.append((cur.clone(), lg, out))
+            cur = out
+        r = self.engine.end_pass()
+        info = {"stats": stats, "records": records, "requests": requests, "layers": layers_io, "pass": r}
+        if keep_layers:
+            torch.cuda.synchronize()
+            info["layers"] = [(xi, lg, yo.clone()) for xi, lg, yo in layers_io]
+        return cur, info
+
+    def _model_logits(self, x: torch.Tensor, layer: int, st) -> torch.Tensor:
+        from .kernels import router_logits
+        if self.gate_w is None:
+            raise RuntimeError("model mode needs gate weights (init_random_weights)")
+        return router_logits(x, self.gate_w[layer], stream=st)
+
+    def device_mrs(self) -> np.ndarray:
+        out = np.empty((self.L, self.N), dtype=np.float64)
+        check(lib.hm_runtime_device_mrs(self._rt, _lib.ptr(out, C.c_double)))
+        return out
+
+    def sync(self) -> None:
+        check(lib.hm_runtime_sync(self._rt))
+        torch.cuda.synchronize()
+
+
+def with_shared_time(profile: HardwareProfile, cfg: ModelConfig) -> HardwareProfile:
+    """Shared chunks run inside every layer's GPU batch; account them like the
+    reference's constant per-layer shared_expert_time (costs.py:44, engine.py:307)."""
+    return replace(profile, shared_expert_time=shared_chunks(cfg) * profile.gpu_time_per_expert)

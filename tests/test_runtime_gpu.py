@@ -1,0 +1,122 @@
+"""End-to-end HybriMoE layer stack on the GPU: router parity against the
+reference's traces, decision parity against the decision core replayed on the
+same LayerRequests, numerics against the fp32 oracle, GPU MRS table bit-exact."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import moe_ref as ref
+from stream import digest, from_records
+
+import paper_2504_05897_b200.core as mcore
+import paper_2504_05897_b200.costs as mcost
+import paper_2504_05897_b200.engine as me
+from paper_2504_05897_b200.moe import SHAPES, HybridMoE, shared_chunks
+from paper_2504_05897_b200.prefetch import predict_layers
+from paper_2504_05897_b200.tracegen import GenParams, generate_router_logits
+from paper_2504_05897_b200.weights import unpack_expert
+
+pytestmark = pytest.mark.gpu
+
+
+def stress_profile(cfg):
+    eb = mcore.expert_bytes(cfg)
+    return mcost.HardwareProfile(gpu_time_per_expert=1.0, cpu_slope=2.0, transfer_bandwidth=eb / 0.5,
+                                 cpu_first_expert_penalty=1.4)
+
+
+def bf(t: torch.Tensor) -> np.ndarray:
+    return ref.bf16_to_f32(t.view(torch.int16).cpu().numpy().view(np.uint16))
+
+
+def _experts(moe, layer):
+    ex = []
+    for e in range(moe.N):
+        g, u, d = unpack_expert(moe.expert_image(layer, e), moe.H, moe.I)
+        ex.append((ref.bf16_to_f32(g), ref.bf16_to_f32(u), ref.bf16_to_f32(d)))
+    for c in range(moe.S):
+        g, u, d = unpack_expert(moe.shared_image(layer, c), moe.H, moe.I)
+        ex.append((ref.bf16_to_f32(g), ref.bf16_to_f32(u), ref.bf16_to_f32(d)))
+    return ex
+
+
+@pytest.mark.parametrize("policy_name,prefetch,ratio", [("mrs", True, 0.5), ("lru", False, 0.25), ("lfu", True, 0.75)])
+def test_tiny_stack_parity(policy_name, prefetch, ratio):
+    cfg = SHAPES["tiny"]
+    prof = stress_profile(cfg)
+    policy = me.EnginePolicy(cache_policy=policy_name, prefetch=prefetch)
+    moe = HybridMoE(cfg, "tiny", policy, ratio, prof, max_tokens=64, residual=False)
+    moe.init_random_weights(3)
+    trace, logits = generate_router_logits(cfg, GenParams(seed=2), 48, 6)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    recs, reqs = [], []
+    for p, fwd in enumerate(trace.passes):
+        lg = [torch.from_numpy(np.ascontiguousarray(logits[p][l], dtype=np.float32)).cuda() for l in range(cfg.num_layers)]
+        x = torch.randn((fwd.token_count, moe.H), generator=g, device="cuda").to(torch.bfloat16)
+        y, info = moe.forward_pass(x, lg, predict=lambda l, p=p, fwd=fwd: predict_layers(
+            fwd.layers, cfg.num_layers, p, l, policy.prediction, 2), decision_log=True, keep_layers=True)
+        torch.cuda.synchronize()
+        for l, (loads, scores) in enumerate(info["requests"]):
+            assert list(loads) == list(fwd.layers[l].loads), (p, l)      # router == reference trace
+            reqs.append((l, loads, scores))
+        recs.extend(info["records"])
+        if p in (0, len(trace.passes) - 1):
+            for l, (xi, lgi, yo) in enumerate(info["layers"]):
+                want = ref.moe_layer(bf(xi), lgi.cpu().numpy(), _experts(moe, l), moe.N, moe.K, True, 0, -1)
+                err = np.abs(bf(yo) - want).max() / np.abs(want).max()
+                assert err <= 1e-2, (p, l, err)
+    # the decision core replayed on the runtime's own LayerRequests gives the same decision stream
+    passes, i = [], 0
+    for fwd in trace.passes:
+        layers = []
+        for l in range(cfg.num_layers):
+            _, loads, scores = reqs[i]
+            i += 1
+            layers.append(mcore.make_layer_request(l, loads.tolist(), scores.tolist()))
+        passes.append(mcore.ForwardPass(fwd.stage, fwd.token_count, tuple(layers)))
+    replay = mcore.Trace(cfg, tuple(passes))
+    m = me.run_trace(replay, policy, ratio, prof, 2, decision_log=True)
+    mrs = policy_name == "mrs"
+    assert digest(from_records(recs, mrs)) == digest(from_records(m.decisions, mrs))
+    if mrs:
+        assert np.array_equal(moe.device_mrs().view(np.uint64), moe.mrs.table().view(np.uint64))
+
+
+@pytest.mark.parametrize("shape", ["deepseek", "qwen2"])
+def test_shared_expert_families_one_layer(shape):
+    base = SHAPES[shape]
+    # two layers of the family's routing/shared structure at a reduced hidden size
+    H = 256
+    I = base.routed_expert_dims[1] if base.routed_expert_dims[1] <= 2560 else 256
+    I = 256 if shape == "qwen2" else 384
+    shared = (H, I * (8 if shape == "qwen2" else 1))
+    cfg = mcore.ModelConfig(num_layers=2, num_routed=16, num_shared=base.num_shared, num_activated=base.num_activated,
+                            routed_expert_dims=(H, I), shared_expert_dims=shared, bytes_per_weight=2)
+    prof = stress_profile(cfg)
+    moe = HybridMoE(cfg, shape, me.EnginePolicy(), 0.5, prof, max_tokens=128, residual=False)
+    moe.init_random_weights(1)
+    rng = np.random.default_rng(0)
+    T = 96
+    lg = [torch.from_numpy(rng.standard_normal((T, moe.ld)).astype(np.float32)).cuda() for _ in range(2)]
+    x = torch.randn((T, H), device="cuda").to(torch.bfloat16)
+    y, info = moe.forward_pass(x, lg, keep_layers=True)
+    torch.cuda.synchronize()
+    fam = moe.family
+    for l, (xi, lgi, yo) in enumerate(info["layers"]):
+        want = ref.moe_layer(bf(xi), lgi.cpu().numpy(), _experts(moe, l), moe.N, moe.K, fam.renormalize,
+                             shared_chunks(cfg), moe.gate_col)
+        err = np.abs(bf(yo) - want).max() / np.abs(want).max()
+        assert err <= 1e-2, (l, err)
+
+
+def test_model_mode_runs_and_is_deterministic():
+    cfg = SHAPES["tiny"]
+    moe = HybridMoE(cfg, "tiny", me.EnginePolicy(), 0.25, stress_profile(cfg), max_tokens=32)
+    moe.init_random_weights(5)
+    x = torch.randn((16, moe.H), device="cuda").to(torch.bfloat16)
+    y1, _ = moe.forward_pass(x, None)
+    y1 = y1.clone()
+    torch.cuda.synchronize()
+    assert torch.isfinite(y1.float()).all()
