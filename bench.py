@@ -199,6 +199,15 @@ def run_ours(args) -> None:
     g = torch.Generator(device="cuda").manual_seed(1234 + rank)
     xs = [torch.randn((f.token_count, H), generator=g, device="cuda").to(torch.bfloat16) for f in trace.passes]
     torch.cuda.synchronize()
+    # host DRAM read bandwidth over (part of) the pinned master store: the host roofline
+    import ctypes as C
+    cp = C.c_void_p()
+    _lib.check(_lib.lib.hm_cpu_pool_create(args.cpu_threads, C.byref(cp)))
+    hbw = C.c_double()
+    nbytes = min(moe.store.nbytes, 16 << 30)
+    _lib.check(_lib.lib.hm_host_read_bw(cp, moe.store.ctypes.data, nbytes, 3, C.byref(hbw)))
+    _lib.lib.hm_cpu_pool_destroy(cp)
+    host_bw_gbs = hbw.value if args.host_bw_gbs <= 0 else args.host_bw_gbs
     setup_s = time.time() - t_setup
 
     def predictor(p):
@@ -288,13 +297,22 @@ def run_ours(args) -> None:
                 "launches": kn.value, "avg_launch_us": 1e3 * kms.value / max(1, kn.value),
                 "bytes_per_launch": kbytes.value / max(1, kn.value), "peak_kind": pk_kind}
     # plan-conditional roofline of the whole step: max(B_gpu/BW_hbm, B_cpu/BW_host, B_h2d/BW_pcie) per layer
-    bw_host = args.host_bw_gbs * 1e9
+    bw_host = host_bw_gbs * 1e9
     bw_pcie = cal.profile.transfer_bandwidth  # bytes / s, fitted at warm-up
     bound_s = sum(max(s.bytes_gpu / (hbm_peak * 1e9), s.bytes_cpu / bw_host, s.bytes_h2d / bw_pcie)
                   for s in stats_all)
     n_cpu = sum(s.n_cpu for s in stats_all) / args.steps
     n_gpu = sum(s.n_gpu for s in stats_all) / args.steps
     n_xfer = sum(s.n_transfer for s in stats_all) / args.steps
+
+    # ---- prefill-side kernel: grouped tcgen05 GEMM over 8 resident experts x 256 tokens
+    from paper_2504_05897_b200.microbench import gemm_bench
+    gb = gemm_bench(H, I, rows_per_expert=256, n_experts=cfg.num_routed if cfg.num_routed <= 8 else 8)
+    tc_peak = float(pk["bf16_tflops"])
+    gemm_roofline = {"bound": "tensor", "achieved": gb["tflops"], "peak": tc_peak, "unit": "TFLOP/s",
+                     "frac": gb["tflops"] / tc_peak, "traffic": None, "peak_kind": pk_kind + " burst",
+                     "kernel": "expert_gemm_kernel (ffn1 SwiGLU + ffn2), 256 tokens x 8 experts",
+                     "ms": gb["ms"], "hbm_gbs": gb["hbm_gbs"]}
 
     # ---- CPU baseline: the oracle port on this host, bounded sample
     cpu = None
@@ -320,9 +338,10 @@ def run_ours(args) -> None:
             "e2e": {"value": world * 1e3 / e2e_ms, "unit": "tok/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "roofline": roofline,
+            "gemm_roofline": gemm_roofline,
             "step_roofline": {"bound": "plan-conditional max(B_gpu/HBM, B_cpu/host DRAM, B_h2d/PCIe)",
                               "bound_ms_per_step": 1e3 * bound_s / args.steps,
-                              "frac": (1e3 * bound_s / args.steps) / ms_step, "host_bw_gbs": args.host_bw_gbs,
+                              "frac": (1e3 * bound_s / args.steps) / ms_step, "host_bw_gbs": host_bw_gbs,
                               "pcie_gbs": bw_pcie / 1e9},
             "per_step": {"gpu_experts": n_gpu, "cpu_experts": n_cpu, "transfers": n_xfer,
                          "host_decide_us_per_layer": statistics.mean(s.t_decide_us for s in stats_all),
@@ -352,7 +371,7 @@ def main() -> None:
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--host-images", type=int, default=None)
     ap.add_argument("--cpu-threads", type=int, default=0)
-    ap.add_argument("--host-bw-gbs", type=float, default=100.0)
+    ap.add_argument("--host-bw-gbs", type=float, default=0.0, help="<= 0: measure")
     ap.add_argument("--ref-layers", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -342,6 +342,8 @@ void hm_cpu_pool_destroy(hm_cpu_pool *p);
 int hm_cpu_expert(hm_cpu_pool *pool, const uint16_t *img, int H, int I, const uint16_t *x, int M,
                   float *out);
 int hm_cpu_has_avx512bf16(void);
+/* Best-of-reps host DRAM read bandwidth (GB/s) over `bytes` at p (64-byte aligned). */
+int hm_host_read_bw(hm_cpu_pool *pool, const void *p, size_t bytes, int reps, double *gbs);
 
 typedef struct hm_runtime hm_runtime;
 typedef struct hm_runtime_config {

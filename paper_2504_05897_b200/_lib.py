@@ -302,3 +302,5 @@ for _name, (_args, _res) in {
     _f = getattr(lib, _name)
     _f.argtypes = _args
     _f.restype = _res
+lib.hm_host_read_bw.argtypes = [vp, vp, C.c_size_t, C.c_int, P(f64)]
+lib.hm_host_read_bw.restype = C.c_int

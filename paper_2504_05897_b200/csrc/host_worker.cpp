@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <condition_variable>
 #include <cstring>
@@ -174,6 +175,39 @@ void phase2(const uint16_t *img, int H, int I, const uint16_t *h, int M, float *
   }
 }
 
+// One token: dot of `n` consecutive rows (stride K) with x, in memory order --
+// a single sequential stream per thread, 4 independent accumulators, software
+// prefetch a few KB ahead.  This is the decode (host-DRAM-bound) path.
+inline void stream_rows(const uint16_t *w, int n, int K, const uint16_t *x, float *out) {
+  constexpr int kAhead = 2048;  // elements (4 KB) ahead of the current load
+  for (int r = 0; r < n; ++r) {
+    const uint16_t *row = w + static_cast<size_t>(r) * K;
+    __m512 a0 = _mm512_setzero_ps(), a1 = _mm512_setzero_ps(), a2 = _mm512_setzero_ps(),
+           a3 = _mm512_setzero_ps();
+    int k = 0;
+    for (; k + 128 <= K; k += 128) {
+      _mm_prefetch(reinterpret_cast<const char *>(row + k + kAhead), _MM_HINT_T0);
+      _mm_prefetch(reinterpret_cast<const char *>(row + k + kAhead + 64), _MM_HINT_T0);
+      a0 = _mm512_dpbf16_ps(a0, ldbh(row + k), ldbh(x + k));
+      a1 = _mm512_dpbf16_ps(a1, ldbh(row + k + 32), ldbh(x + k + 32));
+      a2 = _mm512_dpbf16_ps(a2, ldbh(row + k + 64), ldbh(x + k + 64));
+      a3 = _mm512_dpbf16_ps(a3, ldbh(row + k + 96), ldbh(x + k + 96));
+    }
+    for (; k < K; k += 32) a0 = _mm512_dpbf16_ps(a0, ldbh(row + k), ldbh(x + k));
+    out[r] = _mm512_reduce_add_ps(_mm512_add_ps(_mm512_add_ps(a0, a1), _mm512_add_ps(a2, a3)));
+  }
+}
+
+// Decode phase 1 over whole 128-pair blocks [b0, b1): W13 block b is 128 gate
+// rows then 128 up rows, contiguous -- read it front to back.
+void phase1_stream(const uint16_t *img, int H, int I, const uint16_t *x, uint16_t *h, int b0, int b1) {
+  float gu[2 * kIlv];
+  for (int b = b0; b < b1; ++b) {
+    stream_rows(img + static_cast<size_t>(b) * 2 * kIlv * H, 2 * kIlv, H, x, gu);
+    for (int i = 0; i < kIlv; ++i) h[b * kIlv + i] = f2bf(silu(gu[i]) * gu[kIlv + i]);
+  }
+}
+
 }  // namespace
 
 void cpu_expert(ThreadPool &pool, const uint16_t *img, int H, int I, const uint16_t *x, int M, float *out,
@@ -182,6 +216,21 @@ void cpu_expert(ThreadPool &pool, const uint16_t *img, int H, int I, const uint1
   if (M <= 0) return;
   hbuf.resize(static_cast<size_t>(M) * I);
   uint16_t *h = hbuf.data();
+  if (M == 1) {  // decode: one sequential stream per thread in both phases
+    const int nblk = I / kIlv;
+    pool.run([&](int tid, int nt) {
+      const int b0 = static_cast<int>(static_cast<long>(nblk) * tid / nt);
+      const int b1 = static_cast<int>(static_cast<long>(nblk) * (tid + 1) / nt);
+      if (b0 < b1) phase1_stream(img, H, I, x, h, b0, b1);
+    });
+    const uint16_t *w2 = img + static_cast<size_t>(2) * I * H;
+    pool.run([&](int tid, int nt) {
+      const int j0 = static_cast<int>(static_cast<long>(H) * tid / nt);
+      const int j1 = static_cast<int>(static_cast<long>(H) * (tid + 1) / nt);
+      if (j0 < j1) stream_rows(w2 + static_cast<size_t>(j0) * I, j1 - j0, I, h, out + j0);
+    });
+    return;
+  }
   pool.run([&](int tid, int nt) {
     // pairs in multiples of 16 per thread keep each thread on contiguous rows
     const int per = ((I + nt - 1) / nt + 15) / 16 * 16;
@@ -218,5 +267,34 @@ int hm_cpu_expert(hm_cpu_pool *pool, const uint16_t *img, int H, int I, const ui
 }
 
 int hm_cpu_has_avx512bf16(void) { return __builtin_cpu_supports("avx512bf16") ? 1 : 0; }
+
+// Host DRAM read bandwidth with the worker pool (the host roofline denominator).
+int hm_host_read_bw(hm_cpu_pool *pool, const void *p, size_t bytes, int reps, double *gbs) {
+  HM_API_BEGIN
+  auto &tp = *reinterpret_cast<hm::ThreadPool *>(pool);
+  const size_t n64 = bytes / 64;
+  const char *base = static_cast<const char *>(p);
+  std::vector<double> sink(static_cast<size_t>(tp.size()), 0.0);
+  double best = 0.0;
+  for (int r = 0; r < reps; ++r) {
+    const auto t0 = std::chrono::steady_clock::now();
+    tp.run([&](int tid, int nt) {
+      const size_t per = (n64 + nt - 1) / nt;
+      const size_t a = std::min(n64, static_cast<size_t>(tid) * per), b = std::min(n64, a + per);
+      __m512i acc0 = _mm512_setzero_si512(), acc1 = _mm512_setzero_si512();
+      size_t i = a;
+      for (; i + 1 < b; i += 2) {
+        acc0 = _mm512_xor_si512(acc0, _mm512_load_si512(base + i * 64));
+        acc1 = _mm512_xor_si512(acc1, _mm512_load_si512(base + (i + 1) * 64));
+      }
+      if (i < b) acc0 = _mm512_xor_si512(acc0, _mm512_load_si512(base + i * 64));
+      sink[tid] += static_cast<double>(_mm512_reduce_add_epi64(_mm512_xor_si512(acc0, acc1)) & 1);
+    });
+    const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    best = std::max(best, static_cast<double>(n64 * 64) / s / 1e9);
+  }
+  *gbs = best + 0.0 * sink[0];
+  HM_API_END
+}
 
 }  // extern "C"

@@ -237,14 +237,12 @@ class HybridMoE:
                 records.append(rec)
                 check(lib.hm_runtime_last_request(self._rt, _lib.ptr(loads, C.c_int64), _lib.ptr(scores, C.c_double)))
                 requests.append((loads.copy(), scores.copy()))
-            if keep_layers:
-                layers_io.append((cur.clone(), lg, out))
+            if keep_layers:  # clones are ordered after this layer on the same stream
+                with torch.cuda.stream(st):
+                    layers_io.append((cur.clone(), lg, out.clone()))
             cur = out
         r = self.engine.end_pass()
         info = {"stats": stats, "records": records, "requests": requests, "layers": layers_io, "pass": r}
-        if keep_layers:
-            torch.cuda.synchronize()
-            info["layers"] = [(xi, lg, yo.clone()) for xi, lg, yo in layers_io]
         return cur, info
 
     def _model_logits(self, x: torch.Tensor, layer: int, st) -> torch.Tensor:
