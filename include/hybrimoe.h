@@ -325,6 +325,15 @@ int hm_expert_ffn(const uint16_t *pool, int n_slots, int H, int I, const hm_grou
 /* y[t] = residual[t] (optional) + sum_k w[t,k] * out[pos[t,k]]  (Eq. 1 combine). */
 int hm_combine(const float *out, const int32_t *pos, const float *w, int T, int Kp, int H,
                const uint16_t *residual, uint16_t *y, void *stream);
+/* Expert parallelism helpers: zero the combine weight of every selection whose
+ * expert is not homed on `rank` (routed e: e % world; shared column N+c:
+ * c % world); fp32 combine without residual; y = bf16(residual + y32). */
+int hm_mask_nonhome(const int32_t *sel, float *w, int TKp, int N, int rank, int world,
+                    void *stream);
+int hm_combine_f32(const float *out, const int32_t *pos, const float *w, int T, int Kp, int H,
+                   float *y32, void *stream);
+int hm_residual_add(const float *y32, const uint16_t *residual, int T, int H, uint16_t *y,
+                    void *stream);
 /* Number of kernels this library has launched so far (process-wide). */
 long long hm_launch_count(void);
 /* GPU-side MRS update (caching.py:58-76): S[layer] <- a*TopP(s) + (1-a)*S[layer],
@@ -361,6 +370,8 @@ typedef struct hm_runtime_config {
   int32_t max_tokens;      /* largest T of one forward_layer call */
   int32_t gpu_mrs;         /* keep the GPU copy of S updated with hm_mrs_update_dev */
   int32_t residual;        /* y = x + MoE(x) (1) or y = MoE(x) (0) */
+  int32_t ep_rank;         /* expert parallelism: this rank computes experts e with  */
+  int32_t ep_world;        /* e % ep_world == ep_rank (shared chunk c: c % ep_world) */
 } hm_runtime_config;
 
 typedef struct hm_layer_stats {
@@ -393,6 +404,10 @@ int hm_runtime_last_request(const hm_runtime *rt, int64_t *loads, double *scores
 /* GPU copy of the MRS table S [L, N] (synchronises the device). */
 int hm_runtime_device_mrs(hm_runtime *rt, double *host_out);
 int hm_runtime_sync(hm_runtime *rt);
+/* Expert parallelism (ep_world > 1): forward_layer writes this rank's partial
+ * sum_k w E_k(x) over its home experts to y32 [T, H] fp32 instead of y; the
+ * caller all-reduces y32 across ranks and finishes with hm_residual_add. */
+int hm_runtime_set_ep_output(hm_runtime *rt, float *y32);
 /* CUDA-event timing of every expert-FFN launch (bench roofline): enable, then
  * read and reset the accumulated launch time / algorithmic bytes. */
 int hm_runtime_set_kernel_timing(hm_runtime *rt, int on);

@@ -267,7 +267,7 @@ class RuntimeConfig(C.Structure):
                 ("hidden", C.c_int32), ("inter", C.c_int32), ("n_shared", C.c_int32), ("renormalize", C.c_int32),
                 ("shared_gate_col", C.c_int32), ("capacity", C.c_int64), ("host_images", C.c_int64),
                 ("cpu_threads", C.c_int32), ("max_tokens", C.c_int32), ("gpu_mrs", C.c_int32),
-                ("residual", C.c_int32)]
+                ("residual", C.c_int32), ("ep_rank", C.c_int32), ("ep_world", C.c_int32)]
 
 
 class LayerStats(C.Structure):
@@ -304,3 +304,13 @@ for _name, (_args, _res) in {
     _f.restype = _res
 lib.hm_host_read_bw.argtypes = [vp, vp, C.c_size_t, C.c_int, P(f64)]
 lib.hm_host_read_bw.restype = C.c_int
+
+for _name, (_args, _res) in {
+    "hm_runtime_set_ep_output": ([vp, vp], C.c_int),
+    "hm_mask_nonhome": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp], C.c_int),
+    "hm_combine_f32": ([vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp], C.c_int),
+    "hm_residual_add": ([vp, vp, C.c_int, C.c_int, vp, vp], C.c_int),
+}.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res

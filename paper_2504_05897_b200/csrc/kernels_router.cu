@@ -179,6 +179,49 @@ __global__ void gather_kernel(const uint16_t *__restrict__ x, const int32_t *__r
   for (int c = threadIdx.x; c < H / 8; c += blockDim.x) dst[c] = src[c];
 }
 
+// Expert parallelism: drop selections whose expert lives on another rank.
+__global__ void mask_nonhome_kernel(const int32_t *__restrict__ sel, float *__restrict__ w, int TKp, int N, int rank,
+                                    int world) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= TKp) return;
+  const int e = sel[j];
+  const int owner = (e < N ? e : e - N) % world;
+  if (owner != rank) w[j] = 0.0f;
+}
+
+// y32[t, :] = sum_k w[t, k] * out[pos[t, k], :]  (this rank's partial; zero weights skipped)
+__global__ void combine_f32_kernel(const float *__restrict__ out, const int32_t *__restrict__ pos,
+                                   const float *__restrict__ w, int Kp, int H, float *__restrict__ y32) {
+  const int t = blockIdx.x;
+  for (int c = threadIdx.x * 4; c < H; c += blockDim.x * 4) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < Kp; ++k) {
+      const float wk = w[static_cast<size_t>(t) * Kp + k];
+      if (wk == 0.0f) continue;
+      const float4 o = *reinterpret_cast<const float4 *>(out + static_cast<size_t>(pos[static_cast<size_t>(t) * Kp + k]) * H + c);
+      a.x = fmaf(wk, o.x, a.x);
+      a.y = fmaf(wk, o.y, a.y);
+      a.z = fmaf(wk, o.z, a.z);
+      a.w = fmaf(wk, o.w, a.w);
+    }
+    *reinterpret_cast<float4 *>(y32 + static_cast<size_t>(t) * H + c) = a;
+  }
+}
+
+// y = bf16(residual + y32)
+__global__ void residual_add_kernel(const float *__restrict__ y32, const uint16_t *__restrict__ residual, int H,
+                                    uint16_t *__restrict__ y) {
+  const int t = blockIdx.x;
+  for (int c = threadIdx.x * 4; c < H; c += blockDim.x * 4) {
+    const float4 a = *reinterpret_cast<const float4 *>(y32 + static_cast<size_t>(t) * H + c);
+    const uint2 rv = *reinterpret_cast<const uint2 *>(residual + static_cast<size_t>(t) * H + c);
+    uint2 o2;
+    o2.x = dev::pack_bf2(a.x + dev::bf_lo(rv.x), a.y + dev::bf_hi(rv.x));
+    o2.y = dev::pack_bf2(a.z + dev::bf_lo(rv.y), a.w + dev::bf_hi(rv.y));
+    *reinterpret_cast<uint2 *>(y + static_cast<size_t>(t) * H + c) = o2;
+  }
+}
+
 // y[t, :] = residual[t, :] + sum_k w[t, k] * out[pos[t, k], :]   (k in order)
 __global__ void combine_kernel(const float *__restrict__ out, const int32_t *__restrict__ pos,
                                const float *__restrict__ w, int Kp, int H, const uint16_t *__restrict__ residual,
@@ -188,6 +231,7 @@ __global__ void combine_kernel(const float *__restrict__ out, const int32_t *__r
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
     for (int k = 0; k < Kp; ++k) {
       const float wk = w[static_cast<size_t>(t) * Kp + k];
+      if (wk == 0.0f) continue;  // masked (other rank's expert) or underflowed
       const float4 o = *reinterpret_cast<const float4 *>(out + static_cast<size_t>(pos[static_cast<size_t>(t) * Kp + k]) * H + c);
       a0 = fmaf(wk, o.x, a0);
       a1 = fmaf(wk, o.y, a1);
@@ -312,6 +356,38 @@ int hm_combine(const float *out, const int32_t *pos, const float *w, int T, int 
   HM_REQUIRE(H % 4 == 0, HM_EVALUE, "hidden size must be a multiple of 4");
   if (T > 0) {
     hm::combine_kernel<<<T, 256, 0, static_cast<cudaStream_t>(stream)>>>(out, pos, w, Kp, H, residual, y);
+    HM_LAUNCH_CHECK();
+  }
+  HM_API_END
+}
+
+int hm_mask_nonhome(const int32_t *sel, float *w, int TKp, int N, int rank, int world, void *stream) {
+  HM_API_BEGIN
+  HM_REQUIRE(world >= 1 && rank >= 0 && rank < world, HM_EVALUE, "bad expert-parallel rank");
+  if (TKp > 0 && world > 1) {
+    hm::mask_nonhome_kernel<<<(TKp + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(sel, w, TKp, N, rank,
+                                                                                             world);
+    HM_LAUNCH_CHECK();
+  }
+  HM_API_END
+}
+
+int hm_combine_f32(const float *out, const int32_t *pos, const float *w, int T, int Kp, int H, float *y32,
+                   void *stream) {
+  HM_API_BEGIN
+  HM_REQUIRE(H % 4 == 0, HM_EVALUE, "hidden size must be a multiple of 4");
+  if (T > 0) {
+    hm::combine_f32_kernel<<<T, 256, 0, static_cast<cudaStream_t>(stream)>>>(out, pos, w, Kp, H, y32);
+    HM_LAUNCH_CHECK();
+  }
+  HM_API_END
+}
+
+int hm_residual_add(const float *y32, const uint16_t *residual, int T, int H, uint16_t *y, void *stream) {
+  HM_API_BEGIN
+  HM_REQUIRE(H % 4 == 0, HM_EVALUE, "hidden size must be a multiple of 4");
+  if (T > 0) {
+    hm::residual_add_kernel<<<T, 256, 0, static_cast<cudaStream_t>(stream)>>>(y32, residual, H, y);
     HM_LAUNCH_CHECK();
   }
   HM_API_END

@@ -32,6 +32,8 @@ int hm_expert_ffn(const uint16_t *, int, int, int, const hm_group *, int, const 
                   int, void *);
 int hm_combine(const float *, const int32_t *, const float *, int, int, int, const uint16_t *, uint16_t *, void *);
 int hm_mrs_update_dev(double *, const double *, int, int, int, double, void *);
+int hm_mask_nonhome(const int32_t *, float *, int, int, int, int, void *);
+int hm_combine_f32(const float *, const int32_t *, const float *, int, int, int, float *, void *);
 }
 
 namespace hm {
@@ -57,6 +59,8 @@ struct Runtime {
   hm_runtime_config cfg;
   Engine *engine;
   int N, K, S, E, Kp, H, I, L;
+  int R = 0, W = 1;          // expert-parallel rank / world
+  float *y32 = nullptr;      // EP partial output (caller-owned)
   size_t slot_elems, slot_bytes;
   int64_t n_slots;
   uint16_t *pool = nullptr;        // device: [n_slots][slot_elems]
@@ -118,6 +122,9 @@ struct Runtime {
     Kp = K + S;
     H = c.hidden;
     I = c.inter;
+    W = c.ep_world > 1 ? c.ep_world : 1;
+    R = W > 1 ? c.ep_rank : 0;
+    HM_REQUIRE(R >= 0 && R < W, HM_EVALUE, "bad expert-parallel rank");
     HM_REQUIRE(L >= 1 && N >= 1 && K >= 1 && K <= N && S >= 0 && H > 0 && I > 0, HM_EVALUE, "bad runtime shape");
     HM_REQUIRE(engine->cfg.num_layers == L && engine->cfg.num_routed == N && engine->cache.capacity == c.capacity,
                HM_EVALUE, "engine and runtime disagree on the model shape or cache capacity");
@@ -185,7 +192,10 @@ struct Runtime {
   }
 
   int64_t image_of(int layer, int expert) const {
-    return (static_cast<int64_t>(layer) * N + expert) % cfg.host_images;
+    if (W == 1) return (static_cast<int64_t>(layer) * N + expert) % cfg.host_images;
+    // a rank stores only its home experts e = R + W*j, j < n_home
+    const int64_t n_home = (N - R + W - 1) / W;
+    return (static_cast<int64_t>(layer) * n_home + expert / W) % cfg.host_images;
   }
   int64_t shared_slot(int layer, int chunk) const { return cfg.capacity + static_cast<int64_t>(layer) * S + chunk; }
   uint16_t *slot_ptr(int64_t s) const { return pool + static_cast<size_t>(s) * slot_elems; }
@@ -209,6 +219,7 @@ struct Runtime {
     const int rows = T * Kp;
     // (0) router, LayerRequest, permutation -- all on the compute stream
     ok(hm_router_topk(logits, T, N, ld, K, cfg.renormalize, S, cfg.shared_gate_col, sel, w, probs, counts, vs));
+    if (W > 1) ok(hm_mask_nonhome(sel, w, T * Kp, N, R, W, vs));
     ok(hm_score_sums(probs, T, N, score_sum, vs));
     ok(hm_offsets(counts, E, offsets, vs));
     RT_CUDA(cudaMemcpyAsync(h_counts, counts, E * 4, cudaMemcpyDeviceToHost, st));
@@ -226,7 +237,9 @@ struct Runtime {
     double tot = 0.0;
     for (int e = 0; e < N; ++e) tot += h_score_sum[e];
     for (int e = 0; e < N; ++e) {
-      loads[e] = h_counts[e];
+      // rank-masked LayerRequest under expert parallelism: other ranks' loads
+      // are zeroed, scores stay whole so every rank's S table is identical
+      loads[e] = (W == 1 || e % W == R) ? h_counts[e] : 0;
       scores[e] = tot > 0.0 ? h_score_sum[e] / tot : 0.0;
       h_scores[e] = scores[e];
     }
@@ -263,7 +276,8 @@ struct Runtime {
     }
     s.n_gpu = static_cast<int32_t>(batch.size());
     for (int c = 0; c < S; ++c)
-      batch.push_back(hm_group{static_cast<int32_t>(shared_slot(layer, c)), h_offsets[N + c], h_counts[N + c], 0});
+      if (c % W == R)
+        batch.push_back(hm_group{static_cast<int32_t>(shared_slot(layer, c)), h_offsets[N + c], h_counts[N + c], 0});
     s.bytes_gpu = static_cast<int64_t>(batch.size()) * static_cast<int64_t>(slot_bytes);
     if (!batch.empty()) {
       ffn(batch.data(), static_cast<int>(batch.size()), rows, st);
@@ -313,7 +327,12 @@ struct Runtime {
       }
     }
     // combine (Eq. 1) with the residual stream, then the GPU copy of S
-    ok(hm_combine(out, pos, w, T, Kp, H, cfg.residual ? x : nullptr, y, vs));
+    if (W > 1) {
+      HM_REQUIRE(y32 != nullptr, HM_EVALUE, "expert parallelism needs hm_runtime_set_ep_output");
+      ok(hm_combine_f32(out, pos, w, T, Kp, H, y32, vs));  // partial; the caller all-reduces
+    } else {
+      ok(hm_combine(out, pos, w, T, Kp, H, cfg.residual ? x : nullptr, y, vs));
+    }
     if (cfg.gpu_mrs && engine->cfg.cache_policy == HM_POLICY_MRS && engine->mrs_) {
       RT_CUDA(cudaMemcpyAsync(scores_dev, h_scores, N * 8, cudaMemcpyHostToDevice, st));
       ok(hm_mrs_update_dev(S_dev, scores_dev, layer, N, engine->mrs_->p, engine->mrs_->alpha, vs));
@@ -381,6 +400,12 @@ int hm_runtime_device_mrs(hm_runtime *rt, double *host_out) {
   auto *r = reinterpret_cast<hm::Runtime *>(rt);
   RT_CUDA(cudaDeviceSynchronize());
   RT_CUDA(cudaMemcpy(host_out, r->S_dev, static_cast<size_t>(r->L) * r->N * 8, cudaMemcpyDeviceToHost));
+  HM_API_END
+}
+
+int hm_runtime_set_ep_output(hm_runtime *rt, float *y32) {
+  HM_API_BEGIN
+  reinterpret_cast<hm::Runtime *>(rt)->y32 = y32;
   HM_API_END
 }
 

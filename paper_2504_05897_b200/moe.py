@@ -107,7 +107,8 @@ class HybridMoE:
 
     def __init__(self, config: ModelConfig, family: str, policy: EnginePolicy, capacity_ratio: float,
                  profile: HardwareProfile, *, host_images: int | None = None, max_tokens: int = 1024,
-                 cpu_threads: int = 0, gpu_mrs: bool = True, residual: bool = True) -> None:
+                 cpu_threads: int = 0, gpu_mrs: bool = True, residual: bool = True, ep_rank: int = 0,
+                 ep_world: int = 1, process_group=None) -> None:
         if not torch.cuda.is_available():
             raise RuntimeError("HybridMoE executes on a CUDA device; no CPU fallback exists")
         self.config = config
@@ -118,7 +119,12 @@ class HybridMoE:
         self.H, self.I = H, I
         self.L, self.N, self.K = config.num_layers, config.num_routed, config.num_activated
         self.S = shared_chunks(config)
-        self.capacity = cache_capacity(config, capacity_ratio)
+        self.ep_rank, self.ep_world, self.group = int(ep_rank), max(1, int(ep_world)), process_group
+        if self.ep_world > 1:  # this rank's share of the global budget (ep.py)
+            from .ep import rank_capacity
+            self.capacity = rank_capacity(config, capacity_ratio, self.ep_rank, self.ep_world)
+        else:
+            self.capacity = cache_capacity(config, capacity_ratio)
         self.cache = CacheState(self.capacity)
         self.mrs: MrsState = make_mrs_state(config, alpha=policy.mrs_alpha, p=policy.mrs_p)
         self.evaluator = MakespanEvaluator(profile, expert_bytes(config))
@@ -127,7 +133,8 @@ class HybridMoE:
             split = math.floor(capacity_ratio * config.num_layers)
         self.engine = _NativeEngine(config, policy, self.cache, self.mrs, self.evaluator, profile, split,
                                     frozenset(), collect=True)
-        total = self.L * self.N
+        n_home = (self.N - self.ep_rank + self.ep_world - 1) // self.ep_world
+        total = self.L * n_home
         self.host_images = total if host_images is None else max(1, min(int(host_images), total))
         self.gate_col = self.N if self.family.shared_gate else -1
         self.ld = self.N + (1 if self.family.shared_gate else 0)
@@ -135,10 +142,16 @@ class HybridMoE:
                                 n_shared=self.S, renormalize=int(self.family.renormalize),
                                 shared_gate_col=self.gate_col, capacity=self.capacity,
                                 host_images=self.host_images, cpu_threads=int(cpu_threads),
-                                max_tokens=int(max_tokens), gpu_mrs=int(gpu_mrs), residual=int(residual))
+                                max_tokens=int(max_tokens), gpu_mrs=int(gpu_mrs), residual=int(residual),
+                                ep_rank=self.ep_rank, ep_world=self.ep_world)
         h = C.c_void_p()
         check(lib.hm_runtime_create(C.byref(rc), self.engine._h, C.byref(h)))
         self._rt = h.value
+        self.residual = residual
+        self.y32 = None
+        if self.ep_world > 1:
+            self.y32 = torch.empty((max_tokens, H), dtype=torch.float32, device="cuda")
+            check(lib.hm_runtime_set_ep_output(self._rt, self.y32.data_ptr()))
         pool, store, sb, ns = C.c_void_p(), C.c_void_p(), C.c_size_t(), C.c_int64()
         check(lib.hm_runtime_buffers(self._rt, C.byref(pool), C.byref(store), C.byref(sb), C.byref(ns)))
         self.slot_bytes, self.n_slots = sb.value, ns.value
@@ -230,6 +243,16 @@ class HybridMoE:
             check(lib.hm_runtime_forward_layer(self._rt, l, cur.data_ptr(), lg.data_ptr(), T, lg.shape[1],
                                                out.data_ptr(), _lib.ptr(pl, C.c_int32), _lib.ptr(pload, C.c_int64),
                                                len(preds), st.cuda_stream, C.byref(ls)))
+            if self.ep_world > 1:  # sum the ranks' partial expert outputs, then the residual
+                import torch.distributed as dist
+                part = self.y32[:T]
+                with torch.cuda.stream(st):
+                    dist.all_reduce(part, group=self.group)
+                    if self.residual:
+                        check(lib.hm_residual_add(part.data_ptr(), cur.data_ptr(), T, self.H, out.data_ptr(),
+                                                  st.cuda_stream))
+                    else:  # test configuration: the layer output is the MoE sum alone
+                        out.copy_(part.to(torch.bfloat16))
             stats.append(LayerStats(*[getattr(ls, f) for f, _ in _lib.LayerStats._fields_]))
             if decision_log:
                 rec = self.engine.record()
