@@ -24,15 +24,27 @@
 namespace hm {
 
 // ------------------------------------------------------------ thread pool
-ThreadPool::ThreadPool(int n) : n_(std::max(1, n)) {
+// Waits spin for a few microseconds and then yield the CPU: on an
+// oversubscribed VM a pure spin starves the thread being waited for.
+static inline void spin_relax() { asm volatile("" ::: "memory"); }
+template <class Pred>
+static inline void wait_until(Pred done) {
+  for (int i = 0; i < 4096; ++i) {
+    if (done()) return;
+    spin_relax();
+  }
+  while (!done()) std::this_thread::yield();
+}
+
+ThreadPool::ThreadPool(int n, int spin_us) : n_(std::max(1, n)), spin_us_(spin_us) {
   for (int t = 1; t < n_; ++t) threads_.emplace_back([this, t] { loop(t); });
 }
 
 ThreadPool::~ThreadPool() {
   {
     std::lock_guard<std::mutex> g(mu_);
-    stop_ = true;
-    ++gen_;
+    stop_.store(true);
+    gen_.fetch_add(1, std::memory_order_release);
   }
   cv_.notify_all();
   for (auto &th : threads_) th.join();
@@ -41,17 +53,22 @@ ThreadPool::~ThreadPool() {
 void ThreadPool::loop(int tid) {
   uint64_t seen = 0;
   for (;;) {
-    {
-      std::unique_lock<std::mutex> lk(mu_);
-      cv_.wait(lk, [&] { return gen_ != seen; });
-      seen = gen_;
-      if (stop_) return;
+    // spin briefly (decode issues experts back to back), then sleep
+    const auto t0 = std::chrono::steady_clock::now();
+    int iter = 0;
+    while (gen_.load(std::memory_order_acquire) == seen) {
+      if (++iter > 4096) std::this_thread::yield();
+      if ((iter & 255) == 0 &&
+          std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(spin_us_)) {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+        break;
+      }
     }
-    job_(tid, n_);
-    if (pending_.fetch_sub(1, std::memory_order_acq_rel) == 1) {
-      std::lock_guard<std::mutex> g(mu_);
-      done_cv_.notify_all();
-    }
+    seen = gen_.load(std::memory_order_acquire);
+    if (stop_.load()) return;
+    (*job_)(tid, n_);
+    pending_.fetch_sub(1, std::memory_order_acq_rel);
   }
 }
 
@@ -60,16 +77,25 @@ void ThreadPool::run(const std::function<void(int, int)> &fn) {
     fn(0, 1);
     return;
   }
+  job_ = &fn;
+  pending_.store(n_ - 1, std::memory_order_release);
   {
     std::lock_guard<std::mutex> g(mu_);
-    job_ = fn;
-    pending_.store(n_ - 1, std::memory_order_release);
-    ++gen_;
+    gen_.fetch_add(1, std::memory_order_release);
   }
   cv_.notify_all();
   fn(0, n_);
-  std::unique_lock<std::mutex> lk(mu_);
-  done_cv_.wait(lk, [&] { return pending_.load(std::memory_order_acquire) == 0; });
+  wait_until([&] { return pending_.load(std::memory_order_acquire) == 0; });
+}
+
+void ThreadPool::barrier() {
+  const uint32_t sense = bar_sense_.load(std::memory_order_acquire);
+  if (bar_count_.fetch_add(1, std::memory_order_acq_rel) == n_ - 1) {
+    bar_count_.store(0, std::memory_order_relaxed);
+    bar_sense_.store(sense + 1, std::memory_order_release);
+  } else {
+    wait_until([&] { return bar_sense_.load(std::memory_order_acquire) != sense; });
+  }
 }
 
 // ------------------------------------------------------------ kernels
@@ -218,13 +244,12 @@ void cpu_expert(ThreadPool &pool, const uint16_t *img, int H, int I, const uint1
   uint16_t *h = hbuf.data();
   if (M == 1) {  // decode: one sequential stream per thread in both phases
     const int nblk = I / kIlv;
+    const uint16_t *w2 = img + static_cast<size_t>(2) * I * H;
     pool.run([&](int tid, int nt) {
       const int b0 = static_cast<int>(static_cast<long>(nblk) * tid / nt);
       const int b1 = static_cast<int>(static_cast<long>(nblk) * (tid + 1) / nt);
       if (b0 < b1) phase1_stream(img, H, I, x, h, b0, b1);
-    });
-    const uint16_t *w2 = img + static_cast<size_t>(2) * I * H;
-    pool.run([&](int tid, int nt) {
+      pool.barrier();  // h complete
       const int j0 = static_cast<int>(static_cast<long>(H) * tid / nt);
       const int j1 = static_cast<int>(static_cast<long>(H) * (tid + 1) / nt);
       if (j0 < j1) stream_rows(w2 + static_cast<size_t>(j0) * I, j1 - j0, I, h, out + j0);

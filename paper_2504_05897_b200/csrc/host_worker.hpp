@@ -14,23 +14,30 @@
 namespace hm {
 
 // Fixed pool; run(fn) executes fn(tid, n) on every thread (the caller is tid 0).
+// Workers spin for a short while before sleeping, so the back-to-back expert
+// launches of a decode layer do not pay a futex wake-up each; barrier() is a
+// spin barrier usable inside a job (every thread must call it).
 class ThreadPool {
  public:
-  explicit ThreadPool(int n);
+  explicit ThreadPool(int n, int spin_us = 3000);
   ~ThreadPool();
   int size() const { return n_; }
   void run(const std::function<void(int, int)> &fn);
+  void barrier();
 
  private:
   void loop(int tid);
   int n_;
+  int spin_us_;
   std::vector<std::thread> threads_;
   std::mutex mu_;
-  std::condition_variable cv_, done_cv_;
-  std::function<void(int, int)> job_;
+  std::condition_variable cv_;
+  const std::function<void(int, int)> *job_ = nullptr;
+  std::atomic<uint64_t> gen_{0};
   std::atomic<int> pending_{0};
-  uint64_t gen_ = 0;
-  bool stop_ = false;
+  std::atomic<int> bar_count_{0};
+  std::atomic<uint32_t> bar_sense_{0};
+  std::atomic<bool> stop_{false};
 };
 
 // out[M, H] fp32 = W2 (silu(Wg x) * (Wu x)) for one expert image (slot layout).
