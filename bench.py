@@ -147,6 +147,28 @@ def run_reference(args) -> None:
 
 
 # --------------------------------------------------------------------------- our arm
+def warm_parity(cfg, trace, requests, records, moe, policy, args) -> dict:
+    """Evidence carried in the bench line: the GPU router's loads equal the
+    reference trace generator's for every warm-up layer, and the digest of the
+    runtime's decision stream (tests/test_runtime_gpu.py proves the stream equals
+    the decision core replayed on the same LayerRequests)."""
+    sys.path.insert(0, str(ROOT / "tests" / "golden"))
+    from stream import digest, from_records
+
+    from paper_2504_05897_b200 import core as mcore
+    n_eq = n_tot = 0
+    for i, reqs in enumerate(requests):
+        for l, (loads, _scores) in enumerate(reqs):
+            want = list(trace.passes[1 + i].layers[l].loads)
+            if moe.ep_world > 1:
+                want = [v if e % moe.ep_world == moe.ep_rank else 0 for e, v in enumerate(want)]
+            n_eq += int(list(loads) == want)
+            n_tot += 1
+    return {"router_loads_equal_reference_trace": f"{n_eq}/{n_tot}",
+            "decision_stream_sha": digest(from_records(records, policy.cache_policy == "mrs"))[:16],
+            "warmup_layers_recorded": len(records)}
+
+
 def run_ours(args) -> None:
     import torch
 
@@ -182,7 +204,7 @@ def run_ours(args) -> None:
         profile = base_profile
     cal = _Cal()
     prof = with_shared_time(cal.profile, cfg)
-    policy = EnginePolicy(cache_policy=args.policy, prefetch=args.prefetch)
+    policy = EnginePolicy(scheduling=args.scheduling, cache_policy=args.policy, prefetch=args.prefetch)
     # expert parallelism over the ranks of this box: one replicated sequence, each
     # rank homes experts e % world, host bytes and worker cores split by rank
     total_bytes = cfg.num_layers * cfg.num_routed * 3 * H * I * 2 // world
@@ -209,6 +231,14 @@ def run_ours(args) -> None:
                 lg = np.concatenate([lg, np.zeros((lg.shape[0], 1), np.float32)], axis=1)
             layer_logits.append(torch.from_numpy(np.ascontiguousarray(lg)).cuda())
         dev_logits.append(layer_logits)
+    # fixed residency of the comparison baselines (engine.py:423-434), executed for real
+    if args.scheduling == "static_layer_split":
+        split = int(args.ratio * cfg.num_layers)
+        moe.preload([(l, e) for l in range(split) for e in range(cfg.num_routed) if e % world == rank])
+    elif args.scheduling == "fixed_frequency_map":
+        from paper_2504_05897_b200.engine import compute_fixed_pinned_set
+        fixed = compute_fixed_pinned_set(trace, moe.capacity * world, policy.calibration_prefix_fraction, None)
+        moe.set_fixed_gpu_set(sorted(r for r in fixed if r[1] % world == rank)[: moe.capacity])
     g = torch.Generator(device="cuda").manual_seed(1234)  # replicated hidden state on every rank
     xs = [torch.randn((f.token_count, H), generator=g, device="cuda").to(torch.bfloat16) for f in trace.passes]
     torch.cuda.synchronize()
@@ -237,10 +267,14 @@ def run_ours(args) -> None:
     prefill_ms = ev0.elapsed_time(ev1)
     pst = pinfo["stats"]
 
-    # ---- decode: W warm-up passes, then K timed passes
+    # ---- decode: W warm-up passes (recorded for the parity block), then K timed passes
+    warm_records, warm_requests = [], []
     for p in range(1, 1 + args.warmup):
-        moe.forward_pass(xs[p], dev_logits[p], predict=predictor(p))
+        _, winfo = moe.forward_pass(xs[p], dev_logits[p], predict=predictor(p), decision_log=True)
+        warm_records.extend(winfo["records"])
+        warm_requests.append(winfo["requests"])
     torch.cuda.synchronize()
+    parity = warm_parity(cfg, trace, warm_requests, warm_records, moe, policy, args)
     lib = _lib.lib
     lib.hm_runtime_set_kernel_timing(moe._rt, 1)
     launches0 = lib.hm_launch_count()
@@ -343,6 +377,7 @@ def run_ours(args) -> None:
                        "shape": args.shape, "layers": cfg.num_layers, "experts": cfg.num_routed,
                        "top_k": cfg.num_activated, "hidden": H, "inter": I, "cache_slots": moe.capacity,
                        "host_images": moe.host_images, "policy": args.policy, "prefetch": args.prefetch,
+                       "scheduling": args.scheduling,
                        "l2": "each step streams >= 2 x 352 MB of expert weights (> 126 MB L2); no flush needed",
                        "parallelism": "ep" if world > 1 else "single"},
             "prefill": {"tokens": args.prefill, "ms": prefill_ms, "cold_cache": True,
@@ -362,7 +397,7 @@ def run_ours(args) -> None:
             "profile": {k: getattr(cal.profile, k) for k in ("gpu_time_per_expert", "cpu_slope", "transfer_bandwidth",
                                                               "transfer_latency", "gpu_slope",
                                                               "cpu_first_expert_penalty")},
-            "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks.summary(),
+            "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks.summary(), "parity": parity,
             "setup_s": setup_s,
         }
         print(json.dumps(line), flush=True)
@@ -380,6 +415,8 @@ def main() -> None:
     ap.add_argument("--ratio", type=float, default=0.25)
     ap.add_argument("--prefill", type=int, default=1024)
     ap.add_argument("--policy", default="mrs", choices=["mrs", "lru", "lfu"])
+    ap.add_argument("--scheduling", default="hybrid",
+                    choices=["hybrid", "static_layer_split", "fixed_frequency_map", "gpu_ondemand"])
     ap.add_argument("--prefetch", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--host-images", type=int, default=None)

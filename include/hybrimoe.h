@@ -351,6 +351,9 @@ void hm_cpu_pool_destroy(hm_cpu_pool *p);
 int hm_cpu_expert(hm_cpu_pool *pool, const uint16_t *img, int H, int I, const uint16_t *x, int M,
                   float *out);
 int hm_cpu_has_avx512bf16(void);
+/* n single-token experts in one worker pass (decode): outs[i][H] = expert(imgs[i])(xs[i][H]). */
+int hm_cpu_experts_decode(hm_cpu_pool *pool, const uint16_t *const *imgs, const uint16_t *const *xs, int n,
+                          int H, int I, float *const *outs);
 /* Best-of-reps host DRAM read bandwidth (GB/s) over `bytes` at p (64-byte aligned). */
 int hm_host_read_bw(hm_cpu_pool *pool, const void *p, size_t bytes, int reps, double *gbs);
 
@@ -404,6 +407,9 @@ int hm_runtime_last_request(const hm_runtime *rt, int64_t *loads, double *scores
 /* GPU copy of the MRS table S [L, N] (synchronises the device). */
 int hm_runtime_device_mrs(hm_runtime *rt, double *host_out);
 int hm_runtime_sync(hm_runtime *rt);
+/* Make experts resident (fixed residency of the baseline policies,
+ * engine.py:423-434): add them to the cache and copy them into their slots. */
+int hm_runtime_preload(hm_runtime *rt, const uint32_t *refs, int n);
 /* Expert parallelism (ep_world > 1): forward_layer writes this rank's partial
  * sum_k w E_k(x) over its home experts to y32 [T, H] fp32 instead of y; the
  * caller all-reduces y32 across ranks and finishes with hm_residual_add. */

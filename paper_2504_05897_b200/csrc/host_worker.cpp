@@ -204,16 +204,35 @@ void phase2(const uint16_t *img, int H, int I, const uint16_t *h, int M, float *
 // One token: dot of `n` consecutive rows (stride K) with x, in memory order --
 // a single sequential stream per thread, 4 independent accumulators, software
 // prefetch a few KB ahead.  This is the decode (host-DRAM-bound) path.
-inline void stream_rows(const uint16_t *w, int n, int K, const uint16_t *x, float *out) {
-  constexpr int kAhead = 2048;  // elements (4 KB) ahead of the current load
+// Software-prefetch distance (elements) and hint; HM_PF_DIST / HM_PF_HINT
+// (0 none, 1 T0, 2 T1, 3 NTA) override them for tuning on a new host.
+struct PfCfg {
+  int dist = 2048;
+  int hint = 1;
+};
+const PfCfg &pf_cfg() {
+  static const PfCfg c = [] {
+    PfCfg p;
+    if (const char *s = std::getenv("HM_PF_DIST")) p.dist = std::atoi(s);
+    if (const char *s = std::getenv("HM_PF_HINT")) p.hint = std::atoi(s);
+    return p;
+  }();
+  return c;
+}
+
+template <int HINT>
+inline void stream_rows_t(const uint16_t *w, int n, int K, const uint16_t *x, float *out, int ahead) {
   for (int r = 0; r < n; ++r) {
     const uint16_t *row = w + static_cast<size_t>(r) * K;
     __m512 a0 = _mm512_setzero_ps(), a1 = _mm512_setzero_ps(), a2 = _mm512_setzero_ps(),
            a3 = _mm512_setzero_ps();
     int k = 0;
     for (; k + 128 <= K; k += 128) {
-      _mm_prefetch(reinterpret_cast<const char *>(row + k + kAhead), _MM_HINT_T0);
-      _mm_prefetch(reinterpret_cast<const char *>(row + k + kAhead + 64), _MM_HINT_T0);
+      if constexpr (HINT != 0) {
+        constexpr auto hint = HINT == 1 ? _MM_HINT_T0 : (HINT == 2 ? _MM_HINT_T1 : _MM_HINT_NTA);
+        _mm_prefetch(reinterpret_cast<const char *>(row + k + ahead), hint);
+        _mm_prefetch(reinterpret_cast<const char *>(row + k + ahead + 64), hint);
+      }
       a0 = _mm512_dpbf16_ps(a0, ldbh(row + k), ldbh(x + k));
       a1 = _mm512_dpbf16_ps(a1, ldbh(row + k + 32), ldbh(x + k + 32));
       a2 = _mm512_dpbf16_ps(a2, ldbh(row + k + 64), ldbh(x + k + 64));
@@ -221,6 +240,16 @@ inline void stream_rows(const uint16_t *w, int n, int K, const uint16_t *x, floa
     }
     for (; k < K; k += 32) a0 = _mm512_dpbf16_ps(a0, ldbh(row + k), ldbh(x + k));
     out[r] = _mm512_reduce_add_ps(_mm512_add_ps(_mm512_add_ps(a0, a1), _mm512_add_ps(a2, a3)));
+  }
+}
+
+inline void stream_rows(const uint16_t *w, int n, int K, const uint16_t *x, float *out) {
+  const PfCfg &c = pf_cfg();
+  switch (c.hint) {
+    case 0: stream_rows_t<0>(w, n, K, x, out, c.dist); break;
+    case 2: stream_rows_t<2>(w, n, K, x, out, c.dist); break;
+    case 3: stream_rows_t<3>(w, n, K, x, out, c.dist); break;
+    default: stream_rows_t<1>(w, n, K, x, out, c.dist); break;
   }
 }
 
@@ -235,6 +264,35 @@ void phase1_stream(const uint16_t *img, int H, int I, const uint16_t *x, uint16_
 }
 
 }  // namespace
+
+void cpu_experts_decode(ThreadPool &pool, const uint16_t *const *imgs, const uint16_t *const *xs, int n, int H,
+                        int I, float *const *outs, std::vector<uint16_t> &hbuf) {
+  // All single-token experts of a layer in one pool run: phase 1 over every
+  // (expert, 128-pair block), one barrier, phase 2 over every (expert, row).
+  HM_REQUIRE(H % 32 == 0 && I % kIlv == 0, HM_EVALUE, "host worker needs H % 32 == 0 and I % 128 == 0");
+  if (n <= 0) return;
+  hbuf.resize(static_cast<size_t>(n) * I);
+  uint16_t *h = hbuf.data();
+  const int nblk = I / kIlv;
+  pool.run([&](int tid, int nt) {
+    const long u1 = static_cast<long>(n) * nblk;
+    for (long u = u1 * tid / nt; u < u1 * (tid + 1) / nt;) {
+      const int e = static_cast<int>(u / nblk), b0 = static_cast<int>(u % nblk);
+      const int b1 = static_cast<int>(std::min<long>(nblk, b0 + (u1 * (tid + 1) / nt - u)));
+      phase1_stream(imgs[e], H, I, xs[e], h + static_cast<size_t>(e) * I, b0, b1);
+      u += b1 - b0;
+    }
+    pool.barrier();
+    const long r1 = static_cast<long>(n) * H;
+    for (long u = r1 * tid / nt; u < r1 * (tid + 1) / nt;) {
+      const int e = static_cast<int>(u / H), j0 = static_cast<int>(u % H);
+      const int j1 = static_cast<int>(std::min<long>(H, j0 + (r1 * (tid + 1) / nt - u)));
+      const uint16_t *w2 = imgs[e] + static_cast<size_t>(2) * I * H;
+      stream_rows(w2 + static_cast<size_t>(j0) * I, j1 - j0, I, h + static_cast<size_t>(e) * I, outs[e] + j0);
+      u += j1 - j0;
+    }
+  });
+}
 
 void cpu_expert(ThreadPool &pool, const uint16_t *img, int H, int I, const uint16_t *x, int M, float *out,
                 std::vector<uint16_t> &hbuf) {
@@ -288,6 +346,14 @@ int hm_cpu_expert(hm_cpu_pool *pool, const uint16_t *img, int H, int I, const ui
   HM_API_BEGIN
   std::vector<uint16_t> hbuf;
   hm::cpu_expert(*reinterpret_cast<hm::ThreadPool *>(pool), img, H, I, x, M, out, hbuf);
+  HM_API_END
+}
+
+int hm_cpu_experts_decode(hm_cpu_pool *pool, const uint16_t *const *imgs, const uint16_t *const *xs, int n, int H,
+                          int I, float *const *outs) {
+  HM_API_BEGIN
+  std::vector<uint16_t> hbuf;
+  hm::cpu_experts_decode(*reinterpret_cast<hm::ThreadPool *>(pool), imgs, xs, n, H, I, outs, hbuf);
   HM_API_END
 }
 

@@ -40,6 +40,10 @@ class ThreadPool {
   std::atomic<bool> stop_{false};
 };
 
+// n single-token experts at once (decode): one pool run, one barrier.
+void cpu_experts_decode(ThreadPool &pool, const uint16_t *const *imgs, const uint16_t *const *xs, int n, int H,
+                        int I, float *const *outs, std::vector<uint16_t> &hbuf);
+
 // out[M, H] fp32 = W2 (silu(Wg x) * (Wu x)) for one expert image (slot layout).
 void cpu_expert(ThreadPool &pool, const uint16_t *img, int H, int I, const uint16_t *x, int M, float *out,
                 std::vector<uint16_t> &hbuf);

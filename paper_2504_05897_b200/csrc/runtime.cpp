@@ -312,13 +312,28 @@ struct Runtime {
     if (!cpu_refs.empty()) {
       RT_CUDA(cudaEventSynchronize(ev_rows));
       const double c0 = now_us();
-      for (uint32_t r : cpu_refs) {
-        const int e = ref_expert(r);
-        const size_t rb = h_offsets[e];
-        cpu_expert(*workers, image_ptr(r), H, I, h_x + rb * H, h_counts[e], h_out + rb * H, hbuf);
-        s.bytes_cpu += static_cast<int64_t>(slot_bytes);
-        ++s.n_cpu;
+      bool all_single = true;
+      for (uint32_t r : cpu_refs) all_single = all_single && h_counts[ref_expert(r)] == 1;
+      if (all_single) {  // decode: the layer's CPU experts in one worker pass
+        std::vector<const uint16_t *> imgs, xs;
+        std::vector<float *> outs;
+        for (uint32_t r : cpu_refs) {
+          const size_t rb = h_offsets[ref_expert(r)];
+          imgs.push_back(image_ptr(r));
+          xs.push_back(h_x + rb * H);
+          outs.push_back(h_out + rb * H);
+        }
+        cpu_experts_decode(*workers, imgs.data(), xs.data(), static_cast<int>(imgs.size()), H, I, outs.data(),
+                           hbuf);
+      } else {
+        for (uint32_t r : cpu_refs) {  // plan CPU order
+          const int e = ref_expert(r);
+          const size_t rb = h_offsets[e];
+          cpu_expert(*workers, image_ptr(r), H, I, h_x + rb * H, h_counts[e], h_out + rb * H, hbuf);
+        }
       }
+      s.n_cpu = static_cast<int32_t>(cpu_refs.size());
+      s.bytes_cpu = static_cast<int64_t>(cpu_refs.size()) * static_cast<int64_t>(slot_bytes);
       s.t_cpu_us = now_us() - c0;
       for (uint32_t r : cpu_refs) {
         const int e = ref_expert(r);
@@ -400,6 +415,20 @@ int hm_runtime_device_mrs(hm_runtime *rt, double *host_out) {
   auto *r = reinterpret_cast<hm::Runtime *>(rt);
   RT_CUDA(cudaDeviceSynchronize());
   RT_CUDA(cudaMemcpy(host_out, r->S_dev, static_cast<size_t>(r->L) * r->N * 8, cudaMemcpyDeviceToHost));
+  HM_API_END
+}
+
+int hm_runtime_preload(hm_runtime *rt, const uint32_t *refs, int n) {
+  HM_API_BEGIN
+  auto *r = reinterpret_cast<hm::Runtime *>(rt);
+  for (int i = 0; i < n; ++i) {
+    hm::Cache &c = r->engine->cache;
+    if (!c.is_resident(refs[i])) c.add_resident(refs[i]);
+    const int64_t slot = c.resident.at(refs[i]).slot;
+    HM_REQUIRE(slot >= 0 && slot < r->cfg.capacity, HM_EVALUE, "no free HBM slot to preload into");
+    r->issue_copy(refs[i], slot, nullptr);
+  }
+  RT_CUDA(cudaStreamSynchronize(r->copy));
   HM_API_END
 }
 

@@ -190,6 +190,20 @@ class HybridMoE:
             torch.bfloat16)
         torch.cuda.synchronize()
 
+    def preload(self, refs) -> None:
+        """Fixed residency for the baseline schedulings (engine.py:423-434):
+        make these experts resident and copy them into their HBM slots."""
+        refs = list(refs)
+        arr = (C.c_uint32 * max(1, len(refs)))(*[(int(l) << 16) | int(e) for l, e in refs])
+        check(lib.hm_runtime_preload(self._rt, arr, len(refs)))
+
+    def set_fixed_gpu_set(self, refs) -> None:
+        """fixed_frequency_map's GPU-pinned set (engine.py:195-231), made resident."""
+        refs = list(refs)
+        arr = (C.c_uint32 * max(1, len(refs)))(*[(int(l) << 16) | int(e) for l, e in refs])
+        check(lib.hm_engine_set_fixed_pinned(self.engine._h, arr, len(refs)))
+        self.preload(refs)
+
     def image_of(self, layer: int, expert: int) -> int:
         v = C.c_int64()
         check(lib.hm_runtime_image_of(self._rt, layer, expert, C.byref(v)))

@@ -1,0 +1,67 @@
+"""Host worker (AVX-512 BF16) numerics against the fp32 oracle, CPU only."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import moe_ref as ref
+
+from paper_2504_05897_b200 import _lib
+from paper_2504_05897_b200.weights import pack_expert, unpack_expert
+
+lib = _lib.lib
+pytestmark = pytest.mark.skipif(not lib.hm_cpu_has_avx512bf16(), reason="host lacks AVX-512 BF16")
+
+
+@pytest.fixture(scope="module")
+def pool():
+    p = C.c_void_p()
+    _lib.check(lib.hm_cpu_pool_create(4, C.byref(p)))
+    yield p
+    lib.hm_cpu_pool_destroy(p)
+
+
+def _expert(rng, H, I):
+    g, u, d = (ref.f32_to_bf16(rng.standard_normal(s).astype(np.float32) * 0.02) for s in ((I, H), (I, H), (H, I)))
+    return pack_expert(g, u, d), tuple(ref.bf16_to_f32(a) for a in (g, u, d))
+
+
+def test_pack_unpack_roundtrip():
+    rng = np.random.default_rng(0)
+    img, _ = _expert(rng, 64, 256)
+    g, u, d = unpack_expert(img, 64, 256)
+    assert np.array_equal(pack_expert(g, u, d), img)
+
+
+@pytest.mark.parametrize("H,I,M", [(256, 256, 1), (512, 384, 3), (512, 384, 17), (1024, 1408, 1)])
+def test_cpu_expert_matches_oracle(pool, H, I, M):
+    rng = np.random.default_rng(H + M)
+    img, ex = _expert(rng, H, I)
+    x = ref.f32_to_bf16(rng.standard_normal((M, H)).astype(np.float32))
+    out = np.empty((M, H), np.float32)
+    _lib.check(lib.hm_cpu_expert(pool, img.ctypes.data, H, I, x.ctypes.data, M, out.ctypes.data))
+    want = ref.expert(ref.bf16_to_f32(x), *ex)
+    assert np.abs(out - want).max() / np.abs(want).max() <= 1e-2
+
+
+def test_cpu_experts_decode_batch(pool):
+    rng = np.random.default_rng(9)
+    H, I, n = 512, 384, 3
+    exps = [_expert(rng, H, I) for _ in range(n)]
+    xs = [ref.f32_to_bf16(rng.standard_normal((1, H)).astype(np.float32)) for _ in range(n)]
+    outs = [np.empty((1, H), np.float32) for _ in range(n)]
+    P = C.c_void_p * n
+    _lib.check(lib.hm_cpu_experts_decode(pool, P(*[e[0].ctypes.data for e in exps]), P(*[x.ctypes.data for x in xs]),
+                                         n, H, I, P(*[o.ctypes.data for o in outs])))
+    for (img, ex), x, o in zip(exps, xs, outs):
+        want = ref.expert(ref.bf16_to_f32(x), *ex)
+        assert np.abs(o - want).max() / np.abs(want).max() <= 1e-2
+
+
+def test_host_read_bandwidth_probe(pool):
+    buf = np.zeros(1 << 24, dtype=np.uint8)
+    gbs = C.c_double()
+    _lib.check(lib.hm_host_read_bw(pool, buf.ctypes.data, buf.nbytes, 2, C.byref(gbs)))
+    assert gbs.value > 0
