@@ -282,8 +282,12 @@ def run_ours(args) -> None:
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    # HM_NCU_TIMED=1: bracket the timed region for `ncu --profile-from-start off`
+    ncu_timed = os.environ.get("HM_NCU_TIMED") == "1"
     with ClockSampler(local) as clocks:
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if ncu_timed:
+            torch.cuda.profiler.start()
         t0.record(st)
         for k in range(args.steps):
             p = 1 + args.warmup + k
@@ -292,6 +296,8 @@ def run_ours(args) -> None:
         t1.record(st)
         t1.synchronize()
         torch.cuda.synchronize()
+        if ncu_timed:
+            torch.cuda.profiler.stop()
     if dist:
         dist.barrier()
     launches = lib.hm_launch_count() - launches0

@@ -351,6 +351,8 @@ void hm_cpu_pool_destroy(hm_cpu_pool *p);
 int hm_cpu_expert(hm_cpu_pool *pool, const uint16_t *img, int H, int I, const uint16_t *x, int M,
                   float *out);
 int hm_cpu_has_avx512bf16(void);
+/* Decode-stream tuning: software prefetch distance (elements) and hint (0 none, 1 T0, 2 T1, 3 NTA). */
+int hm_cpu_set_prefetch(int dist, int hint);
 /* n single-token experts in one worker pass (decode): outs[i][H] = expert(imgs[i])(xs[i][H]). */
 int hm_cpu_experts_decode(hm_cpu_pool *pool, const uint16_t *const *imgs, const uint16_t *const *xs, int n,
                           int H, int I, float *const *outs);

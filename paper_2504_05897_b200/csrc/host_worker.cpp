@@ -210,8 +210,8 @@ struct PfCfg {
   int dist = 2048;
   int hint = 1;
 };
-const PfCfg &pf_cfg() {
-  static const PfCfg c = [] {
+PfCfg &pf_cfg() {
+  static PfCfg c = [] {
     PfCfg p;
     if (const char *s = std::getenv("HM_PF_DIST")) p.dist = std::atoi(s);
     if (const char *s = std::getenv("HM_PF_HINT")) p.hint = std::atoi(s);
@@ -358,6 +358,16 @@ int hm_cpu_experts_decode(hm_cpu_pool *pool, const uint16_t *const *imgs, const 
 }
 
 int hm_cpu_has_avx512bf16(void) { return __builtin_cpu_supports("avx512bf16") ? 1 : 0; }
+
+// Tuning knob for the decode stream: software-prefetch distance (bf16
+// elements) and hint (0 none, 1 T0, 2 T1, 3 NTA).  Process-wide.
+int hm_cpu_set_prefetch(int dist, int hint) {
+  HM_API_BEGIN
+  HM_REQUIRE(dist >= 0 && hint >= 0 && hint <= 3, HM_EVALUE, "bad prefetch setting");
+  hm::pf_cfg().dist = dist;
+  hm::pf_cfg().hint = hint;
+  HM_API_END
+}
 
 // Host DRAM read bandwidth with the worker pool (the host roofline denominator).
 int hm_host_read_bw(hm_cpu_pool *pool, const void *p, size_t bytes, int reps, double *gbs) {

@@ -247,7 +247,12 @@ class HybridMoE:
         self.engine.begin_pass()
         for l in range(self.L):
             lg = logits[l] if logits is not None else self._model_logits(cur, l, st)
-            preds = predict(l) if (predict is not None and self.policy.prefetch) else []
+            if not self.policy.prefetch:
+                preds = []
+            elif predict == "live":  # gate look-ahead on the current hidden state
+                preds = self.lookahead(cur, l, stream=st)
+            else:
+                preds = predict(l) if predict is not None else []
             pl = np.array([p.layer for p in preds], dtype=np.int32)
             pload = np.zeros((max(1, len(preds)), self.N), dtype=np.int64)
             for d, p in enumerate(preds):
@@ -281,6 +286,26 @@ class HybridMoE:
         r = self.engine.end_pass()
         info = {"stats": stats, "records": records, "requests": requests, "layers": layers_io, "pass": r}
         return cur, info
+
+    def lookahead(self, x: torch.Tensor, layer: int, horizon: int | None = None, stream=None):
+        """Live-mode prediction: the gates of layers
+        l+1..l+H applied to the current hidden state give the predicted
+        LayerRequests the prefetch decision evaluates (prefetch.py:104-143)."""
+        from .core import LayerRequest
+        from .kernels import router_logits, router_topk
+
+        if self.gate_w is None:
+            raise RuntimeError("live prediction needs gate weights (init_random_weights)")
+        hz = self.policy.prediction.horizon if horizon is None else horizon
+        last = min(layer + hz, self.L - 1)
+        out = []
+        for fl in range(layer + 1, last + 1):
+            lg = router_logits(x, self.gate_w[fl], stream=stream)
+            _, _, _, counts = router_topk(lg, self.N, self.K, self.family.renormalize, 0, -1, stream=stream)
+            loads = counts.cpu().numpy().astype(np.int64)
+            out.append(LayerRequest(layer=fl, loads=tuple(int(v) for v in loads), scores=(),
+                                    activated=frozenset(int(i) for i in np.nonzero(loads)[0])))
+        return out
 
     def _model_logits(self, x: torch.Tensor, layer: int, st) -> torch.Tensor:
         from .kernels import router_logits

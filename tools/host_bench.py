@@ -1,7 +1,10 @@
-"""Host worker GB/s for Mixtral-shaped experts at decode (M=1): single expert and
-a layer's batch of 2, per thread count (prefetch knobs via HM_PF_DIST / HM_PF_HINT)."""
+"""Host worker GB/s for Mixtral-shaped experts at decode (M=1): interleaved
+variants (prefetch distance/hint x thread count) in one process, each next to
+a fresh stream-read measurement, so host-memory noise hits all variants alike.
+
+  python tools/host_bench.py [rounds]
+"""
 import ctypes as C
-import os
 import sys
 import time
 from pathlib import Path
@@ -17,27 +20,35 @@ lib = _lib.lib
 store = np.random.default_rng(0).integers(0, 1 << 14, size=(n_img, 3 * H * I), dtype=np.uint16)
 x = np.full((4, H), 0x3F80, np.uint16)
 out = np.empty((4, H), np.float32)
-tag = f"dist={os.environ.get('HM_PF_DIST', 'def')} hint={os.environ.get('HM_PF_HINT', 'def')}"
-for nt in [int(a) for a in (sys.argv[1:] or ["16"])]:
-    pool = C.c_void_p()
-    lib.hm_cpu_pool_create(nt, C.byref(pool))
-    bw = C.c_double()
-    lib.hm_host_read_bw(pool, store.ctypes.data, store.nbytes, 3, C.byref(bw))
-    lib.hm_cpu_expert(pool, store[0].ctypes.data, H, I, x.ctypes.data, 1, out.ctypes.data)
-    reps = 16
-    t = time.perf_counter()
-    for r in range(reps):
-        lib.hm_cpu_expert(pool, store[r % n_img].ctypes.data, H, I, x.ctypes.data, 1, out.ctypes.data)
-    dt = (time.perf_counter() - t) / reps
-    imgs = (C.c_void_p * 2)()
-    xs = (C.c_void_p * 2)(x[0:1].ctypes.data, x[1:2].ctypes.data)
-    outs = (C.c_void_p * 2)(out[0:1].ctypes.data, out[1:2].ctypes.data)
-    t = time.perf_counter()
-    for r in range(reps // 2):
-        imgs[0], imgs[1] = store[(2 * r) % n_img].ctypes.data, store[(2 * r + 1) % n_img].ctypes.data
-        lib.hm_cpu_experts_decode(pool, imgs, xs, 2, H, I, outs)
-    dt2 = (time.perf_counter() - t) / reps
-    print(f"[{tag}] threads {nt}: single {dt * 1e3:.3f} ms/expert {store[0].nbytes / dt / 1e9:.1f} GB/s | "
-          f"batch-2 {dt2 * 1e3:.3f} ms/expert {store[0].nbytes / dt2 / 1e9:.1f} GB/s | "
-          f"stream-read {bw.value:.1f} GB/s", flush=True)
-    lib.hm_cpu_pool_destroy(pool)
+rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+variants = [(16, 2048, 1), (16, 0, 0), (16, 4096, 2), (16, 8192, 2), (16, 16384, 2), (15, 2048, 1), (15, 8192, 2),
+            (14, 8192, 2)]
+pools = {}
+for nt in sorted({v[0] for v in variants}):
+    p = C.c_void_p()
+    lib.hm_cpu_pool_create(nt, C.byref(p))
+    pools[nt] = p
+res = {v: [] for v in variants}
+for rnd in range(rounds):
+    for v in variants:
+        nt, dist, hint = v
+        lib.hm_cpu_set_prefetch(dist, hint)
+        bw = C.c_double()
+        lib.hm_host_read_bw(pools[nt], store.ctypes.data, store.nbytes, 2, C.byref(bw))
+        imgs = (C.c_void_p * 2)()
+        xs = (C.c_void_p * 2)(x[0:1].ctypes.data, x[1:2].ctypes.data)
+        outs = (C.c_void_p * 2)(out[0:1].ctypes.data, out[1:2].ctypes.data)
+        reps = 12
+        t = time.perf_counter()
+        for r in range(reps // 2):
+            imgs[0], imgs[1] = store[(2 * r) % n_img].ctypes.data, store[(2 * r + 1) % n_img].ctypes.data
+            lib.hm_cpu_experts_decode(pools[nt], imgs, xs, 2, H, I, outs)
+        dt = (time.perf_counter() - t) / reps
+        res[v].append((store[0].nbytes / dt / 1e9, bw.value))
+for v, r in res.items():
+    gb = [a for a, _ in r]
+    sr = [b for _, b in r]
+    print(f"threads {v[0]:2d} pf_dist {v[1]:5d} hint {v[2]}: expert {np.median(gb):6.1f} GB/s "
+          f"(min {min(gb):6.1f}) | stream-read {np.median(sr):6.1f} GB/s | ratio {np.median(gb) / np.median(sr):.2f}")
+for p in pools.values():
+    lib.hm_cpu_pool_destroy(p)

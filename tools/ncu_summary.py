@@ -32,13 +32,34 @@ METRICS = [
 ]
 
 
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "nsecond": 1e-9, "usecond": 1e-6,
+        "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0, "B": 1, "KB": 1e3,
+        "MB": 1e6, "GB": 1e9}
+
+
 def raw(rep: str) -> list[dict]:
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     if len(rows) < 3:
         return []
-    head = rows[0]
-    return [dict(zip(head, r)) for r in rows[2:]]
+    head, units = rows[0], rows[1]
+    recs = []
+    for r in rows[2:]:
+        d = dict(zip(head, r))
+        d["__units__"] = dict(zip(head, units))
+        recs.append(d)
+    return recs
+
+
+def num(rec: dict, key: str) -> float | None:
+    v = rec.get(key)
+    if v is None:
+        return None
+    try:
+        f = float(v.replace(",", ""))
+    except ValueError:
+        return None
+    return f * UNIT.get(rec["__units__"].get(key, ""), 1.0)
 
 
 def fmt(v: str) -> str:
@@ -61,16 +82,13 @@ def summarise_rep(rep: str) -> str:
         for m in METRICS:
             for k in r:
                 if k == m or k.startswith(m + " "):
-                    lines.append(f"| {k} | {fmt(r[k])} |")
+                    lines.append(f"| {k} | {fmt(r[k])} {r['__units__'].get(k, '')} |")
                     break
-        rd, wr, t = (r.get("dram__bytes_read.sum"), r.get("dram__bytes_write.sum"), r.get("gpu__time_duration.sum"))
-        try:
-            traffic = float(rd.replace(",", "")) + float(wr.replace(",", ""))
-            lines.append(f"| dram traffic (read+write) | {traffic:,.0f} B |")
+        rd, wr, t = num(r, "dram__bytes_read.sum"), num(r, "dram__bytes_write.sum"), num(r, "gpu__time_duration.sum")
+        if rd is not None and wr is not None:
+            lines.append(f"| **dram traffic (read+write)** | **{rd + wr:,.0f} B** |")
             if t:
-                lines.append(f"| dram GB/s (traffic / duration) | {traffic / float(t.replace(',', '')):,.1f} |")
-        except (AttributeError, ValueError):
-            pass
+                lines.append(f"| dram GB/s (traffic / duration) | {(rd + wr) / t / 1e9:,.1f} |")
         lines.append("")
     return "\n".join(lines)
 
