@@ -206,9 +206,9 @@ void phase2(const uint16_t *img, int H, int I, const uint16_t *h, int M, float *
 // prefetch a few KB ahead.  This is the decode (host-DRAM-bound) path.
 // Software-prefetch distance (elements) and hint; HM_PF_DIST / HM_PF_HINT
 // (0 none, 1 T0, 2 T1, 3 NTA) override them for tuning on a new host.
-struct PfCfg {
-  int dist = 2048;
-  int hint = 1;
+struct PfCfg {  // tuned on the B200 box's host (tools/host_bench.py): L2 hint, 32 KB ahead
+  int dist = 16384;
+  int hint = 2;
 };
 PfCfg &pf_cfg() {
   static PfCfg c = [] {
@@ -230,8 +230,11 @@ inline void stream_rows_t(const uint16_t *w, int n, int K, const uint16_t *x, fl
     for (; k + 128 <= K; k += 128) {
       if constexpr (HINT != 0) {
         constexpr auto hint = HINT == 1 ? _MM_HINT_T0 : (HINT == 2 ? _MM_HINT_T1 : _MM_HINT_NTA);
-        _mm_prefetch(reinterpret_cast<const char *>(row + k + ahead), hint);
-        _mm_prefetch(reinterpret_cast<const char *>(row + k + ahead + 64), hint);
+        const char *pf = reinterpret_cast<const char *>(row + k + ahead);  // the 4 lines of this step
+        _mm_prefetch(pf, hint);
+        _mm_prefetch(pf + 64, hint);
+        _mm_prefetch(pf + 128, hint);
+        _mm_prefetch(pf + 192, hint);
       }
       a0 = _mm512_dpbf16_ps(a0, ldbh(row + k), ldbh(x + k));
       a1 = _mm512_dpbf16_ps(a1, ldbh(row + k + 32), ldbh(x + k + 32));

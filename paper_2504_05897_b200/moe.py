@@ -190,6 +190,27 @@ class HybridMoE:
             torch.bfloat16)
         torch.cuda.synchronize()
 
+    def init_seeded_weights(self, base_seed: int = 0) -> None:
+        """Per-expert seeded init (torch.Generator seed 1000*layer +
+        expert): the same expert gets the same weights on any rank count, so an
+        expert-parallel run can be compared with a single-GPU one."""
+        n = self.slot_elems
+        for l in range(self.L):
+            for e in range(self.N):
+                if e % self.ep_world != self.ep_rank:
+                    continue
+                g = torch.Generator(device="cuda").manual_seed(base_seed + 1000 * l + e)
+                self.store_t[self.image_of(l, e)].copy_(
+                    (torch.randn(n, generator=g, device="cuda") * 0.02).to(torch.bfloat16))
+            for c in range(self.S):
+                g = torch.Generator(device="cuda").manual_seed(base_seed + 1000 * l + self.N + c)
+                self.pool[self.shared_slot(l, c)].copy_(
+                    (torch.randn(n, generator=g, device="cuda") * 0.02).to(torch.bfloat16))
+        g = torch.Generator(device="cuda").manual_seed(base_seed + 999_999)
+        self.gate_w = (torch.randn((self.L, self.ld, self.H), generator=g, device="cuda") / math.sqrt(self.H)).to(
+            torch.bfloat16)
+        torch.cuda.synchronize()
+
     def preload(self, refs) -> None:
         """Fixed residency for the baseline schedulings (engine.py:423-434):
         make these experts resident and copy them into their HBM slots."""

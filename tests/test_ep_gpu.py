@@ -1,0 +1,88 @@
+"""Expert parallelism through the real runtime: two ranks (processes) sharing
+the one GPU of this environment, exchanging partial expert sums with gloo, must
+reproduce the single-rank layer stack; each rank's LayerRequest is the
+rank-masked one."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(rank: int, world: int, port: int, q) -> None:
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    import torch.distributed as dist
+
+    import paper_2504_05897_b200.core as mcore
+    import paper_2504_05897_b200.costs as mcost
+    from paper_2504_05897_b200.engine import EnginePolicy
+    from paper_2504_05897_b200.moe import SHAPES, HybridMoE
+    from paper_2504_05897_b200.tracegen import GenParams, generate_router_logits
+
+    torch.cuda.set_device(0)
+    if world > 1:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = SHAPES["tiny"]
+        eb = mcore.expert_bytes(cfg)
+        prof = mcost.HardwareProfile(gpu_time_per_expert=1.0, cpu_slope=2.0, transfer_bandwidth=eb / 0.5)
+        moe = HybridMoE(cfg, "tiny", EnginePolicy(), 0.5, prof, max_tokens=48, ep_rank=rank, ep_world=world)
+        moe.init_seeded_weights(7)
+        trace, logits = generate_router_logits(cfg, GenParams(seed=3), 32, 3)
+        g = torch.Generator(device="cuda").manual_seed(5)
+        outs, loads = [], []
+        for p, fwd in enumerate(trace.passes):
+            lg = [torch.from_numpy(np.ascontiguousarray(logits[p][l], dtype=np.float32)).cuda()
+                  for l in range(cfg.num_layers)]
+            x = torch.randn((fwd.token_count, moe.H), generator=g, device="cuda").to(torch.bfloat16)
+            y, info = moe.forward_pass(x, lg, decision_log=True)
+            torch.cuda.synchronize()
+            outs.append(y.float().cpu().numpy())
+            loads.append([r[0].tolist() for r in info["requests"]])
+        q.put((rank, world, outs, loads, moe.capacity))
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+def test_two_ranks_equal_one_rank():
+    ctx = torch.multiprocessing.get_context("spawn")
+    q = ctx.Queue()
+    single = ctx.Process(target=_run, args=(0, 1, 0, q))
+    single.start()
+    single.join(timeout=300)
+    ref = q.get(timeout=10)
+    port = _free_port()
+    procs = [ctx.Process(target=_run, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    got = dict((r[0], r) for r in (q.get(timeout=10), q.get(timeout=10)))
+    assert single.exitcode == 0 and all(p.exitcode == 0 for p in procs)
+    _, _, ref_outs, ref_loads, ref_cap = ref
+    assert got[0][4] + got[1][4] == ref_cap                      # global budget split across ranks
+    for r in (0, 1):
+        for p, (o_ref, o) in enumerate(zip(ref_outs, got[r][2])):
+            err = np.abs(o - o_ref).max() / np.abs(o_ref).max()
+            assert err <= 1e-2, (r, p, err)
+        for p in range(len(ref_loads)):
+            for l, full in enumerate(ref_loads[p]):
+                masked = [v if e % 2 == r else 0 for e, v in enumerate(full)]
+                assert got[r][3][p][l] == masked

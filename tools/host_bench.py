@@ -21,8 +21,8 @@ store = np.random.default_rng(0).integers(0, 1 << 14, size=(n_img, 3 * H * I), d
 x = np.full((4, H), 0x3F80, np.uint16)
 out = np.empty((4, H), np.float32)
 rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-variants = [(16, 2048, 1), (16, 0, 0), (16, 4096, 2), (16, 8192, 2), (16, 16384, 2), (15, 2048, 1), (15, 8192, 2),
-            (14, 8192, 2)]
+variants = [(16, 16384, 2), (16, 0, 0), (16, 8192, 2), (16, 32768, 2), (16, 16384, 1), (16, 65536, 2),
+            (15, 16384, 2)]
 pools = {}
 for nt in sorted({v[0] for v in variants}):
     p = C.c_void_p()
