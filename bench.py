@@ -193,17 +193,29 @@ def run_ours(args) -> None:
     pk, pk_kind = peaks()
     t_setup = time.time()
     from paper_2504_05897_b200.costs import load_profile, save_profile
+    # Stage-calibrated profiles: the reference's cost model is linear in load
+    # (costs.py:68-88), but the host worker is DRAM-bound at decode loads (1-4
+    # tokens) and compute-bound (AMX) at prefill loads, so one fit cannot serve
+    # both; the decode profile is fitted at decode loads, the prefill profile
+    # at prefill loads, and each pass is planned with its stage's profile.
     if args.profile_file:  # e.g. for runs under a profiler, where warm-up timings are distorted
         base_profile = load_profile(args.profile_file)
+        prefill_profile = load_profile(args.prefill_profile_file) if args.prefill_profile_file else base_profile
     else:
         base_profile = calibrate_shape(H, I)[0].profile
+        prefill_profile = base_profile
+        if args.stage_profiles:
+            prefill_profile = calibrate_shape(H, I, cpu_loads=(64, 128, 256), cpu_bursts=1,
+                                              gpu_loads=(64, 128, 256, 384, 512))[0].profile
         if args.save_profile and rank == 0:
             save_profile(base_profile, args.save_profile)
+            save_profile(prefill_profile, args.save_profile + ".prefill")
 
     class _Cal:
         profile = base_profile
     cal = _Cal()
     prof = with_shared_time(cal.profile, cfg)
+    prof_prefill = with_shared_time(prefill_profile, cfg)
     policy = EnginePolicy(scheduling=args.scheduling, cache_policy=args.policy, prefetch=args.prefetch)
     # expert parallelism over the ranks of this box: one replicated sequence, each
     # rank homes experts e % world, host bytes and worker cores split by rank
@@ -261,7 +273,9 @@ def run_ours(args) -> None:
     # ---- prefill: 1k tokens, cold cache (the reference's TTFT, engine.py:465-466)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(st)
+    moe.set_profile(prof_prefill)
     _, pinfo = moe.forward_pass(xs[0], dev_logits[0], predict=predictor(0))
+    moe.set_profile(prof)
     ev1.record(st)
     ev1.synchronize()
     prefill_ms = ev0.elapsed_time(ev1)
@@ -403,6 +417,8 @@ def run_ours(args) -> None:
             "profile": {k: getattr(cal.profile, k) for k in ("gpu_time_per_expert", "cpu_slope", "transfer_bandwidth",
                                                               "transfer_latency", "gpu_slope",
                                                               "cpu_first_expert_penalty")},
+            "prefill_profile": {k: getattr(prefill_profile, k) for k in ("gpu_time_per_expert", "cpu_slope",
+                                                                          "gpu_slope", "cpu_first_expert_penalty")},
             "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks.summary(), "parity": parity,
             "setup_s": setup_s,
         }
@@ -432,6 +448,9 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-file", default=None, help="HardwareProfile key=value file instead of calibrating")
     ap.add_argument("--save-profile", default=None, help="write the calibrated HardwareProfile here")
+    ap.add_argument("--prefill-profile-file", default=None)
+    ap.add_argument("--stage-profiles", action=argparse.BooleanOptionalAction, default=True,
+                    help="calibrate a separate prefill-load profile for the prefill pass")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

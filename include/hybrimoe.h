@@ -235,6 +235,9 @@ int hm_engine_create(const hm_engine_config *cfg, const hm_profile *p, hm_cache 
 void hm_engine_destroy(hm_engine *e);
 /* fixed_frequency_map GPU set (engine.py:195-231); residency is the caller's. */
 int hm_engine_set_fixed_pinned(hm_engine *e, const uint32_t *refs, int n);
+/* Replace the profile between passes (stage-calibrated profiles: a decode
+ * profile and a prefill profile); also resets the evaluator's memo. */
+int hm_engine_set_profile(hm_engine *e, const hm_profile *p);
 int hm_engine_begin_pass(hm_engine *e);
 /* One layer of run_pass in the exact engine.py:288-389 order.  `pred_*` are
  * the predicted future LayerRequests (prefetch.py:54-101), concatenated:

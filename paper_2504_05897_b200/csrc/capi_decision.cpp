@@ -402,6 +402,16 @@ int hm_engine_set_fixed_pinned(hm_engine *e, const uint32_t *refs, int n) {
   for (int i = 0; i < n; ++i) en->fixed_pinned.insert(refs[i]);
   HM_API_END
 }
+int hm_engine_set_profile(hm_engine *e, const hm_profile *p) {
+  HM_API_BEGIN
+  hm::check_profile(*p);
+  hm::Engine *en = E(e);
+  en->profile = *p;
+  en->evaluator.profile = *p;
+  en->evaluator.memo.clear();  // memoised makespans belong to the old profile
+  HM_API_END
+}
+
 int hm_engine_begin_pass(hm_engine *e) {
   HM_API_BEGIN
   E(e)->begin_pass();

@@ -7,6 +7,8 @@
 // Decode (1 token) is a DRAM-bandwidth-bound GEMV split over all threads;
 // prefill blocks 16 weight rows x 4 tokens so weights are reused from L2.
 #include <immintrin.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -266,7 +268,168 @@ void phase1_stream(const uint16_t *img, int H, int I, const uint16_t *x, uint16_
   }
 }
 
+// ------------------------------------------------------------ AMX (prefill)
+// Multi-token experts on the AMX tile unit: out^T = W . X^T with A = 16 weight
+// rows x 32 K (row-major, loaded straight from the image) and B = 16 token
+// pairs x 16 tokens in VNNI order (x and h are repacked once per expert).
+// Register blocking: 2 A x 2 B -> 4 fp32 C tiles (tiles 0-3 C, 4-5 A, 6-7 B).
+struct alignas(64) TileCfg {
+  uint8_t palette = 1;
+  uint8_t start_row = 0;
+  uint8_t reserved[14] = {};
+  uint16_t colsb[16] = {};
+  uint8_t rows[16] = {};
+};
+
+// exp(x) for 16 floats: 2^n * p(r), |r| <= ln2/2, degree-6 polynomial (rel err ~1e-7).
+inline __m512 exp16(__m512 x) {
+  x = _mm512_max_ps(_mm512_min_ps(x, _mm512_set1_ps(88.0f)), _mm512_set1_ps(-88.0f));
+  const __m512 n = _mm512_roundscale_ps(_mm512_mul_ps(x, _mm512_set1_ps(1.4426950408889634f)), _MM_FROUND_TO_NEAREST_INT);
+  const __m512 r = _mm512_fnmadd_ps(n, _mm512_set1_ps(0.6931471805599453f), x);
+  __m512 p = _mm512_set1_ps(1.0f / 720.0f);
+  p = _mm512_fmadd_ps(p, r, _mm512_set1_ps(1.0f / 120.0f));
+  p = _mm512_fmadd_ps(p, r, _mm512_set1_ps(1.0f / 24.0f));
+  p = _mm512_fmadd_ps(p, r, _mm512_set1_ps(1.0f / 6.0f));
+  p = _mm512_fmadd_ps(p, r, _mm512_set1_ps(0.5f));
+  p = _mm512_fmadd_ps(p, r, _mm512_set1_ps(1.0f));
+  p = _mm512_fmadd_ps(p, r, _mm512_set1_ps(1.0f));
+  return _mm512_scalef_ps(p, n);
+}
+
+// silu(g) * u for 16 lanes
+inline __m512 silu_mul16(const float *g, const float *u) {
+  const __m512 gv = _mm512_loadu_ps(g);
+  const __m512 den = _mm512_add_ps(_mm512_set1_ps(1.0f), exp16(_mm512_sub_ps(_mm512_setzero_ps(), gv)));
+  return _mm512_mul_ps(_mm512_div_ps(gv, den), _mm512_loadu_ps(u));
+}
+
+// two 16-float rows -> 32 bf16 interleaved (a0 b0 a1 b1 ...), round to nearest even
+inline __m512i interleave_bf16(__m512 a, __m512 b) {
+  const __m512i v = _mm512_inserti64x4(_mm512_castsi256_si512((__m256i)_mm512_cvtneps_pbh(a)),
+                                       (__m256i)_mm512_cvtneps_pbh(b), 1);
+  const __m512i idx = _mm512_set_epi16(31, 15, 30, 14, 29, 13, 28, 12, 27, 11, 26, 10, 25, 9, 24, 8, 23, 7, 22, 6,
+                                       21, 5, 20, 4, 19, 3, 18, 2, 17, 1, 16, 0);
+  return _mm512_permutexvar_epi16(idx, v);
+}
+
+bool amx_enable() {  // Linux: request the XTILEDATA permission once per process
+  static const bool ok = [] {
+    if (!__builtin_cpu_supports("amx-bf16")) return false;
+    constexpr long kReqPerm = 0x1023, kXtileData = 18;
+    return syscall(SYS_arch_prctl, kReqPerm, kXtileData) == 0;
+  }();
+  return ok;
+}
+
+inline void amx_config() {
+  static thread_local bool done = false;
+  if (done) return;
+  TileCfg c;
+  for (int t = 0; t < 8; ++t) {
+    c.colsb[t] = 64;
+    c.rows[t] = 16;
+  }
+  _tile_loadconfig(&c);
+  done = true;
+}
+
+// VNNI repack: src [M, K] bf16 rows -> dst [K/2][Mpad][2] (zero-padded tokens).
+void vnni_pack(const uint16_t *src, int M, int K, int Mpad, uint16_t *dst) {
+  std::memset(dst, 0, static_cast<size_t>(K) * Mpad * 2);
+  for (int t = 0; t < M; ++t)
+    for (int k = 0; k < K; ++k) dst[(static_cast<size_t>(k >> 1) * Mpad + t) * 2 + (k & 1)] = src[static_cast<size_t>(t) * K + k];
+}
+
+// C[a][b] (16 rows of A-block a x 16 tokens of B-block b) over the full K for
+// two weight row blocks (wa0, wa1; stride ldw bytes) and token blocks tb0, tb0+16.
+inline void amx_block(const uint16_t *wa0, const uint16_t *wa1, size_t ldw, const uint16_t *xv, int Mpad, int tb0,
+                      bool two_b, int K, float (*c)[16][16]) {
+  _tile_zero(0);
+  _tile_zero(1);
+  _tile_zero(2);
+  _tile_zero(3);
+  const size_t ldb = static_cast<size_t>(Mpad) * 4;
+  for (int k = 0; k < K; k += 32) {
+    _tile_loadd(4, wa0 + k, ldw);
+    _tile_loadd(5, wa1 + k, ldw);
+    const uint16_t *b = xv + (static_cast<size_t>(k >> 1) * Mpad + tb0) * 2;
+    _tile_loadd(6, b, ldb);
+    _tile_dpbf16ps(0, 4, 6);
+    _tile_dpbf16ps(2, 5, 6);
+    if (two_b) {
+      _tile_loadd(7, b + 32, ldb);
+      _tile_dpbf16ps(1, 4, 7);
+      _tile_dpbf16ps(3, 5, 7);
+    }
+  }
+  _tile_stored(0, c[0], 64);
+  _tile_stored(2, c[2], 64);
+  if (two_b) {
+    _tile_stored(1, c[1], 64);
+    _tile_stored(3, c[3], 64);
+  }
+}
+
 }  // namespace
+
+bool amx_available() { return amx_enable(); }
+
+void cpu_expert_amx(ThreadPool &pool, const uint16_t *img, int H, int I, const uint16_t *x, int M, float *out,
+                    std::vector<uint16_t> &scratch) {
+  const int Mpad = (M + 15) / 16 * 16;
+  scratch.resize(static_cast<size_t>(H) * Mpad + static_cast<size_t>(I) * Mpad);
+  uint16_t *xv = scratch.data();
+  uint16_t *hv = xv + static_cast<size_t>(H) * Mpad;
+  vnni_pack(x, M, H, Mpad, xv);
+  std::memset(hv, 0, static_cast<size_t>(I) * Mpad * 2);
+  const uint16_t *w2 = img + static_cast<size_t>(2) * I * H;
+  const int nb = Mpad / 16;
+  pool.run([&](int tid, int nt) {
+    amx_config();
+    float c[4][16][16];
+    // phase 1: 16-output blocks of gate rows with their up rows (128-row interleave)
+    const int ob = I / 16;
+    for (int o = ob * tid / nt; o < ob * (tid + 1) / nt; ++o) {
+      const int i0 = o * 16;
+      const size_t grow = static_cast<size_t>((i0 / kIlv) * 2 * kIlv + i0 % kIlv);
+      const uint16_t *wg = img + grow * H, *wu = img + (grow + kIlv) * H;
+      for (int b = 0; b < nb; b += 2) {
+        const bool two = b + 1 < nb;
+        amx_block(wg, wu, static_cast<size_t>(H) * 2, xv, Mpad, b * 16, two, H, c);
+        for (int bb = 0; bb < (two ? 2 : 1); ++bb) {
+          const int tok0 = (b + bb) * 16;
+          const __mmask16 live = tok0 + 16 <= M ? 0xFFFF : static_cast<__mmask16>((1u << (M - tok0)) - 1u);
+          for (int r = 0; r < 16; r += 2) {  // rows r, r+1 -> one 64-byte VNNI row of hv
+            const __m512 h0 = _mm512_maskz_mov_ps(live, silu_mul16(c[bb][r], c[2 + bb][r]));
+            const __m512 h1 = _mm512_maskz_mov_ps(live, silu_mul16(c[bb][r + 1], c[2 + bb][r + 1]));
+            _mm512_storeu_si512(hv + (static_cast<size_t>((i0 + r) >> 1) * Mpad + tok0) * 2, interleave_bf16(h0, h1));
+          }
+        }
+      }
+    }
+    pool.barrier();
+    // phase 2: pairs of 16-row blocks of W2
+    const int rb = H / 16;
+    const int pairs = (rb + 1) / 2;
+    for (int q = pairs * tid / nt; q < pairs * (tid + 1) / nt; ++q) {
+      const int j0 = q * 32;
+      const bool second = j0 + 16 < H;
+      const uint16_t *wa0 = w2 + static_cast<size_t>(j0) * I;
+      const uint16_t *wa1 = second ? wa0 + static_cast<size_t>(16) * I : wa0;
+      for (int b = 0; b < nb; b += 2) {
+        const bool two = b + 1 < nb;
+        amx_block(wa0, wa1, static_cast<size_t>(I) * 2, hv, Mpad, b * 16, two, I, c);
+        for (int a = 0; a < (second ? 2 : 1); ++a)
+          for (int bb = 0; bb < (two ? 2 : 1); ++bb)
+            for (int r = 0; r < 16; ++r)
+              for (int t = 0; t < 16; ++t) {
+                const int tok = (b + bb) * 16 + t;
+                if (tok < M) out[static_cast<size_t>(tok) * H + j0 + a * 16 + r] = c[a * 2 + bb][r][t];
+              }
+      }
+    }
+  });
+}
 
 void cpu_experts_decode(ThreadPool &pool, const uint16_t *const *imgs, const uint16_t *const *xs, int n, int H,
                         int I, float *const *outs, std::vector<uint16_t> &hbuf) {
@@ -315,6 +478,10 @@ void cpu_expert(ThreadPool &pool, const uint16_t *img, int H, int I, const uint1
       const int j1 = static_cast<int>(static_cast<long>(H) * (tid + 1) / nt);
       if (j0 < j1) stream_rows(w2 + static_cast<size_t>(j0) * I, j1 - j0, I, h, out + j0);
     });
+    return;
+  }
+  if (M >= 8 && amx_available()) {  // prefill-sized token groups: AMX tiles
+    cpu_expert_amx(pool, img, H, I, x, M, out, hbuf);
     return;
   }
   pool.run([&](int tid, int nt) {

@@ -40,6 +40,12 @@ class ThreadPool {
   std::atomic<bool> stop_{false};
 };
 
+// AMX path for multi-token experts (prefill); amx_available() requests the
+// XTILEDATA permission on first use.
+bool amx_available();
+void cpu_expert_amx(ThreadPool &pool, const uint16_t *img, int H, int I, const uint16_t *x, int M, float *out,
+                    std::vector<uint16_t> &scratch);
+
 // n single-token experts at once (decode): one pool run, one barrier.
 void cpu_experts_decode(ThreadPool &pool, const uint16_t *const *imgs, const uint16_t *const *xs, int n, int H,
                         int I, float *const *outs, std::vector<uint16_t> &hbuf);

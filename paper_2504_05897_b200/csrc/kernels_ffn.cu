@@ -341,7 +341,27 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2D bf16 tensor [outer, inner] with a (64 x box_rows) box and 128-byte swizzle.
+// Encoded maps are cached by (base, inner, outer, box): the pool and the
+// activation buffers are fixed, so steady state does no host-side encoding.
+CUtensorMap make_map_uncached(const void *base, uint64_t inner, uint64_t outer, uint32_t box_rows);
 CUtensorMap make_map(const void *base, uint64_t inner, uint64_t outer, uint32_t box_rows) {
+  struct Key {
+    const void *b;
+    uint64_t i, o;
+    uint32_t r;
+  };
+  static std::mutex mu;
+  static std::vector<std::pair<Key, CUtensorMap>> cache;
+  std::lock_guard<std::mutex> g(mu);
+  for (auto &kv : cache)
+    if (kv.first.b == base && kv.first.i == inner && kv.first.o == outer && kv.first.r == box_rows) return kv.second;
+  CUtensorMap m = make_map_uncached(base, inner, outer, box_rows);
+  if (cache.size() >= 64) cache.erase(cache.begin());
+  cache.push_back({Key{base, inner, outer, box_rows}, m});
+  return m;
+}
+
+CUtensorMap make_map_uncached(const void *base, uint64_t inner, uint64_t outer, uint32_t box_rows) {
   CUtensorMap m;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {inner * 2};
@@ -365,9 +385,23 @@ int num_sms() {
   return n;
 }
 
+// Raise a kernel's dynamic shared-memory limit only when a launch needs more
+// than it was last set to (the attribute call is not free on the host).
 template <typename K>
 void set_smem(K kernel, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void *, int>> done;
+  std::lock_guard<std::mutex> g(mu);
+  const void *key = reinterpret_cast<const void *>(kernel);
+  for (auto &kv : done)
+    if (kv.first == key && kv.second >= bytes) return;
   HM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  for (auto &kv : done)
+    if (kv.first == key) {
+      kv.second = bytes;
+      return;
+    }
+  done.emplace_back(key, bytes);
 }
 
 void launch_gemv(const uint16_t *pool, size_t slot_elems, int H, int I, const std::vector<hm_group> &gs,

@@ -211,6 +211,14 @@ class HybridMoE:
             torch.bfloat16)
         torch.cuda.synchronize()
 
+    def set_profile(self, profile: HardwareProfile) -> None:
+        """Plan the following passes with another calibrated profile (e.g. the
+        prefill profile for the prefill pass, the decode profile after it)."""
+        from .costs import to_native
+        self.profile = profile
+        self.evaluator.profile = profile
+        check(lib.hm_engine_set_profile(self.engine._h, C.byref(to_native(profile))))
+
     def preload(self, refs) -> None:
         """Fixed residency for the baseline schedulings (engine.py:423-434):
         make these experts resident and copy them into their HBM slots."""
