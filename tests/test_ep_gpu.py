@@ -42,7 +42,8 @@ def _run(rank: int, world: int, port: int, q) -> None:
         cfg = SHAPES["tiny"]
         eb = mcore.expert_bytes(cfg)
         prof = mcost.HardwareProfile(gpu_time_per_expert=1.0, cpu_slope=2.0, transfer_bandwidth=eb / 0.5)
-        moe = HybridMoE(cfg, "tiny", EnginePolicy(), 0.5, prof, max_tokens=48, ep_rank=rank, ep_world=world)
+        moe = HybridMoE(cfg, "tiny", EnginePolicy(), 0.5, prof, max_tokens=48, ep_rank=rank, ep_world=world,
+                        cpu_threads=2)
         moe.init_seeded_weights(7)
         trace, logits = generate_router_logits(cfg, GenParams(seed=3), 32, 3)
         g = torch.Generator(device="cuda").manual_seed(5)
