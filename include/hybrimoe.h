@@ -291,6 +291,14 @@ int hm_engine_record(const hm_engine *e, uint32_t *lookup_refs, uint8_t *lookup_
 int hm_router_topk(const float *logits, int T, int N, int ld, int K, int renormalize,
                    int n_shared, int shared_gate_col, int32_t *sel, float *w, float *probs,
                    int32_t *counts, void *stream);
+/* Decode-sized layers in one launch (T <= 32, T*(K+S) <= 1024): router,
+ * counts, offsets, fp64 score sums, normalised scores, permutation and row
+ * gather.  meta_i = [counts E | offsets E+1], meta_d = [score_sum N | scores N]
+ * where scores[e] = score_sum[e] / sum_e score_sum (sequential fp64 sums). */
+int hm_router_fused_small(const float *logits, int T, int N, int ld, int K, int renormalize,
+                          int n_shared, int shared_gate_col, const uint16_t *x, int H, int32_t *sel,
+                          float *w, int32_t *pos, int32_t *row_src, uint16_t *xp, int32_t *meta_i,
+                          double *meta_d, void *stream);
 /* score_sum[e] = sum_t probs[t, e] in fp64, fixed reduction order; the
  * LayerRequest scores are score_sum normalised (tracegen.py:149-150). */
 int hm_score_sums(const float *probs, int T, int N, double *score_sum, void *stream);

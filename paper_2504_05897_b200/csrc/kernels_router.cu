@@ -95,6 +95,134 @@ __global__ void router_topk_kernel(const float *__restrict__ logits, int T, int 
   }
 }
 
+// Decode-sized layers (T*(K+S) <= 1024, N <= 256, E <= 320) in ONE block:
+// router (same math as router_topk_kernel), counts, fp64 score sums and the
+// normalised LayerRequest scores (sequential sums, bit-identical to the host
+// core's arithmetic), expert offsets, the permutation and the row gather.
+// meta = [counts E | offsets E+1] int32 followed (8-byte aligned) by
+// [score_sum N | scores N] fp64, so one D2H copy carries the LayerRequest.
+constexpr int kFusedMaxRows = 1024;
+constexpr int kFusedMaxE = 320;
+
+__global__ void __launch_bounds__(256) router_fused_small_kernel(
+    const float *__restrict__ logits, int T, int N, int ld, int K, int renorm, int n_shared, int shared_gate_col,
+    const uint16_t *__restrict__ x, int H, int32_t *__restrict__ sel, float *__restrict__ w, int32_t *__restrict__ pos,
+    int32_t *__restrict__ row_src, uint16_t *__restrict__ xp, int32_t *__restrict__ meta_i, double *__restrict__ meta_d) {
+  __shared__ int32_t s_sel[kFusedMaxRows];
+  __shared__ int32_t s_counts[kFusedMaxE];
+  __shared__ int32_t s_off[kFusedMaxE + 1];
+  __shared__ float s_probs[32 * 256];  // T <= 32 tokens x N <= 256
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int E = N + n_shared, Kp = K + n_shared, R = T * Kp;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) s_counts[e] = 0;
+  __syncthreads();
+  for (int t = wid; t < T; t += nw) {
+    const float *row = logits + static_cast<size_t>(t) * ld;
+    float v[kMaxPerLane];
+    float m = -FLT_MAX;
+#pragma unroll
+    for (int j = 0; j < kMaxPerLane; ++j) {
+      const int e = lane + 32 * j;
+      v[j] = e < N ? row[e] : -FLT_MAX;
+      m = fmaxf(m, v[j]);
+    }
+    m = dev::warp_max(m);
+    float s = 0.0f, ex[kMaxPerLane];
+#pragma unroll
+    for (int j = 0; j < kMaxPerLane; ++j) {
+      const int e = lane + 32 * j;
+      ex[j] = e < N ? expf(v[j] - m) : 0.0f;
+      s += ex[j];
+    }
+    s = dev::warp_sum(s);
+    const float inv = 1.0f / s;
+#pragma unroll
+    for (int j = 0; j < kMaxPerLane; ++j) {
+      const int e = lane + 32 * j;
+      if (e < N) s_probs[t * N + e] = ex[j] * inv;
+    }
+    uint32_t taken = 0;
+    float psel[8], psum = 0.0f;
+    for (int k = 0; k < K; ++k) {
+      float bv = -FLT_MAX;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int j = 0; j < kMaxPerLane; ++j) {
+        const int e = lane + 32 * j;
+        if (e < N && !((taken >> j) & 1u) && (v[j] > bv || (v[j] == bv && e < bi))) {
+          bv = v[j];
+          bi = e;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+      const float p = expf(bv - m) * inv;
+      psel[k] = p;
+      psum += p;
+      if (lane == 0) {
+        s_sel[t * Kp + k] = bi;
+        atomicAdd(&s_counts[bi], 1);
+      }
+    }
+    if (lane == 0) {
+      for (int k = 0; k < K; ++k) w[static_cast<size_t>(t) * Kp + k] = renorm ? psel[k] / psum : psel[k];
+      const float g = shared_gate_col >= 0 ? 1.0f / (1.0f + expf(-row[shared_gate_col])) : 1.0f;
+      for (int c = 0; c < n_shared; ++c) {
+        s_sel[t * Kp + K + c] = N + c;
+        w[static_cast<size_t>(t) * Kp + K + c] = g;
+        atomicAdd(&s_counts[N + c], 1);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // offsets, fp64 score sums, normalised scores (sequential, host order)
+    int32_t run = 0;
+    for (int e = 0; e < E; ++e) {
+      s_off[e] = run;
+      meta_i[e] = s_counts[e];
+      meta_i[E + e] = run;
+      run += s_counts[e];
+    }
+    s_off[E] = run;
+    meta_i[2 * E] = run;
+    double tot = 0.0;
+    for (int e = 0; e < N; ++e) {
+      double acc = 0.0;
+      for (int t = 0; t < T; ++t) acc += static_cast<double>(s_probs[t * N + e]);
+      meta_d[e] = acc;
+      tot += acc;
+    }
+    for (int e = 0; e < N; ++e) meta_d[N + e] = tot > 0.0 ? meta_d[e] / tot : 0.0;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < R; j += blockDim.x) {  // stable rank inside the expert
+    const int e = s_sel[j];
+    int r = 0;
+    for (int q = 0; q < j; ++q) r += s_sel[q] == e;
+    const int p = s_off[e] + r;
+    sel[j] = e;
+    pos[j] = p;
+    row_src[p] = j;
+  }
+  __syncthreads();
+  const int H8 = H / 8;
+  for (int v = threadIdx.x; v < R * H8; v += blockDim.x) {  // gather rows in permuted order
+    const int p = v / H8, c = v % H8;
+    // invert: the row at position p came from selection j = row_src[p] (written above, block-visible)
+    const int t = row_src[p] / Kp;
+    reinterpret_cast<uint4 *>(xp + static_cast<size_t>(p) * H)[c] =
+        reinterpret_cast<const uint4 *>(x + static_cast<size_t>(t) * H)[c];
+  }
+}
+
 // score_sum[e] = sum_t probs[t, e] in fp64, fixed reduction order.
 __global__ void score_sum_kernel(const float *__restrict__ probs, int T, int N, double *__restrict__ out) {
   __shared__ double red[256];
@@ -301,6 +429,19 @@ int hm_router_topk(const float *logits, int T, int N, int ld, int K, int renorma
   } else if (n_shared > 0) {
     HM_CUDA(cudaMemsetAsync(counts + N, 0, sizeof(int32_t) * n_shared, st));
   }
+  HM_API_END
+}
+
+int hm_router_fused_small(const float *logits, int T, int N, int ld, int K, int renormalize, int n_shared,
+                          int shared_gate_col, const uint16_t *x, int H, int32_t *sel, float *w, int32_t *pos,
+                          int32_t *row_src, uint16_t *xp, int32_t *meta_i, double *meta_d, void *stream) {
+  HM_API_BEGIN
+  HM_REQUIRE(T >= 1 && T <= 32 && N >= 1 && N <= 256 && K >= 1 && K <= 8 && K <= N && ld >= N &&
+                 T * (K + n_shared) <= hm::kFusedMaxRows && N + n_shared <= hm::kFusedMaxE && H % 8 == 0,
+             HM_EVALUE, "shape outside the fused small-T router");
+  hm::router_fused_small_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      logits, T, N, ld, K, renormalize, n_shared, shared_gate_col, x, H, sel, w, pos, row_src, xp, meta_i, meta_d);
+  HM_LAUNCH_CHECK();
   HM_API_END
 }
 

@@ -33,6 +33,8 @@ int hm_expert_ffn(const uint16_t *, int, int, int, const hm_group *, int, const 
 int hm_combine(const float *, const int32_t *, const float *, int, int, int, const uint16_t *, uint16_t *, void *);
 int hm_mrs_update_dev(double *, const double *, int, int, int, double, void *);
 int hm_mask_nonhome(const int32_t *, float *, int, int, int, int, void *);
+int hm_router_fused_small(const float *, int, int, int, int, int, int, int, const uint16_t *, int, int32_t *,
+                          float *, int32_t *, int32_t *, uint16_t *, int32_t *, double *, void *);
 int hm_combine_f32(const float *, const int32_t *, const float *, int, int, int, float *, void *);
 }
 
@@ -72,6 +74,8 @@ struct Runtime {
   int32_t *sel = nullptr, *counts = nullptr, *offsets = nullptr, *pos = nullptr, *row_src = nullptr;
   float *w = nullptr, *probs = nullptr, *out = nullptr;
   double *score_sum = nullptr, *S_dev = nullptr, *scores_dev = nullptr;
+  void *dmeta = nullptr, *hmeta = nullptr;  // LayerRequest block (device / pinned host)
+  size_t meta_ioff = 0, meta_bytes = 0;
   uint16_t *xp = nullptr, *h = nullptr;
   // pinned host staging
   int32_t *h_counts = nullptr, *h_offsets = nullptr;
@@ -148,21 +152,27 @@ struct Runtime {
     RT_CUDA(cudaMalloc(&sel, rows * 4));
     RT_CUDA(cudaMalloc(&w, rows * 4));
     RT_CUDA(cudaMalloc(&probs, T * N * 4));
-    RT_CUDA(cudaMalloc(&counts, E * 4));
-    RT_CUDA(cudaMalloc(&offsets, (E + 1) * 4));
+    // LayerRequest block: [counts E | offsets E+1] int32, 8-byte aligned, then
+    // [score_sum N | scores N] fp64 -- one buffer on each side, one D2H copy
+    meta_ioff = ((2 * static_cast<size_t>(E) + 1) * 4 + 7) / 8 * 8;
+    meta_bytes = meta_ioff + 2 * static_cast<size_t>(N) * 8;
+    RT_CUDA(cudaMalloc(&dmeta, meta_bytes));
+    RT_CUDA(cudaHostAlloc(&hmeta, meta_bytes, 0));
+    counts = reinterpret_cast<int32_t *>(dmeta);
+    offsets = counts + E;
+    score_sum = reinterpret_cast<double *>(static_cast<char *>(dmeta) + meta_ioff);
+    scores_dev = score_sum + N;
+    h_counts = reinterpret_cast<int32_t *>(hmeta);
+    h_offsets = h_counts + E;
+    h_score_sum = reinterpret_cast<double *>(static_cast<char *>(hmeta) + meta_ioff);
     RT_CUDA(cudaMalloc(&pos, rows * 4));
     RT_CUDA(cudaMalloc(&row_src, rows * 4));
     RT_CUDA(cudaMalloc(&xp, rows * H * 2));
     RT_CUDA(cudaMalloc(&h, rows * I * 2));
     RT_CUDA(cudaMalloc(&out, rows * H * 4));
-    RT_CUDA(cudaMalloc(&score_sum, N * 8));
-    RT_CUDA(cudaMalloc(&scores_dev, N * 8));
     RT_CUDA(cudaMalloc(&S_dev, static_cast<size_t>(L) * N * 8));
     std::vector<double> prior(static_cast<size_t>(L) * N, 1.0 / static_cast<double>(N));
     RT_CUDA(cudaMemcpy(S_dev, prior.data(), prior.size() * 8, cudaMemcpyHostToDevice));
-    RT_CUDA(cudaHostAlloc(&h_counts, E * 4, 0));
-    RT_CUDA(cudaHostAlloc(&h_offsets, (E + 1) * 4, 0));
-    RT_CUDA(cudaHostAlloc(&h_score_sum, N * 8, 0));
     RT_CUDA(cudaHostAlloc(&h_scores, N * 8, 0));
     RT_CUDA(cudaHostAlloc(&h_x, rows * H * 2, 0));
     RT_CUDA(cudaHostAlloc(&h_out, rows * H * 4, 0));
@@ -180,13 +190,11 @@ struct Runtime {
     if (ev_rows) cudaEventDestroy(ev_rows);
     if (copy) cudaStreamDestroy(copy);
     for (void *p : {static_cast<void *>(pool), static_cast<void *>(sel), static_cast<void *>(w),
-                    static_cast<void *>(probs), static_cast<void *>(counts), static_cast<void *>(offsets),
-                    static_cast<void *>(pos), static_cast<void *>(row_src), static_cast<void *>(xp),
-                    static_cast<void *>(h), static_cast<void *>(out), static_cast<void *>(score_sum),
-                    static_cast<void *>(scores_dev), static_cast<void *>(S_dev)})
+                    static_cast<void *>(probs), dmeta, static_cast<void *>(pos), static_cast<void *>(row_src),
+                    static_cast<void *>(xp), static_cast<void *>(h), static_cast<void *>(out),
+                    static_cast<void *>(S_dev)})
       if (p) cudaFree(p);
-    for (void *p : {static_cast<void *>(store), static_cast<void *>(h_counts), static_cast<void *>(h_offsets),
-                    static_cast<void *>(h_score_sum), static_cast<void *>(h_scores), static_cast<void *>(h_x),
+    for (void *p : {static_cast<void *>(store), hmeta, static_cast<void *>(h_scores), static_cast<void *>(h_x),
                     static_cast<void *>(h_out)})
       if (p) cudaFreeHost(p);
   }
@@ -217,17 +225,26 @@ struct Runtime {
     hm_layer_stats s{};
     void *vs = static_cast<void *>(st);
     const int rows = T * Kp;
-    // (0) router, LayerRequest, permutation -- all on the compute stream
-    ok(hm_router_topk(logits, T, N, ld, K, cfg.renormalize, S, cfg.shared_gate_col, sel, w, probs, counts, vs));
-    if (W > 1) ok(hm_mask_nonhome(sel, w, T * Kp, N, R, W, vs));
-    ok(hm_score_sums(probs, T, N, score_sum, vs));
-    ok(hm_offsets(counts, E, offsets, vs));
-    RT_CUDA(cudaMemcpyAsync(h_counts, counts, E * 4, cudaMemcpyDeviceToHost, st));
-    RT_CUDA(cudaMemcpyAsync(h_offsets, offsets, (E + 1) * 4, cudaMemcpyDeviceToHost, st));
-    RT_CUDA(cudaMemcpyAsync(h_score_sum, score_sum, N * 8, cudaMemcpyDeviceToHost, st));
-    RT_CUDA(cudaEventRecord(ev_req, st));
-    ok(hm_permute(sel, T, Kp, E, offsets, pos, row_src, vs));
-    ok(hm_gather_rows(x, row_src, rows, Kp, H, xp, vs));
+    // (0) router, LayerRequest, permutation -- all on the compute stream; the
+    // LayerRequest (counts, offsets, score sums, scores) lands in one pinned
+    // buffer with a single D2H copy: the only per-layer host synchronisation
+    const bool fused = T <= 32 && rows <= 1024 && N <= 256 && E <= 320 && H % 8 == 0;
+    if (fused) {  // decode: one launch does router .. gather
+      ok(hm_router_fused_small(logits, T, N, ld, K, cfg.renormalize, S, cfg.shared_gate_col, x, H, sel, w, pos,
+                               row_src, xp, counts, score_sum, vs));
+      if (W > 1) ok(hm_mask_nonhome(sel, w, T * Kp, N, R, W, vs));
+      RT_CUDA(cudaMemcpyAsync(hmeta, dmeta, meta_bytes, cudaMemcpyDeviceToHost, st));
+      RT_CUDA(cudaEventRecord(ev_req, st));
+    } else {
+      ok(hm_router_topk(logits, T, N, ld, K, cfg.renormalize, S, cfg.shared_gate_col, sel, w, probs, counts, vs));
+      if (W > 1) ok(hm_mask_nonhome(sel, w, T * Kp, N, R, W, vs));
+      ok(hm_score_sums(probs, T, N, score_sum, vs));
+      ok(hm_offsets(counts, E, offsets, vs));
+      RT_CUDA(cudaMemcpyAsync(hmeta, dmeta, meta_bytes, cudaMemcpyDeviceToHost, st));
+      RT_CUDA(cudaEventRecord(ev_req, st));
+      ok(hm_permute(sel, T, Kp, E, offsets, pos, row_src, vs));
+      ok(hm_gather_rows(x, row_src, rows, Kp, H, xp, vs));
+    }
     double t0 = now_us();
     RT_CUDA(cudaEventSynchronize(ev_req));
     double t1 = now_us();
@@ -240,7 +257,7 @@ struct Runtime {
       // rank-masked LayerRequest under expert parallelism: other ranks' loads
       // are zeroed, scores stay whole so every rank's S table is identical
       loads[e] = (W == 1 || e % W == R) ? h_counts[e] : 0;
-      scores[e] = tot > 0.0 ? h_score_sum[e] / tot : 0.0;
+      scores[e] = tot > 0.0 ? h_score_sum[e] / tot : 0.0;  // == the fused kernel's scores, bit for bit
       h_scores[e] = scores[e];
     }
     engine->run_layer(layer, loads.data(), scores.data(), N, pred_layers, pred_loads, n_pred);
@@ -349,7 +366,7 @@ struct Runtime {
       ok(hm_combine(out, pos, w, T, Kp, H, cfg.residual ? x : nullptr, y, vs));
     }
     if (cfg.gpu_mrs && engine->cfg.cache_policy == HM_POLICY_MRS && engine->mrs_) {
-      RT_CUDA(cudaMemcpyAsync(scores_dev, h_scores, N * 8, cudaMemcpyHostToDevice, st));
+      if (!fused) RT_CUDA(cudaMemcpyAsync(scores_dev, h_scores, N * 8, cudaMemcpyHostToDevice, st));
       ok(hm_mrs_update_dev(S_dev, scores_dev, layer, N, engine->mrs_->p, engine->mrs_->alpha, vs));
     }
     if (stats) *stats = s;

@@ -69,6 +69,47 @@ def test_router_parity(T, N, Kk, renorm, S, gate):
         np.testing.assert_allclose(ssum.cpu().numpy(), r_ssum, rtol=1e-5)
 
 
+@pytest.mark.parametrize("T,N,Kk,S,renorm,gate", [(1, 8, 2, 0, True, -1), (1, 64, 6, 2, False, -1),
+                                                  (1, 64, 8, 8, False, 64), (4, 16, 4, 1, False, -1),
+                                                  (32, 8, 2, 0, True, -1)])
+def test_router_fused_small_matches_unfused(T, N, Kk, S, renorm, gate):
+    import ctypes as Cc
+    H = 256
+    rng = np.random.default_rng(T + N)
+    ld = N + (1 if gate >= 0 else 0)
+    logits = torch.from_numpy(rng.standard_normal((T, ld)).astype(np.float32)).cuda()
+    x = torch.randn((T, H), device="cuda").to(torch.bfloat16)
+    kp, E = Kk + S, N + S
+    sel = torch.empty((T, kp), dtype=torch.int32, device="cuda")
+    w = torch.empty((T, kp), device="cuda")
+    pos = torch.empty((T, kp), dtype=torch.int32, device="cuda")
+    row_src = torch.empty((T * kp,), dtype=torch.int32, device="cuda")
+    xp = torch.empty((T * kp, H), dtype=torch.bfloat16, device="cuda")
+    mi = torch.empty((2 * E + 2,), dtype=torch.int32, device="cuda")
+    md = torch.empty((2 * N,), dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.lib.hm_router_fused_small.argtypes = [Cc.c_void_p, Cc.c_int, Cc.c_int, Cc.c_int, Cc.c_int, Cc.c_int,
+                                               Cc.c_int, Cc.c_int, Cc.c_void_p, Cc.c_int] + [Cc.c_void_p] * 8
+    _lib.check(_lib.lib.hm_router_fused_small(logits.data_ptr(), T, N, ld, Kk, int(renorm), S, gate, x.data_ptr(),
+                                              H, sel.data_ptr(), w.data_ptr(), pos.data_ptr(), row_src.data_ptr(),
+                                              xp.data_ptr(), mi.data_ptr(), md.data_ptr(), st))
+    r_sel, r_w, r_probs, r_counts = K.router_topk(logits, N, Kk, renorm, S, gate)
+    r_off = K.offsets(r_counts)
+    r_pos, r_src = K.permute(r_sel, r_off, E)
+    r_xp = K.gather_rows(x, r_src, kp)
+    r_sum = K.score_sums(r_probs)
+    torch.cuda.synchronize()
+    assert torch.equal(sel, r_sel) and torch.equal(w, r_w)
+    assert torch.equal(pos, r_pos) and torch.equal(row_src, r_src) and torch.equal(xp, r_xp)
+    assert torch.equal(mi[:E], r_counts) and torch.equal(mi[E:2 * E + 1], r_off)
+    s = md[:N].cpu().numpy()
+    np.testing.assert_allclose(s, r_sum.cpu().numpy(), rtol=1e-12)
+    tot = 0.0
+    for v in s:
+        tot += float(v)
+    assert np.array_equal(md[N:].cpu().numpy(), np.array([float(v) / tot for v in s]))
+
+
 def test_permute_gather_combine():
     T, N, Kk, S, H = 300, 16, 4, 1, 256
     rng = np.random.default_rng(3)
