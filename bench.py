@@ -265,9 +265,11 @@ def run_ours(args) -> None:
     host_bw_gbs = hbw.value if args.host_bw_gbs <= 0 else args.host_bw_gbs
     setup_s = time.time() - t_setup
 
-    def predictor(p):
-        fwd = trace.passes[p]
-        return lambda l: predict_layers(fwd.layers, cfg.num_layers, p, l, policy.prediction, args.seed)
+    from paper_2504_05897_b200.moe import TracePredictor
+    predictors = [TracePredictor(trace, p, args.seed) for p in range(len(trace.passes))]
+
+    def predictor(p):  # the reference's prediction model on this pass, native
+        return predictors[p]
 
     st = torch.cuda.current_stream()
     # ---- prefill: 1k tokens, cold cache (the reference's TTFT, engine.py:465-466)

@@ -204,6 +204,14 @@ int hm_evaluate_gain(uint32_t candidate, int pred_layer, const int64_t *pred_loa
 int hm_select_prefetches(const hm_candidate *cands, int n, double idle_budget,
                          uint32_t *chosen, int *n_chosen);
 
+/* The prediction model (prefetch.py:54-101) natively: numpy's
+ * default_rng([seed, pass, layer, 0x5EED]) stream (SeedSequence + PCG64,
+ * random(), integers()) restated draw for draw.  pass_loads [L*N]; writes the
+ * predicted loads of layers layer+1..min(layer+horizon, L-1). */
+int hm_predict_layers(const int64_t *pass_loads, int L, int N, int64_t pass_index, int layer,
+                      int64_t seed, int horizon, double accuracy, int32_t *out_layers,
+                      int64_t *out_loads, int *n_out);
+
 /* ---- the per-layer engine step (engine.py:255-398, 401-486) --------------- */
 typedef struct hm_engine_config {
   int32_t num_layers;

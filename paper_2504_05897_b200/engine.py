@@ -24,7 +24,7 @@ from ._lib import check, lib, pack
 from .caching import POLICIES, POLICY_CODE, POLICY_MRS, CacheStats, MrsState, make_mrs_state
 from .core import CacheState, ExpertRef, LayerRequest, ModelConfig, STAGE_PREFILL, Trace, _ref_of, expert_bytes
 from .costs import HardwareProfile, gpu_time, to_native, transfer_time
-from .prefetch import PredictionModel, predict_layers
+from .prefetch import PredictionModel, predict_layers, predict_layers_native
 from .scheduling import (ASSIGN_GPU_CACHED, DEVICE_CPU, DEVICE_GPU, DEVICE_PCIE, KIND_COMPUTE, MakespanEvaluator,
                          SchedulePlan, TimelineEvent, activated_tasks, plan_all_cpu, plan_from_native)
 
@@ -302,9 +302,12 @@ def run_pass(trace: Trace, pass_index: int, policy: EnginePolicy, cache: CacheSt
     predicting = policy.prefetch and policy.scheduling not in _STATIC_SCHEDULINGS and cache.capacity > 0
     plans: list[SchedulePlan] | None = [] if collect_plans else None
     decisions: list[dict] | None = [] if decision_log else None
+    pass_loads = (np.ascontiguousarray([r.loads for r in fwd.layers], dtype=np.int64) if predicting else None)
     for request in fwd.layers:
-        predicted = (predict_layers(fwd.layers, cfg.num_layers, pass_index, request.layer, policy.prediction, seed)
-                     if predicting else [])
+        # the prediction model (prefetch.py:54-101) through its native restatement
+        # of numpy's stream; tests/test_predict_native.py pins it to numpy itself
+        predicted = (predict_layers_native(fwd.layers, cfg.num_layers, pass_index, request.layer, policy.prediction,
+                                           seed, pass_loads) if predicting else [])
         eng.run_layer(request, predicted)
         if collect_plans:
             plans.append(eng.plan())

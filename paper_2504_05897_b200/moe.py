@@ -87,6 +87,16 @@ class _Raw:
             self.__array_interface__ = iface
 
 
+class TracePredictor:
+    """Trace-mode prediction input for forward_pass: the pass's true loads, fed
+    through the reference's noisy-ground-truth model natively (prefetch.py:54-101)."""
+
+    def __init__(self, trace, pass_index: int, seed: int) -> None:
+        self.pass_loads = np.ascontiguousarray([r.loads for r in trace.passes[pass_index].layers], dtype=np.int64)
+        self.pass_index = int(pass_index)
+        self.seed = int(seed)
+
+
 @dataclass
 class LayerStats:
     makespan_planned: float
@@ -274,19 +284,31 @@ class HybridMoE:
         loads = np.zeros(self.N, dtype=np.int64)
         scores = np.zeros(self.N, dtype=np.float64)
         self.engine.begin_pass()
+        hz = self.policy.prediction.horizon
+        npred = C.c_int()
         for l in range(self.L):
             lg = logits[l] if logits is not None else self._model_logits(cur, l, st)
-            if not self.policy.prefetch:
-                preds = []
-            elif predict == "live":  # gate look-ahead on the current hidden state
-                preds = self.lookahead(cur, l, stream=st)
+            if self.policy.prefetch and isinstance(predict, TracePredictor):
+                # the reference's prediction model, natively (csrc/predict.cpp)
+                pl = np.empty(hz, dtype=np.int32)
+                pload = np.empty((hz, self.N), dtype=np.int64)
+                check(lib.hm_predict_layers(_lib.ptr(predict.pass_loads, C.c_int64), self.L, self.N,
+                                            predict.pass_index, l, predict.seed, hz,
+                                            float(self.policy.prediction.accuracy), _lib.ptr(pl, C.c_int32),
+                                            _lib.ptr(pload, C.c_int64), C.byref(npred)))
+                pl = pl[: npred.value]
             else:
-                preds = predict(l) if predict is not None else []
-            pl = np.array([p.layer for p in preds], dtype=np.int32)
-            pload = np.zeros((max(1, len(preds)), self.N), dtype=np.int64)
-            for d, p in enumerate(preds):
-                for i in p.activated:
-                    pload[d, i] = p.loads[i]
+                if not self.policy.prefetch:
+                    preds = []
+                elif predict == "live":  # gate look-ahead on the current hidden state
+                    preds = self.lookahead(cur, l, stream=st)
+                else:
+                    preds = predict(l) if predict is not None else []
+                pl = np.array([p.layer for p in preds], dtype=np.int32)
+                pload = np.zeros((max(1, len(preds)), self.N), dtype=np.int64)
+                for d, p in enumerate(preds):
+                    for i in p.activated:
+                        pload[d, i] = p.loads[i]
             out = a if (l % 2 == 0) else b
             check(lib.hm_runtime_forward_layer(self._rt, l, cur.data_ptr(), lg.data_ptr(), T, lg.shape[1],
                                                out.data_ptr(), _lib.ptr(pl, C.c_int32), _lib.ptr(pload, C.c_int64),

@@ -79,6 +79,25 @@ def predict_layers(layers, n_layers: int, pass_index: int, current_layer: int, m
     return out
 
 
+def predict_layers_native(layers, n_layers: int, pass_index: int, current_layer: int, model: PredictionModel,
+                          seed: int, pass_loads: np.ndarray | None = None) -> list[LayerRequest]:
+    """predict_layers through the native restatement of numpy's stream
+    (csrc/predict.cpp); loads only -- the scores of predicted requests are never
+    read by the prefetch decision.  pass_loads: the pass's [L, N] loads, if cached."""
+    n = len(layers[0].loads)
+    if pass_loads is None:
+        pass_loads = np.ascontiguousarray([r.loads for r in layers], dtype=np.int64)
+    hz = model.horizon
+    out_layers = np.empty(hz, dtype=np.int32)
+    out_loads = np.empty((hz, n), dtype=np.int64)
+    k = C.c_int()
+    check(lib.hm_predict_layers(_lib.ptr(pass_loads, C.c_int64), n_layers, n, int(pass_index), int(current_layer),
+                                int(seed), hz, float(model.accuracy), _lib.ptr(out_layers, C.c_int32),
+                                _lib.ptr(out_loads, C.c_int64), C.byref(k)))
+    return [LayerRequest(layer=int(out_layers[d]), loads=tuple(int(v) for v in out_loads[d]), scores=(),
+                         activated=frozenset(int(i) for i in np.nonzero(out_loads[d])[0])) for d in range(k.value)]
+
+
 def predict_activations(trace: Trace, pass_index: int, current_layer: int, model: PredictionModel,
                         seed: int) -> list[LayerRequest]:
     """Future layer requests of this pass, perturbed per the model accuracy (prefetch.py:54-101)."""
