@@ -67,15 +67,15 @@ def test_two_ranks_equal_one_rank():
     q = ctx.Queue()
     single = ctx.Process(target=_run, args=(0, 1, 0, q))
     single.start()
-    single.join(timeout=300)
-    ref = q.get(timeout=10)
+    ref = q.get(timeout=300)  # drain the queue before joining (large items block the child's exit)
+    single.join(timeout=60)
     port = _free_port()
     procs = [ctx.Process(target=_run, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
+    got = dict((r[0], r) for r in (q.get(timeout=300), q.get(timeout=300)))
     for p in procs:
-        p.join(timeout=300)
-    got = dict((r[0], r) for r in (q.get(timeout=10), q.get(timeout=10)))
+        p.join(timeout=60)
     assert single.exitcode == 0 and all(p.exitcode == 0 for p in procs)
     _, _, ref_outs, ref_loads, ref_cap = ref
     assert got[0][4] + got[1][4] == ref_cap                      # global budget split across ranks
