@@ -312,7 +312,7 @@ class HybridMoE:
             out = a if (l % 2 == 0) else b
             check(lib.hm_runtime_forward_layer(self._rt, l, cur.data_ptr(), lg.data_ptr(), T, lg.shape[1],
                                                out.data_ptr(), _lib.ptr(pl, C.c_int32), _lib.ptr(pload, C.c_int64),
-                                               len(preds), st.cuda_stream, C.byref(ls)))
+                                               len(pl), st.cuda_stream, C.byref(ls)))
             if self.ep_world > 1:  # sum the ranks' partial expert outputs, then the residual
                 import torch.distributed as dist
                 part = self.y32[:T]

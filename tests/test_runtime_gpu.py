@@ -134,6 +134,32 @@ def test_live_lookahead_prefetch_model_mode():
     assert torch.isfinite(x.float()).all()
 
 
+def test_native_trace_predictor_matches_python_predictor():
+    """forward_pass with the native prediction model makes the same decisions
+    as with the Python (numpy) prediction model."""
+    from paper_2504_05897_b200.moe import TracePredictor
+    cfg = SHAPES["tiny"]
+    prof = stress_profile(cfg)
+    policy = me.EnginePolicy(prefetch=True)
+    trace, logits = generate_router_logits(cfg, GenParams(seed=4), 32, 4)
+    streams = []
+    for native in (False, True):
+        moe = HybridMoE(cfg, "tiny", policy, 0.5, prof, max_tokens=64)
+        moe.init_seeded_weights(2)
+        recs = []
+        g = torch.Generator(device="cuda").manual_seed(1)
+        for p, fwd in enumerate(trace.passes):
+            lg = [torch.from_numpy(np.ascontiguousarray(logits[p][l], dtype=np.float32)).cuda()
+                  for l in range(cfg.num_layers)]
+            x = torch.randn((fwd.token_count, moe.H), generator=g, device="cuda").to(torch.bfloat16)
+            pred = (TracePredictor(trace, p, 9) if native else
+                    (lambda l, p=p, fwd=fwd: predict_layers(fwd.layers, cfg.num_layers, p, l, policy.prediction, 9)))
+            _, info = moe.forward_pass(x, lg, predict=pred, decision_log=True)
+            recs.extend(info["records"])
+        streams.append(digest(from_records(recs, True)))
+    assert streams[0] == streams[1]
+
+
 def test_model_mode_runs_and_is_deterministic():
     cfg = SHAPES["tiny"]
     moe = HybridMoE(cfg, "tiny", me.EnginePolicy(), 0.25, stress_profile(cfg), max_tokens=32)
