@@ -175,7 +175,7 @@ def run_ours(args) -> None:
     from paper_2504_05897_b200 import _lib
     from paper_2504_05897_b200.calibration import calibrate_shape
     from paper_2504_05897_b200.engine import EnginePolicy
-    from paper_2504_05897_b200.moe import FAMILIES, SHAPES, HybridMoE, with_shared_time
+    from paper_2504_05897_b200.moe import FAMILIES, SHAPES, HybridMoE, layer_stats, with_shared_time
     from paper_2504_05897_b200.prefetch import predict_layers
     from paper_2504_05897_b200.tracegen import GenParams, generate_router_logits
 
@@ -281,7 +281,7 @@ def run_ours(args) -> None:
     ev1.record(st)
     ev1.synchronize()
     prefill_ms = ev0.elapsed_time(ev1)
-    pst = pinfo["stats"]
+    pst = layer_stats(pinfo)
 
     # ---- decode: W warm-up passes (recorded for the parity block), then K timed passes
     warm_records, warm_requests = [], []
@@ -308,7 +308,7 @@ def run_ours(args) -> None:
         for k in range(args.steps):
             p = 1 + args.warmup + k
             _, info = moe.forward_pass(xs[p], dev_logits[p], predict=predictor(p))
-            stats_all.extend(info["stats"])
+            stats_all.append(info)
         t1.record(st)
         t1.synchronize()
         torch.cuda.synchronize()
@@ -317,6 +317,7 @@ def run_ours(args) -> None:
     if dist:
         dist.barrier()
     launches = lib.hm_launch_count() - launches0
+    stats_all = [s for info in stats_all for s in layer_stats(info)]
     ms_total = t0.elapsed_time(t1)
     import ctypes as C
     kms, kbytes, kn, kmax = C.c_double(), C.c_int64(), C.c_int64(), C.c_double()

@@ -423,6 +423,16 @@ int hm_runtime_forward_layer(hm_runtime *rt, int layer, const uint16_t *x, const
                              int T, int ld, uint16_t *y, const int32_t *pred_layers,
                              const int64_t *pred_loads, int n_pred, void *stream,
                              hm_layer_stats *stats);
+/* A whole pass (all L layers, one call): begin_pass, forward_layer per layer
+ * (ping-pong between buf0/buf1; *y_out receives the final buffer), end_pass.
+ * logits: L device pointers [T, ld].  pass_loads (HOST, [L*N], optional):
+ * the pass's loads for the trace-mode prediction model (hm_predict_layers).
+ * stats: optional [L] array.  Single-GPU only (ep_world == 1). */
+int hm_runtime_forward_pass(hm_runtime *rt, const uint16_t *x, const float *const *logits, int T,
+                            int ld, uint16_t *buf0, uint16_t *buf1, const int64_t *pass_loads,
+                            int64_t pass_index, int64_t seed, int horizon, double accuracy,
+                            void *stream, hm_layer_stats *stats, hm_pass_result *result,
+                            uint16_t **y_out);
 /* The LayerRequest (loads, normalised scores) the router produced last. */
 int hm_runtime_last_request(const hm_runtime *rt, int64_t *loads, double *scores);
 /* GPU copy of the MRS table S [L, N] (synchronises the device). */

@@ -314,6 +314,8 @@ for _name, (_args, _res) in {
     "hm_cpu_experts_decode": ([vp, P(vp), P(vp), C.c_int, C.c_int, C.c_int, P(vp)], C.c_int),
     "hm_cpu_set_prefetch": ([C.c_int, C.c_int], C.c_int),
     "hm_engine_set_profile": ([vp, P(Profile)], C.c_int),
+    "hm_runtime_forward_pass": ([vp, vp, P(vp), C.c_int, C.c_int, vp, vp, P(i64), i64, i64, C.c_int, f64, vp, vp,
+                                 P(PassResult), P(vp)], C.c_int),
     "hm_predict_layers": ([P(i64), C.c_int, C.c_int, i64, C.c_int, i64, C.c_int, f64, P(i32), P(i64),
                            P(C.c_int)], C.c_int),
 }.items():

@@ -33,6 +33,7 @@ int hm_expert_ffn(const uint16_t *, int, int, int, const hm_group *, int, const 
 int hm_combine(const float *, const int32_t *, const float *, int, int, int, const uint16_t *, uint16_t *, void *);
 int hm_mrs_update_dev(double *, const double *, int, int, int, double, void *);
 int hm_mask_nonhome(const int32_t *, float *, int, int, int, int, void *);
+int hm_predict_layers(const int64_t *, int, int, int64_t, int, int64_t, int, double, int32_t *, int64_t *, int *);
 int hm_router_fused_small(const float *, int, int, int, int, int, int, int, const uint16_t *, int, int32_t *,
                           float *, int32_t *, int32_t *, uint16_t *, int32_t *, double *, void *);
 int hm_combine_f32(const float *, const int32_t *, const float *, int, int, int, float *, void *);
@@ -414,6 +415,35 @@ int hm_runtime_forward_layer(hm_runtime *rt, int layer, const uint16_t *x, const
   HM_API_BEGIN
   reinterpret_cast<hm::Runtime *>(rt)->forward_layer(layer, x, logits, T, ld, y, pred_layers, pred_loads, n_pred,
                                                     static_cast<cudaStream_t>(stream), stats);
+  HM_API_END
+}
+
+int hm_runtime_forward_pass(hm_runtime *rt, const uint16_t *x, const float *const *logits, int T, int ld,
+                            uint16_t *buf0, uint16_t *buf1, const int64_t *pass_loads, int64_t pass_index,
+                            int64_t seed, int horizon, double accuracy, void *stream, hm_layer_stats *stats,
+                            hm_pass_result *result, uint16_t **y_out) {
+  HM_API_BEGIN
+  auto *r = reinterpret_cast<hm::Runtime *>(rt);
+  HM_REQUIRE(r->W == 1, HM_EVALUE, "expert-parallel passes exchange partials between layers: use forward_layer");
+  const bool predicting = pass_loads != nullptr && r->engine->cfg.prefetch;
+  std::vector<int32_t> pl(static_cast<size_t>(horizon > 0 ? horizon : 1));
+  std::vector<int64_t> pload(static_cast<size_t>(horizon > 0 ? horizon : 1) * r->N);
+  r->engine->begin_pass();
+  const uint16_t *cur = x;
+  for (int l = 0; l < r->L; ++l) {
+    int n_pred = 0;
+    if (predicting) {
+      const int rc = hm_predict_layers(pass_loads, r->L, r->N, pass_index, l, seed, horizon, accuracy, pl.data(),
+                                       pload.data(), &n_pred);
+      if (rc != HM_OK) hm::raise(rc, hm::last_error());
+    }
+    uint16_t *out = (l % 2 == 0) ? buf0 : buf1;
+    r->forward_layer(l, cur, logits[l], T, ld, out, pl.data(), pload.data(), n_pred, static_cast<cudaStream_t>(stream),
+                     stats ? &stats[l] : nullptr);
+    cur = out;
+  }
+  r->engine->end_pass(result);
+  if (y_out) *y_out = const_cast<uint16_t *>(cur);
   HM_API_END
 }
 

@@ -112,6 +112,13 @@ class LayerStats:
     bytes_h2d: int
 
 
+def layer_stats(info: dict) -> list[LayerStats]:
+    """Per-layer stats of a forward_pass info dict (native passes keep raw structs)."""
+    if "stats" in info:
+        return info["stats"]
+    return [LayerStats(*[getattr(s, f) for f, _ in _lib.LayerStats._fields_]) for s in info["stats_raw"]]
+
+
 class HybridMoE:
     """L MoE layers (router + experts + combine, residual stream) under the HybriMoE schedule."""
 
@@ -278,6 +285,9 @@ class HybridMoE:
             raise ValueError(f"T={T} exceeds max_tokens={self.max_tokens}")
         st = stream if stream is not None else torch.cuda.current_stream()
         a, b = self._ping_pong(T)
+        if (self.ep_world == 1 and logits is not None and not decision_log and not keep_layers
+                and (predict is None or isinstance(predict, TracePredictor) or not self.policy.prefetch)):
+            return self._forward_pass_native(x, logits, predict, a, b, st)
         cur = x
         stats, records, layers_io, requests = [], [], [], []
         ls = _lib.LayerStats()
@@ -337,6 +347,22 @@ class HybridMoE:
         r = self.engine.end_pass()
         info = {"stats": stats, "records": records, "requests": requests, "layers": layers_io, "pass": r}
         return cur, info
+
+    def _forward_pass_native(self, x, logits, predict, a, b, st):
+        """The whole pass in one native call (hm_runtime_forward_pass): no Python per layer."""
+        T = x.shape[0]
+        lgp = (C.c_void_p * self.L)(*[lg.data_ptr() for lg in logits])
+        stats = (_lib.LayerStats * self.L)()
+        res = _lib.PassResult()
+        yp = C.c_void_p()
+        pl = predict if isinstance(predict, TracePredictor) and self.policy.prefetch else None
+        check(lib.hm_runtime_forward_pass(
+            self._rt, x.data_ptr(), lgp, T, logits[0].shape[1], a.data_ptr(), b.data_ptr(),
+            _lib.ptr(pl.pass_loads, C.c_int64) if pl is not None else None, pl.pass_index if pl else 0,
+            pl.seed if pl else 0, self.policy.prediction.horizon, float(self.policy.prediction.accuracy),
+            st.cuda_stream, stats, C.byref(res), C.byref(yp)))
+        y = a if yp.value == a.data_ptr() else b
+        return y, {"stats_raw": stats, "records": [], "requests": [], "layers": [], "pass": res}
 
     def lookahead(self, x: torch.Tensor, layer: int, horizon: int | None = None, stream=None):
         """Live-mode prediction: the gates of layers

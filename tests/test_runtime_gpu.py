@@ -160,6 +160,35 @@ def test_native_trace_predictor_matches_python_predictor():
     assert streams[0] == streams[1]
 
 
+def test_native_pass_equals_per_layer_pass():
+    """hm_runtime_forward_pass (one call per pass) == the Python per-layer loop:
+    same outputs and the same PassResult (decisions)."""
+    from paper_2504_05897_b200.moe import TracePredictor
+    cfg = SHAPES["tiny"]
+    prof = stress_profile(cfg)
+    policy = me.EnginePolicy(prefetch=True)
+    trace, logits = generate_router_logits(cfg, GenParams(seed=6), 32, 4)
+    outs = []
+    for native in (False, True):
+        moe = HybridMoE(cfg, "tiny", policy, 0.5, prof, max_tokens=64)
+        moe.init_seeded_weights(4)
+        g = torch.Generator(device="cuda").manual_seed(3)
+        ys, results = [], []
+        for p, fwd in enumerate(trace.passes):
+            lg = [torch.from_numpy(np.ascontiguousarray(logits[p][l], dtype=np.float32)).cuda()
+                  for l in range(cfg.num_layers)]
+            x = torch.randn((fwd.token_count, moe.H), generator=g, device="cuda").to(torch.bfloat16)
+            y, info = moe.forward_pass(x, lg, predict=TracePredictor(trace, p, 5), decision_log=not native)
+            torch.cuda.synchronize()
+            ys.append(y.float().cpu().numpy())
+            r = info["pass"]
+            results.append((r.latency, r.lookups, r.hits, r.inserts, r.evictions, r.prefetch_issued))
+        outs.append((ys, results))
+    assert outs[0][1] == outs[1][1]
+    for a, b in zip(outs[0][0], outs[1][0]):
+        assert np.array_equal(a, b)
+
+
 def test_model_mode_runs_and_is_deterministic():
     cfg = SHAPES["tiny"]
     moe = HybridMoE(cfg, "tiny", me.EnginePolicy(), 0.25, stress_profile(cfg), max_tokens=32)
