@@ -416,6 +416,7 @@ def run_ours(args) -> None:
                               "pcie_gbs": bw_pcie / 1e9},
             "per_step": {"gpu_experts": n_gpu, "cpu_experts": n_cpu, "transfers": n_xfer,
                          "host_decide_us_per_layer": statistics.mean(s.t_decide_us for s in stats_all),
+                         "host_wait_router_us_per_layer": statistics.mean(s.t_wait_router_us for s in stats_all),
                          "cpu_worker_ms": sum(s.t_cpu_us for s in stats_all) / 1e3 / args.steps},
             "profile": {k: getattr(cal.profile, k) for k in ("gpu_time_per_expert", "cpu_slope", "transfer_bandwidth",
                                                               "transfer_latency", "gpu_slope",

@@ -376,6 +376,8 @@ int hm_cpu_set_prefetch(int dist, int hint);
 int hm_cpu_experts_decode(hm_cpu_pool *pool, const uint16_t *const *imgs, const uint16_t *const *xs, int n,
                           int H, int I, float *const *outs);
 /* Best-of-reps host DRAM read bandwidth (GB/s) over `bytes` at p (64-byte aligned). */
+/* Decode split granularity in gate/up pairs (0: whole 128-pair blocks); tuning knob. */
+int hm_cpu_set_decode_grain(int grain);
 int hm_host_read_bw(hm_cpu_pool *pool, const void *p, size_t bytes, int reps, double *gbs);
 
 typedef struct hm_runtime hm_runtime;

@@ -268,6 +268,33 @@ void phase1_stream(const uint16_t *img, int H, int I, const uint16_t *x, uint16_
   }
 }
 
+// Decode phase 1 over pairs [i0, i1) (any range): inside each 128-pair block
+// the gate rows of the range, then its up rows -- two sequential streams.
+// Pair-granular ranges balance the threads when a layer's experts are small
+// (DeepSeek: 11 blocks per expert would leave 16 threads 9 % imbalanced).
+void phase1_pairs(const uint16_t *img, int H, int I, const uint16_t *x, uint16_t *h, int i0, int i1) {
+  float g[kIlv], u[kIlv];
+  while (i0 < i1) {
+    const int b = i0 / kIlv, s = i0 % kIlv;
+    const int n = std::min(i1, (b + 1) * kIlv) - i0;
+    const uint16_t *blk = img + static_cast<size_t>(b) * 2 * kIlv * H;
+    stream_rows(blk + static_cast<size_t>(s) * H, n, H, x, g);
+    stream_rows(blk + static_cast<size_t>(kIlv + s) * H, n, H, x, u);
+    for (int i = 0; i < n; ++i) h[i0 + i] = f2bf(silu(g[i]) * u[i]);
+    i0 += n;
+  }
+}
+
+// Decode work split granularity (pairs in phase 1, rows in phase 2); 0 = the
+// legacy whole-128-pair-block split.  Process-wide tuning knob.
+int &decode_grain() {
+  static int g = [] {
+    const char *s = std::getenv("HM_DECODE_GRAIN");
+    return s ? std::atoi(s) : 16;
+  }();
+  return g;
+}
+
 // ------------------------------------------------------------ AMX (prefill)
 // Multi-token experts on the AMX tile unit: out^T = W . X^T with A = 16 weight
 // rows x 32 K (row-major, loaded straight from the image) and B = 16 token
@@ -440,13 +467,25 @@ void cpu_experts_decode(ThreadPool &pool, const uint16_t *const *imgs, const uin
   hbuf.resize(static_cast<size_t>(n) * I);
   uint16_t *h = hbuf.data();
   const int nblk = I / kIlv;
+  const int grain = decode_grain();
   pool.run([&](int tid, int nt) {
-    const long u1 = static_cast<long>(n) * nblk;
-    for (long u = u1 * tid / nt; u < u1 * (tid + 1) / nt;) {
-      const int e = static_cast<int>(u / nblk), b0 = static_cast<int>(u % nblk);
-      const int b1 = static_cast<int>(std::min<long>(nblk, b0 + (u1 * (tid + 1) / nt - u)));
-      phase1_stream(imgs[e], H, I, xs[e], h + static_cast<size_t>(e) * I, b0, b1);
-      u += b1 - b0;
+    if (grain <= 0) {
+      const long u1 = static_cast<long>(n) * nblk;
+      for (long u = u1 * tid / nt; u < u1 * (tid + 1) / nt;) {
+        const int e = static_cast<int>(u / nblk), b0 = static_cast<int>(u % nblk);
+        const int b1 = static_cast<int>(std::min<long>(nblk, b0 + (u1 * (tid + 1) / nt - u)));
+        phase1_stream(imgs[e], H, I, xs[e], h + static_cast<size_t>(e) * I, b0, b1);
+        u += b1 - b0;
+      }
+    } else {  // contiguous pair ranges of `grain`-pair units over the flat (expert, pair) space
+      const long nu = (static_cast<long>(n) * I + grain - 1) / grain;
+      const long p0 = nu * tid / nt * grain, p1 = std::min<long>(static_cast<long>(n) * I, nu * (tid + 1) / nt * grain);
+      for (long q = p0; q < p1;) {
+        const int e = static_cast<int>(q / I), i0 = static_cast<int>(q % I);
+        const int i1 = static_cast<int>(std::min<long>(I, i0 + (p1 - q)));
+        phase1_pairs(imgs[e], H, I, xs[e], h + static_cast<size_t>(e) * I, i0, i1);
+        q += i1 - i0;
+      }
     }
     pool.barrier();
     const long r1 = static_cast<long>(n) * H;
@@ -536,6 +575,14 @@ int hm_cpu_set_prefetch(int dist, int hint) {
   HM_REQUIRE(dist >= 0 && hint >= 0 && hint <= 3, HM_EVALUE, "bad prefetch setting");
   hm::pf_cfg().dist = dist;
   hm::pf_cfg().hint = hint;
+  HM_API_END
+}
+
+// Tuning knob for the decode split granularity (pairs; 0 = whole 128-pair blocks).
+int hm_cpu_set_decode_grain(int grain) {
+  HM_API_BEGIN
+  HM_REQUIRE(grain >= 0, HM_EVALUE, "bad decode grain");
+  hm::decode_grain() = grain;
   HM_API_END
 }
 

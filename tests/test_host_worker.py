@@ -47,9 +47,12 @@ def test_cpu_expert_matches_oracle(pool, H, I, M):
     assert np.abs(out - want).max() / np.abs(want).max() <= 1e-2
 
 
-def test_cpu_experts_decode_batch(pool):
-    rng = np.random.default_rng(9)
-    H, I, n = 512, 384, 3
+@pytest.mark.parametrize("grain", [0, 5, 16, 64])
+@pytest.mark.parametrize("H,I,n", [(512, 384, 3), (256, 1408, 4)])
+def test_cpu_experts_decode_batch(pool, grain, H, I, n):
+    rng = np.random.default_rng(9 + grain)
+    lib.hm_cpu_set_decode_grain.argtypes = [C.c_int]
+    _lib.check(lib.hm_cpu_set_decode_grain(grain))
     exps = [_expert(rng, H, I) for _ in range(n)]
     xs = [ref.f32_to_bf16(rng.standard_normal((1, H)).astype(np.float32)) for _ in range(n)]
     outs = [np.empty((1, H), np.float32) for _ in range(n)]
@@ -59,6 +62,7 @@ def test_cpu_experts_decode_batch(pool):
     for (img, ex), x, o in zip(exps, xs, outs):
         want = ref.expert(ref.bf16_to_f32(x), *ex)
         assert np.abs(o - want).max() / np.abs(want).max() <= 1e-2
+    _lib.check(lib.hm_cpu_set_decode_grain(16))
 
 
 def test_host_read_bandwidth_probe(pool):
