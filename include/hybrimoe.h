@@ -307,6 +307,16 @@ int hm_router_fused_small(const float *logits, int T, int N, int ld, int K, int 
                           int n_shared, int shared_gate_col, const uint16_t *x, int H, int32_t *sel,
                           float *w, int32_t *pos, int32_t *row_src, uint16_t *xp, int32_t *meta_i,
                           double *meta_d, void *stream);
+/* hm_router_fused_small plus a mirror in mapped pinned host memory (device
+ * views of cudaHostAlloc(..., cudaHostAllocMapped) buffers): the meta block,
+ * optionally the routed rows of xp (host_xp may be NULL), then *host_flag =
+ * seq after a system-scope fence -- the host spins on the flag instead of a
+ * D2H copy + event wait (the LayerRequest hand-off of engine.py:288-306). */
+int hm_router_fused_mirror(const float *logits, int T, int N, int ld, int K, int renormalize,
+                           int n_shared, int shared_gate_col, const uint16_t *x, int H, int32_t *sel,
+                           float *w, int32_t *pos, int32_t *row_src, uint16_t *xp, int32_t *meta_i,
+                           double *meta_d, int32_t *host_meta_i, double *host_meta_d,
+                           uint16_t *host_xp, uint32_t *host_flag, uint32_t seq, void *stream);
 /* score_sum[e] = sum_t probs[t, e] in fp64, fixed reduction order; the
  * LayerRequest scores are score_sum normalised (tracegen.py:149-150). */
 int hm_score_sums(const float *probs, int T, int N, double *score_sum, void *stream);
@@ -359,6 +369,14 @@ long long hm_launch_count(void);
  * fp64 with explicit round-to-nearest mul/add (bit-identical to the host core). */
 int hm_mrs_update_dev(double *S, const double *scores, int layer, int N, int p,
                       double alpha, void *stream);
+/* Decode tail in one launch: hm_combine (Eq. 1 + residual) where positions
+ * whose bit is set in host_mask4 (4 x 64 bits, positions < 256; NULL = none)
+ * are read zero-copy from host_out (device view of the host worker's mapped
+ * output rows), plus, when S != NULL, hm_mrs_update_dev for `layer` (N <= 256). */
+int hm_combine_tail(const float *out, const float *host_out, const uint64_t *host_mask4,
+                    const int32_t *pos, const float *w, int T, int Kp, int H,
+                    const uint16_t *residual, uint16_t *y, double *S, const double *scores, int layer,
+                    int N, int p, double alpha, void *stream);
 
 /* ======================================================================= */
 /* Host worker (AVX-512 BF16) and the layer executor.                        */

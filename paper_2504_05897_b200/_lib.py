@@ -243,6 +243,12 @@ _DEV_SIGS = {
                       C.c_int),
     "hm_combine": ([vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp, vp], C.c_int),
     "hm_mrs_update_dev": ([vp, vp, C.c_int, C.c_int, C.c_int, f64, vp], C.c_int),
+    "hm_router_fused_small": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int,
+                               vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "hm_router_fused_mirror": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int,
+                                vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_uint32, vp], C.c_int),
+    "hm_combine_tail": ([vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int,
+                         f64, vp], C.c_int),
 }
 for _name, (_args, _res) in _DEV_SIGS.items():
     _f = getattr(lib, _name)

@@ -101,16 +101,30 @@ __global__ void router_topk_kernel(const float *__restrict__ logits, int T, int 
 // core's arithmetic), expert offsets, the permutation and the row gather.
 // meta = [counts E | offsets E+1] int32 followed (8-byte aligned) by
 // [score_sum N | scores N] fp64, so one D2H copy carries the LayerRequest.
+// Optional mirror of the fused router's results in mapped pinned host memory
+// (device pointers of cudaHostAlloc'd buffers): the LayerRequest block, the
+// routed rows of xp for the host worker, and a completion flag the host spins
+// on -- no D2H copy and no event round trip on the per-layer critical path.
+struct HostMirror {
+  int32_t *meta_i;
+  double *meta_d;
+  uint16_t *xp;
+  uint32_t *flag;
+  uint32_t seq;
+};
+
 constexpr int kFusedMaxRows = 1024;
 constexpr int kFusedMaxE = 320;
 
 __global__ void __launch_bounds__(256) router_fused_small_kernel(
     const float *__restrict__ logits, int T, int N, int ld, int K, int renorm, int n_shared, int shared_gate_col,
     const uint16_t *__restrict__ x, int H, int32_t *__restrict__ sel, float *__restrict__ w, int32_t *__restrict__ pos,
-    int32_t *__restrict__ row_src, uint16_t *__restrict__ xp, int32_t *__restrict__ meta_i, double *__restrict__ meta_d) {
+    int32_t *__restrict__ row_src, uint16_t *__restrict__ xp, int32_t *__restrict__ meta_i, double *__restrict__ meta_d,
+    HostMirror hm_) {
   __shared__ int32_t s_sel[kFusedMaxRows];
   __shared__ int32_t s_counts[kFusedMaxE];
   __shared__ int32_t s_off[kFusedMaxE + 1];
+  __shared__ int32_t s_rowtok[kFusedMaxRows];
   __shared__ float s_probs[32 * 256];  // T <= 32 tokens x N <= 256
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int E = N + n_shared, Kp = K + n_shared, R = T * Kp;
@@ -183,24 +197,50 @@ __global__ void __launch_bounds__(256) router_fused_small_kernel(
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {  // offsets, fp64 score sums, normalised scores (sequential, host order)
-    int32_t run = 0;
-    for (int e = 0; e < E; ++e) {
+  // offsets: warp 0 scans the counts (each lane a contiguous run of experts);
+  // fp64 score sums: thread e sums its column over tokens in token order;
+  // everything stays in shared memory (a global store followed by a load of
+  // the same word costs an L2 round trip per element when done serially).
+  __shared__ double s_sum[256];
+  __shared__ double s_tot;
+  if (wid == 0) {
+    const int per = (E + 31) / 32, e0 = min(E, lane * per), e1 = min(E, e0 + per);
+    int32_t local = 0;
+    for (int e = e0; e < e1; ++e) local += s_counts[e];
+    int32_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int32_t run = incl - local;
+    for (int e = e0; e < e1; ++e) {
       s_off[e] = run;
-      meta_i[e] = s_counts[e];
-      meta_i[E + e] = run;
       run += s_counts[e];
     }
-    s_off[E] = run;
-    meta_i[2 * E] = run;
+    if (lane == 31) s_off[E] = incl;
+  }
+  for (int e = threadIdx.x; e < N; e += blockDim.x) {
+    double acc = 0.0;
+    for (int t = 0; t < T; ++t) acc += static_cast<double>(s_probs[t * N + e]);
+    s_sum[e] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // the host core's order: tot = sum_e score_sum[e], e ascending
     double tot = 0.0;
-    for (int e = 0; e < N; ++e) {
-      double acc = 0.0;
-      for (int t = 0; t < T; ++t) acc += static_cast<double>(s_probs[t * N + e]);
-      meta_d[e] = acc;
-      tot += acc;
-    }
-    for (int e = 0; e < N; ++e) meta_d[N + e] = tot > 0.0 ? meta_d[e] / tot : 0.0;
+    for (int e = 0; e < N; ++e) tot += s_sum[e];
+    s_tot = tot;
+  }
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    meta_i[e] = s_counts[e];
+    meta_i[E + e] = s_off[e];
+  }
+  if (threadIdx.x == 0) meta_i[2 * E] = s_off[E];
+  __syncthreads();
+  for (int e = threadIdx.x; e < N; e += blockDim.x) {
+    const double tot = s_tot;
+    meta_d[e] = s_sum[e];
+    meta_d[N + e] = tot > 0.0 ? s_sum[e] / tot : 0.0;
   }
   __syncthreads();
   for (int j = threadIdx.x; j < R; j += blockDim.x) {  // stable rank inside the expert
@@ -211,15 +251,32 @@ __global__ void __launch_bounds__(256) router_fused_small_kernel(
     sel[j] = e;
     pos[j] = p;
     row_src[p] = j;
+    s_rowtok[p] = j / Kp;  // token of the row at position p (shared: no global round trip)
   }
   __syncthreads();
   const int H8 = H / 8;
+  const int n_host = hm_.xp ? s_off[N] : 0;  // routed rows also go to the host worker's input
+#pragma unroll 4
   for (int v = threadIdx.x; v < R * H8; v += blockDim.x) {  // gather rows in permuted order
-    const int p = v / H8, c = v % H8;
-    // invert: the row at position p came from selection j = row_src[p] (written above, block-visible)
-    const int t = row_src[p] / Kp;
-    reinterpret_cast<uint4 *>(xp + static_cast<size_t>(p) * H)[c] =
-        reinterpret_cast<const uint4 *>(x + static_cast<size_t>(t) * H)[c];
+    const int p = v / H8, c = v - p * H8;
+    const uint4 v4 = __ldg(reinterpret_cast<const uint4 *>(x + static_cast<size_t>(s_rowtok[p]) * H) + c);
+    reinterpret_cast<uint4 *>(xp + static_cast<size_t>(p) * H)[c] = v4;
+    if (p < n_host) reinterpret_cast<uint4 *>(hm_.xp + static_cast<size_t>(p) * H)[c] = v4;
+  }
+  if (hm_.flag) {  // LayerRequest straight into mapped host memory, then the flag
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+      hm_.meta_i[e] = s_counts[e];
+      hm_.meta_i[E + e] = s_off[e];
+    }
+    if (threadIdx.x == 0) hm_.meta_i[2 * E] = s_off[E];
+    for (int e = threadIdx.x; e < N; e += blockDim.x) {
+      const double tot = s_tot;
+      hm_.meta_d[e] = s_sum[e];
+      hm_.meta_d[N + e] = tot > 0.0 ? s_sum[e] / tot : 0.0;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) *reinterpret_cast<volatile uint32_t *>(hm_.flag) = hm_.seq;
   }
 }
 
@@ -380,11 +437,110 @@ __global__ void combine_kernel(const float *__restrict__ out, const int32_t *__r
   }
 }
 
+// Decode tail in one launch: blocks [0, T) combine (Eq. 1) + residual, rows
+// whose bit is set in host_mask read straight from the host worker's mapped
+// output buffer (zero-copy, no H2D); block T (if S) folds the layer's scores
+// into the MRS table like mrs_update_kernel.
+struct CombineTail {
+  const float *out, *host_out;
+  const int32_t *pos;
+  const float *w;
+  int Kp, H;
+  const uint16_t *residual;
+  uint16_t *y;
+  unsigned long long host_mask[4];  // positions < 256
+  double *S;
+  const double *scores;
+  int layer, N, p;
+  double a;
+};
+
+__device__ void mrs_row_update(double *__restrict__ S, const double *__restrict__ s, int layer, int N, int p,
+                               double a);
+
+// grid: T * cs column blocks (128 threads x 4 columns each) + 1 MRS block.
+constexpr int kTailThreads = 128;
+constexpr int kTailMaxKp = 64;
+
+__global__ void __launch_bounds__(kTailThreads) combine_tail_kernel(const __grid_constant__ CombineTail c) {
+  __shared__ float s_w[kTailMaxKp];
+  __shared__ int32_t s_pos[kTailMaxKp];
+  __shared__ double s_sc[256];
+  const int cs = (c.H + 4 * kTailThreads - 1) / (4 * kTailThreads);
+  const int b = blockIdx.x;
+  if (c.S && b == static_cast<int>(gridDim.x) - 1) {  // MRS row (scores staged in smem)
+    for (int i = threadIdx.x; i < c.N; i += blockDim.x) s_sc[i] = c.scores[i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < c.N; i += blockDim.x) {
+      const double si = s_sc[i];
+      int rank = 0;
+      for (int j = 0; j < c.N; ++j) {
+        const double sj = s_sc[j];
+        rank += (sj > si || (sj == si && j < i)) ? 1 : 0;
+      }
+      const double t = rank < c.p ? si : 0.0;
+      double *row = c.S + static_cast<size_t>(c.layer) * c.N;
+      row[i] = __dadd_rn(__dmul_rn(c.a, t), __dmul_rn(__dsub_rn(1.0, c.a), row[i]));
+    }
+    return;
+  }
+  const int t = b / cs, col = ((b % cs) * kTailThreads + threadIdx.x) * 4;
+  for (int k = threadIdx.x; k < c.Kp; k += blockDim.x) {
+    s_w[k] = c.w[static_cast<size_t>(t) * c.Kp + k];
+    s_pos[k] = c.pos[static_cast<size_t>(t) * c.Kp + k];
+  }
+  __syncthreads();
+  if (col >= c.H) return;
+  uint2 rv = make_uint2(0u, 0u);
+  if (c.residual) rv = *reinterpret_cast<const uint2 *>(c.residual + static_cast<size_t>(t) * c.H + col);
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  constexpr int U = 8;  // issue U independent row loads before accumulating (k order kept)
+  for (int k0 = 0; k0 < c.Kp; k0 += U) {
+    float4 o[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u;
+      o[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k < c.Kp && s_w[k] != 0.0f) {
+        const int pp = s_pos[k];
+        const bool host = pp < 256 && ((c.host_mask[pp >> 6] >> (pp & 63)) & 1ull);
+        o[u] = *reinterpret_cast<const float4 *>((host ? c.host_out : c.out) + static_cast<size_t>(pp) * c.H + col);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u;
+      if (k < c.Kp && s_w[k] != 0.0f) {
+        const float wk = s_w[k];
+        a0 = fmaf(wk, o[u].x, a0);
+        a1 = fmaf(wk, o[u].y, a1);
+        a2 = fmaf(wk, o[u].z, a2);
+        a3 = fmaf(wk, o[u].w, a3);
+      }
+    }
+  }
+  if (c.residual) {
+    a0 += dev::bf_lo(rv.x);
+    a1 += dev::bf_hi(rv.x);
+    a2 += dev::bf_lo(rv.y);
+    a3 += dev::bf_hi(rv.y);
+  }
+  uint2 o2;
+  o2.x = dev::pack_bf2(a0, a1);
+  o2.y = dev::pack_bf2(a2, a3);
+  *reinterpret_cast<uint2 *>(c.y + static_cast<size_t>(t) * c.H + col) = o2;
+}
+
 // S[layer, i] <- a * TopP(s)[i] + (1 - a) * S[layer, i]   (caching.py:58-76)
 // Round-to-nearest intrinsics keep every operation a separate IEEE rounding,
 // exactly like the host core (no FMA contraction).
 __global__ void mrs_update_kernel(double *__restrict__ S, const double *__restrict__ s, int layer, int N, int p,
                                   double a) {
+  mrs_row_update(S, s, layer, N, p, a);
+}
+
+__device__ void mrs_row_update(double *__restrict__ S, const double *__restrict__ s, int layer, int N, int p,
+                               double a) {
   const int i = threadIdx.x;
   if (i >= N) return;
   const double si = s[i];
@@ -440,7 +596,24 @@ int hm_router_fused_small(const float *logits, int T, int N, int ld, int K, int 
                  T * (K + n_shared) <= hm::kFusedMaxRows && N + n_shared <= hm::kFusedMaxE && H % 8 == 0,
              HM_EVALUE, "shape outside the fused small-T router");
   hm::router_fused_small_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      logits, T, N, ld, K, renormalize, n_shared, shared_gate_col, x, H, sel, w, pos, row_src, xp, meta_i, meta_d);
+      logits, T, N, ld, K, renormalize, n_shared, shared_gate_col, x, H, sel, w, pos, row_src, xp, meta_i, meta_d,
+      hm::HostMirror{});
+  HM_LAUNCH_CHECK();
+  HM_API_END
+}
+
+int hm_router_fused_mirror(const float *logits, int T, int N, int ld, int K, int renormalize, int n_shared,
+                           int shared_gate_col, const uint16_t *x, int H, int32_t *sel, float *w, int32_t *pos,
+                           int32_t *row_src, uint16_t *xp, int32_t *meta_i, double *meta_d, int32_t *host_meta_i,
+                           double *host_meta_d, uint16_t *host_xp, uint32_t *host_flag, uint32_t seq, void *stream) {
+  HM_API_BEGIN
+  HM_REQUIRE(T >= 1 && T <= 32 && N >= 1 && N <= 256 && K >= 1 && K <= 8 && K <= N && ld >= N &&
+                 T * (K + n_shared) <= hm::kFusedMaxRows && N + n_shared <= hm::kFusedMaxE && H % 8 == 0,
+             HM_EVALUE, "shape outside the fused small-T router");
+  HM_REQUIRE(host_meta_i && host_meta_d && host_flag, HM_EVALUE, "host mirror needs meta and flag pointers");
+  hm::router_fused_small_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      logits, T, N, ld, K, renormalize, n_shared, shared_gate_col, x, H, sel, w, pos, row_src, xp, meta_i, meta_d,
+      hm::HostMirror{host_meta_i, host_meta_d, host_xp, host_flag, seq});
   HM_LAUNCH_CHECK();
   HM_API_END
 }
@@ -529,6 +702,39 @@ int hm_residual_add(const float *y32, const uint16_t *residual, int T, int H, ui
   HM_REQUIRE(H % 4 == 0, HM_EVALUE, "hidden size must be a multiple of 4");
   if (T > 0) {
     hm::residual_add_kernel<<<T, 256, 0, static_cast<cudaStream_t>(stream)>>>(y32, residual, H, y);
+    HM_LAUNCH_CHECK();
+  }
+  HM_API_END
+}
+
+int hm_combine_tail(const float *out, const float *host_out, const uint64_t *host_mask4, const int32_t *pos,
+                    const float *w, int T, int Kp, int H, const uint16_t *residual, uint16_t *y, double *S,
+                    const double *scores, int layer, int N, int p, double alpha, void *stream) {
+  HM_API_BEGIN
+  HM_REQUIRE(H % 4 == 0, HM_EVALUE, "hidden size must be a multiple of 4");
+  HM_REQUIRE(!S || (N >= 1 && N <= 256), HM_EVALUE, "MRS row too wide for the fused tail");
+  hm::CombineTail c{};
+  c.out = out;
+  c.host_out = host_out;
+  c.pos = pos;
+  c.w = w;
+  c.Kp = Kp;
+  c.H = H;
+  c.residual = residual;
+  c.y = y;
+  for (int i = 0; i < 4; ++i) c.host_mask[i] = host_mask4 ? host_mask4[i] : 0ull;
+  HM_REQUIRE(!host_mask4 || host_out, HM_EVALUE, "host rows need the host output buffer");
+  c.S = S;
+  c.scores = scores;
+  c.layer = layer;
+  c.N = N;
+  c.p = p;
+  c.a = alpha;
+  HM_REQUIRE(Kp <= hm::kTailMaxKp, HM_EVALUE, "too many selections per token for the fused tail");
+  const int cs = (H + 4 * hm::kTailThreads - 1) / (4 * hm::kTailThreads);
+  const long blocks = static_cast<long>(T) * cs + (S ? 1 : 0);
+  if (blocks > 0) {
+    hm::combine_tail_kernel<<<static_cast<unsigned>(blocks), hm::kTailThreads, 0, static_cast<cudaStream_t>(stream)>>>(c);
     HM_LAUNCH_CHECK();
   }
   HM_API_END

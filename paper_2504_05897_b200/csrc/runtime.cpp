@@ -14,7 +14,9 @@
 // same layer, engine.py:318-330), and a kernel waits for its slot's copy.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -37,6 +39,11 @@ int hm_predict_layers(const int64_t *, int, int, int64_t, int, int64_t, int, dou
 int hm_router_fused_small(const float *, int, int, int, int, int, int, int, const uint16_t *, int, int32_t *,
                           float *, int32_t *, int32_t *, uint16_t *, int32_t *, double *, void *);
 int hm_combine_f32(const float *, const int32_t *, const float *, int, int, int, float *, void *);
+int hm_router_fused_mirror(const float *, int, int, int, int, int, int, int, const uint16_t *, int, int32_t *, float *,
+                           int32_t *, int32_t *, uint16_t *, int32_t *, double *, int32_t *, double *, uint16_t *,
+                           uint32_t *, uint32_t, void *);
+int hm_combine_tail(const float *, const float *, const uint64_t *, const int32_t *, const float *, int, int, int,
+                    const uint16_t *, uint16_t *, double *, const double *, int, int, int, double, void *);
 }
 
 namespace hm {
@@ -83,6 +90,14 @@ struct Runtime {
   double *h_score_sum = nullptr, *h_scores = nullptr;
   uint16_t *h_x = nullptr;
   float *h_out = nullptr;
+  // zero-copy decode path (HM_ZERO_COPY, default on): device views of the
+  // mapped pinned buffers above, and the router's completion flag
+  bool zero_copy = true;
+  void *dv_hmeta = nullptr;
+  uint16_t *dv_h_x = nullptr;
+  float *dv_h_out = nullptr;
+  uint32_t *h_flag = nullptr, *dv_flag = nullptr;
+  uint32_t seq = 0;
   std::unique_ptr<ThreadPool> workers;
   std::vector<uint16_t> hbuf;
   std::vector<int64_t> loads;
@@ -158,7 +173,7 @@ struct Runtime {
     meta_ioff = ((2 * static_cast<size_t>(E) + 1) * 4 + 7) / 8 * 8;
     meta_bytes = meta_ioff + 2 * static_cast<size_t>(N) * 8;
     RT_CUDA(cudaMalloc(&dmeta, meta_bytes));
-    RT_CUDA(cudaHostAlloc(&hmeta, meta_bytes, 0));
+    RT_CUDA(cudaHostAlloc(&hmeta, meta_bytes, cudaHostAllocMapped));
     counts = reinterpret_cast<int32_t *>(dmeta);
     offsets = counts + E;
     score_sum = reinterpret_cast<double *>(static_cast<char *>(dmeta) + meta_ioff);
@@ -175,8 +190,15 @@ struct Runtime {
     std::vector<double> prior(static_cast<size_t>(L) * N, 1.0 / static_cast<double>(N));
     RT_CUDA(cudaMemcpy(S_dev, prior.data(), prior.size() * 8, cudaMemcpyHostToDevice));
     RT_CUDA(cudaHostAlloc(&h_scores, N * 8, 0));
-    RT_CUDA(cudaHostAlloc(&h_x, rows * H * 2, 0));
-    RT_CUDA(cudaHostAlloc(&h_out, rows * H * 4, 0));
+    RT_CUDA(cudaHostAlloc(&h_x, rows * H * 2, cudaHostAllocMapped));
+    RT_CUDA(cudaHostAlloc(&h_out, rows * H * 4, cudaHostAllocMapped));
+    RT_CUDA(cudaHostAlloc(&h_flag, 64, cudaHostAllocMapped));
+    *reinterpret_cast<volatile uint32_t *>(h_flag) = 0;
+    if (const char *zc = std::getenv("HM_ZERO_COPY")) zero_copy = std::atoi(zc) != 0;
+    RT_CUDA(cudaHostGetDevicePointer(&dv_hmeta, hmeta, 0));
+    RT_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dv_h_x), h_x, 0));
+    RT_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dv_h_out), h_out, 0));
+    RT_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dv_flag), h_flag, 0));
     workers.reset(new ThreadPool(c.cpu_threads > 0 ? c.cpu_threads
                                                    : static_cast<int>(std::thread::hardware_concurrency())));
     loads.assign(N, 0);
@@ -196,7 +218,7 @@ struct Runtime {
                     static_cast<void *>(S_dev)})
       if (p) cudaFree(p);
     for (void *p : {static_cast<void *>(store), hmeta, static_cast<void *>(h_scores), static_cast<void *>(h_x),
-                    static_cast<void *>(h_out)})
+                    static_cast<void *>(h_out), static_cast<void *>(h_flag)})
       if (p) cudaFreeHost(p);
   }
 
@@ -210,6 +232,22 @@ struct Runtime {
   uint16_t *slot_ptr(int64_t s) const { return pool + static_cast<size_t>(s) * slot_elems; }
   const uint16_t *image_ptr(uint32_t ref) const {
     return store + static_cast<size_t>(image_of(ref_layer(ref), ref_expert(ref))) * slot_elems;
+  }
+
+  // Spin until the router kernel raised this layer's flag; poll the stream now
+  // and then so a failed launch surfaces as an error instead of a hang.
+  void wait_flag(cudaStream_t st) {
+    volatile uint32_t *f = h_flag;
+    for (uint64_t i = 1;; ++i) {
+      if (*f == seq) break;
+      if ((i & 4095) == 0) {
+        const cudaError_t e = cudaStreamQuery(st);
+        if (e != cudaSuccess && e != cudaErrorNotReady) RT_CUDA(e);
+        if (e == cudaSuccess && *f != seq) raise(HM_ECUDA, "router finished without raising the host flag");
+      }
+      __builtin_ia32_pause();
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
   }
 
   void issue_copy(uint32_t ref, int64_t slot, cudaStream_t /*compute*/) {
@@ -230,7 +268,18 @@ struct Runtime {
     // LayerRequest (counts, offsets, score sums, scores) lands in one pinned
     // buffer with a single D2H copy: the only per-layer host synchronisation
     const bool fused = T <= 32 && rows <= 1024 && N <= 256 && E <= 320 && H % 8 == 0;
-    if (fused) {  // decode: one launch does router .. gather
+    // zero-copy: the router writes the LayerRequest (and, when small, the routed
+    // rows) into mapped host memory and raises a flag the host spins on
+    const bool mirror = fused && zero_copy;
+    const bool mirror_rows = mirror && static_cast<size_t>(T) * K * H * 2 <= (512u << 10);
+    if (mirror) {
+      ++seq;
+      ok(hm_router_fused_mirror(logits, T, N, ld, K, cfg.renormalize, S, cfg.shared_gate_col, x, H, sel, w, pos,
+                                row_src, xp, counts, score_sum, static_cast<int32_t *>(dv_hmeta),
+                                reinterpret_cast<double *>(static_cast<char *>(dv_hmeta) + meta_ioff),
+                                mirror_rows ? dv_h_x : nullptr, dv_flag, seq, vs));
+      if (W > 1) ok(hm_mask_nonhome(sel, w, T * Kp, N, R, W, vs));
+    } else if (fused) {  // decode: one launch does router .. gather
       ok(hm_router_fused_small(logits, T, N, ld, K, cfg.renormalize, S, cfg.shared_gate_col, x, H, sel, w, pos,
                                row_src, xp, counts, score_sum, vs));
       if (W > 1) ok(hm_mask_nonhome(sel, w, T * Kp, N, R, W, vs));
@@ -247,7 +296,11 @@ struct Runtime {
       ok(hm_gather_rows(x, row_src, rows, Kp, H, xp, vs));
     }
     double t0 = now_us();
-    RT_CUDA(cudaEventSynchronize(ev_req));
+    if (mirror) {
+      wait_flag(st);
+    } else {
+      RT_CUDA(cudaEventSynchronize(ev_req));
+    }
     double t1 = now_us();
     s.t_wait_router_us = t1 - t0;
 
@@ -271,12 +324,14 @@ struct Runtime {
     std::vector<uint32_t> cpu_refs;
     for (const Event &ev : rec.plan.events)
       if (ev.device == HM_DEV_CPU) cpu_refs.push_back(ev.ref);
-    for (uint32_t r : cpu_refs) {
-      const int e = ref_expert(r);
-      const size_t rb = h_offsets[e], rc = h_counts[e];
-      RT_CUDA(cudaMemcpyAsync(h_x + rb * H, xp + rb * H, rc * H * 2, cudaMemcpyDeviceToHost, st));
+    if (!mirror_rows) {
+      for (uint32_t r : cpu_refs) {
+        const int e = ref_expert(r);
+        const size_t rb = h_offsets[e], rc = h_counts[e];
+        RT_CUDA(cudaMemcpyAsync(h_x + rb * H, xp + rb * H, rc * H * 2, cudaMemcpyDeviceToHost, st));
+      }
+      if (!cpu_refs.empty()) RT_CUDA(cudaEventRecord(ev_rows, st));
     }
-    if (!cpu_refs.empty()) RT_CUDA(cudaEventRecord(ev_rows, st));
 
     auto assign_of = [&](uint32_t ref) {
       for (auto &a : rec.plan.assign)
@@ -327,8 +382,20 @@ struct Runtime {
     }
 
     // CPU experts in plan CPU order (scheduling.py:257-268)
+    // CPU outputs reach the combine either zero-copy (positions < 256, the
+    // combine reads the mapped host rows) or by H2D copies into `out`
+    const bool do_mrs = cfg.gpu_mrs && engine->cfg.cache_policy == HM_POLICY_MRS && engine->mrs_;
+    const bool tail = W == 1 && (!do_mrs || fused) && N <= 256;  // combine_tail launch
+    bool zc_out = zero_copy && tail;
+    uint64_t host_mask[4] = {0, 0, 0, 0};
+    for (uint32_t r : cpu_refs) {
+      const int e = ref_expert(r);
+      const int rb = h_offsets[e], rc = h_counts[e];
+      if (rb + rc > 256) zc_out = false;
+      for (int q = rb; q < rb + rc && q < 256; ++q) host_mask[q >> 6] |= 1ull << (q & 63);
+    }
     if (!cpu_refs.empty()) {
-      RT_CUDA(cudaEventSynchronize(ev_rows));
+      if (!mirror_rows) RT_CUDA(cudaEventSynchronize(ev_rows));
       const double c0 = now_us();
       bool all_single = true;
       for (uint32_t r : cpu_refs) all_single = all_single && h_counts[ref_expert(r)] == 1;
@@ -353,11 +420,21 @@ struct Runtime {
       s.n_cpu = static_cast<int32_t>(cpu_refs.size());
       s.bytes_cpu = static_cast<int64_t>(cpu_refs.size()) * static_cast<int64_t>(slot_bytes);
       s.t_cpu_us = now_us() - c0;
-      for (uint32_t r : cpu_refs) {
-        const int e = ref_expert(r);
-        const size_t rb = h_offsets[e], rc = h_counts[e];
-        RT_CUDA(cudaMemcpyAsync(out + rb * H, h_out + rb * H, rc * H * 4, cudaMemcpyHostToDevice, st));
+      if (!zc_out) {
+        for (uint32_t r : cpu_refs) {
+          const int e = ref_expert(r);
+          const size_t rb = h_offsets[e], rc = h_counts[e];
+          RT_CUDA(cudaMemcpyAsync(out + rb * H, h_out + rb * H, rc * H * 4, cudaMemcpyHostToDevice, st));
+        }
       }
+    }
+    if (tail) {
+      // one launch: combine (+ residual, host rows zero-copy) and the MRS row
+      ok(hm_combine_tail(out, dv_h_out, zc_out && !cpu_refs.empty() ? host_mask : nullptr, pos, w, T, Kp, H,
+                         cfg.residual ? x : nullptr, y, do_mrs ? S_dev : nullptr, scores_dev, layer, N,
+                         do_mrs ? engine->mrs_->p : 0, do_mrs ? engine->mrs_->alpha : 0.0, vs));
+      if (stats) *stats = s;
+      return;
     }
     // combine (Eq. 1) with the residual stream, then the GPU copy of S
     if (W > 1) {
