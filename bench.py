@@ -230,7 +230,8 @@ def run_ours(args) -> None:
         host_images = None if avail > 1.3 * total_bytes else max(16, int(0.5 * avail / (3 * H * I * 2)))
     threads = args.cpu_threads or max(1, (os.cpu_count() or 1) // world)
     moe = HybridMoE(cfg, args.shape, policy, args.ratio, prof, host_images=host_images,
-                    max_tokens=max(args.prefill, 1), cpu_threads=threads, ep_rank=rank, ep_world=world)
+                    max_tokens=max(args.prefill, 1), cpu_threads=threads, ep_rank=rank, ep_world=world,
+                    exchange=args.exchange)
     moe.init_random_weights(seed=args.seed + rank)
     n_dec = args.warmup + args.steps
     trace, logits = generate_router_logits(cfg, GenParams(seed=args.seed), args.prefill, 2 * n_dec + 1)
@@ -402,7 +403,8 @@ def run_ours(args) -> None:
                        "host_images": moe.host_images, "policy": args.policy, "prefetch": args.prefetch,
                        "scheduling": args.scheduling,
                        "l2": "each step streams >= 2 x 352 MB of expert weights (> 126 MB L2); no flush needed",
-                       "parallelism": "ep" if world > 1 else "single"},
+                       "parallelism": f"ep{world}" if world > 1 else "single",
+                       "ep_exchange": moe.exchange},
             "prefill": {"tokens": args.prefill, "ms": prefill_ms, "cold_cache": True,
                         "gpu_experts": sum(s.n_gpu for s in pst), "cpu_experts": sum(s.n_cpu for s in pst),
                         "transfers": sum(s.n_transfer for s in pst)},
@@ -439,6 +441,8 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--shape", default="mixtral", choices=["tiny", "mixtral", "deepseek", "qwen2"])
     ap.add_argument("--ratio", type=float, default=0.25)
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "allreduce"],
+                    help="expert-parallel partial-sum exchange: fused peer-memory kernel or process-group all-reduce")
     ap.add_argument("--prefill", type=int, default=1024)
     ap.add_argument("--policy", default="mrs", choices=["mrs", "lru", "lfu"])
     ap.add_argument("--scheduling", default="hybrid",

@@ -447,7 +447,8 @@ int hm_runtime_forward_layer(hm_runtime *rt, int layer, const uint16_t *x, const
  * (ping-pong between buf0/buf1; *y_out receives the final buffer), end_pass.
  * logits: L device pointers [T, ld].  pass_loads (HOST, [L*N], optional):
  * the pass's loads for the trace-mode prediction model (hm_predict_layers).
- * stats: optional [L] array.  Single-GPU only (ep_world == 1). */
+ * stats: optional [L] array.  Under expert parallelism it needs the peer-memory
+ * exchange (hm_runtime_set_ep_exchange). */
 int hm_runtime_forward_pass(hm_runtime *rt, const uint16_t *x, const float *const *logits, int T,
                             int ld, uint16_t *buf0, uint16_t *buf1, const int64_t *pass_loads,
                             int64_t pass_index, int64_t seed, int horizon, double accuracy,
@@ -461,6 +462,30 @@ int hm_runtime_sync(hm_runtime *rt);
 /* Make experts resident (fixed residency of the baseline policies,
  * engine.py:423-434): add them to the cache and copy them into their slots. */
 int hm_runtime_preload(hm_runtime *rt, const uint32_t *refs, int n);
+/* ---- expert-parallel exchange over peer memory ---------- */
+/* One process per GPU; every rank holds the replicated hidden state and its
+ * home experts.  hm_ep owns a double-buffered fp32 inbox [2][world][max_rows*H]
+ * and per-tile flags on this GPU; peers' buffers are mapped with CUDA IPC
+ * (NVLink P2P on an NVSwitch box).  No reference counterpart: multi-GPU is a
+ * non-goal of the reference. */
+typedef struct hm_ep hm_ep;
+int hm_ep_create(int rank, int world, int max_rows, int H, hm_ep **out);
+void hm_ep_destroy(hm_ep *ep);
+/* Writes two cudaIpcMemHandle_t (64 bytes each) for this rank's buffers. */
+int hm_ep_ipc_handles(hm_ep *ep, void *inbox_handle, void *flags_handle);
+int hm_ep_open_peer(hm_ep *ep, int peer, const void *inbox_handle, const void *flags_handle);
+/* ONE kernel: this rank's partial combine (Eq. 1 over its home experts; rows in
+ * host_mask4 read zero-copy from host_out) pushed into every rank's inbox,
+ * per-tile flags, then y = residual + sum over ranks in rank order (bf16; y32
+ * optional fp32 sum without residual).  Every rank must call it the same
+ * number of times with the same T. */
+int hm_ep_combine_allreduce(hm_ep *ep, const float *out, const float *host_out,
+                            const uint64_t *host_mask4, const int32_t *pos, const float *w, int T,
+                            int Kp, int H, const uint16_t *residual, uint16_t *y, float *y32,
+                            void *stream);
+/* Route forward_layer's expert-parallel combine through `ep` (NULL: partial
+ * to hm_runtime_set_ep_output's buffer for an external all-reduce). */
+int hm_runtime_set_ep_exchange(hm_runtime *rt, hm_ep *ep);
 /* Expert parallelism (ep_world > 1): forward_layer writes this rank's partial
  * sum_k w E_k(x) over its home experts to y32 [T, H] fp32 instead of y; the
  * caller all-reduces y32 across ranks and finishes with hm_residual_add. */

@@ -42,6 +42,8 @@ int hm_combine_f32(const float *, const int32_t *, const float *, int, int, int,
 int hm_router_fused_mirror(const float *, int, int, int, int, int, int, int, const uint16_t *, int, int32_t *, float *,
                            int32_t *, int32_t *, uint16_t *, int32_t *, double *, int32_t *, double *, uint16_t *,
                            uint32_t *, uint32_t, void *);
+int hm_ep_combine_allreduce(hm_ep *, const float *, const float *, const uint64_t *, const int32_t *, const float *,
+                            int, int, int, const uint16_t *, uint16_t *, float *, void *);
 int hm_combine_tail(const float *, const float *, const uint64_t *, const int32_t *, const float *, int, int, int,
                     const uint16_t *, uint16_t *, double *, const double *, int, int, int, double, void *);
 }
@@ -71,12 +73,26 @@ struct Runtime {
   int N, K, S, E, Kp, H, I, L;
   int R = 0, W = 1;          // expert-parallel rank / world
   float *y32 = nullptr;      // EP partial output (caller-owned)
+  hm_ep *ep = nullptr;       // EP peer-memory exchange (caller-owned)
   size_t slot_elems, slot_bytes;
   int64_t n_slots;
   uint16_t *pool = nullptr;        // device: [n_slots][slot_elems]
   uint16_t *store = nullptr;       // pinned host: [host_images][slot_elems]
   cudaStream_t copy = nullptr;
   std::vector<cudaEvent_t> ready, last_use;
+  // Event bookkeeping that skips redundant stream waits/records (each is a
+  // driver call on the per-layer critical path):
+  //  * copy_pending[s]: a copy into slot s was issued and the compute stream
+  //    has not waited on it yet (once it has, stream order covers later work);
+  //  * one "use" event per expert-FFN launch (a ring), slot_use_seq[s] = the
+  //    launch that last read slot s; the copy stream waits only if it has not
+  //    already waited on that launch or a later one.
+  std::vector<uint8_t> copy_pending;
+  std::vector<int64_t> slot_use_seq;
+  static constexpr int kUseRing = 256;
+  std::vector<cudaEvent_t> use_ev;
+  int64_t use_seq = 0, copy_waited_seq = 0;
+  cudaStream_t last_compute = nullptr;
   cudaEvent_t ev_req = nullptr, ev_rows = nullptr;
   // device scratch
   int32_t *sel = nullptr, *counts = nullptr, *offsets = nullptr, *pos = nullptr, *row_src = nullptr;
@@ -157,6 +173,10 @@ struct Runtime {
     RT_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
     ready.resize(static_cast<size_t>(n_slots));
     last_use.resize(static_cast<size_t>(n_slots));
+    copy_pending.assign(static_cast<size_t>(n_slots), 0);
+    slot_use_seq.assign(static_cast<size_t>(n_slots), 0);
+    use_ev.resize(kUseRing);
+    for (auto &e : use_ev) RT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (int64_t s = 0; s < n_slots; ++s) {
       RT_CUDA(cudaEventCreateWithFlags(&ready[s], cudaEventDisableTiming));
       RT_CUDA(cudaEventCreateWithFlags(&last_use[s], cudaEventDisableTiming));
@@ -209,6 +229,7 @@ struct Runtime {
     if (copy) cudaStreamSynchronize(copy);
     for (auto e : ready) cudaEventDestroy(e);
     for (auto e : last_use) cudaEventDestroy(e);
+    for (auto e : use_ev) cudaEventDestroy(e);
     if (ev_req) cudaEventDestroy(ev_req);
     if (ev_rows) cudaEventDestroy(ev_rows);
     if (copy) cudaStreamDestroy(copy);
@@ -251,9 +272,28 @@ struct Runtime {
   }
 
   void issue_copy(uint32_t ref, int64_t slot, cudaStream_t /*compute*/) {
-    RT_CUDA(cudaStreamWaitEvent(copy, last_use[slot], 0));
+    const int64_t u = slot_use_seq[slot];
+    if (u > copy_waited_seq) {  // wait for the last kernel that read this slot
+      RT_CUDA(cudaStreamWaitEvent(copy, use_ev[u % kUseRing], 0));
+      copy_waited_seq = u;
+    }
     RT_CUDA(cudaMemcpyAsync(slot_ptr(slot), image_ptr(ref), slot_bytes, cudaMemcpyHostToDevice, copy));
     RT_CUDA(cudaEventRecord(ready[slot], copy));
+    copy_pending[slot] = 1;
+  }
+
+  // Order the compute stream after the latest copy into `slot` (if not already).
+  void wait_ready(int64_t slot, cudaStream_t st) {
+    if (!copy_pending[slot]) return;
+    RT_CUDA(cudaStreamWaitEvent(st, ready[slot], 0));
+    copy_pending[slot] = 0;
+  }
+
+  // Record that the kernels just launched on `st` read these slots.
+  void mark_used(const hm_group *g, int n, cudaStream_t st) {
+    ++use_seq;
+    RT_CUDA(cudaEventRecord(use_ev[use_seq % kUseRing], st));
+    for (int i = 0; i < n; ++i) slot_use_seq[g[i].slot] = use_seq;
   }
 
   void forward_layer(int layer, const uint16_t *x, const float *logits, int T, int ld, uint16_t *y,
@@ -264,6 +304,10 @@ struct Runtime {
     hm_layer_stats s{};
     void *vs = static_cast<void *>(st);
     const int rows = T * Kp;
+    if (st != last_compute) {  // a new compute stream: order it after every expert kernel so far
+      if (use_seq > 0) RT_CUDA(cudaStreamWaitEvent(st, use_ev[use_seq % kUseRing], 0));
+      last_compute = st;
+    }
     // (0) router, LayerRequest, permutation -- all on the compute stream; the
     // LayerRequest (counts, offsets, score sums, scores) lands in one pinned
     // buffer with a single D2H copy: the only per-layer host synchronisation
@@ -344,7 +388,7 @@ struct Runtime {
       if (ev.device != HM_DEV_GPU || assign_of(ev.ref) != HM_ASSIGN_GPU_CACHED) continue;
       const int e = ref_expert(ev.ref);
       const int64_t slot = engine->cache.resident.at(ev.ref).slot;
-      RT_CUDA(cudaStreamWaitEvent(st, ready[slot], 0));  // a prefetch may still be in flight
+      wait_ready(slot, st);  // a prefetch may still be in flight
       batch.push_back(hm_group{static_cast<int32_t>(slot), h_offsets[e], h_counts[e], 0});
     }
     s.n_gpu = static_cast<int32_t>(batch.size());
@@ -354,7 +398,7 @@ struct Runtime {
     s.bytes_gpu = static_cast<int64_t>(batch.size()) * static_cast<int64_t>(slot_bytes);
     if (!batch.empty()) {
       ffn(batch.data(), static_cast<int>(batch.size()), rows, st);
-      for (auto &g : batch) RT_CUDA(cudaEventRecord(last_use[g.slot], st));
+      mark_used(batch.data(), static_cast<int>(batch.size()), st);
     }
     // Copies in plan transfer order (== insert order), then prefetches; an
     // expert the plan computes on the GPU is launched right after its copy so
@@ -364,10 +408,10 @@ struct Runtime {
       s.bytes_h2d += static_cast<int64_t>(slot_bytes);
       if (demand && assign_of(ref) == HM_ASSIGN_GPU_TRANSFER) {
         const int e = ref_expert(ref);
-        RT_CUDA(cudaStreamWaitEvent(st, ready[slot], 0));
+        wait_ready(slot, st);
         hm_group g{static_cast<int32_t>(slot), h_offsets[e], h_counts[e], 0};
         ffn(&g, 1, rows, st);
-        RT_CUDA(cudaEventRecord(last_use[slot], st));
+        mark_used(&g, 1, st);
         ++s.n_gpu;
         s.bytes_gpu += static_cast<int64_t>(slot_bytes);
       }
@@ -386,7 +430,7 @@ struct Runtime {
     // combine reads the mapped host rows) or by H2D copies into `out`
     const bool do_mrs = cfg.gpu_mrs && engine->cfg.cache_policy == HM_POLICY_MRS && engine->mrs_;
     const bool tail = W == 1 && (!do_mrs || fused) && N <= 256;  // combine_tail launch
-    bool zc_out = zero_copy && tail;
+    bool zc_out = zero_copy && (tail || (W > 1 && ep));
     uint64_t host_mask[4] = {0, 0, 0, 0};
     for (uint32_t r : cpu_refs) {
       const int e = ref_expert(r);
@@ -437,7 +481,10 @@ struct Runtime {
       return;
     }
     // combine (Eq. 1) with the residual stream, then the GPU copy of S
-    if (W > 1) {
+    if (W > 1 && ep) {  // combine + cross-rank sum + residual: one kernel over peer memory
+      ok(hm_ep_combine_allreduce(ep, out, dv_h_out, zc_out && !cpu_refs.empty() ? host_mask : nullptr, pos, w, T, Kp,
+                                 H, cfg.residual ? x : nullptr, y, nullptr, vs));
+    } else if (W > 1) {
       HM_REQUIRE(y32 != nullptr, HM_EVALUE, "expert parallelism needs hm_runtime_set_ep_output");
       ok(hm_combine_f32(out, pos, w, T, Kp, H, y32, vs));  // partial; the caller all-reduces
     } else {
@@ -501,7 +548,8 @@ int hm_runtime_forward_pass(hm_runtime *rt, const uint16_t *x, const float *cons
                             hm_pass_result *result, uint16_t **y_out) {
   HM_API_BEGIN
   auto *r = reinterpret_cast<hm::Runtime *>(rt);
-  HM_REQUIRE(r->W == 1, HM_EVALUE, "expert-parallel passes exchange partials between layers: use forward_layer");
+  HM_REQUIRE(r->W == 1 || r->ep, HM_EVALUE,
+             "expert-parallel passes need the peer-memory exchange (hm_runtime_set_ep_exchange) or forward_layer");
   const bool predicting = pass_loads != nullptr && r->engine->cfg.prefetch;
   std::vector<int32_t> pl(static_cast<size_t>(horizon > 0 ? horizon : 1));
   std::vector<int64_t> pload(static_cast<size_t>(horizon > 0 ? horizon : 1) * r->N);
@@ -559,6 +607,12 @@ int hm_runtime_preload(hm_runtime *rt, const uint32_t *refs, int n) {
 int hm_runtime_set_ep_output(hm_runtime *rt, float *y32) {
   HM_API_BEGIN
   reinterpret_cast<hm::Runtime *>(rt)->y32 = y32;
+  HM_API_END
+}
+
+int hm_runtime_set_ep_exchange(hm_runtime *rt, hm_ep *ep) {
+  HM_API_BEGIN
+  reinterpret_cast<hm::Runtime *>(rt)->ep = ep;
   HM_API_END
 }
 

@@ -9,9 +9,12 @@ rank's MRS table is the same.  Per-rank decisions therefore equal the
 reference's ``run_trace`` on the rank-masked trace (tests/test_ep.py).
 
 Exchange: the hidden state of the sequence is replicated; every rank routes
-it identically, computes the partial ``sum_k w_k E_k(x)`` over its home
-experts and the partials are summed with one all-reduce per layer (NCCL over
-NVLink on the GPUs; gloo in the CPU tests), then the residual is added.
+it identically and computes the partial ``sum_k w_k E_k(x)`` over its home
+experts.  The partials are summed by ``P2PExchange`` -- one kernel per layer
+(csrc/ep_exchange.cu) that fuses the combine with the cross-rank sum and the
+residual, pushing partials into the peers' inboxes over NVLink through CUDA
+IPC mappings -- or, as the baseline, by an all-reduce on the process group
+(NCCL on the GPUs; gloo in the CPU tests) followed by the residual add.
 """
 from __future__ import annotations
 
@@ -54,3 +57,39 @@ def rank_ratio(config: ModelConfig, ratio: float, rank: int, world: int) -> floa
     """A capacity ratio whose floor(ratio * L * N) is exactly this rank's slot count."""
     cap = rank_capacity(config, ratio, rank, world)
     return min(1.0, (cap + 0.5) / config.total_routed_experts)
+
+
+class P2PExchange:
+    """The peer-memory exchange of one rank (include/hybrimoe.h, hm_ep_*).
+
+    Collective constructor: every rank of ``group`` creates its buffers, the
+    CUDA IPC handles are all-gathered through the process group (control plane
+    only), and each rank maps its peers' inboxes and flags."""
+
+    def __init__(self, rank: int, world: int, max_rows: int, hidden: int, group=None) -> None:
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from . import _lib
+        h = C.c_void_p()
+        _lib.check(_lib.lib.hm_ep_create(rank, world, max_rows, hidden, C.byref(h)))
+        self._h = h.value
+        hi, hf = C.create_string_buffer(64), C.create_string_buffer(64)
+        _lib.check(_lib.lib.hm_ep_ipc_handles(self._h, hi, hf))
+        handles = [None] * world
+        dist.all_gather_object(handles, (rank, hi.raw, hf.raw), group=group)
+        for r, bi, bf in handles:
+            _lib.check(_lib.lib.hm_ep_open_peer(self._h, r, bi, bf))
+        dist.barrier(group=group)
+        self.rank, self.world = rank, world
+
+    @property
+    def handle(self) -> int:
+        return self._h
+
+    def close(self) -> None:
+        from . import _lib
+        if getattr(self, "_h", None):
+            _lib.lib.hm_ep_destroy(self._h)
+            self._h = None

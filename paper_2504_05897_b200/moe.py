@@ -125,7 +125,7 @@ class HybridMoE:
     def __init__(self, config: ModelConfig, family: str, policy: EnginePolicy, capacity_ratio: float,
                  profile: HardwareProfile, *, host_images: int | None = None, max_tokens: int = 1024,
                  cpu_threads: int = 0, gpu_mrs: bool = True, residual: bool = True, ep_rank: int = 0,
-                 ep_world: int = 1, process_group=None) -> None:
+                 ep_world: int = 1, process_group=None, exchange: str = "p2p") -> None:
         if not torch.cuda.is_available():
             raise RuntimeError("HybridMoE executes on a CUDA device; no CPU fallback exists")
         self.config = config
@@ -166,9 +166,18 @@ class HybridMoE:
         self._rt = h.value
         self.residual = residual
         self.y32 = None
+        self.exchange = exchange if self.ep_world > 1 else "none"
+        self._ep = None
         if self.ep_world > 1:
-            self.y32 = torch.empty((max_tokens, H), dtype=torch.float32, device="cuda")
-            check(lib.hm_runtime_set_ep_output(self._rt, self.y32.data_ptr()))
+            if exchange == "p2p":  # combine + cross-rank sum in one kernel over peer memory
+                from .ep import P2PExchange
+                self._ep = P2PExchange(self.ep_rank, self.ep_world, max_tokens, H, process_group)
+                check(lib.hm_runtime_set_ep_exchange(self._rt, self._ep.handle))
+            elif exchange == "allreduce":  # baseline: partials all-reduced on the process group
+                self.y32 = torch.empty((max_tokens, H), dtype=torch.float32, device="cuda")
+                check(lib.hm_runtime_set_ep_output(self._rt, self.y32.data_ptr()))
+            else:
+                raise ValueError(f"unknown expert-parallel exchange {exchange!r} (p2p | allreduce)")
         pool, store, sb, ns = C.c_void_p(), C.c_void_p(), C.c_size_t(), C.c_int64()
         check(lib.hm_runtime_buffers(self._rt, C.byref(pool), C.byref(store), C.byref(sb), C.byref(ns)))
         self.slot_bytes, self.n_slots = sb.value, ns.value
@@ -187,6 +196,9 @@ class HybridMoE:
             torch.cuda.synchronize()
             lib.hm_runtime_destroy(self._rt)
             self._rt = None
+        if getattr(self, "_ep", None) is not None:
+            self._ep.close()
+            self._ep = None
 
     # -------------------------------------------------------------- weights
     def init_random_weights(self, seed: int = 0, chunk_images: int = 8) -> None:
@@ -285,7 +297,7 @@ class HybridMoE:
             raise ValueError(f"T={T} exceeds max_tokens={self.max_tokens}")
         st = stream if stream is not None else torch.cuda.current_stream()
         a, b = self._ping_pong(T)
-        if (self.ep_world == 1 and logits is not None and not decision_log and not keep_layers
+        if ((self.ep_world == 1 or self._ep is not None) and logits is not None and not decision_log and not keep_layers
                 and (predict is None or isinstance(predict, TracePredictor) or not self.policy.prefetch)):
             return self._forward_pass_native(x, logits, predict, a, b, st)
         cur = x
@@ -323,7 +335,7 @@ class HybridMoE:
             check(lib.hm_runtime_forward_layer(self._rt, l, cur.data_ptr(), lg.data_ptr(), T, lg.shape[1],
                                                out.data_ptr(), _lib.ptr(pl, C.c_int32), _lib.ptr(pload, C.c_int64),
                                                len(pl), st.cuda_stream, C.byref(ls)))
-            if self.ep_world > 1:  # sum the ranks' partial expert outputs, then the residual
+            if self.ep_world > 1 and self._ep is None:  # all-reduce the ranks' partials, then the residual
                 import torch.distributed as dist
                 part = self.y32[:T]
                 with torch.cuda.stream(st):

@@ -1,7 +1,10 @@
 """Expert parallelism through the real runtime: two ranks (processes) sharing
-the one GPU of this environment, exchanging partial expert sums with gloo, must
-reproduce the single-rank layer stack; each rank's LayerRequest is the
-rank-masked one."""
+the one GPU of this environment must reproduce the single-rank layer stack;
+each rank's LayerRequest is the rank-masked one.  Exchanges:
+"p2p" -- the fused combine + cross-rank sum kernel writing into the peer's
+inbox through a CUDA IPC mapping (csrc/ep_exchange.cu; on one GPU the two
+contexts time-slice, so the flags are crossed between processes exactly as
+between GPUs) -- and "allreduce", the process-group baseline (gloo here)."""
 from __future__ import annotations
 
 import os
@@ -22,7 +25,7 @@ def _free_port() -> int:
     return p
 
 
-def _run(rank: int, world: int, port: int, q) -> None:
+def _run(rank: int, world: int, port: int, q, exchange: str = "p2p") -> None:
     import sys
     from pathlib import Path
     sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
@@ -43,7 +46,7 @@ def _run(rank: int, world: int, port: int, q) -> None:
         eb = mcore.expert_bytes(cfg)
         prof = mcost.HardwareProfile(gpu_time_per_expert=1.0, cpu_slope=2.0, transfer_bandwidth=eb / 0.5)
         moe = HybridMoE(cfg, "tiny", EnginePolicy(), 0.5, prof, max_tokens=48, ep_rank=rank, ep_world=world,
-                        cpu_threads=2)
+                        cpu_threads=2, exchange=exchange)
         moe.init_seeded_weights(7)
         trace, logits = generate_router_logits(cfg, GenParams(seed=3), 32, 3)
         g = torch.Generator(device="cuda").manual_seed(5)
@@ -56,13 +59,27 @@ def _run(rank: int, world: int, port: int, q) -> None:
             torch.cuda.synchronize()
             outs.append(y.float().cpu().numpy())
             loads.append([r[0].tolist() for r in info["requests"]])
-        q.put((rank, world, outs, loads, moe.capacity))
+        native = []
+        if world == 1 or exchange == "p2p":  # the one-call native pass (no Python per layer) on a fresh stack
+            moe2 = HybridMoE(cfg, "tiny", EnginePolicy(), 0.5, prof, max_tokens=48, ep_rank=rank, ep_world=world,
+                             cpu_threads=2, exchange=exchange)
+            moe2.init_seeded_weights(7)
+            g = torch.Generator(device="cuda").manual_seed(5)
+            for p, fwd in enumerate(trace.passes):
+                lg = [torch.from_numpy(np.ascontiguousarray(logits[p][l], dtype=np.float32)).cuda()
+                      for l in range(cfg.num_layers)]
+                x = torch.randn((fwd.token_count, moe2.H), generator=g, device="cuda").to(torch.bfloat16)
+                y, _ = moe2.forward_pass(x, lg)
+                torch.cuda.synchronize()
+                native.append(y.float().cpu().numpy())
+        q.put((rank, world, outs, loads, moe.capacity, native))
     finally:
         if world > 1:
             dist.destroy_process_group()
 
 
-def test_two_ranks_equal_one_rank():
+@pytest.mark.parametrize("exchange", ["p2p", "allreduce"])
+def test_two_ranks_equal_one_rank(exchange):
     ctx = torch.multiprocessing.get_context("spawn")
     q = ctx.Queue()
     single = ctx.Process(target=_run, args=(0, 1, 0, q))
@@ -70,19 +87,24 @@ def test_two_ranks_equal_one_rank():
     ref = q.get(timeout=300)  # drain the queue before joining (large items block the child's exit)
     single.join(timeout=60)
     port = _free_port()
-    procs = [ctx.Process(target=_run, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_run, args=(r, 2, port, q, exchange)) for r in range(2)]
     for p in procs:
         p.start()
     got = dict((r[0], r) for r in (q.get(timeout=300), q.get(timeout=300)))
     for p in procs:
         p.join(timeout=60)
     assert single.exitcode == 0 and all(p.exitcode == 0 for p in procs)
-    _, _, ref_outs, ref_loads, ref_cap = ref
+    _, _, ref_outs, ref_loads, ref_cap, _ = ref
     assert got[0][4] + got[1][4] == ref_cap                      # global budget split across ranks
     for r in (0, 1):
         for p, (o_ref, o) in enumerate(zip(ref_outs, got[r][2])):
             err = np.abs(o - o_ref).max() / np.abs(o_ref).max()
             assert err <= 1e-2, (r, p, err)
+        for o, o_py in zip(got[r][5], got[r][2]):  # native pass == per-layer pass, bit for bit
+            assert np.array_equal(o, o_py)
+        if exchange == "p2p":  # the fused exchange sums in rank order: both ranks hold identical y
+            for a, b in zip(got[0][2], got[1][2]):
+                assert np.array_equal(a, b)
         for p in range(len(ref_loads)):
             for l, full in enumerate(ref_loads[p]):
                 masked = [v if e % 2 == r else 0 for e, v in enumerate(full)]
