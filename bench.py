@@ -182,11 +182,20 @@ def run_ours(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # HM_SAME_GPU=1: every rank on cuda:0 with a gloo control plane -- only to
+    # exercise the multi-rank harness on a one-GPU box (timings meaningless:
+    # the ranks' contexts time-slice the GPU)
+    same_gpu = os.environ.get("HM_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     cfg = SHAPES[args.shape]
     H, I = cfg.routed_expert_dims
@@ -402,7 +411,8 @@ def run_ours(args) -> None:
                        "top_k": cfg.num_activated, "hidden": H, "inter": I, "cache_slots": moe.capacity,
                        "host_images": moe.host_images, "policy": args.policy, "prefetch": args.prefetch,
                        "scheduling": args.scheduling,
-                       "l2": "each step streams >= 2 x 352 MB of expert weights (> 126 MB L2); no flush needed",
+                       "l2": f"each step streams {cfg.num_layers * cfg.num_activated} expert evaluations x "
+                             f"{3 * H * I * 2 / 1e6:.1f} MB of weights (>> 126 MB L2); no flush needed",
                        "parallelism": f"ep{world}" if world > 1 else "single",
                        "ep_exchange": moe.exchange},
             "prefill": {"tokens": args.prefill, "ms": prefill_ms, "cold_cache": True,

@@ -313,6 +313,7 @@ def run_pass(trace: Trace, pass_index: int, policy: EnginePolicy, cache: CacheSt
             plans.append(eng.plan())
         if decision_log:
             rec = eng.record()
+            rec["layer"] = request.layer
             rec["mrs_row"] = (mrs.table()[request.layer].copy()
                               if mrs is not None and policy.cache_policy == POLICY_MRS else None)
             decisions.append(rec)

@@ -348,6 +348,7 @@ class HybridMoE:
             stats.append(LayerStats(*[getattr(ls, f) for f, _ in _lib.LayerStats._fields_]))
             if decision_log:
                 rec = self.engine.record()
+                rec["layer"] = l
                 rec["mrs_row"] = self.mrs.table()[l].copy()
                 records.append(rec)
                 check(lib.hm_runtime_last_request(self._rt, _lib.ptr(loads, C.c_int64), _lib.ptr(scores, C.c_double)))

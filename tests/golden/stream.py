@@ -53,7 +53,10 @@ def from_records(records: list[dict], mrs_policy: bool) -> list:
         out.append(plan_item(rec["plan"]))
         out.extend(insert_item(r, v) for r, v in rec["demand_inserts"])
         if mrs_policy:
-            layer = rec["plan"].events[0].expert[0] if rec["plan"].events else rec["lookups"][0][0][0]
+            if "layer" in rec:
+                layer = rec["layer"]
+            else:
+                layer = rec["plan"].events[0].expert[0] if rec["plan"].events else rec["lookups"][0][0][0]
             out.append(["M", int(layer), row_hash(rec["mrs_row"])])
         if rec["budget"] is not None:
             out.extend(["G", int(r[0]), int(r[1]), fx(g)] for r, _, g, _ in rec["candidates"])
