@@ -351,6 +351,12 @@ typedef struct hm_group {
 int hm_expert_ffn(const uint16_t *pool, int n_slots, int H, int I, const hm_group *groups,
                   int n_groups, const uint16_t *xp, int total_rows, uint16_t *h, float *out,
                   int path, void *stream);
+/* Micro-benchmark: `reps` back-to-back hm_expert_ffn calls from the library
+ * (n_groups experts x rows_per_group rows, slots rotating mod n_slots), timed
+ * with events on `stream`; *ms = milliseconds per call. */
+int hm_bench_expert_ffn(const uint16_t *pool, int n_slots, int H, int I, int n_groups,
+                        int rows_per_group, const uint16_t *xp, uint16_t *h, float *out, int path,
+                        int reps, void *stream, float *ms);
 /* y[t] = residual[t] (optional) + sum_k w[t,k] * out[pos[t,k]]  (Eq. 1 combine). */
 int hm_combine(const float *out, const int32_t *pos, const float *w, int T, int Kp, int H,
                const uint16_t *residual, uint16_t *y, void *stream);
@@ -369,6 +375,10 @@ long long hm_launch_count(void);
  * fp64 with explicit round-to-nearest mul/add (bit-identical to the host core). */
 int hm_mrs_update_dev(double *S, const double *scores, int layer, int N, int p,
                       double alpha, void *stream);
+/* Hold `stream` until the host stores `seq` into *flag (device view of mapped
+ * pinned memory): lets CUDA events time a group of kernels without the host's
+ * launch latency in between (kernel-timing mode of the runtime). */
+int hm_gate_wait(const uint32_t *flag, uint32_t seq, void *stream);
 /* Decode tail in one launch: hm_combine (Eq. 1 + residual) where positions
  * whose bit is set in host_mask4 (4 x 64 bits, positions < 256; NULL = none)
  * are read zero-copy from host_out (device view of the host worker's mapped

@@ -325,6 +325,8 @@ for _name, (_args, _res) in {
     "hm_predict_layers": ([P(i64), C.c_int, C.c_int, i64, C.c_int, i64, C.c_int, f64, P(i32), P(i64),
                            P(C.c_int)], C.c_int),
     "hm_cpu_set_decode_grain": ([C.c_int], C.c_int),
+    "hm_bench_expert_ffn": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, C.c_int, C.c_int, vp,
+                             P(C.c_float)], C.c_int),
     "hm_ep_create": ([C.c_int, C.c_int, C.c_int, C.c_int, P(vp)], C.c_int),
     "hm_ep_destroy": ([vp], None),
     "hm_ep_ipc_handles": ([vp, C.c_char_p, C.c_char_p], C.c_int),

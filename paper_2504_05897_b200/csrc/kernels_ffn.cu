@@ -17,6 +17,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -36,6 +37,7 @@ struct GemvParams {
   int n_groups;
   int bpg;    // blocks per group
   int chunk;  // pairs (ffn1) or rows (ffn2) per block
+  int l2_prefetch;  // ffn2: warm L2 with the block's W2 rows before waiting on ffn1
   const uint16_t *xp;
   uint16_t *h;
   float *out;
@@ -48,6 +50,9 @@ struct GemvParams {
 template <int MR>
 __global__ void __launch_bounds__(256) ffn1_gemv_kernel(const __grid_constant__ GemvParams p) {
   extern __shared__ __align__(16) uint16_t xs[];  // [MR][H]
+  // let ffn2 (launched with programmatic stream serialization) get scheduled
+  // onto SMs as this grid's blocks retire: its prologue overlaps our tail
+  asm volatile("griddepcontrol.launch_dependents;");
   const int g = blockIdx.x / p.bpg, cid = blockIdx.x % p.bpg;
   const int M = p.row_count[g], rb = p.row_begin[g], H = p.H, I = p.I;
   for (int v = threadIdx.x; v < M * H / 8; v += blockDim.x)
@@ -105,6 +110,16 @@ __global__ void __launch_bounds__(256) ffn2_gemv_kernel(const __grid_constant__ 
   extern __shared__ __align__(16) uint16_t hs[];  // [MR][I]
   const int g = blockIdx.x / p.bpg, cid = blockIdx.x % p.bpg;
   const int M = p.row_count[g], rb = p.row_begin[g], H = p.H, I = p.I;
+  if (p.l2_prefetch) {  // prologue independent of ffn1: pull this block's W2 rows into L2
+    const int j0 = cid * p.chunk, j1 = min(H, (cid + 1) * p.chunk);
+    const char *base = reinterpret_cast<const char *>(p.pool + static_cast<size_t>(p.slot[g]) * p.slot_elems +
+                                                      static_cast<size_t>(2) * I * H + static_cast<size_t>(j0) * I);
+    const size_t bytes = j1 > j0 ? static_cast<size_t>(j1 - j0) * I * 2 : 0;
+    for (size_t o = static_cast<size_t>(threadIdx.x) * 128; o < bytes; o += static_cast<size_t>(blockDim.x) * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(base + o));
+  }
+  // h comes from ffn1: wait for the primary grid (no-op without PDL)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int v = threadIdx.x; v < M * I / 8; v += blockDim.x)
     reinterpret_cast<uint4 *>(hs)[v] = reinterpret_cast<const uint4 *>(p.h + static_cast<size_t>(rb) * I)[v];
   __syncthreads();
@@ -404,6 +419,34 @@ void set_smem(K kernel, int bytes) {
   done.emplace_back(key, bytes);
 }
 
+// Programmatic dependent launch (HM_PDL=0 disables): the kernel may start
+// while the previous kernel on the stream finishes; it calls
+// griddepcontrol.wait before touching that kernel's output.
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *e = std::getenv("HM_PDL");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+template <typename K>
+void launch_pdl(K kernel, int grid, int smem, cudaStream_t st, const GemvParams &p) {
+  set_smem(kernel, smem);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  HM_CUDA(cudaLaunchKernelEx(&cfg, kernel, p));
+  HM_LAUNCH_CHECK();
+}
+
 void launch_gemv(const uint16_t *pool, size_t slot_elems, int H, int I, const std::vector<hm_group> &gs,
                  const uint16_t *xp, uint16_t *h, float *out, cudaStream_t st) {
   if (gs.empty()) return;
@@ -446,12 +489,13 @@ void launch_gemv(const uint16_t *pool, size_t slot_elems, int H, int I, const st
   p.bpg = (H + chunk - 1) / chunk;
   smem = mr * I * 2;
   HM_REQUIRE(smem <= 200 * 1024, HM_EVALUE, "decode rows do not fit shared memory");
+  // warm L2 only while the layer's W2 bytes fit comfortably in the 126 MB L2
+  p.l2_prefetch = static_cast<long>(G) * H * I * 2 <= (64L << 20) ? 1 : 0;
   switch (mr) {
-    case 1: set_smem(ffn2_gemv_kernel<1>, smem); ffn2_gemv_kernel<1><<<G * p.bpg, 256, smem, st>>>(p); break;
-    case 2: set_smem(ffn2_gemv_kernel<2>, smem); ffn2_gemv_kernel<2><<<G * p.bpg, 256, smem, st>>>(p); break;
-    default: set_smem(ffn2_gemv_kernel<4>, smem); ffn2_gemv_kernel<4><<<G * p.bpg, 256, smem, st>>>(p); break;
+    case 1: launch_pdl(ffn2_gemv_kernel<1>, G * p.bpg, smem, st, p); break;
+    case 2: launch_pdl(ffn2_gemv_kernel<2>, G * p.bpg, smem, st, p); break;
+    default: launch_pdl(ffn2_gemv_kernel<4>, G * p.bpg, smem, st, p); break;
   }
-  HM_LAUNCH_CHECK();
 }
 
 template <int BN, int MODE>
@@ -524,6 +568,38 @@ void launch_gemm(const uint16_t *pool, int n_slots, int H, int I, const std::vec
 }  // namespace hm
 
 extern "C" {
+
+// Back-to-back launches from the host library (no Python between launches):
+// `reps` calls of hm_expert_ffn, group r of call i on slot (i*n + r) % n_slots,
+// timed with events on `stream`.  Kernel micro-benchmark for the roofline.
+int hm_bench_expert_ffn(const uint16_t *pool, int n_slots, int H, int I, int n_groups, int rows_per_group,
+                        const uint16_t *xp, uint16_t *h, float *out, int path, int reps, void *stream, float *ms) {
+  HM_API_BEGIN
+  HM_REQUIRE(n_groups >= 1 && n_groups <= n_slots && rows_per_group >= 1 && reps >= 1, HM_EVALUE, "bad bench");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::vector<hm_group> g(n_groups);
+  auto one = [&](int i) {
+    for (int r = 0; r < n_groups; ++r)
+      g[r] = hm_group{static_cast<int32_t>((static_cast<long>(i) * n_groups + r) % n_slots), r * rows_per_group,
+                      rows_per_group, 0};
+    const int rc = hm_expert_ffn(pool, n_slots, H, I, g.data(), n_groups, xp, n_groups * rows_per_group, h, out,
+                                 path, stream);
+    if (rc != HM_OK) hm::raise(rc, hm::last_error());
+  };
+  for (int i = 0; i < 3; ++i) one(i);
+  cudaEvent_t a, b;
+  HM_CUDA(cudaEventCreate(&a));
+  HM_CUDA(cudaEventCreate(&b));
+  HM_CUDA(cudaEventRecord(a, st));
+  for (int i = 0; i < reps; ++i) one(3 + i);
+  HM_CUDA(cudaEventRecord(b, st));
+  HM_CUDA(cudaEventSynchronize(b));
+  HM_CUDA(cudaEventElapsedTime(ms, a, b));
+  *ms /= static_cast<float>(reps);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  HM_API_END
+}
 
 int hm_expert_ffn(const uint16_t *pool, int n_slots, int H, int I, const hm_group *groups, int n_groups,
                   const uint16_t *xp, int total_rows, uint16_t *h, float *out, int path, void *stream) {

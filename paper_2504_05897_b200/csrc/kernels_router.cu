@@ -531,6 +531,14 @@ __global__ void __launch_bounds__(kTailThreads) combine_tail_kernel(const __grid
   *reinterpret_cast<uint2 *>(c.y + static_cast<size_t>(t) * c.H + col) = o2;
 }
 
+// One thread spins until the host writes `seq` into a mapped flag: holds the
+// stream while the host enqueues the kernels to be timed, so the CUDA events
+// around them measure GPU time, not host launch latency (bench roofline).
+__global__ void gate_kernel(const uint32_t *flag, uint32_t seq) {
+  while (*reinterpret_cast<const volatile uint32_t *>(flag) != seq) {
+  }
+}
+
 // S[layer, i] <- a * TopP(s)[i] + (1 - a) * S[layer, i]   (caching.py:58-76)
 // Round-to-nearest intrinsics keep every operation a separate IEEE rounding,
 // exactly like the host core (no FMA contraction).
@@ -737,6 +745,13 @@ int hm_combine_tail(const float *out, const float *host_out, const uint64_t *hos
     hm::combine_tail_kernel<<<static_cast<unsigned>(blocks), hm::kTailThreads, 0, static_cast<cudaStream_t>(stream)>>>(c);
     HM_LAUNCH_CHECK();
   }
+  HM_API_END
+}
+
+int hm_gate_wait(const uint32_t *flag, uint32_t seq, void *stream) {
+  HM_API_BEGIN
+  hm::gate_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(flag, seq);
+  HM_LAUNCH_CHECK();
   HM_API_END
 }
 

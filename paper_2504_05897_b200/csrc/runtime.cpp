@@ -44,6 +44,7 @@ int hm_router_fused_mirror(const float *, int, int, int, int, int, int, int, con
                            uint32_t *, uint32_t, void *);
 int hm_ep_combine_allreduce(hm_ep *, const float *, const float *, const uint64_t *, const int32_t *, const float *,
                             int, int, int, const uint16_t *, uint16_t *, float *, void *);
+int hm_gate_wait(const uint32_t *, uint32_t, void *);
 int hm_combine_tail(const float *, const float *, const uint64_t *, const int32_t *, const float *, int, int, int,
                     const uint16_t *, uint16_t *, double *, const double *, int, int, int, double, void *);
 }
@@ -109,11 +110,12 @@ struct Runtime {
   // zero-copy decode path (HM_ZERO_COPY, default on): device views of the
   // mapped pinned buffers above, and the router's completion flag
   bool zero_copy = true;
+  bool timing_gate = true;  // HM_TIMING_GATE: gate kernel-timing launches (see ffn())
   void *dv_hmeta = nullptr;
   uint16_t *dv_h_x = nullptr;
   float *dv_h_out = nullptr;
   uint32_t *h_flag = nullptr, *dv_flag = nullptr;
-  uint32_t seq = 0;
+  uint32_t seq = 0, gate_seq = 0;  // h_flag[0]: router flag; h_flag[8]: kernel-timing gate
   std::unique_ptr<ThreadPool> workers;
   std::vector<uint16_t> hbuf;
   std::vector<int64_t> loads;
@@ -135,8 +137,20 @@ struct Runtime {
       }
       a = kev[kused].first;
       b = kev[kused].second;
+      // gate the stream until the launches below are enqueued (released right after)
+      if (timing_gate) ok(hm_gate_wait(dv_flag + 8, ++gate_seq, static_cast<void *>(st)));
       RT_CUDA(cudaEventRecord(a, st));
     }
+    struct Release {  // never leave the gate closed, even on an exception
+      Runtime *r;
+      bool on;
+      ~Release() {
+        if (on) {
+          std::atomic_thread_fence(std::memory_order_release);
+          reinterpret_cast<volatile uint32_t *>(r->h_flag)[8] = r->gate_seq;
+        }
+      }
+    } release{this, time_kernels && timing_gate};
     ok(hm_expert_ffn(pool, static_cast<int>(n_slots), H, I, g, n, xp, rows, h, out, HM_FFN_AUTO,
                      static_cast<void *>(st)));
     if (time_kernels) {
@@ -213,8 +227,9 @@ struct Runtime {
     RT_CUDA(cudaHostAlloc(&h_x, rows * H * 2, cudaHostAllocMapped));
     RT_CUDA(cudaHostAlloc(&h_out, rows * H * 4, cudaHostAllocMapped));
     RT_CUDA(cudaHostAlloc(&h_flag, 64, cudaHostAllocMapped));
-    *reinterpret_cast<volatile uint32_t *>(h_flag) = 0;
+    for (int i = 0; i < 16; ++i) reinterpret_cast<volatile uint32_t *>(h_flag)[i] = 0;
     if (const char *zc = std::getenv("HM_ZERO_COPY")) zero_copy = std::atoi(zc) != 0;
+    if (const char *tg = std::getenv("HM_TIMING_GATE")) timing_gate = std::atoi(tg) != 0;
     RT_CUDA(cudaHostGetDevicePointer(&dv_hmeta, hmeta, 0));
     RT_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dv_h_x), h_x, 0));
     RT_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dv_h_out), h_out, 0));
