@@ -230,6 +230,12 @@ struct Runtime {
     for (int i = 0; i < 16; ++i) reinterpret_cast<volatile uint32_t *>(h_flag)[i] = 0;
     if (const char *zc = std::getenv("HM_ZERO_COPY")) zero_copy = std::atoi(zc) != 0;
     if (const char *tg = std::getenv("HM_TIMING_GATE")) timing_gate = std::atoi(tg) != 0;
+    // under a kernel profiler (ncu injects itself) launches are serialised and
+    // replayed: a kernel waiting for the host would never be released
+    // (nor would a host-mapped flag survive the profiler's save/restore of the
+    // kernel's writes): fall back to the event-synchronised copy path
+    if (std::getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") || std::getenv("CUDA_INJECTION64_PATH"))
+      timing_gate = zero_copy = false;
     RT_CUDA(cudaHostGetDevicePointer(&dv_hmeta, hmeta, 0));
     RT_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dv_h_x), h_x, 0));
     RT_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dv_h_out), h_out, 0));
