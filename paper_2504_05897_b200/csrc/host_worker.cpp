@@ -397,12 +397,187 @@ inline void amx_block(const uint16_t *wa0, const uint16_t *wa1, size_t ldw, cons
   }
 }
 
+// Cache-blocked AMX GEMM over weight rows (A, row-major straight from the
+// expert image) and tokens (B, VNNI):  for each unit o in [o0, o1) two 16-row
+// weight blocks (rowptr(o, 0/1)) times all nbt token blocks over the full K,
+// accumulated in C[o - o0][2][nbt][16 x 16] fp32 (cbuf).
+// Loop order: units in groups of GO (their C stays in L2) -> K chunks of KC
+// (a unit's 2 x 16 x KC weight chunk is loaded from DRAM once and reused
+// from L1 for every token-block pair; the chunk of the next unit is software-
+// prefetched meanwhile) -> token-block pairs (2 x 2 register blocking: 4 C,
+// 2 A, 2 B tiles).  The previous kernel re-read the whole token matrix from
+// L2/L3 for every 16-row block and ran at ~3.5 TF/s.
+struct AmxCfg {
+  int kc = 128;  // K chunk (elements)
+  int go = 8;    // units per group
+};
+AmxCfg &amx_cfg() {
+  static AmxCfg c = [] {
+    AmxCfg a;
+    if (const char *e = std::getenv("HM_AMX_KC")) a.kc = std::max(32, std::atoi(e) / 32 * 32);
+    if (const char *e = std::getenv("HM_AMX_GO")) a.go = std::max(1, std::atoi(e));
+    return a;
+  }();
+  return c;
+}
+// 1: cache-blocked, 0: the first kernel, -1 (default): cache-blocked from 256
+// tokens up -- on the box's host the two are within noise below that and the
+// blocked kernel is 15-25 % faster at 256-512 tokens (tools/host_prefill_bench.py).
+int &amx_algo() {
+  static int a = [] {
+    const char *e = std::getenv("HM_AMX_ALGO");
+    return e ? std::atoi(e) : -1;
+  }();
+  return a;
+}
+
+template <class RowPtr>
+void amx_gemm_units(RowPtr rowptr, int o0, int o1, size_t lda_bytes, const uint16_t *bv, int Mpad, int K,
+                    float *cbuf) {
+  const int nbt = Mpad / 16;
+  const size_t ldb = static_cast<size_t>(Mpad) * 4;
+  const size_t cu = static_cast<size_t>(2) * nbt * 256;  // floats of C per unit
+  const int KC = amx_cfg().kc;
+  for (int kc = 0; kc < K; kc += KC) {
+    const int kend = std::min(K, kc + KC);
+    for (int o = o0; o < o1; ++o) {
+      const uint16_t *a0 = rowptr(o, 0), *a1 = rowptr(o, 1);
+      // prefetch the next unit's chunk (or this unit's next chunk) into L2
+      {
+        const bool last = o + 1 >= o1;
+        const int po = last ? o0 : o + 1;
+        const int pk = last ? kend : kc;
+        if (pk < K) {
+          const uint16_t *p0 = rowptr(po, 0), *p1 = rowptr(po, 1);
+          const int pn = std::min(K, pk + KC) - pk;
+          for (int r = 0; r < 16; ++r)
+            for (int c = 0; c < pn * 2; c += 64) {
+              _mm_prefetch(reinterpret_cast<const char *>(p0) + r * lda_bytes + pk * 2 + c, _MM_HINT_T1);
+              _mm_prefetch(reinterpret_cast<const char *>(p1) + r * lda_bytes + pk * 2 + c, _MM_HINT_T1);
+            }
+        }
+      }
+      float *cb = cbuf + static_cast<size_t>(o - o0) * cu;
+      for (int b = 0; b < nbt; b += 2) {
+        const bool two = b + 1 < nbt;
+        float *c00 = cb + static_cast<size_t>(b) * 256, *c01 = c00 + 256;
+        float *c10 = cb + (static_cast<size_t>(nbt) + b) * 256, *c11 = c10 + 256;
+        if (kc == 0) {
+          _tile_zero(0);
+          _tile_zero(1);
+          _tile_zero(2);
+          _tile_zero(3);
+        } else {
+          _tile_loadd(0, c00, 64);
+          _tile_loadd(2, c10, 64);
+          if (two) {
+            _tile_loadd(1, c01, 64);
+            _tile_loadd(3, c11, 64);
+          }
+        }
+        for (int k = kc; k < kend; k += 32) {
+          _tile_loadd(4, a0 + k, lda_bytes);
+          _tile_loadd(5, a1 + k, lda_bytes);
+          const uint16_t *bp = bv + (static_cast<size_t>(k >> 1) * Mpad + b * 16) * 2;
+          _tile_loadd(6, bp, ldb);
+          _tile_dpbf16ps(0, 4, 6);
+          _tile_dpbf16ps(2, 5, 6);
+          if (two) {
+            _tile_loadd(7, bp + 32, ldb);
+            _tile_dpbf16ps(1, 4, 7);
+            _tile_dpbf16ps(3, 5, 7);
+          }
+        }
+        _tile_stored(0, c00, 64);
+        _tile_stored(2, c10, 64);
+        if (two) {
+          _tile_stored(1, c01, 64);
+          _tile_stored(3, c11, 64);
+        }
+      }
+    }
+  }
+}
+
+void cpu_expert_amx2(ThreadPool &pool, const uint16_t *img, int H, int I, const uint16_t *x, int M, float *out,
+                     std::vector<uint16_t> &scratch) {
+  const int Mpad = (M + 31) / 32 * 32;  // token blocks in pairs
+  const int nbt = Mpad / 16;
+  scratch.resize(static_cast<size_t>(H) * Mpad + static_cast<size_t>(I) * Mpad);
+  uint16_t *xv = scratch.data();
+  uint16_t *hv = xv + static_cast<size_t>(H) * Mpad;
+  vnni_pack(x, M, H, Mpad, xv);
+  const uint16_t *w2 = img + static_cast<size_t>(2) * I * H;
+  const int GO = amx_cfg().go;
+  pool.run([&](int tid, int nt) {
+    amx_config();
+    std::vector<float> cbuf(static_cast<size_t>(GO) * 2 * nbt * 256);
+    // phase 1: unit o = 16 gate rows (block 0) + their 16 up rows (block 1)
+    const int ob = I / 16;
+    const int u0 = static_cast<int>(static_cast<long>(ob) * tid / nt), u1 = static_cast<int>(static_cast<long>(ob) * (tid + 1) / nt);
+    auto row1 = [&](int o, int which) {
+      const int i0 = o * 16;
+      const size_t grow = static_cast<size_t>((i0 / kIlv) * 2 * kIlv + i0 % kIlv);
+      return img + (grow + (which ? kIlv : 0)) * H;
+    };
+    for (int g0 = u0; g0 < u1; g0 += GO) {
+      const int g1 = std::min(u1, g0 + GO);
+      amx_gemm_units(row1, g0, g1, static_cast<size_t>(H) * 2, xv, Mpad, H, cbuf.data());
+      for (int o = g0; o < g1; ++o) {
+        const float *cb = cbuf.data() + static_cast<size_t>(o - g0) * 2 * nbt * 256;
+        const int i0 = o * 16;
+        for (int b = 0; b < nbt; ++b) {
+          const int tok0 = b * 16;
+          if (tok0 >= M) {  // padded tokens: zero h
+            for (int r = 0; r < 16; r += 2)
+              _mm512_storeu_si512(hv + (static_cast<size_t>((i0 + r) >> 1) * Mpad + tok0) * 2, _mm512_setzero_si512());
+            continue;
+          }
+          const __mmask16 live = tok0 + 16 <= M ? 0xFFFF : static_cast<__mmask16>((1u << (M - tok0)) - 1u);
+          const float *cg = cb + static_cast<size_t>(b) * 256, *cu = cb + (static_cast<size_t>(nbt) + b) * 256;
+          for (int r = 0; r < 16; r += 2) {
+            const __m512 h0 = _mm512_maskz_mov_ps(live, silu_mul16(cg + r * 16, cu + r * 16));
+            const __m512 h1 = _mm512_maskz_mov_ps(live, silu_mul16(cg + (r + 1) * 16, cu + (r + 1) * 16));
+            _mm512_storeu_si512(hv + (static_cast<size_t>((i0 + r) >> 1) * Mpad + tok0) * 2, interleave_bf16(h0, h1));
+          }
+        }
+      }
+    }
+    pool.barrier();
+    // phase 2: unit q = W2 rows 32q..32q+15 (block 0) and 32q+16..32q+31 (block 1)
+    const int pairs = H / 32;
+    const int q0 = static_cast<int>(static_cast<long>(pairs) * tid / nt), q1 = static_cast<int>(static_cast<long>(pairs) * (tid + 1) / nt);
+    auto row2 = [&](int q, int which) { return w2 + static_cast<size_t>(q * 32 + which * 16) * I; };
+    for (int g0 = q0; g0 < q1; g0 += GO) {
+      const int g1 = std::min(q1, g0 + GO);
+      amx_gemm_units(row2, g0, g1, static_cast<size_t>(I) * 2, hv, Mpad, I, cbuf.data());
+      for (int q = g0; q < g1; ++q) {
+        const float *cb = cbuf.data() + static_cast<size_t>(q - g0) * 2 * nbt * 256;
+        for (int a = 0; a < 2; ++a)
+          for (int b = 0; b < nbt; ++b) {
+            const float *c = cb + (static_cast<size_t>(a) * nbt + b) * 256;
+            for (int t = 0; t < 16; ++t) {
+              const int tok = b * 16 + t;
+              if (tok >= M) break;
+              float *o = out + static_cast<size_t>(tok) * H + q * 32 + a * 16;
+              for (int r = 0; r < 16; ++r) o[r] = c[r * 16 + t];
+            }
+          }
+      }
+    }
+  });
+}
+
 }  // namespace
 
 bool amx_available() { return amx_enable(); }
 
 void cpu_expert_amx(ThreadPool &pool, const uint16_t *img, int H, int I, const uint16_t *x, int M, float *out,
                     std::vector<uint16_t> &scratch) {
+  if ((amx_algo() == 1 || (amx_algo() < 0 && M >= 256)) && H % 32 == 0) {
+    cpu_expert_amx2(pool, img, H, I, x, M, out, scratch);
+    return;
+  }
   const int Mpad = (M + 15) / 16 * 16;
   scratch.resize(static_cast<size_t>(H) * Mpad + static_cast<size_t>(I) * Mpad);
   uint16_t *xv = scratch.data();

@@ -36,7 +36,7 @@ def test_pack_unpack_roundtrip():
 
 
 @pytest.mark.parametrize("H,I,M", [(256, 256, 1), (512, 384, 3), (512, 384, 17), (1024, 1408, 1), (1024, 1408, 40),
-                                   (512, 256, 8), (512, 256, 33), (2048, 1408, 96)])
+                                   (512, 256, 8), (512, 256, 33), (2048, 1408, 96), (256, 384, 300)])
 def test_cpu_expert_matches_oracle(pool, H, I, M):
     rng = np.random.default_rng(H + M)
     img, ex = _expert(rng, H, I)
