@@ -72,14 +72,17 @@ def measure_samples(H: int, I: int, gpu_loads=(1, 2, 4, 8, 32, 128, 256, 384, 51
 
     for frac in (4, 2, 1):
         n = slot_elems // frac
-        flat[:n].copy_(host[0, :n], non_blocking=True)
-        for r in range(reps):
+        for i in range(n_images):  # warm every source range first: a cold first touch
+            flat[:n].copy_(host[i, :n], non_blocking=True)  # reads ~25 % slower and skews the fit
+        torch.cuda.synchronize()
+        for r in range(reps + 1):  # the first copy after an idle gap is slow (link wake-up): not a sample
             a, b = _events()
             a.record(st)
             flat[:n].copy_(host[1 + r % (n_images - 1), :n], non_blocking=True)
             b.record(st)
             b.synchronize()
-            samples.append(CalibrationSample("pcie", float(n * 2), 0, a.elapsed_time(b) / 1e3))
+            if r > 0:
+                samples.append(CalibrationSample("pcie", float(n * 2), 0, a.elapsed_time(b) / 1e3))
     torch.cuda.synchronize()
     return samples
 
