@@ -169,6 +169,12 @@ def warm_parity(cfg, trace, requests, records, moe, policy, args) -> dict:
             "warmup_layers_recorded": len(records)}
 
 
+def _trace(msg: str) -> None:
+    """HM_BENCH_TRACE=1: stage markers on stderr (debugging multi-rank runs)."""
+    if os.environ.get("HM_BENCH_TRACE") == "1":
+        print(f"[rank {os.environ.get('RANK', '0')} {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def run_ours(args) -> None:
     if os.environ.get("HM_NCU_TIMED") == "1":
         # under ncu's serialised replay nothing may wait on the host: no timing
@@ -268,6 +274,12 @@ def run_ours(args) -> None:
         moe.set_fixed_gpu_set(sorted(r for r in fixed if r[1] % world == rank)[: moe.capacity])
     g = torch.Generator(device="cuda").manual_seed(1234)  # replicated hidden state on every rank
     xs = [torch.randn((f.token_count, H), generator=g, device="cuda").to(torch.bfloat16) for f in trace.passes]
+    if world > 1 and args.exchange == "dispatch":  # token-sharded: rank r keeps tokens [r*T/G, (r+1)*T/G)
+        def shard(t):
+            T = t.shape[0]
+            return t[rank * T // world:(rank + 1) * T // world].contiguous()
+        xs = [shard(x) for x in xs]
+        dev_logits = [[shard(t) for t in layer_logits] for layer_logits in dev_logits]
     torch.cuda.synchronize()
     # host DRAM read bandwidth over (part of) the pinned master store: the host roofline
     import ctypes as C
@@ -279,6 +291,7 @@ def run_ours(args) -> None:
     _lib.lib.hm_cpu_pool_destroy(cp)
     host_bw_gbs = hbw.value if args.host_bw_gbs <= 0 else args.host_bw_gbs
     setup_s = time.time() - t_setup
+    _trace(f"setup done in {setup_s:.1f} s")
 
     from paper_2504_05897_b200.moe import TracePredictor
     predictors = [TracePredictor(trace, p, args.seed) for p in range(len(trace.passes))]
@@ -288,6 +301,7 @@ def run_ours(args) -> None:
 
     st = torch.cuda.current_stream()
     # ---- prefill: 1k tokens, cold cache (the reference's TTFT, engine.py:465-466)
+    _trace('prefill')
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(st)
     moe.set_profile(prof_prefill)
@@ -299,8 +313,10 @@ def run_ours(args) -> None:
     pst = layer_stats(pinfo)
 
     # ---- decode: W warm-up passes (recorded for the parity block), then K timed passes
+    _trace('decode')
     warm_records, warm_requests = [], []
     for p in range(1, 1 + args.warmup):
+        _trace(f"warm-up pass {p}")
         _, winfo = moe.forward_pass(xs[p], dev_logits[p], predict=predictor(p), decision_log=True)
         warm_records.extend(winfo["records"])
         warm_requests.append(winfo["requests"])
@@ -322,6 +338,7 @@ def run_ours(args) -> None:
         t0.record(st)
         for k in range(args.steps):
             p = 1 + args.warmup + k
+            _trace(f"timed pass {p}")
             _, info = moe.forward_pass(xs[p], dev_logits[p], predict=predictor(p))
             stats_all.append(info)
         t1.record(st)
@@ -346,11 +363,12 @@ def run_ours(args) -> None:
     tok_s = 1e3 / ms_step  # one sequence, experts sharded: tokens of the whole job per second
 
     # ---- e2e: host buffers through the public API, copies inside the timed region
+    _trace('e2e')
     e2e_passes = range(1 + n_dec, 1 + 2 * n_dec)
     host_x = [xs[p].cpu().pin_memory() for p in e2e_passes]
     host_lg = [torch.stack([t.cpu() for t in dev_logits[p]]).pin_memory() for p in e2e_passes]
-    y_host = torch.empty((1, H), dtype=torch.bfloat16).pin_memory()
-    dx = torch.empty((1, H), dtype=torch.bfloat16, device="cuda")
+    y_host = torch.empty((host_x[0].shape[0], H), dtype=torch.bfloat16).pin_memory()
+    dx = torch.empty_like(host_x[0], device="cuda")
     dlg = torch.empty_like(host_lg[0], device="cuda")
     for i in range(args.warmup):
         p = list(e2e_passes)[i]
@@ -370,10 +388,11 @@ def run_ours(args) -> None:
     e1.record(st)
     e1.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps
-    h2d = H * 2 + host_lg[0].numel() * 4
-    d2h = H * 2
+    h2d = host_x[0].numel() * 2 + host_lg[0].numel() * 4
+    d2h = y_host.numel() * 2
 
     # ---- roofline of the dominant GPU kernel (decode expert FFN, HBM-bound)
+    _trace('roofline of the dominant GPU kernel (decode expert FFN, HBM-bound)')
     achieved_gbs = kbytes.value / (kms.value / 1e3) / 1e9 if kms.value > 0 else 0.0
     hbm_peak = float(pk["hbm_gbs"])
     # DRAM traffic of the same kernels from the committed ncu --set full capture
@@ -468,8 +487,10 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--shape", default="mixtral", choices=["tiny", "mixtral", "deepseek", "qwen2"])
     ap.add_argument("--ratio", type=float, default=0.25)
-    ap.add_argument("--exchange", default="p2p", choices=["p2p", "allreduce"],
-                    help="expert-parallel partial-sum exchange: fused peer-memory kernel or process-group all-reduce")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "dispatch", "allreduce"],
+                    help="expert parallelism: replicated tokens + fused peer-memory reduce (p2p), token-sharded "
+                         "all-to-all dispatch/return over peer memory (dispatch), or replicated + process-group "
+                         "all-reduce (allreduce)")
     ap.add_argument("--prefill", type=int, default=1024)
     ap.add_argument("--policy", default="mrs", choices=["mrs", "lru", "lfu"])
     ap.add_argument("--scheduling", default="hybrid",

@@ -493,6 +493,35 @@ int hm_ep_combine_allreduce(hm_ep *ep, const float *out, const float *host_out,
                             const uint64_t *host_mask4, const int32_t *pos, const float *w, int T,
                             int Kp, int H, const uint16_t *residual, uint16_t *y, float *y32,
                             void *stream);
+/* Token-sharded mode ("dispatch: all-to-all(v) of token rows to
+ * home ranks ... combine: all-to-all(v) back plus weighted sum"): every rank
+ * routes only its own tokens.  hm_ep_enable_dispatch allocates one more IPC
+ * region (metadata slots, flags, received rows, returned rows) and writes its
+ * 64-byte handle; peers map it with hm_ep_open_peer_dispatch.  Per layer:
+ *   hm_ep_dispatch_meta  all-gather of the ranks' per-expert counts [E] and
+ *                        fp64 score sums [N]: global LayerRequest (rank-order
+ *                        sums), home-rank row layout into dev/host meta
+ *                        ([counts E | offsets E+1] int32, [sums N | scores N]
+ *                        fp64), then *host_flag = host_seq;
+ *   hm_ep_dispatch_rows  all-to-all of the local permuted rows to their
+ *                        experts' home ranks (expert e homed on e % world,
+ *                        shared chunk c on c % world);
+ *   hm_ep_return_rows    all-to-all of the home rank's expert-output rows back
+ *                        to their source ranks' permuted positions.
+ * Each completes only when every rank's rows for this rank have landed. */
+int hm_ep_enable_dispatch(hm_ep *ep, int n_experts_total, int n_routed, int Kp, void *region_handle);
+int hm_ep_open_peer_dispatch(hm_ep *ep, int peer, const void *region_handle);
+int hm_ep_dispatch_meta(hm_ep *ep, const int32_t *counts, const double *score_sum, int32_t *dev_meta_i,
+                        double *dev_meta_d, int32_t *host_meta_i, double *host_meta_d,
+                        uint32_t *host_flag, uint32_t host_seq, void *stream);
+int hm_ep_dispatch_rows(hm_ep *ep, const uint16_t *xp, const int32_t *sel, const int32_t *row_src,
+                        int rows, void *stream);
+int hm_ep_return_rows(hm_ep *ep, const float *out, int rows, void *stream);
+/* Device pointers of this rank's received-rows (bf16) and returned-rows (fp32) buffers. */
+int hm_ep_dispatch_buffers(hm_ep *ep, uint16_t **xrecv, float **ret);
+/* Run forward_layer token-sharded through `ep` (dispatch mode enabled): x and
+ * logits hold this rank's tokens only (T may be 0). */
+int hm_runtime_set_ep_dispatch(hm_runtime *rt, hm_ep *ep);
 /* Route forward_layer's expert-parallel combine through `ep` (NULL: partial
  * to hm_runtime_set_ep_output's buffer for an external all-reduce). */
 int hm_runtime_set_ep_exchange(hm_runtime *rt, hm_ep *ep);

@@ -333,6 +333,9 @@ for _name, (_args, _res) in {
     "hm_ep_open_peer": ([vp, C.c_int, C.c_char_p, C.c_char_p], C.c_int),
     "hm_ep_combine_allreduce": ([vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp], C.c_int),
     "hm_runtime_set_ep_exchange": ([vp, vp], C.c_int),
+    "hm_ep_enable_dispatch": ([vp, C.c_int, C.c_int, C.c_int, C.c_char_p], C.c_int),
+    "hm_ep_open_peer_dispatch": ([vp, C.c_int, C.c_char_p], C.c_int),
+    "hm_runtime_set_ep_dispatch": ([vp, vp], C.c_int),
 }.items():
     _f = getattr(lib, _name)
     _f.argtypes = _args

@@ -20,6 +20,7 @@
 // call sequence number: a rank can run at most one exchange ahead of a peer.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -143,6 +144,202 @@ __global__ void __launch_bounds__(kEpThreads) ep_combine_allreduce_kernel(const 
   }
 }
 
+// ---------------------------------------------------------------- dispatch mode
+// Token-sharded expert parallelism (SURVEY.md §8e "dispatch: all-to-all(v) of
+// token rows to home ranks ... combine: all-to-all(v) back plus weighted
+// sum"): each rank routes only ITS tokens; three kernels per layer move data
+// over peer memory:
+//   ep_meta_kernel      all-gather of every rank's per-expert counts and fp64
+//                       score sums -> global LayerRequest (rank-order sums,
+//                       identical on every rank), the home-rank row layout and
+//                       the host mirror + flag the decision core waits on
+//   ep_dispatch_kernel  all-to-all: each local permuted row -> its expert's
+//                       home rank, at (home base of e) + (rows of e from lower
+//                       ranks) + (rank within e)
+//   ep_return_kernel    all-to-all back: each expert output row -> its source
+//                       rank, at the source's own permuted position
+// after which the source combines locally (hm_combine).  Home layout: experts
+// in index order, inside an expert rows by source rank then source order.
+constexpr int kDispMaxE = 320;
+
+struct DispParams {
+  // region layout (byte offsets, identical on every rank)
+  size_t off_meta, off_mflags, off_dflags, off_rflags, off_xrecv, off_ret, meta_slot;
+  char *region[kEpMaxWorld];  // every rank's region (own included)
+  int rank, world, E, N, H, Kp;
+  uint32_t seq;
+  // local tables (device)
+  int32_t *counts_all;  // [world][E]
+  int32_t *recv_base;   // [E]   row base of expert e inside its home rank's layout
+  int32_t *src_base;    // [world + 1][E] rows of e from ranks < s
+  int32_t *local_off;   // [world][E + 1] rank s's own permuted offsets
+  int32_t *gcount;      // [E]
+  int32_t *ret_map;     // [max received rows] (source rank << 24) | source position
+  int32_t *done;        // [2] block-completion counters (dispatch, return)
+};
+
+__device__ __forceinline__ int home_of(int e, int N, int world) { return (e < N ? e : e - N) % world; }
+
+// Last-block protocol: every block fences its peer stores; the last block to
+// finish raises this rank's flag on every rank, then waits for every rank's
+// flag on its own region (so the kernel completes only when all incoming
+// rows have landed), and resets the counter.
+__device__ void all_to_all_handshake(const DispParams &p, size_t off_flags, int *done) {
+  __threadfence_system();
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(done, 1) == static_cast<int>(gridDim.x) - 1;
+  __syncthreads();
+  if (!last) return;
+  if (threadIdx.x < p.world)
+    st_release_sys(reinterpret_cast<uint32_t *>(p.region[threadIdx.x] + off_flags) + p.rank, p.seq);
+  if (threadIdx.x < p.world) {
+    const uint32_t *f = reinterpret_cast<const uint32_t *>(p.region[p.rank] + off_flags) + threadIdx.x;
+    while (ld_acquire_sys(f) != p.seq) {
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *done = 0;
+}
+
+__global__ void __launch_bounds__(256) ep_meta_kernel(const __grid_constant__ DispParams p,
+                                                      const int32_t *__restrict__ counts,
+                                                      const double *__restrict__ score_sum, int32_t *dev_meta_i,
+                                                      double *dev_meta_d, int32_t *host_meta_i, double *host_meta_d,
+                                                      uint32_t *host_flag, uint32_t host_seq) {
+  __shared__ int32_t s_cnt[kEpMaxWorld][kDispMaxE];
+  __shared__ double s_sum[kEpMaxWorld][256];
+  __shared__ int32_t s_gc[kDispMaxE], s_rb[kDispMaxE];
+  __shared__ double s_gs[256];
+  __shared__ double s_tot;
+  const int par = static_cast<int>(p.seq & 1u), E = p.E, N = p.N, G = p.world;
+  // 1. my counts and score sums into every rank's slot [par][me]
+  for (int r = 0; r < G; ++r) {
+    char *slot = p.region[r] + p.off_meta + (static_cast<size_t>(par) * G + p.rank) * p.meta_slot;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) reinterpret_cast<int32_t *>(slot)[e] = counts[e];
+    double *d = reinterpret_cast<double *>(slot + (static_cast<size_t>(E) * 4 + 7) / 8 * 8);
+    for (int e = threadIdx.x; e < N; e += blockDim.x) d[e] = score_sum[e];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < G)
+    st_release_sys(reinterpret_cast<uint32_t *>(p.region[threadIdx.x] + p.off_mflags) + par * G + p.rank, p.seq);
+  if (threadIdx.x < G) {
+    const uint32_t *f = reinterpret_cast<const uint32_t *>(p.region[p.rank] + p.off_mflags) + par * G + threadIdx.x;
+    while (ld_acquire_sys(f) != p.seq) {
+    }
+  }
+  __syncthreads();
+  // 2. gather every rank's slot from my own region
+  for (int s = 0; s < G; ++s) {
+    const char *slot = p.region[p.rank] + p.off_meta + (static_cast<size_t>(par) * G + s) * p.meta_slot;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) s_cnt[s][e] = __ldcv(reinterpret_cast<const int32_t *>(slot) + e);
+    const double *d = reinterpret_cast<const double *>(slot + (static_cast<size_t>(E) * 4 + 7) / 8 * 8);
+    for (int e = threadIdx.x; e < N; e += blockDim.x) s_sum[s][e] = __ldcv(d + e);
+  }
+  __syncthreads();
+  // 3. global counts / score sums (rank order), tables
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int32_t c = 0, run = 0;
+    for (int s = 0; s < G; ++s) {
+      p.src_base[s * E + e] = run;
+      run += s_cnt[s][e];
+      p.counts_all[s * E + e] = s_cnt[s][e];
+    }
+    p.src_base[G * E + e] = run;
+    c = run;
+    s_gc[e] = c;
+    p.gcount[e] = c;
+  }
+  for (int e = threadIdx.x; e < N; e += blockDim.x) {
+    double acc = 0.0;
+    for (int s = 0; s < G; ++s) acc += s_sum[s][e];
+    s_gs[e] = acc;
+  }
+  if (threadIdx.x < G) {  // rank s's own permuted offsets (its local layout)
+    const int s = threadIdx.x;
+    int32_t run = 0;
+    for (int e = 0; e < E; ++e) {
+      p.local_off[s * (E + 1) + e] = run;
+      run += s_cnt[s][e];
+    }
+    p.local_off[s * (E + 1) + E] = run;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // home layouts (per home rank, experts in index order) and the tot of scores
+    int32_t run[kEpMaxWorld];
+    for (int r = 0; r < G; ++r) run[r] = 0;
+    for (int e = 0; e < E; ++e) {
+      const int h = home_of(e, N, G);
+      s_rb[e] = run[h];
+      run[h] += s_gc[e];
+    }
+    double tot = 0.0;
+    for (int e = 0; e < N; ++e) tot += s_gs[e];
+    s_tot = tot;
+    dev_meta_i[2 * E] = run[p.rank];   // total rows this rank receives
+    host_meta_i[2 * E] = run[p.rank];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    p.recv_base[e] = s_rb[e];
+    dev_meta_i[e] = s_gc[e];
+    dev_meta_i[E + e] = s_rb[e];
+    host_meta_i[e] = s_gc[e];
+    host_meta_i[E + e] = s_rb[e];
+  }
+  for (int e = threadIdx.x; e < N; e += blockDim.x) {
+    const double tot = s_tot;
+    const double sc = tot > 0.0 ? s_gs[e] / tot : 0.0;
+    dev_meta_d[e] = s_gs[e];
+    dev_meta_d[N + e] = sc;
+    host_meta_d[e] = s_gs[e];
+    host_meta_d[N + e] = sc;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) *reinterpret_cast<volatile uint32_t *>(host_flag) = host_seq;
+  // off the host's critical path: where each received row goes back to
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    if (home_of(e, N, G) != p.rank) continue;
+    for (int s = 0; s < G; ++s) {
+      const int base = s_rb[e] + p.src_base[s * E + e], n = s_cnt[s][e], lo = p.local_off[s * (E + 1) + e];
+      for (int i = 0; i < n; ++i) p.ret_map[base + i] = (s << 24) | (lo + i);
+    }
+  }
+}
+
+// one block per 256 (row, 16-byte column) items of the local permuted rows
+__global__ void __launch_bounds__(256) ep_dispatch_kernel(const __grid_constant__ DispParams p,
+                                                          const uint16_t *__restrict__ xp,
+                                                          const int32_t *__restrict__ sel,
+                                                          const int32_t *__restrict__ row_src, int rows) {
+  const int H8 = p.H / 8;
+  const long v = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v < static_cast<long>(rows) * H8) {
+    const int q = static_cast<int>(v / H8), c = static_cast<int>(v - static_cast<long>(q) * H8);
+    const int e = sel[row_src[q]];
+    const int h = home_of(e, p.N, p.world);
+    const int dst = p.recv_base[e] + p.src_base[p.rank * p.E + e] + (q - p.local_off[p.rank * (p.E + 1) + e]);
+    uint4 *d = reinterpret_cast<uint4 *>(p.region[h] + p.off_xrecv) + static_cast<size_t>(dst) * H8 + c;
+    *d = reinterpret_cast<const uint4 *>(xp)[static_cast<size_t>(q) * H8 + c];
+  }
+  all_to_all_handshake(p, p.off_dflags, p.done);
+}
+
+// one block per received row: expert output row -> its source rank's position
+__global__ void __launch_bounds__(256) ep_return_kernel(const __grid_constant__ DispParams p,
+                                                        const float *__restrict__ out, int rows) {
+  const int q = blockIdx.x;
+  if (q < rows) {
+    const int m = p.ret_map[q], src = m >> 24, dst = m & 0xffffff;
+    float4 *d = reinterpret_cast<float4 *>(p.region[src] + p.off_ret) + static_cast<size_t>(dst) * (p.H / 4);
+    const float4 *row = reinterpret_cast<const float4 *>(out) + static_cast<size_t>(q) * (p.H / 4);
+    for (int c = threadIdx.x; c < p.H / 4; c += blockDim.x) d[c] = row[c];
+  }
+  all_to_all_handshake(p, p.off_rflags, p.done + 1);
+}
+
 }  // namespace
 
 struct EpExchange {
@@ -155,6 +352,87 @@ struct EpExchange {
   bool opened[kEpMaxWorld] = {};
   uint32_t seq = 0;
   int grid = 0;
+  // dispatch mode (hm_ep_enable_dispatch)
+  bool disp = false;
+  int E = 0, N = 0, Kp = 0;
+  char *region = nullptr;  // local IPC region
+  char *peer_region[kEpMaxWorld] = {};
+  bool region_opened[kEpMaxWorld] = {};
+  size_t off_meta = 0, off_mflags = 0, off_dflags = 0, off_rflags = 0, off_xrecv = 0, off_ret = 0, meta_slot = 0,
+         region_bytes = 0;
+  int32_t *tables = nullptr;  // counts_all | recv_base | src_base | local_off | gcount | ret_map | done
+  uint32_t dseq = 0;
+
+  static size_t align256(size_t v) { return (v + 255) / 256 * 256; }
+
+  void enable_dispatch(int e_total, int n_routed, int kp) {
+    HM_REQUIRE(!disp, HM_EVALUE, "dispatch mode already enabled");
+    HM_REQUIRE(e_total >= 1 && e_total <= kDispMaxE && n_routed >= 1 && n_routed <= 256 && n_routed <= e_total &&
+                   kp >= 1 && H % 8 == 0,
+               HM_EVALUE, "dispatch mode shape out of range");
+    E = e_total;
+    N = n_routed;
+    Kp = kp;
+    meta_slot = align256((static_cast<size_t>(E) * 4 + 7) / 8 * 8 + static_cast<size_t>(N) * 8);
+    size_t o = 0;
+    off_meta = o;
+    o += align256(2ull * world * meta_slot);
+    off_mflags = o;
+    o += align256(2ull * world * 4);
+    off_dflags = o;
+    o += align256(world * 4ull);
+    off_rflags = o;
+    o += align256(world * 4ull);
+    off_xrecv = o;
+    o += align256(static_cast<size_t>(max_rows) * Kp * H * 2);
+    off_ret = o;
+    o += align256(static_cast<size_t>(max_rows) * Kp * H * 4);
+    region_bytes = o;
+    HM_CUDA(cudaMalloc(&region, region_bytes));
+    HM_CUDA(cudaMemset(region, 0, off_xrecv));  // metadata and flags
+    peer_region[rank] = region;
+    region_opened[rank] = true;
+    const size_t nt = static_cast<size_t>(world) * E + E + (world + 1ull) * E + world * (E + 1ull) + E +
+                      static_cast<size_t>(max_rows) * Kp + 2;
+    HM_CUDA(cudaMalloc(&tables, nt * 4));
+    HM_CUDA(cudaMemset(tables, 0, nt * 4));
+    HM_CUDA(cudaDeviceSynchronize());
+    disp = true;
+  }
+
+  DispParams params() const {
+    DispParams p{};
+    p.off_meta = off_meta;
+    p.off_mflags = off_mflags;
+    p.off_dflags = off_dflags;
+    p.off_rflags = off_rflags;
+    p.off_xrecv = off_xrecv;
+    p.off_ret = off_ret;
+    p.meta_slot = meta_slot;
+    for (int r = 0; r < world; ++r) p.region[r] = peer_region[r];
+    p.rank = rank;
+    p.world = world;
+    p.E = E;
+    p.N = N;
+    p.H = H;
+    p.Kp = Kp;
+    p.seq = dseq;
+    int32_t *t = tables;
+    p.counts_all = t;
+    t += static_cast<size_t>(world) * E;
+    p.recv_base = t;
+    t += E;
+    p.src_base = t;
+    t += (world + 1ull) * E;
+    p.local_off = t;
+    t += world * (E + 1ull);
+    p.gcount = t;
+    t += E;
+    p.ret_map = t;
+    t += static_cast<size_t>(max_rows) * Kp;
+    p.done = t;
+    return p;
+  }
 
   EpExchange(int r, int w, int rows, int h) : rank(r), world(w), max_rows(rows), H(h) {
     HM_REQUIRE(w >= 1 && w <= kEpMaxWorld && r >= 0 && r < w, HM_EVALUE, "expert-parallel world must be 1..8");
@@ -181,8 +459,12 @@ struct EpExchange {
         cudaIpcCloseMemHandle(peer_inbox[r]);
         cudaIpcCloseMemHandle(peer_flags[r]);
       }
+    for (int r = 0; r < world; ++r)
+      if (r != rank && region_opened[r]) cudaIpcCloseMemHandle(peer_region[r]);
     if (inbox) cudaFree(inbox);
     if (flags) cudaFree(flags);
+    if (region) cudaFree(region);
+    if (tables) cudaFree(tables);
   }
 };
 
@@ -261,6 +543,74 @@ int hm_ep_combine_allreduce(hm_ep *ep, const float *out, const float *host_out, 
   const int grid = p.n_tiles < e->grid ? p.n_tiles : e->grid;
   hm::ep_combine_allreduce_kernel<<<grid, hm::kEpThreads, 0, static_cast<cudaStream_t>(stream)>>>(p);
   HM_LAUNCH_CHECK();
+  HM_API_END
+}
+
+int hm_ep_enable_dispatch(hm_ep *ep, int n_experts_total, int n_routed, int Kp, void *region_handle) {
+  HM_API_BEGIN
+  auto *e = reinterpret_cast<hm::EpExchange *>(ep);
+  e->enable_dispatch(n_experts_total, n_routed, Kp);
+  HM_REQUIRE(region_handle, HM_EVALUE, "null handle buffer");
+  HM_CUDA(cudaIpcGetMemHandle(static_cast<cudaIpcMemHandle_t *>(region_handle), e->region));
+  HM_API_END
+}
+
+int hm_ep_open_peer_dispatch(hm_ep *ep, int peer, const void *region_handle) {
+  HM_API_BEGIN
+  auto *e = reinterpret_cast<hm::EpExchange *>(ep);
+  HM_REQUIRE(e->disp && peer >= 0 && peer < e->world, HM_EVALUE, "dispatch mode not enabled or bad peer");
+  if (peer == e->rank || e->region_opened[peer]) return HM_OK;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, region_handle, sizeof h);
+  void *ptr = nullptr;
+  HM_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  e->peer_region[peer] = static_cast<char *>(ptr);
+  e->region_opened[peer] = true;
+  HM_API_END
+}
+
+int hm_ep_dispatch_meta(hm_ep *ep, const int32_t *counts, const double *score_sum, int32_t *dev_meta_i,
+                        double *dev_meta_d, int32_t *host_meta_i, double *host_meta_d, uint32_t *host_flag,
+                        uint32_t host_seq, void *stream) {
+  HM_API_BEGIN
+  auto *e = reinterpret_cast<hm::EpExchange *>(ep);
+  HM_REQUIRE(e->disp, HM_EVALUE, "dispatch mode not enabled");
+  for (int r = 0; r < e->world; ++r) HM_REQUIRE(e->region_opened[r], HM_EVALUE, "dispatch peers not opened");
+  ++e->dseq;
+  hm::ep_meta_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(e->params(), counts, score_sum, dev_meta_i,
+                                                                      dev_meta_d, host_meta_i, host_meta_d,
+                                                                      host_flag, host_seq);
+  HM_LAUNCH_CHECK();
+  HM_API_END
+}
+
+int hm_ep_dispatch_rows(hm_ep *ep, const uint16_t *xp, const int32_t *sel, const int32_t *row_src, int rows,
+                        void *stream) {
+  HM_API_BEGIN
+  auto *e = reinterpret_cast<hm::EpExchange *>(ep);
+  HM_REQUIRE(e->disp && rows >= 0 && rows <= e->max_rows * e->Kp, HM_EVALUE, "bad dispatch");
+  const long items = static_cast<long>(rows) * (e->H / 8);
+  const int grid = static_cast<int>(std::max<long>(1, (items + 255) / 256));
+  hm::ep_dispatch_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(e->params(), xp, sel, row_src, rows);
+  HM_LAUNCH_CHECK();
+  HM_API_END
+}
+
+int hm_ep_return_rows(hm_ep *ep, const float *out, int rows, void *stream) {
+  HM_API_BEGIN
+  auto *e = reinterpret_cast<hm::EpExchange *>(ep);
+  HM_REQUIRE(e->disp && rows >= 0 && rows <= e->max_rows * e->Kp, HM_EVALUE, "bad return");
+  hm::ep_return_kernel<<<std::max(1, rows), 256, 0, static_cast<cudaStream_t>(stream)>>>(e->params(), out, rows);
+  HM_LAUNCH_CHECK();
+  HM_API_END
+}
+
+int hm_ep_dispatch_buffers(hm_ep *ep, uint16_t **xrecv, float **ret) {
+  HM_API_BEGIN
+  auto *e = reinterpret_cast<hm::EpExchange *>(ep);
+  HM_REQUIRE(e->disp, HM_EVALUE, "dispatch mode not enabled");
+  if (xrecv) *xrecv = reinterpret_cast<uint16_t *>(e->region + e->off_xrecv);
+  if (ret) *ret = reinterpret_cast<float *>(e->region + e->off_ret);
   HM_API_END
 }
 

@@ -45,6 +45,11 @@ int hm_router_fused_mirror(const float *, int, int, int, int, int, int, int, con
 int hm_ep_combine_allreduce(hm_ep *, const float *, const float *, const uint64_t *, const int32_t *, const float *,
                             int, int, int, const uint16_t *, uint16_t *, float *, void *);
 int hm_gate_wait(const uint32_t *, uint32_t, void *);
+int hm_ep_dispatch_meta(hm_ep *, const int32_t *, const double *, int32_t *, double *, int32_t *, double *, uint32_t *,
+                        uint32_t, void *);
+int hm_ep_dispatch_rows(hm_ep *, const uint16_t *, const int32_t *, const int32_t *, int, void *);
+int hm_ep_return_rows(hm_ep *, const float *, int, void *);
+int hm_ep_dispatch_buffers(hm_ep *, uint16_t **, float **);
 int hm_combine_tail(const float *, const float *, const uint64_t *, const int32_t *, const float *, int, int, int,
                     const uint16_t *, uint16_t *, double *, const double *, int, int, int, double, void *);
 }
@@ -75,6 +80,13 @@ struct Runtime {
   int R = 0, W = 1;          // expert-parallel rank / world
   float *y32 = nullptr;      // EP partial output (caller-owned)
   hm_ep *ep = nullptr;       // EP peer-memory exchange (caller-owned)
+  // token-sharded EP (hm_runtime_set_ep_dispatch): local routing, all-to-all
+  // of rows to home ranks and back; xcur = the rows the expert kernels read
+  bool disp = false;
+  uint16_t *xrecv = nullptr, *xcur = nullptr;
+  float *retbuf = nullptr;
+  int32_t *lcounts = nullptr, *loffsets = nullptr;
+  double *lsums = nullptr;
   size_t slot_elems, slot_bytes;
   int64_t n_slots;
   uint16_t *pool = nullptr;        // device: [n_slots][slot_elems]
@@ -151,7 +163,7 @@ struct Runtime {
         }
       }
     } release{this, time_kernels && timing_gate};
-    ok(hm_expert_ffn(pool, static_cast<int>(n_slots), H, I, g, n, xp, rows, h, out, HM_FFN_AUTO,
+    ok(hm_expert_ffn(pool, static_cast<int>(n_slots), H, I, g, n, xcur, rows, h, out, HM_FFN_AUTO,
                      static_cast<void *>(st)));
     if (time_kernels) {
       RT_CUDA(cudaEventRecord(b, st));
@@ -236,6 +248,10 @@ struct Runtime {
     // kernel's writes): fall back to the event-synchronised copy path
     if (std::getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") || std::getenv("CUDA_INJECTION64_PATH"))
       timing_gate = zero_copy = false;
+    // under expert parallelism the stream also carries kernels that wait for
+    // peers; a host-held gate in front of them was seen to stall two ranks
+    // sharing one GPU, so kernel timing there runs ungated
+    if (W > 1) timing_gate = false;
     RT_CUDA(cudaHostGetDevicePointer(&dv_hmeta, hmeta, 0));
     RT_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dv_h_x), h_x, 0));
     RT_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dv_h_out), h_out, 0));
@@ -254,6 +270,8 @@ struct Runtime {
     if (ev_req) cudaEventDestroy(ev_req);
     if (ev_rows) cudaEventDestroy(ev_rows);
     if (copy) cudaStreamDestroy(copy);
+    if (lcounts) cudaFree(lcounts);
+    if (lsums) cudaFree(lsums);
     for (void *p : {static_cast<void *>(pool), static_cast<void *>(sel), static_cast<void *>(w),
                     static_cast<void *>(probs), dmeta, static_cast<void *>(pos), static_cast<void *>(row_src),
                     static_cast<void *>(xp), static_cast<void *>(h), static_cast<void *>(out),
@@ -321,7 +339,8 @@ struct Runtime {
                      const int32_t *pred_layers, const int64_t *pred_loads, int n_pred, cudaStream_t st,
                      hm_layer_stats *stats) {
     HM_REQUIRE(layer >= 0 && layer < L, HM_EVALUE, "layer out of range");
-    HM_REQUIRE(T >= 1 && T <= cfg.max_tokens, HM_EVALUE, "token count exceeds the runtime's max_tokens");
+    HM_REQUIRE((T >= 1 || disp) && T >= 0 && T <= cfg.max_tokens, HM_EVALUE,
+               "token count exceeds the runtime's max_tokens");
     hm_layer_stats s{};
     void *vs = static_cast<void *>(st);
     const int rows = T * Kp;
@@ -332,7 +351,8 @@ struct Runtime {
     // (0) router, LayerRequest, permutation -- all on the compute stream; the
     // LayerRequest (counts, offsets, score sums, scores) lands in one pinned
     // buffer with a single D2H copy: the only per-layer host synchronisation
-    const bool fused = T <= 32 && rows <= 1024 && N <= 256 && E <= 320 && H % 8 == 0;
+    const bool fused = !disp && T <= 32 && rows <= 1024 && N <= 256 && E <= 320 && H % 8 == 0;
+    xcur = xp;
     // zero-copy: the router writes the LayerRequest (and, when small, the routed
     // rows) into mapped host memory and raises a flag the host spins on
     const bool mirror = fused && zero_copy;
@@ -350,6 +370,16 @@ struct Runtime {
       if (W > 1) ok(hm_mask_nonhome(sel, w, T * Kp, N, R, W, vs));
       RT_CUDA(cudaMemcpyAsync(hmeta, dmeta, meta_bytes, cudaMemcpyDeviceToHost, st));
       RT_CUDA(cudaEventRecord(ev_req, st));
+    } else if (disp) {  // this rank's tokens: local routing, then the all-gather + all-to-all
+      ok(hm_router_topk(logits, T, N, ld, K, cfg.renormalize, S, cfg.shared_gate_col, sel, w, probs, lcounts, vs));
+      ok(hm_score_sums(probs, T, N, lsums, vs));
+      ok(hm_offsets(lcounts, E, loffsets, vs));
+      ok(hm_permute(sel, T, Kp, E, loffsets, pos, row_src, vs));
+      ok(hm_gather_rows(x, row_src, rows, Kp, H, xp, vs));
+      ++seq;
+      ok(hm_ep_dispatch_meta(ep, lcounts, lsums, counts, score_sum, static_cast<int32_t *>(dv_hmeta),
+                             reinterpret_cast<double *>(static_cast<char *>(dv_hmeta) + meta_ioff), dv_flag, seq, vs));
+      ok(hm_ep_dispatch_rows(ep, xp, sel, row_src, rows, vs));
     } else {
       ok(hm_router_topk(logits, T, N, ld, K, cfg.renormalize, S, cfg.shared_gate_col, sel, w, probs, counts, vs));
       if (W > 1) ok(hm_mask_nonhome(sel, w, T * Kp, N, R, W, vs));
@@ -361,7 +391,7 @@ struct Runtime {
       ok(hm_gather_rows(x, row_src, rows, Kp, H, xp, vs));
     }
     double t0 = now_us();
-    if (mirror) {
+    if (mirror || disp) {
       wait_flag(st);
     } else {
       RT_CUDA(cudaEventSynchronize(ev_req));
@@ -385,6 +415,10 @@ struct Runtime {
     double t2 = now_us();
     s.t_decide_us = t2 - t1;
 
+    // the rows the experts read: local permuted rows, or (token-sharded EP) the
+    // rows every rank dispatched to this home rank, h_offsets[E] of them
+    const int rows_used = disp ? h_offsets[E] : rows;
+    if (disp) xcur = xrecv;
     // CPU rows to host first so the worker can start while the GPU computes
     std::vector<uint32_t> cpu_refs;
     for (const Event &ev : rec.plan.events)
@@ -393,7 +427,7 @@ struct Runtime {
       for (uint32_t r : cpu_refs) {
         const int e = ref_expert(r);
         const size_t rb = h_offsets[e], rc = h_counts[e];
-        RT_CUDA(cudaMemcpyAsync(h_x + rb * H, xp + rb * H, rc * H * 2, cudaMemcpyDeviceToHost, st));
+        RT_CUDA(cudaMemcpyAsync(h_x + rb * H, xcur + rb * H, rc * H * 2, cudaMemcpyDeviceToHost, st));
       }
       if (!cpu_refs.empty()) RT_CUDA(cudaEventRecord(ev_rows, st));
     }
@@ -418,7 +452,7 @@ struct Runtime {
         batch.push_back(hm_group{static_cast<int32_t>(shared_slot(layer, c)), h_offsets[N + c], h_counts[N + c], 0});
     s.bytes_gpu = static_cast<int64_t>(batch.size()) * static_cast<int64_t>(slot_bytes);
     if (!batch.empty()) {
-      ffn(batch.data(), static_cast<int>(batch.size()), rows, st);
+      ffn(batch.data(), static_cast<int>(batch.size()), rows_used, st);
       mark_used(batch.data(), static_cast<int>(batch.size()), st);
     }
     // Copies in plan transfer order (== insert order), then prefetches; an
@@ -431,7 +465,7 @@ struct Runtime {
         const int e = ref_expert(ref);
         wait_ready(slot, st);
         hm_group g{static_cast<int32_t>(slot), h_offsets[e], h_counts[e], 0};
-        ffn(&g, 1, rows, st);
+        ffn(&g, 1, rows_used, st);
         mark_used(&g, 1, st);
         ++s.n_gpu;
         s.bytes_gpu += static_cast<int64_t>(slot_bytes);
@@ -451,7 +485,7 @@ struct Runtime {
     // combine reads the mapped host rows) or by H2D copies into `out`
     const bool do_mrs = cfg.gpu_mrs && engine->cfg.cache_policy == HM_POLICY_MRS && engine->mrs_;
     const bool tail = W == 1 && (!do_mrs || fused) && N <= 256;  // combine_tail launch
-    bool zc_out = zero_copy && (tail || (W > 1 && ep));
+    bool zc_out = zero_copy && !disp && (tail || (W > 1 && ep));
     uint64_t host_mask[4] = {0, 0, 0, 0};
     for (uint32_t r : cpu_refs) {
       const int e = ref_expert(r);
@@ -502,7 +536,10 @@ struct Runtime {
       return;
     }
     // combine (Eq. 1) with the residual stream, then the GPU copy of S
-    if (W > 1 && ep) {  // combine + cross-rank sum + residual: one kernel over peer memory
+    if (W > 1 && disp) {  // expert outputs back to their source ranks, then the local combine
+      ok(hm_ep_return_rows(ep, out, rows_used, vs));
+      ok(hm_combine(retbuf, pos, w, T, Kp, H, cfg.residual ? x : nullptr, y, vs));
+    } else if (W > 1 && ep) {  // combine + cross-rank sum + residual: one kernel over peer memory
       ok(hm_ep_combine_allreduce(ep, out, dv_h_out, zc_out && !cpu_refs.empty() ? host_mask : nullptr, pos, w, T, Kp,
                                  H, cfg.residual ? x : nullptr, y, nullptr, vs));
     } else if (W > 1) {
@@ -512,7 +549,7 @@ struct Runtime {
       ok(hm_combine(out, pos, w, T, Kp, H, cfg.residual ? x : nullptr, y, vs));
     }
     if (cfg.gpu_mrs && engine->cfg.cache_policy == HM_POLICY_MRS && engine->mrs_) {
-      if (!fused) RT_CUDA(cudaMemcpyAsync(scores_dev, h_scores, N * 8, cudaMemcpyHostToDevice, st));
+      if (!fused && !disp) RT_CUDA(cudaMemcpyAsync(scores_dev, h_scores, N * 8, cudaMemcpyHostToDevice, st));
       ok(hm_mrs_update_dev(S_dev, scores_dev, layer, N, engine->mrs_->p, engine->mrs_->alpha, vs));
     }
     if (stats) *stats = s;
@@ -628,6 +665,26 @@ int hm_runtime_preload(hm_runtime *rt, const uint32_t *refs, int n) {
 int hm_runtime_set_ep_output(hm_runtime *rt, float *y32) {
   HM_API_BEGIN
   reinterpret_cast<hm::Runtime *>(rt)->y32 = y32;
+  HM_API_END
+}
+
+int hm_runtime_set_ep_dispatch(hm_runtime *rt, hm_ep *ep) {
+  HM_API_BEGIN
+  auto *r = reinterpret_cast<hm::Runtime *>(rt);
+  HM_REQUIRE(r->W > 1 && ep, HM_EVALUE, "token-sharded dispatch needs ep_world > 1 and an exchange");
+  uint16_t *xr = nullptr;
+  float *rb = nullptr;
+  const int rc = hm_ep_dispatch_buffers(ep, &xr, &rb);
+  if (rc != HM_OK) hm::raise(rc, hm::last_error());
+  if (!r->lcounts) {
+    RT_CUDA(cudaMalloc(&r->lcounts, (2 * static_cast<size_t>(r->E) + 1) * 4));
+    r->loffsets = r->lcounts + r->E;
+    RT_CUDA(cudaMalloc(&r->lsums, static_cast<size_t>(r->N) * 8));
+  }
+  r->ep = ep;
+  r->xrecv = xr;
+  r->retbuf = rb;
+  r->disp = true;
   HM_API_END
 }
 

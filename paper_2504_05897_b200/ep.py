@@ -8,13 +8,20 @@ LayerRequest: loads of non-home experts zeroed, scores kept whole so every
 rank's MRS table is the same.  Per-rank decisions therefore equal the
 reference's ``run_trace`` on the rank-masked trace (tests/test_ep.py).
 
-Exchange: the hidden state of the sequence is replicated; every rank routes
+Exchange (replicated mode): the hidden state of the sequence is replicated; every rank routes
 it identically and computes the partial ``sum_k w_k E_k(x)`` over its home
 experts.  The partials are summed by ``P2PExchange`` -- one kernel per layer
 (csrc/ep_exchange.cu) that fuses the combine with the cross-rank sum and the
 residual, pushing partials into the peers' inboxes over NVLink through CUDA
 IPC mappings -- or, as the baseline, by an all-reduce on the process group
 (NCCL on the GPUs; gloo in the CPU tests) followed by the residual add.
+
+Token-sharded mode (``exchange="dispatch"``): every rank holds and routes only
+its own tokens; the global LayerRequest comes from an all-gather of the ranks'
+counts and score sums (rank-order sums, identical everywhere), token rows go
+to their experts' home ranks by an all-to-all over peer memory and the expert
+outputs come back by the reverse all-to-all before the local combine
+(csrc/ep_exchange.cu: ep_meta / ep_dispatch / ep_return kernels).
 """
 from __future__ import annotations
 
@@ -66,7 +73,9 @@ class P2PExchange:
     CUDA IPC handles are all-gathered through the process group (control plane
     only), and each rank maps its peers' inboxes and flags."""
 
-    def __init__(self, rank: int, world: int, max_rows: int, hidden: int, group=None) -> None:
+    def __init__(self, rank: int, world: int, max_rows: int, hidden: int, group=None,
+                 dispatch: tuple[int, int, int] | None = None) -> None:
+        """dispatch = (E, N, Kp) also sets up the token-sharded all-to-all region."""
         import ctypes as C
 
         import torch.distributed as dist
@@ -75,14 +84,18 @@ class P2PExchange:
         h = C.c_void_p()
         _lib.check(_lib.lib.hm_ep_create(rank, world, max_rows, hidden, C.byref(h)))
         self._h = h.value
-        hi, hf = C.create_string_buffer(64), C.create_string_buffer(64)
+        hi, hf, hd = C.create_string_buffer(64), C.create_string_buffer(64), C.create_string_buffer(64)
         _lib.check(_lib.lib.hm_ep_ipc_handles(self._h, hi, hf))
+        if dispatch is not None:
+            _lib.check(_lib.lib.hm_ep_enable_dispatch(self._h, *dispatch, hd))
         handles = [None] * world
-        dist.all_gather_object(handles, (rank, hi.raw, hf.raw), group=group)
-        for r, bi, bf in handles:
+        dist.all_gather_object(handles, (rank, hi.raw, hf.raw, hd.raw), group=group)
+        for r, bi, bf, bd in handles:
             _lib.check(_lib.lib.hm_ep_open_peer(self._h, r, bi, bf))
+            if dispatch is not None:
+                _lib.check(_lib.lib.hm_ep_open_peer_dispatch(self._h, r, bd))
         dist.barrier(group=group)
-        self.rank, self.world = rank, world
+        self.rank, self.world, self.dispatch = rank, world, dispatch is not None
 
     @property
     def handle(self) -> int:

@@ -173,11 +173,16 @@ class HybridMoE:
                 from .ep import P2PExchange
                 self._ep = P2PExchange(self.ep_rank, self.ep_world, max_tokens, H, process_group)
                 check(lib.hm_runtime_set_ep_exchange(self._rt, self._ep.handle))
+            elif exchange == "dispatch":  # token-sharded: all-to-all of rows to home ranks and back
+                from .ep import P2PExchange
+                self._ep = P2PExchange(self.ep_rank, self.ep_world, max_tokens, H, process_group,
+                                       dispatch=(self.N + self.S, self.N, self.K + self.S))
+                check(lib.hm_runtime_set_ep_dispatch(self._rt, self._ep.handle))
             elif exchange == "allreduce":  # baseline: partials all-reduced on the process group
                 self.y32 = torch.empty((max_tokens, H), dtype=torch.float32, device="cuda")
                 check(lib.hm_runtime_set_ep_output(self._rt, self.y32.data_ptr()))
             else:
-                raise ValueError(f"unknown expert-parallel exchange {exchange!r} (p2p | allreduce)")
+                raise ValueError(f"unknown expert-parallel exchange {exchange!r} (p2p | dispatch | allreduce)")
         pool, store, sb, ns = C.c_void_p(), C.c_void_p(), C.c_size_t(), C.c_int64()
         check(lib.hm_runtime_buffers(self._rt, C.byref(pool), C.byref(store), C.byref(sb), C.byref(ns)))
         self.slot_bytes, self.n_slots = sb.value, ns.value

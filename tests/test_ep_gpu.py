@@ -109,3 +109,82 @@ def test_two_ranks_equal_one_rank(exchange):
             for l, full in enumerate(ref_loads[p]):
                 masked = [v if e % 2 == r else 0 for e, v in enumerate(full)]
                 assert got[r][3][p][l] == masked
+
+
+def _run_dispatch(rank: int, world: int, port: int, q) -> None:
+    """Token-sharded expert parallelism: rank r holds tokens [r*T/G, (r+1)*T/G)
+    of every pass (a decode token lives on rank 0; rank 1 has none)."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    import torch.distributed as dist
+
+    import paper_2504_05897_b200.core as mcore
+    import paper_2504_05897_b200.costs as mcost
+    from paper_2504_05897_b200.engine import EnginePolicy
+    from paper_2504_05897_b200.moe import SHAPES, HybridMoE
+    from paper_2504_05897_b200.tracegen import GenParams, generate_router_logits
+
+    torch.cuda.set_device(0)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = SHAPES["tiny"]
+        eb = mcore.expert_bytes(cfg)
+        prof = mcost.HardwareProfile(gpu_time_per_expert=1.0, cpu_slope=2.0, transfer_bandwidth=eb / 0.5)
+        trace, logits = generate_router_logits(cfg, GenParams(seed=3), 32, 3)
+        res = {}
+        for native in (False, True):
+            moe = HybridMoE(cfg, "tiny", EnginePolicy(), 0.5, prof, max_tokens=48, ep_rank=rank, ep_world=world,
+                            cpu_threads=2, exchange="dispatch")
+            moe.init_seeded_weights(7)
+            g = torch.Generator(device="cuda").manual_seed(5)
+            outs, loads = [], []
+            for p, fwd in enumerate(trace.passes):
+                T = fwd.token_count
+                a, b = rank * T // world, (rank + 1) * T // world
+                lg = [torch.from_numpy(np.ascontiguousarray(logits[p][l][a:b], dtype=np.float32)).cuda()
+                      for l in range(cfg.num_layers)]
+                x = torch.randn((T, moe.H), generator=g, device="cuda").to(torch.bfloat16)[a:b].contiguous()
+                y, info = moe.forward_pass(x, lg, decision_log=not native)
+                torch.cuda.synchronize()
+                outs.append((a, b, y.float().cpu().numpy()))
+                if not native:
+                    loads.append([r[0].tolist() for r in info["requests"]])
+            res[native] = (outs, loads)
+            del moe
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_token_sharded_dispatch_equals_one_rank():
+    ctx = torch.multiprocessing.get_context("spawn")
+    q = ctx.Queue()
+    single = ctx.Process(target=_run, args=(0, 1, 0, q))
+    single.start()
+    ref = q.get(timeout=300)
+    single.join(timeout=60)
+    port = _free_port()
+    procs = [ctx.Process(target=_run_dispatch, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    assert single.exitcode == 0 and all(p.exitcode == 0 for p in procs)
+    _, _, ref_outs, ref_loads, _, _ = ref
+    for r in (0, 1):
+        outs, loads = got[r][False]
+        n_outs, _ = got[r][True]
+        for p, ((a, b, o), (_, _, o_nat)) in enumerate(zip(outs, n_outs)):
+            assert np.array_equal(o, o_nat)                         # native pass == per-layer pass
+            if b > a:
+                want = ref_outs[p][a:b]
+                err = np.abs(o - want).max() / np.abs(want).max()
+                assert err <= 1e-2, (r, p, err)
+            else:
+                assert o.shape[0] == 0
+        for p in range(len(ref_loads)):                          # global, rank-masked LayerRequests
+            for l, full in enumerate(ref_loads[p]):
+                assert loads[p][l] == [v if e % 2 == r else 0 for e, v in enumerate(full)]
