@@ -136,3 +136,104 @@ def test_gloo_world2_partial_sums_equal_full_layer():
     res = dict(q.get(timeout=5) for _ in range(2))
     assert all(p.exitcode == 0 for p in procs)
     assert max(res.values()) < 1e-5
+
+
+def _dispatch_worker(rank, world, port, q):
+    """Token-sharded mode's algorithm (csrc/ep_exchange.cu) restated on CPU:
+    local routing of this rank's tokens, all-gather of per-expert counts and
+    fp64 score sums, home layout (experts in index order, rows by source rank
+    then source order), all-to-all of rows to home ranks, expert compute at
+    home, all-to-all back, local combine."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(1)
+        T, N, K, S, H, I = 13, 8, 2, 1, 32, 128
+        E, Kp = N + S, K + S
+        x = rng.standard_normal((T, H)).astype(np.float32)
+        logits = rng.standard_normal((T, N)).astype(np.float32)
+        experts = [tuple(rng.standard_normal(s).astype(np.float32) * 0.05 for s in ((I, H), (I, H), (H, I)))
+                   for _ in range(E)]
+        home = [(e if e < N else e - N) % world for e in range(E)]
+        a, b = rank * T // world, (rank + 1) * T // world
+        xl, ll = x[a:b], logits[a:b]
+        sel, w, probs, counts, _ = ref.router(ll, N, K, False, S)
+        counts = np.asarray(counts, dtype=np.int64)
+        sums = probs.astype(np.float64).sum(axis=0) if len(ll) else np.zeros(N)
+        # all-gather counts and score sums; global LayerRequest in rank order
+        ca = [torch.zeros(E, dtype=torch.int64) for _ in range(world)]
+        sa = [torch.zeros(N, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(ca, torch.from_numpy(counts))
+        dist.all_gather(sa, torch.from_numpy(sums))
+        ca = np.stack([c.numpy() for c in ca])
+        gsum = np.zeros(N)
+        for s in range(world):
+            gsum = gsum + sa[s].numpy()
+        # local permutation: rows grouped by expert, token order inside
+        order = sorted(range(len(xl) * Kp), key=lambda j: (int(sel.reshape(-1)[j]), j))
+        lrows = [(int(sel.reshape(-1)[j]), j // Kp) for j in order]
+        local_off = np.concatenate([[0], np.cumsum(counts)])
+        # home layout and destinations
+        run = [0] * world
+        recv_base = np.zeros(E, dtype=np.int64)
+        for e in range(E):
+            recv_base[e] = run[home[e]]
+            run[home[e]] += int(ca[:, e].sum())
+        src_base = np.concatenate([np.zeros((1, E), np.int64), np.cumsum(ca, axis=0)])
+        send = [[] for _ in range(world)]
+        for p, (e, t) in enumerate(lrows):
+            send[home[e]].append((int(recv_base[e] + src_base[rank, e] + p - local_off[e]), e, xl[t]))
+        # all-to-all of rows (object lists stand in for the P2P stores)
+        got = [None] * world
+        for dst in range(world):
+            gl = [None] * world
+            dist.all_gather_object(gl, send[dst])
+            if dst == rank:
+                got = gl
+        recv = {}
+        for s in range(world):
+            for pos, e, row in got[s]:
+                recv[pos] = (s, e, row)
+        assert sorted(recv) == list(range(run[rank]))
+        # experts at home, then back to the sources' permuted positions
+        back = [[] for _ in range(world)]
+        for pos, (s, e, row) in recv.items():
+            r = pos - recv_base[e]
+            lo = ca[s, :e].sum()
+            back[s].append((int(lo + r - src_base[s, e]), ref.expert(row[None], *experts[e])[0]))
+        ret = {}
+        for src in range(world):
+            gl = [None] * world
+            dist.all_gather_object(gl, back[src])
+            if src == rank:
+                for lst in gl:
+                    ret.update(dict(lst))
+        # local combine
+        pos_of = {(t, e): p for p, (e, t) in enumerate(lrows)}
+        y = xl.copy()
+        for t in range(len(xl)):
+            for k in range(Kp):
+                e = int(sel[t, k])
+                y[t] += w[t, k] * ret[pos_of[(t, e)]]
+        want = ref.moe_layer(x, logits, experts, N, K, False, S, residual=True)[a:b]
+        ref_sel, _, ref_probs, ref_counts, _ = ref.router(logits, N, K, False, S)
+        ok_counts = list(ca.sum(axis=0)) == [int(v) for v in ref_counts]
+        err = float(np.abs(y - want).max() / np.abs(want).max()) if len(y) else 0.0
+        q.put((rank, err, ok_counts, float(np.abs(gsum - ref_probs.astype(np.float64).sum(axis=0)).max())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_token_sharded_dispatch_equals_full_layer():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dispatch_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    res = {r: (e, ok, ds) for r, e, ok, ds in (q.get(timeout=5) for _ in range(2))}
+    assert all(p.exitcode == 0 for p in procs)
+    for r, (err, ok_counts, dsum) in res.items():
+        assert ok_counts and err < 1e-5 and dsum < 1e-12, (r, err, ok_counts, dsum)
