@@ -18,7 +18,7 @@ lib.hm_cpu_set_decode_grain.argtypes = [C.c_int]
 # (name, H, I, experts per layer call, distinct images)
 shapes = [("mixtral", 4096, 14336, 1, 6), ("mixtral", 4096, 14336, 2, 6), ("deepseek", 2048, 1408, 4, 64),
           ("qwen2", 3584, 2560, 4, 32)]
-grains = [0, 16, 64]
+grains = [int(g) for g in __import__("os").environ.get("HM_BENCH_GRAINS", "0,16,64").split(",")]
 rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 pool = C.c_void_p()
 lib.hm_cpu_pool_create(0, C.byref(pool))
