@@ -249,9 +249,19 @@ def run_ours(args) -> None:
             avail = 0
         host_images = None if avail > 1.3 * total_bytes else max(16, int(0.5 * avail / (3 * H * I * 2)))
     threads = args.cpu_threads or max(1, (os.cpu_count() or 1) // world)
-    moe = HybridMoE(cfg, args.shape, policy, args.ratio, prof, host_images=host_images,
-                    max_tokens=max(args.prefill, 1), cpu_threads=threads, ep_rank=rank, ep_world=world,
-                    exchange=args.exchange)
+    from paper_2504_05897_b200.ep import PeerMemoryUnavailable
+    exchange_note = None
+    try:
+        moe = HybridMoE(cfg, args.shape, policy, args.ratio, prof, host_images=host_images,
+                        max_tokens=max(args.prefill, 1), cpu_threads=threads, ep_rank=rank, ep_world=world,
+                        exchange=args.exchange)
+    except PeerMemoryUnavailable as e:  # every rank sees the same verdict: use the NCCL all-reduce exchange
+        if args.exchange == "dispatch":
+            raise
+        exchange_note = f"p2p unavailable ({e}); NCCL all-reduce used"
+        moe = HybridMoE(cfg, args.shape, policy, args.ratio, prof, host_images=host_images,
+                        max_tokens=max(args.prefill, 1), cpu_threads=threads, ep_rank=rank, ep_world=world,
+                        exchange="allreduce")
     moe.init_random_weights(seed=args.seed + rank)
     n_dec = args.warmup + args.steps
     trace, logits = generate_router_logits(cfg, GenParams(seed=args.seed), args.prefill, 2 * n_dec + 1)
@@ -450,7 +460,7 @@ def run_ours(args) -> None:
                        "l2": f"each step streams {cfg.num_layers * cfg.num_activated} expert evaluations x "
                              f"{3 * H * I * 2 / 1e6:.1f} MB of weights (>> 126 MB L2); no flush needed",
                        "parallelism": f"ep{world}" if world > 1 else "single",
-                       "ep_exchange": moe.exchange},
+                       "ep_exchange": moe.exchange if exchange_note is None else exchange_note},
             "prefill": {"tokens": args.prefill, "ms": prefill_ms, "cold_cache": True,
                         "gpu_experts": sum(s.n_gpu for s in pst), "cpu_experts": sum(s.n_cpu for s in pst),
                         "transfers": sum(s.n_transfer for s in pst)},

@@ -66,6 +66,10 @@ def rank_ratio(config: ModelConfig, ratio: float, rank: int, world: int) -> floa
     return min(1.0, (cap + 0.5) / config.total_routed_experts)
 
 
+class PeerMemoryUnavailable(RuntimeError):
+    """Some rank could not map a peer's buffers (raised on every rank alike)."""
+
+
 class P2PExchange:
     """The peer-memory exchange of one rank (include/hybrimoe.h, hm_ep_*).
 
@@ -90,10 +94,21 @@ class P2PExchange:
             _lib.check(_lib.lib.hm_ep_enable_dispatch(self._h, *dispatch, hd))
         handles = [None] * world
         dist.all_gather_object(handles, (rank, hi.raw, hf.raw, hd.raw), group=group)
-        for r, bi, bf, bd in handles:
-            _lib.check(_lib.lib.hm_ep_open_peer(self._h, r, bi, bf))
-            if dispatch is not None:
-                _lib.check(_lib.lib.hm_ep_open_peer_dispatch(self._h, r, bd))
+        err = ""
+        try:
+            for r, bi, bf, bd in handles:
+                _lib.check(_lib.lib.hm_ep_open_peer(self._h, r, bi, bf))
+                if dispatch is not None:
+                    _lib.check(_lib.lib.hm_ep_open_peer_dispatch(self._h, r, bd))
+        except Exception as e:  # e.g. no CUDA IPC between these processes
+            err = f"{type(e).__name__}: {e}"
+        # collective verdict: every rank must agree before any kernel waits on a peer
+        errs = [None] * world
+        dist.all_gather_object(errs, err, group=group)
+        bad = [f"rank {r}: {m}" for r, m in enumerate(errs) if m]
+        if bad:
+            self.close()
+            raise PeerMemoryUnavailable("; ".join(bad))
         dist.barrier(group=group)
         self.rank, self.world, self.dispatch = rank, world, dispatch is not None
 
