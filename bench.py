@@ -313,6 +313,7 @@ def run_ours(args) -> None:
     # ---- prefill: 1k tokens, cold cache (the reference's TTFT, engine.py:465-466)
     _trace('prefill')
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    _lib.lib.hm_runtime_set_copy_timing(moe._rt, 1)
     ev0.record(st)
     moe.set_profile(prof_prefill)
     _, pinfo = moe.forward_pass(xs[0], dev_logits[0], predict=predictor(0))
@@ -320,6 +321,16 @@ def run_ours(args) -> None:
     ev1.record(st)
     ev1.synchronize()
     prefill_ms = ev0.elapsed_time(ev1)
+    import ctypes as C
+    cms, cby, cn, cmx = C.c_double(), C.c_int64(), C.c_int64(), C.c_double()
+    _lib.check(_lib.lib.hm_runtime_copy_times(moe._rt, C.byref(cms), C.byref(cby), C.byref(cn), C.byref(cmx)))
+    _lib.lib.hm_runtime_set_copy_timing(moe._rt, 0)
+    # PCIe roofline of the prefill's expert copies (CUDA events on the copy stream)
+    h2d_roofline = {"bound": "pcie", "copies": cn.value, "bytes": cby.value, "copy_ms": cms.value,
+                    "achieved_gbs": cby.value / (cms.value / 1e3) / 1e9 if cms.value > 0 else None,
+                    "peak_gbs_gen5_x16": 64.0,
+                    "frac_of_gen5": (cby.value / (cms.value / 1e3) / 1e9 / 64.0) if cms.value > 0 else None,
+                    "link_busy_frac_of_prefill": cms.value / prefill_ms if prefill_ms > 0 else None}
     pst = layer_stats(pinfo)
 
     # ---- decode: W warm-up passes (recorded for the parity block), then K timed passes
@@ -468,6 +479,7 @@ def run_ours(args) -> None:
                     "d2h_bytes_per_step": d2h},
             "roofline": roofline,
             "gemm_roofline": gemm_roofline,
+            "h2d_roofline": h2d_roofline,
             "step_roofline": {"bound": "plan-conditional max(B_gpu/HBM, B_cpu/host DRAM, B_h2d/PCIe)",
                               "bound_ms_per_step": 1e3 * bound_s / args.steps,
                               "frac": (1e3 * bound_s / args.steps) / ms_step, "host_bw_gbs": host_bw_gbs,

@@ -532,6 +532,11 @@ int hm_runtime_set_ep_output(hm_runtime *rt, float *y32);
 /* CUDA-event timing of every expert-FFN launch (bench roofline): enable, then
  * read and reset the accumulated launch time / algorithmic bytes. */
 int hm_runtime_set_kernel_timing(hm_runtime *rt, int on);
+/* Optional CUDA-event timing of every H2D expert copy (demand and prefetch) on
+ * the copy stream: achieved PCIe GB/s = total_bytes / total_ms. */
+int hm_runtime_set_copy_timing(hm_runtime *rt, int on);
+int hm_runtime_copy_times(hm_runtime *rt, double *total_ms, int64_t *total_bytes, int64_t *n,
+                          double *max_ms);
 int hm_runtime_kernel_times(hm_runtime *rt, double *total_ms, int64_t *total_bytes, int64_t *n,
                             double *max_ms);
 

@@ -303,6 +303,8 @@ for _name, (_args, _res) in _RT_SIGS.items():
 for _name, (_args, _res) in {
     "hm_runtime_set_kernel_timing": ([vp, C.c_int], C.c_int),
     "hm_runtime_kernel_times": ([vp, P(f64), P(i64), P(i64), P(f64)], C.c_int),
+    "hm_runtime_set_copy_timing": ([vp, C.c_int], C.c_int),
+    "hm_runtime_copy_times": ([vp, P(f64), P(i64), P(i64), P(f64)], C.c_int),
     "hm_launch_count": ([], C.c_longlong),
 }.items():
     _f = getattr(lib, _name)

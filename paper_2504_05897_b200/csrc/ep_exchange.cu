@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(kEpThreads) ep_combine_allreduce_kernel(const 
     }
     if (threadIdx.x < p.world) {  // wait for every rank's partial of this tile
       const uint32_t *f = p.flags[p.rank] + (static_cast<size_t>(par) * p.world + threadIdx.x) * p.max_tiles + tile;
-      while (ld_acquire_sys(f) != p.seq) {
+      while (static_cast<int32_t>(ld_acquire_sys(f) - p.seq) < 0) {  // reached (wrap-safe)
       }
     }
     __syncthreads();
@@ -195,7 +195,7 @@ __device__ void all_to_all_handshake(const DispParams &p, size_t off_flags, int 
     st_release_sys(reinterpret_cast<uint32_t *>(p.region[threadIdx.x] + off_flags) + p.rank, p.seq);
   if (threadIdx.x < p.world) {
     const uint32_t *f = reinterpret_cast<const uint32_t *>(p.region[p.rank] + off_flags) + threadIdx.x;
-    while (ld_acquire_sys(f) != p.seq) {
+    while (static_cast<int32_t>(ld_acquire_sys(f) - p.seq) < 0) {  // reached (wrap-safe)
     }
   }
   __syncthreads();
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(256) ep_meta_kernel(const __grid_constant__ Di
     st_release_sys(reinterpret_cast<uint32_t *>(p.region[threadIdx.x] + p.off_mflags) + par * G + p.rank, p.seq);
   if (threadIdx.x < G) {
     const uint32_t *f = reinterpret_cast<const uint32_t *>(p.region[p.rank] + p.off_mflags) + par * G + threadIdx.x;
-    while (ld_acquire_sys(f) != p.seq) {
+    while (static_cast<int32_t>(ld_acquire_sys(f) - p.seq) < 0) {  // reached (wrap-safe)
     }
   }
   __syncthreads();

@@ -534,8 +534,11 @@ __global__ void __launch_bounds__(kTailThreads) combine_tail_kernel(const __grid
 // One thread spins until the host writes `seq` into a mapped flag: holds the
 // stream while the host enqueues the kernels to be timed, so the CUDA events
 // around them measure GPU time, not host launch latency (bench roofline).
+// The host releases gates in order and may run several gates ahead of the GPU
+// (e.g. launches queued behind H2D copies), so a gate opens once the flag has
+// reached ITS sequence number, not only while it equals it (wrap-safe compare).
 __global__ void gate_kernel(const uint32_t *flag, uint32_t seq) {
-  while (*reinterpret_cast<const volatile uint32_t *>(flag) != seq) {
+  while (static_cast<int32_t>(*reinterpret_cast<const volatile uint32_t *>(flag) - seq) < 0) {
   }
 }
 

@@ -248,10 +248,7 @@ struct Runtime {
     // kernel's writes): fall back to the event-synchronised copy path
     if (std::getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") || std::getenv("CUDA_INJECTION64_PATH"))
       timing_gate = zero_copy = false;
-    // under expert parallelism the stream also carries kernels that wait for
-    // peers; a host-held gate in front of them was seen to stall two ranks
-    // sharing one GPU, so kernel timing there runs ungated
-    if (W > 1) timing_gate = false;
+
     RT_CUDA(cudaHostGetDevicePointer(&dv_hmeta, hmeta, 0));
     RT_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dv_h_x), h_x, 0));
     RT_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dv_h_out), h_out, 0));
@@ -267,6 +264,10 @@ struct Runtime {
     for (auto e : ready) cudaEventDestroy(e);
     for (auto e : last_use) cudaEventDestroy(e);
     for (auto e : use_ev) cudaEventDestroy(e);
+    for (auto &e : cev) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
     if (ev_req) cudaEventDestroy(ev_req);
     if (ev_rows) cudaEventDestroy(ev_rows);
     if (copy) cudaStreamDestroy(copy);
@@ -316,10 +317,23 @@ struct Runtime {
       RT_CUDA(cudaStreamWaitEvent(copy, use_ev[u % kUseRing], 0));
       copy_waited_seq = u;
     }
+    if (time_copies) {  // H2D achieved GB/s: events on the copy stream around each copy
+      if (cused == cev.size()) {
+        cudaEvent_t e0, e1;
+        RT_CUDA(cudaEventCreate(&e0));
+        RT_CUDA(cudaEventCreate(&e1));
+        cev.emplace_back(e0, e1);
+      }
+      RT_CUDA(cudaEventRecord(cev[cused].first, copy));
+    }
     RT_CUDA(cudaMemcpyAsync(slot_ptr(slot), image_ptr(ref), slot_bytes, cudaMemcpyHostToDevice, copy));
+    if (time_copies) RT_CUDA(cudaEventRecord(cev[cused++].second, copy));
     RT_CUDA(cudaEventRecord(ready[slot], copy));
     copy_pending[slot] = 1;
   }
+  bool time_copies = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> cev;
+  size_t cused = 0;
 
   // Order the compute stream after the latest copy into `slot` (if not already).
   void wait_ready(int64_t slot, cudaStream_t st) {
@@ -699,6 +713,33 @@ int hm_runtime_set_kernel_timing(hm_runtime *rt, int on) {
   auto *r = reinterpret_cast<hm::Runtime *>(rt);
   r->time_kernels = on != 0;
   r->kused = 0;
+  HM_API_END
+}
+
+int hm_runtime_set_copy_timing(hm_runtime *rt, int on) {
+  HM_API_BEGIN
+  auto *r = reinterpret_cast<hm::Runtime *>(rt);
+  r->time_copies = on != 0;
+  r->cused = 0;
+  HM_API_END
+}
+
+int hm_runtime_copy_times(hm_runtime *rt, double *total_ms, int64_t *total_bytes, int64_t *n, double *max_ms) {
+  HM_API_BEGIN
+  auto *r = reinterpret_cast<hm::Runtime *>(rt);
+  RT_CUDA(cudaStreamSynchronize(r->copy));
+  double tot = 0.0, mx = 0.0;
+  for (size_t i = 0; i < r->cused; ++i) {
+    float ms = 0.f;
+    RT_CUDA(cudaEventElapsedTime(&ms, r->cev[i].first, r->cev[i].second));
+    tot += ms;
+    mx = ms > mx ? ms : mx;
+  }
+  if (total_ms) *total_ms = tot;
+  if (total_bytes) *total_bytes = static_cast<int64_t>(r->cused) * static_cast<int64_t>(r->slot_bytes);
+  if (n) *n = static_cast<int64_t>(r->cused);
+  if (max_ms) *max_ms = mx;
+  r->cused = 0;
   HM_API_END
 }
 
