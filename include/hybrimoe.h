@@ -351,6 +351,23 @@ typedef struct hm_group {
 int hm_expert_ffn(const uint16_t *pool, int n_slots, int H, int I, const hm_group *groups,
                   int n_groups, const uint16_t *xp, int total_rows, uint16_t *h, float *out,
                   int path, void *stream);
+/* ---- 4-bit experts (bytes_per_weight 0.5, core.py:55; Marlin,
+ * PAPER.md:217).  Weight-only int4, symmetric, one bf16 scale per 128 weights
+ * of a row: w = (nibble - 8) * scale.  Image: W13 nibbles [2I][H/2] | W2
+ * nibbles [H][I/2] | W13 scales [2I][H/128] | W2 scales [H][I/128], rows in the
+ * bf16 image's order; hm_q4_image_bytes gives its size. */
+int hm_q4_image_bytes(int H, int I, size_t *bytes);
+/* bf16 image (device) -> 4-bit image (device): per (row, 128 weights)
+ * scale = bf16(max|w| / 7), nibble = 8 + clamp(rint(w / scale), -8, 7). */
+int hm_q4_quantize(const uint16_t *bf16_image, int H, int I, uint8_t *q4_image, void *stream);
+int hm_q4_dequantize(const uint8_t *q4_image, int H, int I, uint16_t *bf16_image, void *stream);
+/* hm_expert_ffn over a pool of 4-bit images (slot_bytes apart): decode groups
+ * (<= 4 rows) on the int4 weight-streaming GEMV; larger groups dequantized into
+ * `scratch` (n_scratch bf16 images) and run on the tcgen05 GEMM. */
+int hm_expert_ffn_q4(const uint8_t *pool, size_t slot_bytes, int n_slots, int H, int I,
+                     const hm_group *groups, int n_groups, const uint16_t *xp, int total_rows,
+                     uint16_t *h, float *out, uint16_t *scratch, int n_scratch, int path,
+                     void *stream);
 /* Micro-benchmark: `reps` back-to-back hm_expert_ffn calls from the library
  * (n_groups experts x rows_per_group rows, slots rotating mod n_slots), timed
  * with events on `stream`; *ms = milliseconds per call. */

@@ -78,3 +78,56 @@ def moe_layer(x: np.ndarray, logits: np.ndarray, experts: list, n_routed: int, k
         wt = np.array([w[t, list(sel[t]).index(e)] for t in rows], dtype=np.float32)
         y[rows] += wt[:, None] * out
     return y + x if residual else y
+
+
+# ---------------------------------------------------------------- 4-bit experts
+# Restatement of the 4-bit expert image (include/hybrimoe.h, hm_q4_*): weight-
+# only int4, one bf16 scale per 128 weights of a row, w = (nibble - 8) * scale,
+# rows in the bf16 image's order (W13 gate/up interleaved in 128-row blocks,
+# then W2).  Layout: W13 nibbles [2I][H/2] | W2 nibbles [H][I/2] | W13 scales
+# [2I][H/128] bf16 | W2 scales [H][I/128] bf16.
+Q4G = 128
+
+
+def q4_quantize_rows(w_bf16: np.ndarray):
+    """uint16 bf16 rows [R, K] -> (nibble bytes [R, K/2] uint8, scales [R, K/128] uint16 bf16)."""
+    w = bf16_to_f32(w_bf16)
+    R, K = w.shape
+    g = w.reshape(R, K // Q4G, Q4G)
+    s_bits = f32_to_bf16(np.abs(g).max(axis=2) / np.float32(7.0))
+    s = bf16_to_f32(s_bits)[:, :, None]
+    with np.errstate(divide="ignore", invalid="ignore"):
+        q = np.where(s > 0, np.rint(g / np.where(s > 0, s, 1)), 0)
+    nib = (np.clip(q, -8, 7) + 8).astype(np.uint8).reshape(R, K)
+    return (nib[:, 0::2] | (nib[:, 1::2] << 4)).astype(np.uint8), s_bits
+
+
+def q4_dequantize_rows(nib: np.ndarray, scales: np.ndarray) -> np.ndarray:
+    """(nibble bytes [R, K/2], bf16 scales [R, K/128]) -> fp32 rows [R, K]."""
+    R = nib.shape[0]
+    vals = np.empty((R, nib.shape[1] * 2), dtype=np.float32)
+    vals[:, 0::2] = (nib & 15).astype(np.float32) - 8
+    vals[:, 1::2] = (nib >> 4).astype(np.float32) - 8
+    s = bf16_to_f32(scales)
+    return (vals.reshape(R, -1, Q4G) * s[:, :, None]).reshape(R, -1)
+
+
+def q4_image(w13_bf16: np.ndarray, w2_bf16: np.ndarray) -> np.ndarray:
+    """bf16 rows of W13 [2I, H] (image order) and W2 [H, I] -> the 4-bit image bytes."""
+    n13, s13 = q4_quantize_rows(w13_bf16)
+    n2, s2 = q4_quantize_rows(w2_bf16)
+    return np.concatenate([n13.reshape(-1), n2.reshape(-1), s13.reshape(-1).view(np.uint8),
+                           s2.reshape(-1).view(np.uint8)])
+
+
+def q4_expert(img: np.ndarray, H: int, I: int):
+    """4-bit image bytes -> fp32 (gate [I, H], up [I, H], down [H, I])."""
+    hi = H * I
+    n13 = img[:hi].reshape(2 * I, H // 2)
+    n2 = img[hi: hi + hi // 2].reshape(H, I // 2)
+    o = hi + hi // 2
+    s13 = img[o: o + 2 * I * (H // Q4G) * 2].view(np.uint16).reshape(2 * I, H // Q4G)
+    o += 2 * I * (H // Q4G) * 2
+    s2 = img[o: o + H * (I // Q4G) * 2].view(np.uint16).reshape(H, I // Q4G)
+    w13 = q4_dequantize_rows(n13, s13).reshape(I // 128, 2, 128, H)
+    return w13[:, 0].reshape(I, H), w13[:, 1].reshape(I, H), q4_dequantize_rows(n2, s2)

@@ -1,0 +1,335 @@
+// 4-bit expert weights (the paper runs Marlin 4-bit
+// experts; the reference's default bytes_per_weight is 0.5,
+// core.py:55).  Weight-only int4, symmetric, one bf16 scale per 128 weights
+// of a row:  w = (nibble - 8) * scale.
+//
+// Expert image (bytes), rows in the same order as the bf16 image (W13 with
+// gate/up rows interleaved in 128-row blocks, then W2):
+//   [0, HI)                 W13 nibbles  [2I rows][H/2]   (element 2k: low nibble of byte k)
+//   [HI, 3HI/2)             W2 nibbles   [H rows][I/2]
+//   [3HI/2, +2I*H/64)       W13 scales   [2I rows][H/128] bf16
+//   [.., +H*I/64)           W2 scales    [H rows][I/128]  bf16
+// = 3HI/2 + 3HI/64 bytes (expert_bytes at bytes_per_weight 0.5, plus 3.1 % scales).
+//
+// Kernels: quantize (bf16 image -> q4 image), dequantize (q4 -> bf16 image,
+// feeding the tcgen05 GEMM for prefill-sized groups), and the decode GEMV on
+// the q4 image: nibbles -> fp16 pairs with one LOP3 + one HSUB2 per pair
+// (the 0x6400 exponent trick), HFMA2 against x held in shared memory as fp16
+// in the matching pair order, fp16 partials over 32 weights, fp32 across.
+#include <cuda_fp16.h>
+
+#include <vector>
+
+#include "device.cuh"
+
+namespace hm {
+namespace {
+
+constexpr int kQG = 128;  // weights per scale
+constexpr int kQ4MaxGroups = 96;
+constexpr int kIlvQ = 128;
+
+struct Q4Layout {
+  size_t w2_off, s13_off, s2_off, bytes;
+};
+__host__ __device__ inline Q4Layout q4_layout(int H, int I) {
+  const size_t hi = static_cast<size_t>(H) * I;
+  Q4Layout l;
+  l.w2_off = hi;
+  l.s13_off = hi + hi / 2;
+  l.s2_off = l.s13_off + static_cast<size_t>(2) * I * (H / kQG) * 2;
+  l.bytes = l.s2_off + static_cast<size_t>(H) * (I / kQG) * 2;
+  return l;
+}
+
+// one thread per (row, 128-group) of W13 then W2
+__global__ void q4_quantize_kernel(const uint16_t *__restrict__ img, int H, int I, uint8_t *__restrict__ q) {
+  const Q4Layout L = q4_layout(H, I);
+  const long g13 = static_cast<long>(2) * I * (H / kQG), g2 = static_cast<long>(H) * (I / kQG);
+  const long t = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= g13 + g2) return;
+  const bool w13 = t < g13;
+  const long tt = w13 ? t : t - g13;
+  const int K = w13 ? H : I, gpr = K / kQG;
+  const long row = tt / gpr, grp = tt % gpr;
+  const uint16_t *src = img + (w13 ? 0 : static_cast<size_t>(2) * I * H) + row * K + grp * kQG;
+  float mx = 0.f;
+  for (int i = 0; i < kQG; ++i) mx = fmaxf(mx, fabsf(dev::bf2f(src[i])));
+  const uint16_t sb = dev::f2bf(mx / 7.0f);
+  const float s = dev::bf2f(sb);
+  uint8_t *dst = q + (w13 ? 0 : L.w2_off) + row * (K / 2) + grp * (kQG / 2);
+  for (int i = 0; i < kQG; i += 2) {
+    int a = 8, b = 8;
+    if (s > 0.f) {
+      a = 8 + max(-8, min(7, __float2int_rn(dev::bf2f(src[i]) / s)));
+      b = 8 + max(-8, min(7, __float2int_rn(dev::bf2f(src[i + 1]) / s)));
+    }
+    dst[i / 2] = static_cast<uint8_t>(a | (b << 4));
+  }
+  reinterpret_cast<uint16_t *>(q + (w13 ? L.s13_off : L.s2_off))[row * gpr + grp] = sb;
+}
+
+__global__ void q4_dequantize_kernel(const uint8_t *__restrict__ q, int H, int I, uint16_t *__restrict__ img) {
+  const Q4Layout L = q4_layout(H, I);
+  const long g13 = static_cast<long>(2) * I * (H / kQG), g2 = static_cast<long>(H) * (I / kQG);
+  const long t = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= g13 + g2) return;
+  const bool w13 = t < g13;
+  const long tt = w13 ? t : t - g13;
+  const int K = w13 ? H : I, gpr = K / kQG;
+  const long row = tt / gpr, grp = tt % gpr;
+  const float s = dev::bf2f(reinterpret_cast<const uint16_t *>(q + (w13 ? L.s13_off : L.s2_off))[row * gpr + grp]);
+  const uint8_t *src = q + (w13 ? 0 : L.w2_off) + row * (K / 2) + grp * (kQG / 2);
+  uint16_t *dst = img + (w13 ? 0 : static_cast<size_t>(2) * I * H) + row * K + grp * kQG;
+  for (int i = 0; i < kQG / 2; ++i) {
+    const uint8_t b = src[i];
+    dst[2 * i] = dev::f2bf(static_cast<float>((b & 15) - 8) * s);
+    dst[2 * i + 1] = dev::f2bf(static_cast<float>((b >> 4) - 8) * s);
+  }
+}
+
+// 8 nibbles of v (elements e0..e7, e0 in bits 0-3) -> four fp16 pairs
+// (e0,e4) (e1,e5) (e2,e6) (e3,e7), each value = nibble - 8, exactly.
+__device__ __forceinline__ void nib8_to_h2(uint32_t v, __half2 (&o)[4]) {
+  const uint32_t bias = 0x64086408u;  // fp16 1032.0 = 1024 + 8
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t t;
+    const uint32_t sh = v >> (4 * j);
+    asm("lop3.b32 %0, %1, %2, %3, 0xea;" : "=r"(t) : "r"(sh), "r"(0x000F000Fu), "r"(0x64006400u));  // (a & b) | c
+    o[j] = __hsub2(*reinterpret_cast<__half2 *>(&t), *reinterpret_cast<const __half2 *>(&bias));
+  }
+}
+
+// x (bf16, K values) -> fp16 in pair order: for each 8 elements
+// [x0 x4 x1 x5 x2 x6 x3 x7], matching nib8_to_h2.
+__device__ __forceinline__ void stage_x_h2(const uint16_t *__restrict__ x, int K, __half *xs) {
+  for (int i = threadIdx.x; i < K; i += blockDim.x) {
+    const int blk = i & ~7, e = i & 7;
+    const int p = blk + (e < 4 ? 2 * e : 2 * (e - 4) + 1);
+    xs[p] = __float2half_rn(dev::bf2f(x[i]));
+  }
+}
+
+// dot of one q4 row segment (32 weights per lane per step) with staged x; returns the lane's partial (fp32)
+__device__ __forceinline__ float q4_row_dot(const uint8_t *__restrict__ row, const uint16_t *__restrict__ sc,
+                                            const __half *xs, int K, int lane) {
+  float acc = 0.f;
+  for (int c = lane * 32; c < K; c += 32 * 32) {
+    const uint4 w = dev::ld_stream(row + c / 2);
+    const float s = dev::bf2f(sc[c / kQG]);
+    const uint4 *xv = reinterpret_cast<const uint4 *>(xs + c);  // 32 halfs = 4 x uint4
+    __half2 a0 = __float2half2_rn(0.f), a1 = a0;
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      __half2 n[4];
+      nib8_to_h2(ws[q], n);
+      const uint4 xq = xv[q];
+      a0 = __hfma2(n[0], *reinterpret_cast<const __half2 *>(&xq.x), a0);
+      a1 = __hfma2(n[1], *reinterpret_cast<const __half2 *>(&xq.y), a1);
+      a0 = __hfma2(n[2], *reinterpret_cast<const __half2 *>(&xq.z), a0);
+      a1 = __hfma2(n[3], *reinterpret_cast<const __half2 *>(&xq.w), a1);
+    }
+    const float2 f0 = __half22float2(a0), f1 = __half22float2(a1);
+    acc = fmaf(s, (f0.x + f0.y) + (f1.x + f1.y), acc);
+  }
+  return acc;
+}
+
+struct Q4GemvParams {
+  const uint8_t *pool;
+  size_t slot_bytes;
+  int H, I, n_groups, bpg, chunk;
+  const uint16_t *xp;
+  uint16_t *h;
+  float *out;
+  int32_t slot[kQ4MaxGroups], row_begin[kQ4MaxGroups], row_count[kQ4MaxGroups];
+};
+
+template <int MR>
+__global__ void __launch_bounds__(256) ffn1_q4_kernel(const __grid_constant__ Q4GemvParams p) {
+  extern __shared__ __align__(16) __half xs1[];  // [MR][H]
+  const int g = blockIdx.x / p.bpg, cid = blockIdx.x % p.bpg;
+  const int M = p.row_count[g], rb = p.row_begin[g], H = p.H, I = p.I;
+  for (int m = 0; m < M; ++m) stage_x_h2(p.xp + static_cast<size_t>(rb + m) * H, H, xs1 + m * H);
+  __syncthreads();
+  const Q4Layout L = q4_layout(H, I);
+  const uint8_t *img = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_bytes;
+  const uint16_t *s13 = reinterpret_cast<const uint16_t *>(img + L.s13_off);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int i_end = min(I, (cid + 1) * p.chunk);
+  for (int i = cid * p.chunk + wid; i < i_end; i += nw) {
+    const size_t grow = static_cast<size_t>((i / kIlvQ) * 2 * kIlvQ + (i % kIlvQ));
+    const uint8_t *wg = img + grow * (H / 2), *wu = wg + static_cast<size_t>(kIlvQ) * (H / 2);
+    const uint16_t *sg = s13 + grow * (H / kQG), *su = sg + static_cast<size_t>(kIlvQ) * (H / kQG);
+#pragma unroll
+    for (int m = 0; m < MR; ++m) {
+      if (m < M) {
+        const float gs = dev::warp_sum(q4_row_dot(wg, sg, xs1 + m * H, H, lane));
+        const float us = dev::warp_sum(q4_row_dot(wu, su, xs1 + m * H, H, lane));
+        if (lane == 0) p.h[static_cast<size_t>(rb + m) * I + i] = dev::f2bf(dev::silu(gs) * us);
+      }
+    }
+  }
+}
+
+template <int MR>
+__global__ void __launch_bounds__(256) ffn2_q4_kernel(const __grid_constant__ Q4GemvParams p) {
+  extern __shared__ __align__(16) __half hs2[];  // [MR][I]
+  const int g = blockIdx.x / p.bpg, cid = blockIdx.x % p.bpg;
+  const int M = p.row_count[g], rb = p.row_begin[g], H = p.H, I = p.I;
+  for (int m = 0; m < M; ++m) stage_x_h2(p.h + static_cast<size_t>(rb + m) * I, I, hs2 + m * I);
+  __syncthreads();
+  const Q4Layout L = q4_layout(H, I);
+  const uint8_t *img = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_bytes;
+  const uint8_t *w2 = img + L.w2_off;
+  const uint16_t *s2 = reinterpret_cast<const uint16_t *>(img + L.s2_off);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int j_end = min(H, (cid + 1) * p.chunk);
+  for (int j = cid * p.chunk + wid; j < j_end; j += nw) {
+    const uint8_t *wr = w2 + static_cast<size_t>(j) * (I / 2);
+    const uint16_t *sr = s2 + static_cast<size_t>(j) * (I / kQG);
+#pragma unroll
+    for (int m = 0; m < MR; ++m) {
+      if (m < M) {
+        const float s = dev::warp_sum(q4_row_dot(wr, sr, hs2 + m * I, I, lane));
+        if (lane == 0) p.out[static_cast<size_t>(rb + m) * H + j] = s;
+      }
+    }
+  }
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <typename K>
+void q4_smem(K kernel, int bytes) {
+  if (bytes > 48 * 1024) HM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
+void launch_q4_gemv(const uint8_t *pool, size_t slot_bytes, int H, int I, const std::vector<hm_group> &gs,
+                    const uint16_t *xp, uint16_t *h, float *out, cudaStream_t st) {
+  if (gs.empty()) return;
+  Q4GemvParams p{};
+  p.pool = pool;
+  p.slot_bytes = slot_bytes;
+  p.H = H;
+  p.I = I;
+  p.n_groups = static_cast<int>(gs.size());
+  p.xp = xp;
+  p.h = h;
+  p.out = out;
+  int mr = 1;
+  for (size_t g = 0; g < gs.size(); ++g) {
+    p.slot[g] = gs[g].slot;
+    p.row_begin[g] = gs[g].row_begin;
+    p.row_count[g] = gs[g].row_count;
+    mr = std::max(mr, gs[g].row_count);
+  }
+  const int target = sm_count() * 4, G = p.n_groups;
+  p.chunk = std::max(8, static_cast<int>((static_cast<long>(G) * I + target - 1) / target + 7) / 8 * 8);
+  p.bpg = (I + p.chunk - 1) / p.chunk;
+  int smem = mr * H * 2;
+  switch (mr) {
+    case 1: q4_smem(ffn1_q4_kernel<1>, smem); ffn1_q4_kernel<1><<<G * p.bpg, 256, smem, st>>>(p); break;
+    case 2: q4_smem(ffn1_q4_kernel<2>, smem); ffn1_q4_kernel<2><<<G * p.bpg, 256, smem, st>>>(p); break;
+    default: q4_smem(ffn1_q4_kernel<4>, smem); ffn1_q4_kernel<4><<<G * p.bpg, 256, smem, st>>>(p); break;
+  }
+  HM_LAUNCH_CHECK();
+  p.chunk = std::max(8, static_cast<int>((static_cast<long>(G) * H + target - 1) / target + 7) / 8 * 8);
+  p.bpg = (H + p.chunk - 1) / p.chunk;
+  smem = mr * I * 2;
+  switch (mr) {
+    case 1: q4_smem(ffn2_q4_kernel<1>, smem); ffn2_q4_kernel<1><<<G * p.bpg, 256, smem, st>>>(p); break;
+    case 2: q4_smem(ffn2_q4_kernel<2>, smem); ffn2_q4_kernel<2><<<G * p.bpg, 256, smem, st>>>(p); break;
+    default: q4_smem(ffn2_q4_kernel<4>, smem); ffn2_q4_kernel<4><<<G * p.bpg, 256, smem, st>>>(p); break;
+  }
+  HM_LAUNCH_CHECK();
+}
+
+}  // namespace
+}  // namespace hm
+
+extern "C" {
+
+int hm_expert_ffn(const uint16_t *, int, int, int, const hm_group *, int, const uint16_t *, int, uint16_t *, float *,
+                  int, void *);
+
+int hm_q4_image_bytes(int H, int I, size_t *bytes) {
+  HM_API_BEGIN
+  HM_REQUIRE(H > 0 && I > 0 && H % 128 == 0 && I % 128 == 0, HM_EVALUE, "4-bit experts need H, I multiples of 128");
+  *bytes = hm::q4_layout(H, I).bytes;
+  HM_API_END
+}
+
+int hm_q4_quantize(const uint16_t *bf16_image, int H, int I, uint8_t *q4_image, void *stream) {
+  HM_API_BEGIN
+  HM_REQUIRE(H % 128 == 0 && I % 128 == 0, HM_EVALUE, "4-bit experts need H, I multiples of 128");
+  const long n = static_cast<long>(3) * H * I / hm::kQG;
+  hm::q4_quantize_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      bf16_image, H, I, q4_image);
+  HM_LAUNCH_CHECK();
+  HM_API_END
+}
+
+int hm_q4_dequantize(const uint8_t *q4_image, int H, int I, uint16_t *bf16_image, void *stream) {
+  HM_API_BEGIN
+  HM_REQUIRE(H % 128 == 0 && I % 128 == 0, HM_EVALUE, "4-bit experts need H, I multiples of 128");
+  const long n = static_cast<long>(3) * H * I / hm::kQG;
+  hm::q4_dequantize_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      q4_image, H, I, bf16_image);
+  HM_LAUNCH_CHECK();
+  HM_API_END
+}
+
+int hm_expert_ffn_q4(const uint8_t *pool, size_t slot_bytes, int n_slots, int H, int I, const hm_group *groups,
+                     int n_groups, const uint16_t *xp, int total_rows, uint16_t *h, float *out, uint16_t *scratch,
+                     int n_scratch, int path, void *stream) {
+  HM_API_BEGIN
+  HM_REQUIRE(H % 128 == 0 && I % 128 == 0, HM_EVALUE, "4-bit experts need H, I multiples of 128");
+  HM_REQUIRE(slot_bytes >= hm::q4_layout(H, I).bytes, HM_EVALUE, "slot smaller than a 4-bit expert image");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::vector<hm_group> small, big;
+  for (int g = 0; g < n_groups; ++g) {
+    const hm_group &gr = groups[g];
+    HM_REQUIRE(gr.slot >= 0 && gr.slot < n_slots && gr.row_begin >= 0 && gr.row_count >= 0 &&
+                   gr.row_begin + gr.row_count <= total_rows,
+               HM_EVALUE, "expert group outside the pool or the row range");
+    if (gr.row_count == 0) continue;
+    const bool gemv = path == HM_FFN_GEMV || (path == HM_FFN_AUTO && gr.row_count <= 4);
+    HM_REQUIRE(!gemv || gr.row_count <= 4, HM_EVALUE, "GEMV path takes at most 4 rows per expert");
+    (gemv ? small : big).push_back(gr);
+  }
+  for (size_t b = 0; b < small.size(); b += hm::kQ4MaxGroups) {
+    std::vector<hm_group> part(small.begin() + b, small.begin() + std::min(small.size(), b + hm::kQ4MaxGroups));
+    hm::launch_q4_gemv(pool, slot_bytes, H, I, part, xp, h, out, st);
+  }
+  // prefill-sized groups: dequantize into bf16 scratch slots, then the tcgen05 GEMM
+  const size_t elems = static_cast<size_t>(3) * H * I;
+  for (size_t b = 0; b < big.size(); b += static_cast<size_t>(std::max(1, n_scratch))) {
+    HM_REQUIRE(scratch && n_scratch >= 1, HM_EVALUE, "4-bit GEMM path needs bf16 scratch slots");
+    std::vector<hm_group> part;
+    for (size_t i = b; i < std::min(big.size(), b + static_cast<size_t>(n_scratch)); ++i) {
+      const int k = static_cast<int>(i - b);
+      const int rc = hm_q4_dequantize(pool + static_cast<size_t>(big[i].slot) * slot_bytes, H, I,
+                                      scratch + static_cast<size_t>(k) * elems, stream);
+      if (rc != HM_OK) hm::raise(rc, hm::last_error());
+      part.push_back(hm_group{k, big[i].row_begin, big[i].row_count, 0});
+    }
+    const int rc = hm_expert_ffn(scratch, n_scratch, H, I, part.data(), static_cast<int>(part.size()), xp,
+                                 total_rows, h, out, HM_FFN_GEMM, stream);
+    if (rc != HM_OK) hm::raise(rc, hm::last_error());
+  }
+  HM_API_END
+}
+
+}  // extern "C"

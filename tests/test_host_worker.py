@@ -70,3 +70,13 @@ def test_host_read_bandwidth_probe(pool):
     gbs = C.c_double()
     _lib.check(lib.hm_host_read_bw(pool, buf.ctypes.data, buf.nbytes, 2, C.byref(gbs)))
     assert gbs.value > 0
+
+
+def test_oracle_q4_roundtrip():
+    """The 4-bit restatement: dequantize(quantize(w)) within half a scale step of w."""
+    rng = np.random.default_rng(3)
+    w = ref.f32_to_bf16(rng.standard_normal((6, 256)).astype(np.float32) * 0.02)
+    nib, s = ref.q4_quantize_rows(w)
+    back = ref.q4_dequantize_rows(nib, s)
+    step = np.repeat(ref.bf16_to_f32(s), 128, axis=1)
+    assert np.all(np.abs(back - ref.bf16_to_f32(w)) <= 0.5 * step * (1 + 1e-6) + 1e-12)

@@ -225,3 +225,48 @@ def test_moe_layer_end_to_end(T, N, Kk, S, renorm, gate):
     want = ref.moe_layer(bf16_numpy(x), logits, experts, N, Kk, renorm, S, gate)
     assert rel_err(bf16_numpy(y), want) <= TOL
 
+
+
+@pytest.mark.parametrize("H,I,rows", [(256, 384, (1, 1, 1)), (512, 256, (2, 4, 1)), (1024, 1408, (1, 3)),
+                                       (256, 256, (40, 1, 130))])
+def test_q4_quantize_and_ffn(H, I, rows):
+    """4-bit experts: the GPU quantizer reproduces the numpy restatement byte for
+    byte; decode GEMV (<= 4 rows) and dequantize + tcgen05 GEMM (larger groups)
+    match the fp32 oracle on the dequantized weights."""
+    import ctypes as Cc
+    lib = _lib.lib
+    nb = Cc.c_size_t()
+    _lib.check(lib.hm_q4_image_bytes(H, I, Cc.byref(nb)))
+    n = len(rows)
+    bf_pool, experts = make_pool(n, H, I, seed=H + I)
+    q = torch.empty((n, nb.value), dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    lib.hm_q4_quantize.argtypes = [Cc.c_void_p, Cc.c_int, Cc.c_int, Cc.c_void_p, Cc.c_void_p]
+    for s in range(n):
+        _lib.check(lib.hm_q4_quantize(bf_pool.data_ptr() + s * 3 * H * I * 2, H, I, q[s].data_ptr(), st))
+    torch.cuda.synchronize()
+    img0 = bf_pool[: 3 * H * I].view(torch.int16).cpu().numpy().view(np.uint16)
+    want_img = ref.q4_image(img0[: 2 * I * H].reshape(2 * I, H), img0[2 * I * H:].reshape(H, I))
+    assert np.array_equal(q[0].cpu().numpy(), want_img)
+    total = sum(rows)
+    x = torch.randn((total, H), device="cuda").to(torch.bfloat16)
+    h = torch.empty((total, I), dtype=torch.bfloat16, device="cuda")
+    out = torch.empty((total, H), device="cuda")
+    scratch = torch.empty((2, 3 * H * I), dtype=torch.bfloat16, device="cuda")
+    groups, rb = [], 0
+    for s, m in enumerate(rows):
+        groups.append((s, rb, m))
+        rb += m
+    arr = K.groups_array(groups)
+    lib.hm_expert_ffn_q4.argtypes = [Cc.c_void_p, Cc.c_size_t, Cc.c_int, Cc.c_int, Cc.c_int, Cc.c_void_p, Cc.c_int,
+                                     Cc.c_void_p, Cc.c_int, Cc.c_void_p, Cc.c_void_p, Cc.c_void_p, Cc.c_int, Cc.c_int,
+                                     Cc.c_void_p]
+    _lib.check(lib.hm_expert_ffn_q4(q.data_ptr(), nb.value, n, H, I, arr, n, x.data_ptr(), total, h.data_ptr(),
+                                    out.data_ptr(), scratch.data_ptr(), 2, _lib.FFN_AUTO, st))
+    torch.cuda.synchronize()
+    xs = bf16_numpy(x)
+    o = out.cpu().numpy()
+    for s, (slot, r0, m) in enumerate(groups):
+        gq, uq, dq = ref.q4_expert(q[s].cpu().numpy(), H, I)
+        want = ref.expert(xs[r0:r0 + m], gq, uq, dq)
+        assert rel_err(o[r0:r0 + m], want) <= TOL, (s, m, rel_err(o[r0:r0 + m], want))
