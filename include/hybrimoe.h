@@ -414,7 +414,13 @@ void hm_cpu_pool_destroy(hm_cpu_pool *p);
 /* out[M, H] fp32 = expert(img)(x[M, H] bf16) on the host; img in slot layout (HOST pointers). */
 int hm_cpu_expert(hm_cpu_pool *pool, const uint16_t *img, int H, int I, const uint16_t *x, int M,
                   float *out);
+/* 4-bit expert images on the host worker (same rules as hm_cpu_expert). */
+int hm_cpu_expert_q4(hm_cpu_pool *pool, const uint8_t *img, int H, int I, const uint16_t *x, int M,
+                     float *out);
+int hm_cpu_experts_decode_q4(hm_cpu_pool *pool, const uint8_t *const *imgs, const uint16_t *const *xs,
+                             int n, int H, int I, float *const *outs);
 int hm_cpu_has_avx512bf16(void);
+int hm_cpu_has_amx_bf16(void); /* AMX-BF16 present and XTILEDATA granted */
 /* Decode-stream tuning: software prefetch distance (elements) and hint (0 none, 1 T0, 2 T1, 3 NTA). */
 int hm_cpu_set_prefetch(int dist, int hint);
 /* n single-token experts in one worker pass (decode): outs[i][H] = expert(imgs[i])(xs[i][H]). */

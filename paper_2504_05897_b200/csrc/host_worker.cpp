@@ -568,7 +568,188 @@ void cpu_expert_amx2(ThreadPool &pool, const uint16_t *img, int H, int I, const 
   });
 }
 
+// ------------------------------------------------------------ 4-bit experts
+// Image layout and value rule: include/hybrimoe.h (hm_q4_*), oracle/moe_ref.py.
+struct Q4View {
+  const uint8_t *n13, *n2;
+  const uint16_t *s13, *s2;
+};
+inline Q4View q4_view(const uint8_t *img, int H, int I) {
+  const size_t hi = static_cast<size_t>(H) * I;
+  Q4View v;
+  v.n13 = img;
+  v.n2 = img + hi;
+  v.s13 = reinterpret_cast<const uint16_t *>(img + hi + hi / 2);
+  v.s2 = v.s13 + static_cast<size_t>(2) * I * (H / 128);
+  return v;
+}
+
+// x (bf16 [K]) -> even / odd elements in fp32 and, per 128-group, the lane-wise
+// partial sums of x (so that sum_k (n_k - 8) x_k = sum_k n_k x_k - 8 sum_k x_k).
+struct Q4X {
+  std::vector<float> xe, xo, sx;  // [K/2], [K/2], [K/128][16]
+};
+inline void q4_prep_x(const uint16_t *x, int K, Q4X &q) {
+  q.xe.resize(K / 2);
+  q.xo.resize(K / 2);
+  q.sx.assign(static_cast<size_t>(K / 128) * 16, 0.0f);
+  for (int k = 0; k < K / 2; ++k) {
+    q.xe[k] = bf2f(x[2 * k]);
+    q.xo[k] = bf2f(x[2 * k + 1]);
+  }
+  for (int g = 0; g < K / 128; ++g)
+    for (int c = 0; c < 4; ++c)
+      for (int l = 0; l < 16; ++l) q.sx[g * 16 + l] += q.xe[g * 64 + c * 16 + l] + q.xo[g * 64 + c * 16 + l];
+}
+
+// out[r] = sum_k w[r][k] x[k] for n 4-bit rows (K/2 bytes, K/128 scales each)
+inline void dot_rows_q4(const uint8_t *nib, const uint16_t *sc, int n, int K, const Q4X &q, float *out) {
+  const __m512i m15 = _mm512_set1_epi32(15);
+  const __m512 eight = _mm512_set1_ps(8.0f);
+  for (int r = 0; r < n; ++r) {
+    const uint8_t *row = nib + static_cast<size_t>(r) * (K / 2);
+    const uint16_t *srow = sc + static_cast<size_t>(r) * (K / 128);
+    _mm_prefetch(reinterpret_cast<const char *>(row + 16 * (K / 2)), _MM_HINT_T1);
+    __m512 acc = _mm512_setzero_ps();
+    for (int g = 0; g < K / 128; ++g) {
+      __m512 d0 = _mm512_setzero_ps(), d1 = _mm512_setzero_ps();
+      for (int c = 0; c < 4; ++c) {  // 16 bytes = 32 weights
+        const __m512i b = _mm512_cvtepu8_epi32(_mm_loadu_si128(reinterpret_cast<const __m128i *>(row + g * 64 + c * 16)));
+        const __m512 lo = _mm512_cvtepi32_ps(_mm512_and_epi32(b, m15));
+        const __m512 hi = _mm512_cvtepi32_ps(_mm512_srli_epi32(b, 4));
+        d0 = _mm512_fmadd_ps(lo, _mm512_loadu_ps(&q.xe[g * 64 + c * 16]), d0);
+        d1 = _mm512_fmadd_ps(hi, _mm512_loadu_ps(&q.xo[g * 64 + c * 16]), d1);
+      }
+      const __m512 dg = _mm512_fnmadd_ps(eight, _mm512_loadu_ps(&q.sx[g * 16]), _mm512_add_ps(d0, d1));
+      acc = _mm512_fmadd_ps(_mm512_set1_ps(bf2f(srow[g])), dg, acc);
+    }
+    out[r] = _mm512_reduce_add_ps(acc);
+  }
+}
+
+// dequantize n 4-bit rows to bf16 rows (w = bf16((nibble - 8) * scale), as the GPU dequantizer)
+inline void dequant_rows_q4(const uint8_t *nib, const uint16_t *sc, int n, int K, uint16_t *dst) {
+  for (int r = 0; r < n; ++r)
+    for (int g = 0; g < K / 128; ++g) {
+      const float s = bf2f(sc[static_cast<size_t>(r) * (K / 128) + g]);
+      const uint8_t *b = nib + static_cast<size_t>(r) * (K / 2) + g * 64;
+      uint16_t *o = dst + static_cast<size_t>(r) * K + g * 128;
+      for (int i = 0; i < 64; ++i) {
+        o[2 * i] = f2bf(static_cast<float>((b[i] & 15) - 8) * s);
+        o[2 * i + 1] = f2bf(static_cast<float>((b[i] >> 4) - 8) * s);
+      }
+    }
+}
+
 }  // namespace
+
+void cpu_experts_decode_q4(ThreadPool &pool, const uint8_t *const *imgs, const uint16_t *const *xs, int n, int H,
+                           int I, float *const *outs, std::vector<uint16_t> &hbuf) {
+  HM_REQUIRE(H % 128 == 0 && I % 128 == 0, HM_EVALUE, "4-bit host worker needs H, I multiples of 128");
+  if (n <= 0) return;
+  hbuf.resize(static_cast<size_t>(n) * I);
+  uint16_t *h = hbuf.data();
+  std::vector<Q4X> qx(n);
+  for (int e = 0; e < n; ++e) q4_prep_x(xs[e], H, qx[e]);
+  pool.run([&](int tid, int nt) {
+    // phase 1: 16-pair units over the flat (expert, pair) space, gate and up rows
+    const long nu = static_cast<long>(n) * I / 16;
+    float g[16], u[16];
+    for (long q = nu * tid / nt; q < nu * (tid + 1) / nt; ++q) {
+      const int e = static_cast<int>(q / (I / 16)), i0 = static_cast<int>(q % (I / 16)) * 16;
+      const Q4View v = q4_view(imgs[e], H, I);
+      const size_t grow = static_cast<size_t>((i0 / kIlv) * 2 * kIlv + i0 % kIlv);
+      dot_rows_q4(v.n13 + grow * (H / 2), v.s13 + grow * (H / 128), 16, H, qx[e], g);
+      dot_rows_q4(v.n13 + (grow + kIlv) * (H / 2), v.s13 + (grow + kIlv) * (H / 128), 16, H, qx[e], u);
+      for (int i = 0; i < 16; ++i) h[static_cast<size_t>(e) * I + i0 + i] = f2bf(silu(g[i]) * u[i]);
+    }
+    pool.barrier();
+    Q4X hx;
+    int he = -1;
+    const long r1 = static_cast<long>(n) * H / 16;
+    for (long q = r1 * tid / nt; q < r1 * (tid + 1) / nt; ++q) {
+      const int e = static_cast<int>(q / (H / 16)), j0 = static_cast<int>(q % (H / 16)) * 16;
+      if (e != he) {
+        q4_prep_x(h + static_cast<size_t>(e) * I, I, hx);
+        he = e;
+      }
+      const Q4View v = q4_view(imgs[e], H, I);
+      dot_rows_q4(v.n2 + static_cast<size_t>(j0) * (I / 2), v.s2 + static_cast<size_t>(j0) * (I / 128), 16, I, hx,
+                  outs[e] + j0);
+    }
+  });
+}
+
+void cpu_expert_q4(ThreadPool &pool, const uint8_t *img, int H, int I, const uint16_t *x, int M, float *out,
+                   std::vector<uint16_t> &scratch) {
+  HM_REQUIRE(H % 128 == 0 && I % 128 == 0, HM_EVALUE, "4-bit host worker needs H, I multiples of 128");
+  if (M <= 0) return;
+  if (M == 1) {
+    const uint8_t *imgs[1] = {img};
+    const uint16_t *xs[1] = {x};
+    float *outs[1] = {out};
+    cpu_experts_decode_q4(pool, imgs, xs, 1, H, I, outs, scratch);
+    return;
+  }
+  HM_REQUIRE(amx_enable(), HM_ERUNTIME, "4-bit prefill on the host needs AMX");
+  // multi-token groups: each 32-row unit is dequantized to bf16 in a per-thread
+  // buffer (L2-resident) and multiplied on the AMX tiles like a bf16 expert
+  const int Mpad = (M + 31) / 32 * 32, nbt = Mpad / 16;
+  scratch.resize(static_cast<size_t>(H) * Mpad + static_cast<size_t>(I) * Mpad);
+  uint16_t *xv = scratch.data();
+  uint16_t *hv = xv + static_cast<size_t>(H) * Mpad;
+  vnni_pack(x, M, H, Mpad, xv);
+  const Q4View v = q4_view(img, H, I);
+  pool.run([&](int tid, int nt) {
+    amx_config();
+    std::vector<float> cbuf(static_cast<size_t>(2) * nbt * 256);
+    std::vector<uint16_t> wbuf(static_cast<size_t>(32) * std::max(H, I));
+    const int ob = I / 16;
+    for (int o = ob * tid / nt; o < ob * (tid + 1) / nt; ++o) {
+      const int i0 = o * 16;
+      const size_t grow = static_cast<size_t>((i0 / kIlv) * 2 * kIlv + i0 % kIlv);
+      dequant_rows_q4(v.n13 + grow * (H / 2), v.s13 + grow * (H / 128), 16, H, wbuf.data());
+      dequant_rows_q4(v.n13 + (grow + kIlv) * (H / 2), v.s13 + (grow + kIlv) * (H / 128), 16, H,
+                      wbuf.data() + static_cast<size_t>(16) * H);
+      auto rowp = [&](int, int which) { return wbuf.data() + static_cast<size_t>(which) * 16 * H; };
+      amx_gemm_units(rowp, 0, 1, static_cast<size_t>(H) * 2, xv, Mpad, H, cbuf.data());
+      for (int b = 0; b < nbt; ++b) {
+        const int tok0 = b * 16;
+        if (tok0 >= M) {
+          for (int r = 0; r < 16; r += 2)
+            _mm512_storeu_si512(hv + (static_cast<size_t>((i0 + r) >> 1) * Mpad + tok0) * 2, _mm512_setzero_si512());
+          continue;
+        }
+        const __mmask16 live = tok0 + 16 <= M ? 0xFFFF : static_cast<__mmask16>((1u << (M - tok0)) - 1u);
+        const float *cg = cbuf.data() + static_cast<size_t>(b) * 256;
+        const float *cu = cbuf.data() + (static_cast<size_t>(nbt) + b) * 256;
+        for (int r = 0; r < 16; r += 2) {
+          const __m512 h0 = _mm512_maskz_mov_ps(live, silu_mul16(cg + r * 16, cu + r * 16));
+          const __m512 h1 = _mm512_maskz_mov_ps(live, silu_mul16(cg + (r + 1) * 16, cu + (r + 1) * 16));
+          _mm512_storeu_si512(hv + (static_cast<size_t>((i0 + r) >> 1) * Mpad + tok0) * 2, interleave_bf16(h0, h1));
+        }
+      }
+    }
+    pool.barrier();
+    const int pairs = H / 32;
+    for (int q = pairs * tid / nt; q < pairs * (tid + 1) / nt; ++q) {
+      dequant_rows_q4(v.n2 + static_cast<size_t>(q * 32) * (I / 2), v.s2 + static_cast<size_t>(q * 32) * (I / 128),
+                      32, I, wbuf.data());
+      auto rowp = [&](int, int which) { return wbuf.data() + static_cast<size_t>(which) * 16 * I; };
+      amx_gemm_units(rowp, 0, 1, static_cast<size_t>(I) * 2, hv, Mpad, I, cbuf.data());
+      for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < nbt; ++b) {
+          const float *c = cbuf.data() + (static_cast<size_t>(a) * nbt + b) * 256;
+          for (int t = 0; t < 16; ++t) {
+            const int tok = b * 16 + t;
+            if (tok >= M) break;
+            float *o = out + static_cast<size_t>(tok) * H + q * 32 + a * 16;
+            for (int r = 0; r < 16; ++r) o[r] = c[r * 16 + t];
+          }
+        }
+    }
+  });
+}
 
 bool amx_available() { return amx_enable(); }
 
@@ -741,7 +922,24 @@ int hm_cpu_experts_decode(hm_cpu_pool *pool, const uint16_t *const *imgs, const 
   HM_API_END
 }
 
+int hm_cpu_expert_q4(hm_cpu_pool *pool, const uint8_t *img, int H, int I, const uint16_t *x, int M, float *out) {
+  HM_API_BEGIN
+  std::vector<uint16_t> hbuf;
+  hm::cpu_expert_q4(*reinterpret_cast<hm::ThreadPool *>(pool), img, H, I, x, M, out, hbuf);
+  HM_API_END
+}
+
+int hm_cpu_experts_decode_q4(hm_cpu_pool *pool, const uint8_t *const *imgs, const uint16_t *const *xs, int n, int H,
+                             int I, float *const *outs) {
+  HM_API_BEGIN
+  std::vector<uint16_t> hbuf;
+  hm::cpu_experts_decode_q4(*reinterpret_cast<hm::ThreadPool *>(pool), imgs, xs, n, H, I, outs, hbuf);
+  HM_API_END
+}
+
 int hm_cpu_has_avx512bf16(void) { return __builtin_cpu_supports("avx512bf16") ? 1 : 0; }
+
+int hm_cpu_has_amx_bf16(void) { return hm::amx_available() ? 1 : 0; }
 
 // Tuning knob for the decode stream: software-prefetch distance (bf16
 // elements) and hint (0 none, 1 T0, 2 T1, 3 NTA).  Process-wide.

@@ -50,6 +50,13 @@ void cpu_expert_amx(ThreadPool &pool, const uint16_t *img, int H, int I, const u
 void cpu_experts_decode(ThreadPool &pool, const uint16_t *const *imgs, const uint16_t *const *xs, int n, int H,
                         int I, float *const *outs, std::vector<uint16_t> &hbuf);
 
+// 4-bit expert images (include/hybrimoe.h, hm_q4_*): decode GEMV on the
+// nibbles; multi-token groups dequantize 32-row units and run on AMX.
+void cpu_experts_decode_q4(ThreadPool &pool, const uint8_t *const *imgs, const uint16_t *const *xs, int n, int H,
+                           int I, float *const *outs, std::vector<uint16_t> &hbuf);
+void cpu_expert_q4(ThreadPool &pool, const uint8_t *img, int H, int I, const uint16_t *x, int M, float *out,
+                   std::vector<uint16_t> &scratch);
+
 // out[M, H] fp32 = W2 (silu(Wg x) * (Wu x)) for one expert image (slot layout).
 void cpu_expert(ThreadPool &pool, const uint16_t *img, int H, int I, const uint16_t *x, int M, float *out,
                 std::vector<uint16_t> &hbuf);

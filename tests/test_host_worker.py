@@ -80,3 +80,37 @@ def test_oracle_q4_roundtrip():
     back = ref.q4_dequantize_rows(nib, s)
     step = np.repeat(ref.bf16_to_f32(s), 128, axis=1)
     assert np.all(np.abs(back - ref.bf16_to_f32(w)) <= 0.5 * step * (1 + 1e-6) + 1e-12)
+
+
+def _q4_expert(rng, H, I):
+    img, _ = _expert(rng, H, I)
+    q = ref.q4_image(img[: 2 * I * H].reshape(2 * I, H), img[2 * I * H:].reshape(H, I))
+    return q, ref.q4_expert(q, H, I)
+
+
+@pytest.mark.parametrize("H,I,M", [(256, 256, 1), (512, 384, 1), (256, 384, 3), (512, 256, 17), (256, 256, 40)])
+def test_cpu_expert_q4_matches_oracle(pool, H, I, M):
+    if M > 1 and not lib.hm_cpu_has_amx_bf16():
+        pytest.skip("4-bit prefill on the host needs AMX")
+    rng = np.random.default_rng(H * 7 + M)
+    q, ex = _q4_expert(rng, H, I)
+    x = ref.f32_to_bf16(rng.standard_normal((M, H)).astype(np.float32))
+    out = np.empty((M, H), np.float32)
+    _lib.check(lib.hm_cpu_expert_q4(pool, q.ctypes.data, H, I, x.ctypes.data, M, out.ctypes.data))
+    want = ref.expert(ref.bf16_to_f32(x), *ex)
+    assert np.abs(out - want).max() / np.abs(want).max() <= 1e-2
+
+
+def test_cpu_experts_decode_q4_batch(pool):
+    rng = np.random.default_rng(11)
+    H, I, n = 256, 384, 3
+    exps = [_q4_expert(rng, H, I) for _ in range(n)]
+    xs = [ref.f32_to_bf16(rng.standard_normal((1, H)).astype(np.float32)) for _ in range(n)]
+    outs = [np.empty((1, H), np.float32) for _ in range(n)]
+    P = C.c_void_p * n
+    _lib.check(lib.hm_cpu_experts_decode_q4(pool, P(*[e[0].ctypes.data for e in exps]),
+                                            P(*[x.ctypes.data for x in xs]), n, H, I,
+                                            P(*[o.ctypes.data for o in outs])))
+    for (q, ex), x, o in zip(exps, xs, outs):
+        want = ref.expert(ref.bf16_to_f32(x), *ex)
+        assert np.abs(o - want).max() / np.abs(want).max() <= 1e-2
