@@ -449,6 +449,8 @@ typedef struct hm_runtime_config {
   int32_t residual;        /* y = x + MoE(x) (1) or y = MoE(x) (0) */
   int32_t ep_rank;         /* expert parallelism: this rank computes experts e with  */
   int32_t ep_world;        /* e % ep_world == ep_rank (shared chunk c: c % ep_world) */
+  int32_t weight_bits;     /* 16 (or 0): bf16 expert images; 4: 4-bit images (hm_q4_*) */
+  int32_t _pad;
 } hm_runtime_config;
 
 typedef struct hm_layer_stats {

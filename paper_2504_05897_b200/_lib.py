@@ -273,7 +273,8 @@ class RuntimeConfig(C.Structure):
                 ("hidden", C.c_int32), ("inter", C.c_int32), ("n_shared", C.c_int32), ("renormalize", C.c_int32),
                 ("shared_gate_col", C.c_int32), ("capacity", C.c_int64), ("host_images", C.c_int64),
                 ("cpu_threads", C.c_int32), ("max_tokens", C.c_int32), ("gpu_mrs", C.c_int32),
-                ("residual", C.c_int32), ("ep_rank", C.c_int32), ("ep_world", C.c_int32)]
+                ("residual", C.c_int32), ("ep_rank", C.c_int32), ("ep_world", C.c_int32),
+                ("weight_bits", C.c_int32), ("_pad", C.c_int32)]
 
 
 class LayerStats(C.Structure):
@@ -330,6 +331,11 @@ for _name, (_args, _res) in {
     "hm_cpu_expert_q4": ([vp, vp, C.c_int, C.c_int, vp, C.c_int, vp], C.c_int),
     "hm_cpu_experts_decode_q4": ([vp, P(vp), P(vp), C.c_int, C.c_int, C.c_int, P(vp)], C.c_int),
     "hm_cpu_has_amx_bf16": ([], C.c_int),
+    "hm_q4_image_bytes": ([C.c_int, C.c_int, P(C.c_size_t)], C.c_int),
+    "hm_q4_quantize": ([vp, C.c_int, C.c_int, vp, vp], C.c_int),
+    "hm_q4_dequantize": ([vp, C.c_int, C.c_int, vp, vp], C.c_int),
+    "hm_expert_ffn_q4": ([vp, C.c_size_t, C.c_int, C.c_int, C.c_int, P(HmGroup), C.c_int, vp, C.c_int, vp, vp, vp,
+                          C.c_int, C.c_int, vp], C.c_int),
     "hm_bench_expert_ffn": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, C.c_int, C.c_int, vp,
                              P(C.c_float)], C.c_int),
     "hm_ep_create": ([C.c_int, C.c_int, C.c_int, C.c_int, P(vp)], C.c_int),

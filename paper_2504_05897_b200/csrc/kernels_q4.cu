@@ -102,13 +102,29 @@ __device__ __forceinline__ void nib8_to_h2(uint32_t v, __half2 (&o)[4]) {
 }
 
 // x (bf16, K values) -> fp16 in pair order: for each 8 elements
-// [x0 x4 x1 x5 x2 x6 x3 x7], matching nib8_to_h2.
-__device__ __forceinline__ void stage_x_h2(const uint16_t *__restrict__ x, int K, __half *xs) {
+// [x0 x4 x1 x5 x2 x6 x3 x7], matching nib8_to_h2.  fp16 has a narrow range,
+// so the row is scaled by a power of two that brings max|x| to [1, 2)
+// (exact); the returned factor undoes it on the dot products.  All threads
+// of the block must call it (block-wide max).
+__device__ float stage_x_h2(const uint16_t *__restrict__ x, int K, __half *xs) {
+  __shared__ float s_red[32];
+  float m = 0.f;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) m = fmaxf(m, fabsf(dev::bf2f(x[i])));
+  m = dev::warp_max(m);
+  __syncthreads();  // s_red reuse across calls
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  m = 0.f;
+  for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) m = fmaxf(m, s_red[w]);
+  int e = 0;
+  if (m > 0.f) frexpf(m, &e);  // m = f * 2^e, f in [0.5, 1)
+  const float up = ldexpf(1.0f, 1 - e), down = ldexpf(1.0f, e - 1);
   for (int i = threadIdx.x; i < K; i += blockDim.x) {
-    const int blk = i & ~7, e = i & 7;
-    const int p = blk + (e < 4 ? 2 * e : 2 * (e - 4) + 1);
-    xs[p] = __float2half_rn(dev::bf2f(x[i]));
+    const int blk = i & ~7, el = i & 7;
+    const int p = blk + (el < 4 ? 2 * el : 2 * (el - 4) + 1);
+    xs[p] = __float2half_rn(dev::bf2f(x[i]) * up);
   }
+  return down;
 }
 
 // dot of one q4 row segment (32 weights per lane per step) with staged x; returns the lane's partial (fp32)
@@ -152,7 +168,9 @@ __global__ void __launch_bounds__(256) ffn1_q4_kernel(const __grid_constant__ Q4
   extern __shared__ __align__(16) __half xs1[];  // [MR][H]
   const int g = blockIdx.x / p.bpg, cid = blockIdx.x % p.bpg;
   const int M = p.row_count[g], rb = p.row_begin[g], H = p.H, I = p.I;
-  for (int m = 0; m < M; ++m) stage_x_h2(p.xp + static_cast<size_t>(rb + m) * H, H, xs1 + m * H);
+  float down[MR];
+#pragma unroll
+  for (int m = 0; m < MR; ++m) down[m] = m < M ? stage_x_h2(p.xp + static_cast<size_t>(rb + m) * H, H, xs1 + m * H) : 1.f;
   __syncthreads();
   const Q4Layout L = q4_layout(H, I);
   const uint8_t *img = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_bytes;
@@ -166,8 +184,8 @@ __global__ void __launch_bounds__(256) ffn1_q4_kernel(const __grid_constant__ Q4
 #pragma unroll
     for (int m = 0; m < MR; ++m) {
       if (m < M) {
-        const float gs = dev::warp_sum(q4_row_dot(wg, sg, xs1 + m * H, H, lane));
-        const float us = dev::warp_sum(q4_row_dot(wu, su, xs1 + m * H, H, lane));
+        const float gs = down[m] * dev::warp_sum(q4_row_dot(wg, sg, xs1 + m * H, H, lane));
+        const float us = down[m] * dev::warp_sum(q4_row_dot(wu, su, xs1 + m * H, H, lane));
         if (lane == 0) p.h[static_cast<size_t>(rb + m) * I + i] = dev::f2bf(dev::silu(gs) * us);
       }
     }
@@ -179,7 +197,9 @@ __global__ void __launch_bounds__(256) ffn2_q4_kernel(const __grid_constant__ Q4
   extern __shared__ __align__(16) __half hs2[];  // [MR][I]
   const int g = blockIdx.x / p.bpg, cid = blockIdx.x % p.bpg;
   const int M = p.row_count[g], rb = p.row_begin[g], H = p.H, I = p.I;
-  for (int m = 0; m < M; ++m) stage_x_h2(p.h + static_cast<size_t>(rb + m) * I, I, hs2 + m * I);
+  float down[MR];
+#pragma unroll
+  for (int m = 0; m < MR; ++m) down[m] = m < M ? stage_x_h2(p.h + static_cast<size_t>(rb + m) * I, I, hs2 + m * I) : 1.f;
   __syncthreads();
   const Q4Layout L = q4_layout(H, I);
   const uint8_t *img = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_bytes;
@@ -193,7 +213,7 @@ __global__ void __launch_bounds__(256) ffn2_q4_kernel(const __grid_constant__ Q4
 #pragma unroll
     for (int m = 0; m < MR; ++m) {
       if (m < M) {
-        const float s = dev::warp_sum(q4_row_dot(wr, sr, hs2 + m * I, I, lane));
+        const float s = down[m] * dev::warp_sum(q4_row_dot(wr, sr, hs2 + m * I, I, lane));
         if (lane == 0) p.out[static_cast<size_t>(rb + m) * H + j] = s;
       }
     }

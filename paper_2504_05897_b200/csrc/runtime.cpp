@@ -45,6 +45,9 @@ int hm_router_fused_mirror(const float *, int, int, int, int, int, int, int, con
 int hm_ep_combine_allreduce(hm_ep *, const float *, const float *, const uint64_t *, const int32_t *, const float *,
                             int, int, int, const uint16_t *, uint16_t *, float *, void *);
 int hm_gate_wait(const uint32_t *, uint32_t, void *);
+int hm_q4_image_bytes(int, int, size_t *);
+int hm_expert_ffn_q4(const uint8_t *, size_t, int, int, int, const hm_group *, int, const uint16_t *, int, uint16_t *,
+                     float *, uint16_t *, int, int, void *);
 int hm_ep_dispatch_meta(hm_ep *, const int32_t *, const double *, int32_t *, double *, int32_t *, double *, uint32_t *,
                         uint32_t, void *);
 int hm_ep_dispatch_rows(hm_ep *, const uint16_t *, const int32_t *, const int32_t *, int, void *);
@@ -88,6 +91,9 @@ struct Runtime {
   int32_t *lcounts = nullptr, *loffsets = nullptr;
   double *lsums = nullptr;
   size_t slot_elems, slot_bytes;
+  bool q4 = false;                 // 4-bit expert images (weight_bits == 4)
+  uint16_t *q4_scratch = nullptr;  // bf16 images for the prefill GEMM on 4-bit experts
+  static constexpr int kQ4Scratch = 8;
   int64_t n_slots;
   uint16_t *pool = nullptr;        // device: [n_slots][slot_elems]
   uint16_t *store = nullptr;       // pinned host: [host_images][slot_elems]
@@ -163,8 +169,17 @@ struct Runtime {
         }
       }
     } release{this, time_kernels && timing_gate};
-    ok(hm_expert_ffn(pool, static_cast<int>(n_slots), H, I, g, n, xcur, rows, h, out, HM_FFN_AUTO,
-                     static_cast<void *>(st)));
+    if (q4) {
+      bool big = false;
+      for (int i = 0; i < n; ++i) big = big || g[i].row_count > 4;
+      if (big && !q4_scratch)
+        RT_CUDA(cudaMalloc(&q4_scratch, static_cast<size_t>(kQ4Scratch) * 3 * H * I * 2));
+      ok(hm_expert_ffn_q4(reinterpret_cast<const uint8_t *>(pool), slot_bytes, static_cast<int>(n_slots), H, I, g, n,
+                          xcur, rows, h, out, q4_scratch, kQ4Scratch, HM_FFN_AUTO, static_cast<void *>(st)));
+    } else {
+      ok(hm_expert_ffn(pool, static_cast<int>(n_slots), H, I, g, n, xcur, rows, h, out, HM_FFN_AUTO,
+                       static_cast<void *>(st)));
+    }
     if (time_kernels) {
       RT_CUDA(cudaEventRecord(b, st));
       int64_t by = 0;
@@ -191,8 +206,17 @@ struct Runtime {
     HM_REQUIRE(engine->cfg.num_layers == L && engine->cfg.num_routed == N && engine->cache.capacity == c.capacity,
                HM_EVALUE, "engine and runtime disagree on the model shape or cache capacity");
     HM_REQUIRE(c.host_images >= 1 && c.max_tokens >= 1, HM_EVALUE, "bad runtime sizes");
-    slot_elems = static_cast<size_t>(3) * H * I;
-    slot_bytes = slot_elems * 2;
+    HM_REQUIRE(c.weight_bits == 0 || c.weight_bits == 16 || c.weight_bits == 4, HM_EVALUE,
+               "weight_bits must be 16 (bf16) or 4");
+    q4 = c.weight_bits == 4;
+    if (q4) {
+      size_t b = 0;
+      ok(hm_q4_image_bytes(H, I, &b));
+      slot_bytes = (b + 255) / 256 * 256;  // keep every image 256-byte aligned
+    } else {
+      slot_bytes = static_cast<size_t>(3) * H * I * 2;
+    }
+    slot_elems = slot_bytes / 2;
     n_slots = c.capacity + static_cast<int64_t>(L) * S;
     if (n_slots > 0) RT_CUDA(cudaMalloc(&pool, static_cast<size_t>(n_slots) * slot_bytes));
     RT_CUDA(cudaHostAlloc(&store, static_cast<size_t>(c.host_images) * slot_bytes, cudaHostAllocPortable));
@@ -272,6 +296,7 @@ struct Runtime {
     if (ev_rows) cudaEventDestroy(ev_rows);
     if (copy) cudaStreamDestroy(copy);
     if (lcounts) cudaFree(lcounts);
+    if (q4_scratch) cudaFree(q4_scratch);
     if (lsums) cudaFree(lsums);
     for (void *p : {static_cast<void *>(pool), static_cast<void *>(sel), static_cast<void *>(w),
                     static_cast<void *>(probs), dmeta, static_cast<void *>(pos), static_cast<void *>(row_src),
@@ -521,13 +546,24 @@ struct Runtime {
           xs.push_back(h_x + rb * H);
           outs.push_back(h_out + rb * H);
         }
-        cpu_experts_decode(*workers, imgs.data(), xs.data(), static_cast<int>(imgs.size()), H, I, outs.data(),
-                           hbuf);
+        if (q4) {
+          std::vector<const uint8_t *> qimgs;
+          for (auto *p : imgs) qimgs.push_back(reinterpret_cast<const uint8_t *>(p));
+          cpu_experts_decode_q4(*workers, qimgs.data(), xs.data(), static_cast<int>(imgs.size()), H, I, outs.data(),
+                                hbuf);
+        } else {
+          cpu_experts_decode(*workers, imgs.data(), xs.data(), static_cast<int>(imgs.size()), H, I, outs.data(),
+                             hbuf);
+        }
       } else {
         for (uint32_t r : cpu_refs) {  // plan CPU order
           const int e = ref_expert(r);
           const size_t rb = h_offsets[e];
-          cpu_expert(*workers, image_ptr(r), H, I, h_x + rb * H, h_counts[e], h_out + rb * H, hbuf);
+          if (q4)
+            cpu_expert_q4(*workers, reinterpret_cast<const uint8_t *>(image_ptr(r)), H, I, h_x + rb * H, h_counts[e],
+                          h_out + rb * H, hbuf);
+          else
+            cpu_expert(*workers, image_ptr(r), H, I, h_x + rb * H, h_counts[e], h_out + rb * H, hbuf);
         }
       }
       s.n_cpu = static_cast<int32_t>(cpu_refs.size());

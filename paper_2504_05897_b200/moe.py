@@ -125,7 +125,7 @@ class HybridMoE:
     def __init__(self, config: ModelConfig, family: str, policy: EnginePolicy, capacity_ratio: float,
                  profile: HardwareProfile, *, host_images: int | None = None, max_tokens: int = 1024,
                  cpu_threads: int = 0, gpu_mrs: bool = True, residual: bool = True, ep_rank: int = 0,
-                 ep_world: int = 1, process_group=None, exchange: str = "p2p") -> None:
+                 ep_world: int = 1, process_group=None, exchange: str = "p2p", weight_bits: int = 16) -> None:
         if not torch.cuda.is_available():
             raise RuntimeError("HybridMoE executes on a CUDA device; no CPU fallback exists")
         self.config = config
@@ -160,7 +160,7 @@ class HybridMoE:
                                 shared_gate_col=self.gate_col, capacity=self.capacity,
                                 host_images=self.host_images, cpu_threads=int(cpu_threads),
                                 max_tokens=int(max_tokens), gpu_mrs=int(gpu_mrs), residual=int(residual),
-                                ep_rank=self.ep_rank, ep_world=self.ep_world)
+                                ep_rank=self.ep_rank, ep_world=self.ep_world, weight_bits=int(weight_bits))
         h = C.c_void_p()
         check(lib.hm_runtime_create(C.byref(rc), self.engine._h, C.byref(h)))
         self._rt = h.value
@@ -192,6 +192,12 @@ class HybridMoE:
         self.store = np.asarray(_Raw(store.value, self.host_images * self.slot_elems, False)).reshape(
             self.host_images, self.slot_elems)
         self.store_t = torch.from_numpy(self.store.view(np.int16)).view(torch.bfloat16)
+        self.weight_bits = int(weight_bits)
+        self.image_bytes = 3 * H * I * 2
+        if self.weight_bits == 4:  # 4-bit images: bytes of one image inside its (aligned) slot
+            nb = C.c_size_t()
+            check(lib.hm_q4_image_bytes(H, I, C.byref(nb)))
+            self.image_bytes = nb.value
         self.gate_w: torch.Tensor | None = None
         self.max_tokens = max_tokens
         self._bufs: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
@@ -206,20 +212,33 @@ class HybridMoE:
             self._ep = None
 
     # -------------------------------------------------------------- weights
+    def _encode(self, bf16_images: torch.Tensor) -> torch.Tensor:
+        """bf16 expert images [k, 3HI] (device) -> slot contents [k, slot_elems]
+        (bf16 view): the images themselves, or their 4-bit quantization."""
+        if self.weight_bits != 4:
+            return bf16_images
+        k = bf16_images.shape[0]
+        q = torch.zeros((k, self.slot_bytes), dtype=torch.uint8, device="cuda")
+        st = torch.cuda.current_stream().cuda_stream
+        for i in range(k):
+            check(lib.hm_q4_quantize(bf16_images[i].data_ptr(), self.H, self.I, q[i].data_ptr(), st))
+        return q.view(torch.bfloat16)
+
     def init_random_weights(self, seed: int = 0, chunk_images: int = 8) -> None:
         """Random-init N(0, 0.02^2) bf16 experts, generated on the
-        GPU and written to the pinned master store / shared slots; router gate
-        weights N(0, 1/H) for model mode."""
+        GPU (4-bit runs quantize them there) and written to the pinned master
+        store / shared slots; router gate weights N(0, 1/H) for model mode."""
         g = torch.Generator(device="cuda").manual_seed(seed)
-        n = self.slot_elems
+        n = 3 * self.H * self.I
         for i0 in range(0, self.host_images, chunk_images):
             k = min(chunk_images, self.host_images - i0)
             buf = (torch.randn((k, n), generator=g, device="cuda", dtype=torch.float32) * 0.02).to(torch.bfloat16)
-            self.store_t[i0:i0 + k].copy_(buf)
+            self.store_t[i0:i0 + k].copy_(self._encode(buf))
         for l in range(self.L):
             for c in range(self.S):
                 s = self.shared_slot(l, c)
-                self.pool[s].copy_((torch.randn(n, generator=g, device="cuda") * 0.02).to(torch.bfloat16))
+                self.pool[s].copy_(self._encode((torch.randn((1, n), generator=g, device="cuda") * 0.02).to(
+                    torch.bfloat16))[0])
         self.gate_w = (torch.randn((self.L, self.ld, self.H), generator=g, device="cuda") / math.sqrt(self.H)).to(
             torch.bfloat16)
         torch.cuda.synchronize()
@@ -228,18 +247,18 @@ class HybridMoE:
         """Per-expert seeded init (torch.Generator seed 1000*layer +
         expert): the same expert gets the same weights on any rank count, so an
         expert-parallel run can be compared with a single-GPU one."""
-        n = self.slot_elems
+        n = 3 * self.H * self.I
         for l in range(self.L):
             for e in range(self.N):
                 if e % self.ep_world != self.ep_rank:
                     continue
                 g = torch.Generator(device="cuda").manual_seed(base_seed + 1000 * l + e)
-                self.store_t[self.image_of(l, e)].copy_(
-                    (torch.randn(n, generator=g, device="cuda") * 0.02).to(torch.bfloat16))
+                self.store_t[self.image_of(l, e)].copy_(self._encode(
+                    (torch.randn((1, n), generator=g, device="cuda") * 0.02).to(torch.bfloat16))[0])
             for c in range(self.S):
                 g = torch.Generator(device="cuda").manual_seed(base_seed + 1000 * l + self.N + c)
-                self.pool[self.shared_slot(l, c)].copy_(
-                    (torch.randn(n, generator=g, device="cuda") * 0.02).to(torch.bfloat16))
+                self.pool[self.shared_slot(l, c)].copy_(self._encode(
+                    (torch.randn((1, n), generator=g, device="cuda") * 0.02).to(torch.bfloat16))[0])
         g = torch.Generator(device="cuda").manual_seed(base_seed + 999_999)
         self.gate_w = (torch.randn((self.L, self.ld, self.H), generator=g, device="cuda") / math.sqrt(self.H)).to(
             torch.bfloat16)
@@ -278,11 +297,14 @@ class HybridMoE:
         return v.value
 
     def expert_image(self, layer: int, expert: int) -> np.ndarray:
-        """Host bytes of routed expert (layer, expert) in slot layout (uint16 bf16 bits)."""
-        return self.store[self.image_of(layer, expert)]
+        """Host bytes of routed expert (layer, expert) in slot layout (uint16 bf16
+        bits; for 4-bit runs the uint8 bytes of the 4-bit image)."""
+        img = self.store[self.image_of(layer, expert)]
+        return img.view(np.uint8)[: self.image_bytes] if self.weight_bits == 4 else img
 
     def shared_image(self, layer: int, chunk: int) -> np.ndarray:
-        return self.pool[self.shared_slot(layer, chunk)].view(torch.int16).cpu().numpy().view(np.uint16)
+        img = self.pool[self.shared_slot(layer, chunk)].view(torch.int16).cpu().numpy().view(np.uint16)
+        return img.view(np.uint8)[: self.image_bytes] if self.weight_bits == 4 else img
 
     # -------------------------------------------------------------- forward
     def _ping_pong(self, T: int) -> tuple[torch.Tensor, torch.Tensor]:
