@@ -209,6 +209,9 @@ def run_ours(args) -> None:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     cfg = SHAPES[args.shape]
+    if args.bits == 4:  # the paper's 4-bit experts: expert_bytes at 0.5 bytes per weight (core.py:55)
+        from dataclasses import replace as _replace
+        cfg = _replace(cfg, bytes_per_weight=0.5)
     H, I = cfg.routed_expert_dims
     pk, pk_kind = peaks()
     t_setup = time.time()
@@ -222,11 +225,11 @@ def run_ours(args) -> None:
         base_profile = load_profile(args.profile_file)
         prefill_profile = load_profile(args.prefill_profile_file) if args.prefill_profile_file else base_profile
     else:
-        base_profile = calibrate_shape(H, I)[0].profile
+        base_profile = calibrate_shape(H, I, weight_bits=args.bits)[0].profile
         prefill_profile = base_profile
         if args.stage_profiles:
             prefill_profile = calibrate_shape(H, I, cpu_loads=(64, 128, 256), cpu_bursts=1,
-                                              gpu_loads=(64, 128, 256, 384, 512))[0].profile
+                                              gpu_loads=(64, 128, 256, 384, 512), weight_bits=args.bits)[0].profile
         if args.save_profile and rank == 0:
             save_profile(base_profile, args.save_profile)
             save_profile(prefill_profile, args.save_profile + ".prefill")
@@ -239,7 +242,8 @@ def run_ours(args) -> None:
     policy = EnginePolicy(scheduling=args.scheduling, cache_policy=args.policy, prefetch=args.prefetch)
     # expert parallelism over the ranks of this box: one replicated sequence, each
     # rank homes experts e % world, host bytes and worker cores split by rank
-    total_bytes = cfg.num_layers * cfg.num_routed * 3 * H * I * 2 // world
+    image_bytes = 3 * H * I * 2 if args.bits == 16 else 3 * H * I // 2 + 3 * H * I // 64
+    total_bytes = cfg.num_layers * cfg.num_routed * image_bytes // world
     host_images = args.host_images
     if host_images is None:
         try:
@@ -247,21 +251,21 @@ def run_ours(args) -> None:
             avail = psutil.virtual_memory().available // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world)))
         except Exception:
             avail = 0
-        host_images = None if avail > 1.3 * total_bytes else max(16, int(0.5 * avail / (3 * H * I * 2)))
+        host_images = None if avail > 1.3 * total_bytes else max(16, int(0.5 * avail / image_bytes))
     threads = args.cpu_threads or max(1, (os.cpu_count() or 1) // world)
     from paper_2504_05897_b200.ep import PeerMemoryUnavailable
     exchange_note = None
     try:
         moe = HybridMoE(cfg, args.shape, policy, args.ratio, prof, host_images=host_images,
                         max_tokens=max(args.prefill, 1), cpu_threads=threads, ep_rank=rank, ep_world=world,
-                        exchange=args.exchange)
+                        exchange=args.exchange, weight_bits=args.bits)
     except PeerMemoryUnavailable as e:  # every rank sees the same verdict: use the NCCL all-reduce exchange
         if args.exchange == "dispatch":
             raise
         exchange_note = f"p2p unavailable ({e}); NCCL all-reduce used"
         moe = HybridMoE(cfg, args.shape, policy, args.ratio, prof, host_images=host_images,
                         max_tokens=max(args.prefill, 1), cpu_threads=threads, ep_rank=rank, ep_world=world,
-                        exchange="allreduce")
+                        exchange="allreduce", weight_bits=args.bits)
     moe.init_random_weights(seed=args.seed + rank)
     n_dec = args.warmup + args.steps
     trace, logits = generate_router_logits(cfg, GenParams(seed=args.seed), args.prefill, 2 * n_dec + 1)
@@ -421,14 +425,15 @@ def run_ours(args) -> None:
     # algorithmic bytes -- traffic ~ algorithmic means weights are read once
     traffic = {}
     tp = ROOT / "profiles" / "r01b_traffic.json"
-    if tp.exists() and args.shape == "mixtral":
+    if tp.exists() and args.shape == "mixtral" and args.bits == 16:
         traffic = json.loads(tp.read_text())
     tg = traffic.get("decode_gemv", {})
     roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved_gbs / hbm_peak, "traffic": tg.get("dram_bytes"),
                 "traffic_launch": tg.get("launch"), "traffic_algorithmic_bytes": tg.get("algorithmic_bytes"),
                 "traffic_source": traffic.get("source"),
-                "kernel": "decode expert FFN (ffn1_gemv + ffn2_gemv, weights streamed once)",
+                "kernel": "decode expert FFN (ffn1_gemv + ffn2_gemv, weights streamed once)" if args.bits == 16 else
+                          "decode expert FFN on 4-bit images (ffn1_q4 + ffn2_q4)",
                 "launches": kn.value, "avg_launch_us": 1e3 * kms.value / max(1, kn.value),
                 "bytes_per_launch": kbytes.value / max(1, kn.value), "peak_kind": pk_kind}
     # plan-conditional roofline of the whole step: max(B_gpu/BW_hbm, B_cpu/BW_host, B_h2d/BW_pcie) per layer
@@ -461,7 +466,7 @@ def run_ours(args) -> None:
         line = {
             "metric": "decode tok/s at 25% expert-cache budget", "value": tok_s, "unit": "tok/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16" if args.bits == 16 else "int4 weights, bf16 activations",
             "data": "synthetic (reference trace-generator routing GenParams(1.0,0.85,0.6), random-init N(0,0.02^2) bf16 weights)",
             "config": {"workload": f"{args.shape}-shaped MoE decode, batch 1, {args.ratio:.0%} expert-cache budget",
                        "shape": args.shape, "layers": cfg.num_layers, "experts": cfg.num_routed,
@@ -469,8 +474,8 @@ def run_ours(args) -> None:
                        "host_images": moe.host_images, "policy": args.policy, "prefetch": args.prefetch,
                        "scheduling": args.scheduling,
                        "l2": f"each step streams {cfg.num_layers * cfg.num_activated} expert evaluations x "
-                             f"{3 * H * I * 2 / 1e6:.1f} MB of weights (>> 126 MB L2); no flush needed",
-                       "parallelism": f"ep{world}" if world > 1 else "single",
+                             f"{image_bytes / 1e6:.1f} MB of weights (>> 126 MB L2); no flush needed",
+                       "parallelism": f"ep{world}" if world > 1 else "single", "weight_bits": args.bits,
                        "ep_exchange": moe.exchange if exchange_note is None else exchange_note},
             "prefill": {"tokens": args.prefill, "ms": prefill_ms, "cold_cache": True,
                         "gpu_experts": sum(s.n_gpu for s in pst), "cpu_experts": sum(s.n_cpu for s in pst),
@@ -509,6 +514,8 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--shape", default="mixtral", choices=["tiny", "mixtral", "deepseek", "qwen2"])
     ap.add_argument("--ratio", type=float, default=0.25)
+    ap.add_argument("--bits", type=int, default=16, choices=[16, 4],
+                    help="expert weights: bf16 (BASELINE config) or the paper's 4-bit (int4 g128)")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "dispatch", "allreduce"],
                     help="expert parallelism: replicated tokens + fused peer-memory reduce (p2p), token-sharded "
                          "all-to-all dispatch/return over peer memory (dispatch), or replicated + process-group "

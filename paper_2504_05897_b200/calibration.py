@@ -28,15 +28,41 @@ def _events():
 
 def measure_samples(H: int, I: int, gpu_loads=(1, 2, 4, 8, 32, 128, 256, 384, 512), cpu_loads=(1, 2, 3, 4),
                     reps: int = 3, cpu_bursts: int = 2, n_images: int = 4, cpu_threads: int = 0,
-                    seed: int = 0) -> list[CalibrationSample]:
-    from .kernels import expert_ffn
+                    seed: int = 0, weight_bits: int = 16) -> list[CalibrationSample]:
+    """weight_bits 4: the same measurements on 4-bit expert images (hm_q4_*)."""
+    from .kernels import expert_ffn, groups_array
 
-    slot_elems = 3 * H * I
+    q4 = weight_bits == 4
+    elems = 3 * H * I
+    slot_elems = elems
+    if q4:
+        nb = C.c_size_t()
+        check(lib.hm_q4_image_bytes(H, I, C.byref(nb)))
+        slot_elems = (nb.value + 255) // 256 * 256 // 2
     g = torch.Generator(device="cuda").manual_seed(seed)
-    pool = (torch.randn((1, slot_elems), generator=g, device="cuda") * 0.02).to(torch.bfloat16)
+    st0 = torch.cuda.current_stream().cuda_stream
+
+    def image() -> torch.Tensor:  # one expert image in slot layout (bf16 view)
+        w = (torch.randn(elems, generator=g, device="cuda") * 0.02).to(torch.bfloat16)
+        if not q4:
+            return w
+        q = torch.zeros(slot_elems * 2, dtype=torch.uint8, device="cuda")
+        check(lib.hm_q4_quantize(w.data_ptr(), H, I, q.data_ptr(), st0))
+        return q.view(torch.bfloat16)
+
+    pool = image().view(1, slot_elems)
     host = torch.empty((n_images, slot_elems), dtype=torch.bfloat16).pin_memory()
     for i in range(n_images):
-        host[i].copy_((torch.randn(slot_elems, generator=g, device="cuda") * 0.02).to(torch.bfloat16))
+        host[i].copy_(image())
+    scratch = torch.empty((1, elems), dtype=torch.bfloat16, device="cuda") if q4 else None
+
+    def ffn(m: int) -> None:
+        if q4:
+            check(lib.hm_expert_ffn_q4(pool.data_ptr(), slot_elems * 2, 1, H, I, groups_array([(0, 0, m)]), 1,
+                                       x.data_ptr(), maxm, h.data_ptr(), out.data_ptr(), scratch.data_ptr(), 1, 0,
+                                       st0))
+        else:
+            expert_ffn(flat, 1, H, I, [(0, 0, m)], x, h, out)
     samples: list[CalibrationSample] = []
     st = torch.cuda.current_stream()
     maxm = max(gpu_loads)
@@ -45,11 +71,11 @@ def measure_samples(H: int, I: int, gpu_loads=(1, 2, 4, 8, 32, 128, 256, 384, 51
     out = torch.empty((maxm, H), device="cuda")
     flat = pool.view(-1)
     for m in gpu_loads:
-        expert_ffn(flat, 1, H, I, [(0, 0, m)], x, h, out)
+        ffn(m)
         a, b = _events()
         a.record(st)
         for _ in range(reps):
-            expert_ffn(flat, 1, H, I, [(0, 0, m)], x, h, out)
+            ffn(m)
         b.record(st)
         b.synchronize()
         samples.append(CalibrationSample("gpu", float(m), 0, a.elapsed_time(b) / 1e3 / reps))
@@ -65,7 +91,8 @@ def measure_samples(H: int, I: int, gpu_loads=(1, 2, 4, 8, 32, 128, 256, 384, 51
                 for pos in range(3):
                     img = host[(burst * 3 + pos) % n_images]
                     t0 = time.perf_counter()
-                    check(lib.hm_cpu_expert(cpool, img.data_ptr(), H, I, xs.ctypes.data, m, outs.ctypes.data))
+                    fn = lib.hm_cpu_expert_q4 if q4 else lib.hm_cpu_expert
+                    check(fn(cpool, img.data_ptr(), H, I, xs.ctypes.data, m, outs.ctypes.data))
                     samples.append(CalibrationSample("cpu", float(m), pos, time.perf_counter() - t0))
     finally:
         lib.hm_cpu_pool_destroy(cpool)
@@ -88,6 +115,7 @@ def measure_samples(H: int, I: int, gpu_loads=(1, 2, 4, 8, 32, 128, 256, 384, 51
 
 
 def calibrate_shape(H: int, I: int, gpu_saturation_load: int = 256, **kw):
-    """Measure and fit; returns (CalibrationResult, samples)."""
+    """Measure and fit; returns (CalibrationResult, samples).  kw: measure_samples'
+    options (e.g. weight_bits=4)."""
     samples = measure_samples(H, I, **kw)
     return calibrate(samples, gpu_saturation_load=gpu_saturation_load), samples
