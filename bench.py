@@ -225,7 +225,9 @@ def run_ours(args) -> None:
         base_profile = load_profile(args.profile_file)
         prefill_profile = load_profile(args.prefill_profile_file) if args.prefill_profile_file else base_profile
     else:
-        base_profile = calibrate_shape(H, I, weight_bits=args.bits)[0].profile
+        # decode profile at decode loads on every device (the GPU's flat cost
+        # is the GEMV's, not an average with prefill-sized GEMMs)
+        base_profile = calibrate_shape(H, I, weight_bits=args.bits, gpu_loads=(1, 2, 3, 4))[0].profile
         prefill_profile = base_profile
         if args.stage_profiles:
             prefill_profile = calibrate_shape(H, I, cpu_loads=(64, 128, 256), cpu_bursts=1,

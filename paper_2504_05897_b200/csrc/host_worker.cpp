@@ -627,16 +627,66 @@ inline void dot_rows_q4(const uint8_t *nib, const uint16_t *sc, int n, int K, co
   }
 }
 
+// Up to 4 tokens at once: the nibbles of each 128-group are decoded once and
+// reused for every token.  out[t * ldo + r].
+template <int MT>
+inline void dot_rows_q4_mt(const uint8_t *nib, const uint16_t *sc, int n, int K, const Q4X *const *q, float *out,
+                           size_t ldo) {
+  const __m512i m15 = _mm512_set1_epi32(15);
+  const __m512 eight = _mm512_set1_ps(8.0f);
+  for (int r = 0; r < n; ++r) {
+    const uint8_t *row = nib + static_cast<size_t>(r) * (K / 2);
+    const uint16_t *srow = sc + static_cast<size_t>(r) * (K / 128);
+    _mm_prefetch(reinterpret_cast<const char *>(row + 16 * (K / 2)), _MM_HINT_T1);
+    __m512 acc[MT];
+    for (int t = 0; t < MT; ++t) acc[t] = _mm512_setzero_ps();
+    for (int g = 0; g < K / 128; ++g) {
+      __m512 lo[4], hi[4];
+      for (int c = 0; c < 4; ++c) {
+        const __m512i b = _mm512_cvtepu8_epi32(_mm_loadu_si128(reinterpret_cast<const __m128i *>(row + g * 64 + c * 16)));
+        lo[c] = _mm512_cvtepi32_ps(_mm512_and_epi32(b, m15));
+        hi[c] = _mm512_cvtepi32_ps(_mm512_srli_epi32(b, 4));
+      }
+      const __m512 sv = _mm512_set1_ps(bf2f(srow[g]));
+      for (int t = 0; t < MT; ++t) {
+        __m512 d0 = _mm512_setzero_ps(), d1 = _mm512_setzero_ps();
+        for (int c = 0; c < 4; ++c) {
+          d0 = _mm512_fmadd_ps(lo[c], _mm512_loadu_ps(&q[t]->xe[g * 64 + c * 16]), d0);
+          d1 = _mm512_fmadd_ps(hi[c], _mm512_loadu_ps(&q[t]->xo[g * 64 + c * 16]), d1);
+        }
+        const __m512 dg = _mm512_fnmadd_ps(eight, _mm512_loadu_ps(&q[t]->sx[g * 16]), _mm512_add_ps(d0, d1));
+        acc[t] = _mm512_fmadd_ps(sv, dg, acc[t]);
+      }
+    }
+    for (int t = 0; t < MT; ++t) out[static_cast<size_t>(t) * ldo + r] = _mm512_reduce_add_ps(acc[t]);
+  }
+}
+
+inline void dot_rows_q4_tokens(const uint8_t *nib, const uint16_t *sc, int n, int K, const Q4X *const *q, int mt,
+                               float *out, size_t ldo) {
+  switch (mt) {
+    case 1: dot_rows_q4_mt<1>(nib, sc, n, K, q, out, ldo); break;
+    case 2: dot_rows_q4_mt<2>(nib, sc, n, K, q, out, ldo); break;
+    case 3: dot_rows_q4_mt<3>(nib, sc, n, K, q, out, ldo); break;
+    default: dot_rows_q4_mt<4>(nib, sc, n, K, q, out, ldo); break;
+  }
+}
+
 // dequantize n 4-bit rows to bf16 rows (w = bf16((nibble - 8) * scale), as the GPU dequantizer)
 inline void dequant_rows_q4(const uint8_t *nib, const uint16_t *sc, int n, int K, uint16_t *dst) {
+  const __m512i m15 = _mm512_set1_epi32(15);
+  const __m512 eight = _mm512_set1_ps(8.0f);
   for (int r = 0; r < n; ++r)
     for (int g = 0; g < K / 128; ++g) {
-      const float s = bf2f(sc[static_cast<size_t>(r) * (K / 128) + g]);
+      const __m512 s = _mm512_set1_ps(bf2f(sc[static_cast<size_t>(r) * (K / 128) + g]));
       const uint8_t *b = nib + static_cast<size_t>(r) * (K / 2) + g * 64;
       uint16_t *o = dst + static_cast<size_t>(r) * K + g * 128;
-      for (int i = 0; i < 64; ++i) {
-        o[2 * i] = f2bf(static_cast<float>((b[i] & 15) - 8) * s);
-        o[2 * i + 1] = f2bf(static_cast<float>((b[i] >> 4) - 8) * s);
+      for (int c = 0; c < 4; ++c) {  // 16 bytes -> 32 bf16 (element 2k low nibble, 2k+1 high nibble)
+        const __m512i v = _mm512_cvtepu8_epi32(_mm_loadu_si128(reinterpret_cast<const __m128i *>(b + c * 16)));
+        const __m512 lo = _mm512_mul_ps(_mm512_sub_ps(_mm512_cvtepi32_ps(_mm512_and_epi32(v, m15)), eight), s);
+        const __m512 hi = _mm512_mul_ps(_mm512_sub_ps(_mm512_cvtepi32_ps(_mm512_srli_epi32(v, 4)), eight), s);
+        // bf16 pairs (lo_k, hi_k) in each 32-bit lane == memory order; RNE like f2bf
+        _mm512_storeu_si512(o + c * 32, interleave_bf16(lo, hi));
       }
     }
 }
@@ -689,6 +739,41 @@ void cpu_expert_q4(ThreadPool &pool, const uint8_t *img, int H, int I, const uin
     const uint16_t *xs[1] = {x};
     float *outs[1] = {out};
     cpu_experts_decode_q4(pool, imgs, xs, 1, H, I, outs, scratch);
+    return;
+  }
+  if (M <= 4) {  // few tokens: stream the nibbles once, decode each group once for all tokens
+    std::vector<Q4X> qx(M);
+    const Q4X *qp[4];
+    for (int t = 0; t < M; ++t) {
+      q4_prep_x(x + static_cast<size_t>(t) * H, H, qx[t]);
+      qp[t] = &qx[t];
+    }
+    scratch.resize(static_cast<size_t>(M) * I);
+    uint16_t *hh = scratch.data();
+    const Q4View v = q4_view(img, H, I);
+    pool.run([&](int tid, int nt) {
+      const int nu = I / 16;
+      float g[4 * 16], u[4 * 16];
+      for (int q = nu * tid / nt; q < nu * (tid + 1) / nt; ++q) {
+        const int i0 = q * 16;
+        const size_t grow = static_cast<size_t>((i0 / kIlv) * 2 * kIlv + i0 % kIlv);
+        dot_rows_q4_tokens(v.n13 + grow * (H / 2), v.s13 + grow * (H / 128), 16, H, qp, M, g, 16);
+        dot_rows_q4_tokens(v.n13 + (grow + kIlv) * (H / 2), v.s13 + (grow + kIlv) * (H / 128), 16, H, qp, M, u, 16);
+        for (int t = 0; t < M; ++t)
+          for (int i = 0; i < 16; ++i) hh[static_cast<size_t>(t) * I + i0 + i] = f2bf(silu(g[t * 16 + i]) * u[t * 16 + i]);
+      }
+      pool.barrier();
+      std::vector<Q4X> hx(M);
+      const Q4X *hp[4];
+      for (int t = 0; t < M; ++t) {
+        q4_prep_x(hh + static_cast<size_t>(t) * I, I, hx[t]);
+        hp[t] = &hx[t];
+      }
+      const int nr = H / 16;
+      for (int q = nr * tid / nt; q < nr * (tid + 1) / nt; ++q)
+        dot_rows_q4_tokens(v.n2 + static_cast<size_t>(q * 16) * (I / 2), v.s2 + static_cast<size_t>(q * 16) * (I / 128),
+                           16, I, hp, M, out + q * 16, static_cast<size_t>(H));
+    });
     return;
   }
   HM_REQUIRE(amx_enable(), HM_ERUNTIME, "4-bit prefill on the host needs AMX");

@@ -18,6 +18,7 @@
 // in the matching pair order, fp16 partials over 32 weights, fp32 across.
 #include <cuda_fp16.h>
 
+#include <cstdlib>
 #include <vector>
 
 #include "device.cuh"
@@ -106,6 +107,9 @@ __device__ __forceinline__ void nib8_to_h2(uint32_t v, __half2 (&o)[4]) {
 // so the row is scaled by a power of two that brings max|x| to [1, 2)
 // (exact); the returned factor undoes it on the dot products.  All threads
 // of the block must call it (block-wide max).
+// staged rows are padded to whole 1024-element chunks (the lane-major layout)
+__host__ __device__ inline int q4_pad(int K) { return (K + 1023) / 1024 * 1024; }
+
 __device__ float stage_x_h2(const uint16_t *__restrict__ x, int K, __half *xs) {
   __shared__ float s_red[32];
   float m = 0.f;
@@ -120,37 +124,68 @@ __device__ float stage_x_h2(const uint16_t *__restrict__ x, int K, __half *xs) {
   if (m > 0.f) frexpf(m, &e);  // m = f * 2^e, f in [0.5, 1)
   const float up = ldexpf(1.0f, 1 - e), down = ldexpf(1.0f, e - 1);
   for (int i = threadIdx.x; i < K; i += blockDim.x) {
-    const int blk = i & ~7, el = i & 7;
-    const int p = blk + (el < 4 ? 2 * el : 2 * (el - 4) + 1);
+    // conflict-free layout for the GEMV: lane L reads its q-th 8 values of
+    // chunk j at ((j*4 + q)*32 + L)*8 (consecutive lanes, consecutive 16 B)
+    const int j = i >> 10, L = (i >> 5) & 31, q = (i >> 3) & 3, el = i & 7;
+    const int p = ((j * 4 + q) * 32 + L) * 8 + (el < 4 ? 2 * el : 2 * (el - 4) + 1);
     xs[p] = __float2half_rn(dev::bf2f(x[i]) * up);
   }
   return down;
 }
 
-// dot of one q4 row segment (32 weights per lane per step) with staged x; returns the lane's partial (fp32)
-__device__ __forceinline__ float q4_row_dot(const uint8_t *__restrict__ row, const uint16_t *__restrict__ sc,
-                                            const __half *xs, int K, int lane) {
-  float acc = 0.f;
-  for (int c = lane * 32; c < K; c += 32 * 32) {
-    const uint4 w = dev::ld_stream(row + c / 2);
-    const float s = dev::bf2f(sc[c / kQG]);
-    const uint4 *xv = reinterpret_cast<const uint4 *>(xs + c);  // 32 halfs = 4 x uint4
-    __half2 a0 = __float2half2_rn(0.f), a1 = a0;
-    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+// 32 weights (one 16-byte load) of a row against 32 staged x values -> fp32
+// partial; xq[q] = the lane's q-th 8 staged values (pair order)
+__device__ __forceinline__ float q4_dot32(const uint4 w, const uint4 (&xq)[4]) {
+  __half2 a[4] = {__float2half2_rn(0.f), __float2half2_rn(0.f), __float2half2_rn(0.f), __float2half2_rn(0.f)};
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      __half2 n[4];
-      nib8_to_h2(ws[q], n);
-      const uint4 xq = xv[q];
-      a0 = __hfma2(n[0], *reinterpret_cast<const __half2 *>(&xq.x), a0);
-      a1 = __hfma2(n[1], *reinterpret_cast<const __half2 *>(&xq.y), a1);
-      a0 = __hfma2(n[2], *reinterpret_cast<const __half2 *>(&xq.z), a0);
-      a1 = __hfma2(n[3], *reinterpret_cast<const __half2 *>(&xq.w), a1);
-    }
-    const float2 f0 = __half22float2(a0), f1 = __half22float2(a1);
-    acc = fmaf(s, (f0.x + f0.y) + (f1.x + f1.y), acc);
+  for (int q = 0; q < 4; ++q) {
+    __half2 n[4];
+    nib8_to_h2(ws[q], n);
+    a[0] = __hfma2(n[0], *reinterpret_cast<const __half2 *>(&xq[q].x), a[0]);
+    a[1] = __hfma2(n[1], *reinterpret_cast<const __half2 *>(&xq[q].y), a[1]);
+    a[2] = __hfma2(n[2], *reinterpret_cast<const __half2 *>(&xq[q].z), a[2]);
+    a[3] = __hfma2(n[3], *reinterpret_cast<const __half2 *>(&xq[q].w), a[3]);
   }
-  return acc;
+  const __half2 t = __hadd2(__hadd2(a[0], a[1]), __hadd2(a[2], a[3]));
+  const float2 f = __half22float2(t);
+  return f.x + f.y;
+}
+
+// NR rows (sharing x) dotted with the staged x; each lane handles 32-weight
+// chunks lane*32 + 1024*j, U chunks per row loaded before any is consumed (the
+// memory-level parallelism of the bf16 GEMV).  Returns the lane's partials.
+template <int NR, int U>
+__device__ __forceinline__ void q4_rows_dot(const uint8_t *const (&rows)[NR], const uint16_t *const (&sc)[NR],
+                                            const __half *xs, int K, int lane, float (&acc)[NR]) {
+#pragma unroll
+  for (int r = 0; r < NR; ++r) acc[r] = 0.f;
+  for (int c0 = lane * 32; c0 < K; c0 += 1024 * U) {
+    uint4 w[NR][U];
+    float s[NR][U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u * 1024;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        if (c < K) {
+          w[r][u] = dev::ld_stream(rows[r] + c / 2);
+          s[r][u] = dev::bf2f(sc[r][c / kQG]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u * 1024;
+      if (c < K) {
+        const int j = c >> 10;
+        const uint4 *xb = reinterpret_cast<const uint4 *>(xs) + (j * 4) * 32 + lane;
+        const uint4 xq[4] = {xb[0], xb[32], xb[64], xb[96]};
+#pragma unroll
+        for (int r = 0; r < NR; ++r) acc[r] = fmaf(s[r][u], q4_dot32(w[r][u], xq), acc[r]);
+      }
+    }
+  }
 }
 
 struct Q4GemvParams {
@@ -170,7 +205,8 @@ __global__ void __launch_bounds__(256) ffn1_q4_kernel(const __grid_constant__ Q4
   const int M = p.row_count[g], rb = p.row_begin[g], H = p.H, I = p.I;
   float down[MR];
 #pragma unroll
-  for (int m = 0; m < MR; ++m) down[m] = m < M ? stage_x_h2(p.xp + static_cast<size_t>(rb + m) * H, H, xs1 + m * H) : 1.f;
+  const int Hp = q4_pad(H);
+  for (int m = 0; m < MR; ++m) down[m] = m < M ? stage_x_h2(p.xp + static_cast<size_t>(rb + m) * H, H, xs1 + m * Hp) : 1.f;
   __syncthreads();
   const Q4Layout L = q4_layout(H, I);
   const uint8_t *img = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_bytes;
@@ -181,11 +217,15 @@ __global__ void __launch_bounds__(256) ffn1_q4_kernel(const __grid_constant__ Q4
     const size_t grow = static_cast<size_t>((i / kIlvQ) * 2 * kIlvQ + (i % kIlvQ));
     const uint8_t *wg = img + grow * (H / 2), *wu = wg + static_cast<size_t>(kIlvQ) * (H / 2);
     const uint16_t *sg = s13 + grow * (H / kQG), *su = sg + static_cast<size_t>(kIlvQ) * (H / kQG);
+    const uint8_t *rows[2] = {wg, wu};
+    const uint16_t *scs[2] = {sg, su};
 #pragma unroll
     for (int m = 0; m < MR; ++m) {
       if (m < M) {
-        const float gs = down[m] * dev::warp_sum(q4_row_dot(wg, sg, xs1 + m * H, H, lane));
-        const float us = down[m] * dev::warp_sum(q4_row_dot(wu, su, xs1 + m * H, H, lane));
+        float a[2];
+        q4_rows_dot<2, 4>(rows, scs, xs1 + m * Hp, H, lane, a);
+        const float gs = down[m] * dev::warp_sum(a[0]);
+        const float us = down[m] * dev::warp_sum(a[1]);
         if (lane == 0) p.h[static_cast<size_t>(rb + m) * I + i] = dev::f2bf(dev::silu(gs) * us);
       }
     }
@@ -199,7 +239,8 @@ __global__ void __launch_bounds__(256) ffn2_q4_kernel(const __grid_constant__ Q4
   const int M = p.row_count[g], rb = p.row_begin[g], H = p.H, I = p.I;
   float down[MR];
 #pragma unroll
-  for (int m = 0; m < MR; ++m) down[m] = m < M ? stage_x_h2(p.h + static_cast<size_t>(rb + m) * I, I, hs2 + m * I) : 1.f;
+  const int Ip = q4_pad(I);
+  for (int m = 0; m < MR; ++m) down[m] = m < M ? stage_x_h2(p.h + static_cast<size_t>(rb + m) * I, I, hs2 + m * Ip) : 1.f;
   __syncthreads();
   const Q4Layout L = q4_layout(H, I);
   const uint8_t *img = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_bytes;
@@ -210,10 +251,14 @@ __global__ void __launch_bounds__(256) ffn2_q4_kernel(const __grid_constant__ Q4
   for (int j = cid * p.chunk + wid; j < j_end; j += nw) {
     const uint8_t *wr = w2 + static_cast<size_t>(j) * (I / 2);
     const uint16_t *sr = s2 + static_cast<size_t>(j) * (I / kQG);
+    const uint8_t *rows[1] = {wr};
+    const uint16_t *scs[1] = {sr};
 #pragma unroll
     for (int m = 0; m < MR; ++m) {
       if (m < M) {
-        const float s = down[m] * dev::warp_sum(q4_row_dot(wr, sr, hs2 + m * I, I, lane));
+        float a[1];
+        q4_rows_dot<1, 4>(rows, scs, hs2 + m * Ip, I, lane, a);
+        const float s = down[m] * dev::warp_sum(a[0]);
         if (lane == 0) p.out[static_cast<size_t>(rb + m) * H + j] = s;
       }
     }
@@ -256,18 +301,22 @@ void launch_q4_gemv(const uint8_t *pool, size_t slot_bytes, int H, int I, const 
     mr = std::max(mr, gs[g].row_count);
   }
   const int target = sm_count() * 4, G = p.n_groups;
-  p.chunk = std::max(8, static_cast<int>((static_cast<long>(G) * I + target - 1) / target + 7) / 8 * 8);
+  static const int c1 = [] { const char *e = std::getenv("HM_Q4_CHUNK1"); return e ? std::atoi(e) : 8; }();
+  static const int c2 = [] { const char *e = std::getenv("HM_Q4_CHUNK2"); return e ? std::atoi(e) : 32; }();
+  p.chunk = std::max(c1, static_cast<int>((static_cast<long>(G) * I + target - 1) / target + 7) / 8 * 8);
   p.bpg = (I + p.chunk - 1) / p.chunk;
-  int smem = mr * H * 2;
+  int smem = mr * q4_pad(H) * 2;
   switch (mr) {
     case 1: q4_smem(ffn1_q4_kernel<1>, smem); ffn1_q4_kernel<1><<<G * p.bpg, 256, smem, st>>>(p); break;
     case 2: q4_smem(ffn1_q4_kernel<2>, smem); ffn1_q4_kernel<2><<<G * p.bpg, 256, smem, st>>>(p); break;
     default: q4_smem(ffn1_q4_kernel<4>, smem); ffn1_q4_kernel<4><<<G * p.bpg, 256, smem, st>>>(p); break;
   }
   HM_LAUNCH_CHECK();
-  p.chunk = std::max(8, static_cast<int>((static_cast<long>(G) * H + target - 1) / target + 7) / 8 * 8);
+  // W2 rows: at least 32 per block -- every block stages (and scans) the whole
+  // h row, which at 8 rows per block cost as much traffic as the weights
+  p.chunk = std::max(c2, static_cast<int>((static_cast<long>(G) * H + target - 1) / target + 7) / 8 * 8);
   p.bpg = (H + p.chunk - 1) / p.chunk;
-  smem = mr * I * 2;
+  smem = mr * q4_pad(I) * 2;
   switch (mr) {
     case 1: q4_smem(ffn2_q4_kernel<1>, smem); ffn2_q4_kernel<1><<<G * p.bpg, 256, smem, st>>>(p); break;
     case 2: q4_smem(ffn2_q4_kernel<2>, smem); ffn2_q4_kernel<2><<<G * p.bpg, 256, smem, st>>>(p); break;
