@@ -188,3 +188,77 @@ def test_token_sharded_dispatch_equals_one_rank():
         for p in range(len(ref_loads)):                          # global, rank-masked LayerRequests
             for l, full in enumerate(ref_loads[p]):
                 assert loads[p][l] == [v if e % 2 == r else 0 for e, v in enumerate(full)]
+
+
+def _run_dispatch_shared(rank: int, world: int, port: int, q) -> None:
+    """Token-sharded EP on a Qwen2-style layer (16 routed experts top-8 plus a
+    shared expert split into 8 chunks homed c % world, sigmoid-gated): each rank's
+    token slice against the fp32 oracle on the same seeded weights."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    import torch.distributed as dist
+
+    from oracle import moe_ref as ref
+    import paper_2504_05897_b200.core as mcore
+    import paper_2504_05897_b200.costs as mcost
+    from paper_2504_05897_b200.engine import EnginePolicy
+    from paper_2504_05897_b200.moe import HybridMoE, shared_chunks
+    from paper_2504_05897_b200.weights import unpack_expert
+
+    torch.cuda.set_device(0)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        H, I = 256, 256
+        cfg = mcore.ModelConfig(num_layers=2, num_routed=16, num_shared=1, num_activated=8,
+                                routed_expert_dims=(H, I), shared_expert_dims=(H, 8 * I), bytes_per_weight=2)
+        eb = mcore.expert_bytes(cfg)
+        prof = mcost.HardwareProfile(gpu_time_per_expert=1.0, cpu_slope=2.0, transfer_bandwidth=eb / 0.5)
+        moe = HybridMoE(cfg, "qwen2", EnginePolicy(), 0.5, prof, max_tokens=64, residual=False, ep_rank=rank,
+                        ep_world=world, cpu_threads=2, exchange="dispatch")
+        moe.init_seeded_weights(3)
+        rng = np.random.default_rng(0)
+        T = 40
+        a, b = rank * T // world, (rank + 1) * T // world
+        logits = [rng.standard_normal((T, moe.ld)).astype(np.float32) for _ in range(2)]
+        xf = torch.from_numpy(rng.standard_normal((T, H)).astype(np.float32)).to(torch.bfloat16)
+        y, info = moe.forward_pass(xf[a:b].contiguous().cuda(), [torch.from_numpy(lg[a:b].copy()).cuda()
+                                                                  for lg in logits], keep_layers=True)
+        torch.cuda.synchronize()
+        # oracle: full layer on the same per-expert seeded weights (regenerated here, every rank)
+        S = shared_chunks(cfg)
+        errs = []
+        g = torch.Generator(device="cuda")
+        n = 3 * H * I
+        for l, (xi, lgi, yo) in enumerate(info["layers"]):
+            ex = []
+            for e in range(cfg.num_routed + S):
+                seed = 3 + 1000 * l + e
+                g.manual_seed(seed)
+                img = (torch.randn(n, generator=g, device="cuda") * 0.02).to(torch.bfloat16)
+                gu, uu, du = unpack_expert(img.view(torch.int16).cpu().numpy().view(np.uint16), H, I)
+                ex.append((ref.bf16_to_f32(gu), ref.bf16_to_f32(uu), ref.bf16_to_f32(du)))
+            xl = ref.bf16_to_f32(xi.view(torch.int16).cpu().numpy().view(np.uint16))
+            want = ref.moe_layer(xl, lgi.cpu().numpy(), ex, cfg.num_routed, cfg.num_activated, False, S,
+                                 moe.gate_col)
+            got = ref.bf16_to_f32(yo.view(torch.int16).cpu().numpy().view(np.uint16))
+            errs.append(float(np.abs(got - want).max() / max(np.abs(want).max(), 1e-30)) if len(xl) else 0.0)
+        q.put((rank, errs))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_token_sharded_dispatch_shared_expert_family():
+    ctx = torch.multiprocessing.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_run_dispatch_shared, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    for r, errs in got.items():
+        assert max(errs) <= 1e-2, (r, errs)
