@@ -13,11 +13,9 @@
 //
 // Kernels: quantize (bf16 image -> q4 image), dequantize (q4 -> bf16 image,
 // feeding the tcgen05 GEMM for prefill-sized groups), and the decode GEMV on
-// the q4 image: nibbles -> fp16 pairs with one LOP3 + one HSUB2 per pair
-// (the 0x6400 exponent trick), HFMA2 against x held in shared memory as fp16
-// in the matching pair order, fp16 partials over 32 weights, fp32 across.
-#include <cuda_fp16.h>
-
+// the q4 image: activations staged per 32-element block as two int8 digits
+// (x ~= sx * (hi + lo/256)), nibble words masked into bytes and multiplied
+// with DP4A (4 MACs per instruction, exact int32), fp32 across blocks.
 #include <cstdlib>
 #include <vector>
 
@@ -89,67 +87,74 @@ __global__ void q4_dequantize_kernel(const uint8_t *__restrict__ q, int H, int I
   }
 }
 
-// 8 nibbles of v (elements e0..e7, e0 in bits 0-3) -> four fp16 pairs
-// (e0,e4) (e1,e5) (e2,e6) (e3,e7), each value = nibble - 8, exactly.
-__device__ __forceinline__ void nib8_to_h2(uint32_t v, __half2 (&o)[4]) {
-  const uint32_t bias = 0x64086408u;  // fp16 1032.0 = 1024 + 8
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    uint32_t t;
-    const uint32_t sh = v >> (4 * j);
-    asm("lop3.b32 %0, %1, %2, %3, 0xea;" : "=r"(t) : "r"(sh), "r"(0x000F000Fu), "r"(0x64006400u));  // (a & b) | c
-    o[j] = __hsub2(*reinterpret_cast<__half2 *>(&t), *reinterpret_cast<const __half2 *>(&bias));
-  }
-}
-
-// x (bf16, K values) -> fp16 in pair order: for each 8 elements
-// [x0 x4 x1 x5 x2 x6 x3 x7], matching nib8_to_h2.  fp16 has a narrow range,
-// so the row is scaled by a power of two that brings max|x| to [1, 2)
-// (exact); the returned factor undoes it on the dot products.  All threads
-// of the block must call it (block-wide max).
-// staged rows are padded to whole 1024-element chunks (the lane-major layout)
+// Activations for the int4 GEMV: per 32-element block b, scale sx = max|x|/127
+// and two int8 digits per element, x ~= sx * (hi + lo/256) (|error| <= sx/512,
+// i.e. ~1e-5 of the block max), split into even / odd elements so that the
+// DP4A against a nibble word's low (even elements) and high (odd) nibbles
+// multiplies matching pairs.  Per block in shared memory: 4 x 16 int8 (even
+// hi, odd hi, even lo, odd lo) = 64 bytes, then sx and sq = sum(hi) + sum(lo)/256.
+// Lane L reads block j*32 + L: consecutive lanes, consecutive 16-byte words.
 __host__ __device__ inline int q4_pad(int K) { return (K + 1023) / 1024 * 1024; }
+__host__ __device__ inline int q4_stage_bytes(int K) { return q4_pad(K) / 32 * 72; }
 
-__device__ float stage_x_h2(const uint16_t *__restrict__ x, int K, __half *xs) {
-  __shared__ float s_red[32];
-  float m = 0.f;
-  for (int i = threadIdx.x; i < K; i += blockDim.x) m = fmaxf(m, fabsf(dev::bf2f(x[i])));
-  m = dev::warp_max(m);
-  __syncthreads();  // s_red reuse across calls
-  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
-  __syncthreads();
-  m = 0.f;
-  for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) m = fmaxf(m, s_red[w]);
-  int e = 0;
-  if (m > 0.f) frexpf(m, &e);  // m = f * 2^e, f in [0.5, 1)
-  const float up = ldexpf(1.0f, 1 - e), down = ldexpf(1.0f, e - 1);
-  for (int i = threadIdx.x; i < K; i += blockDim.x) {
-    // conflict-free layout for the GEMV: lane L reads its q-th 8 values of
-    // chunk j at ((j*4 + q)*32 + L)*8 (consecutive lanes, consecutive 16 B)
-    const int j = i >> 10, L = (i >> 5) & 31, q = (i >> 3) & 3, el = i & 7;
-    const int p = ((j * 4 + q) * 32 + L) * 8 + (el < 4 ? 2 * el : 2 * (el - 4) + 1);
-    xs[p] = __float2half_rn(dev::bf2f(x[i]) * up);
+__device__ void stage_x_q8(const uint16_t *__restrict__ x, int K, uint8_t *st) {
+  const int nb = q4_pad(K) / 32;
+  int8_t *q = reinterpret_cast<int8_t *>(st);
+  float *sx = reinterpret_cast<float *>(st + static_cast<size_t>(nb) * 64);
+  float *sq = sx + nb;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    int8_t *d = q + static_cast<size_t>(b) * 64;
+    if (b * 32 >= K) {  // padding block: zeros
+      for (int i = 0; i < 64; ++i) d[i] = 0;
+      sx[b] = 0.f;
+      sq[b] = 0.f;
+      continue;
+    }
+    float v[32], m = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      v[i] = dev::bf2f(x[b * 32 + i]);
+      m = fmaxf(m, fabsf(v[i]));
+    }
+    const float s = m > 0.f ? m / 127.f : 1.f, inv = 1.f / s;
+    int sh = 0, sl = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float t = v[i] * inv;
+      const float hi = rintf(t);
+      const int lo = max(-127, min(127, __float2int_rn((t - hi) * 256.f)));
+      const int hq = static_cast<int>(hi);
+      d[(i & 1) * 16 + (i >> 1)] = static_cast<int8_t>(hq);       // even / odd hi
+      d[32 + (i & 1) * 16 + (i >> 1)] = static_cast<int8_t>(lo);  // even / odd lo
+      sh += hq;
+      sl += lo;
+    }
+    sx[b] = s;
+    sq[b] = static_cast<float>(sh) + static_cast<float>(sl) * (1.f / 256.f);
   }
-  return down;
 }
 
-// 32 weights (one 16-byte load) of a row against 32 staged x values -> fp32
-// partial; xq[q] = the lane's q-th 8 staged values (pair order)
-__device__ __forceinline__ float q4_dot32(const uint4 w, const uint4 (&xq)[4]) {
-  __half2 a[4] = {__float2half2_rn(0.f), __float2half2_rn(0.f), __float2half2_rn(0.f), __float2half2_rn(0.f)};
+// 32 weights (one 16-byte nibble load) of a row against staged block b ->
+// sum_k (n_k - 8) x_k in fp32
+__device__ __forceinline__ float q4_dot32(const uint4 w, const uint8_t *st, int nb, int b) {
+  const int4 *blk = reinterpret_cast<const int4 *>(st + static_cast<size_t>(b) * 64);
+  const int4 eh = blk[0], oh = blk[1], el = blk[2], ol = blk[3];
+  const float sx = reinterpret_cast<const float *>(st + static_cast<size_t>(nb) * 64)[b];
+  const float sq = reinterpret_cast<const float *>(st + static_cast<size_t>(nb) * 64)[nb + b];
   const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+  const int ehv[4] = {eh.x, eh.y, eh.z, eh.w}, ohv[4] = {oh.x, oh.y, oh.z, oh.w};
+  const int elv[4] = {el.x, el.y, el.z, el.w}, olv[4] = {ol.x, ol.y, ol.z, ol.w};
+  int ah = 0, al = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    __half2 n[4];
-    nib8_to_h2(ws[q], n);
-    a[0] = __hfma2(n[0], *reinterpret_cast<const __half2 *>(&xq[q].x), a[0]);
-    a[1] = __hfma2(n[1], *reinterpret_cast<const __half2 *>(&xq[q].y), a[1]);
-    a[2] = __hfma2(n[2], *reinterpret_cast<const __half2 *>(&xq[q].z), a[2]);
-    a[3] = __hfma2(n[3], *reinterpret_cast<const __half2 *>(&xq[q].w), a[3]);
+    const int lo = static_cast<int>(ws[q] & 0x0F0F0F0Fu);         // elements 8q + 0, 2, 4, 6
+    const int hi = static_cast<int>((ws[q] >> 4) & 0x0F0F0F0Fu);  // elements 8q + 1, 3, 5, 7
+    ah = __dp4a(lo, ehv[q], ah);
+    ah = __dp4a(hi, ohv[q], ah);
+    al = __dp4a(lo, elv[q], al);
+    al = __dp4a(hi, olv[q], al);
   }
-  const __half2 t = __hadd2(__hadd2(a[0], a[1]), __hadd2(a[2], a[3]));
-  const float2 f = __half22float2(t);
-  return f.x + f.y;
+  return sx * (static_cast<float>(ah) + static_cast<float>(al) * (1.f / 256.f) - 8.f * sq);
 }
 
 // NR rows (sharing x) dotted with the staged x; each lane handles 32-weight
@@ -157,7 +162,8 @@ __device__ __forceinline__ float q4_dot32(const uint4 w, const uint4 (&xq)[4]) {
 // memory-level parallelism of the bf16 GEMV).  Returns the lane's partials.
 template <int NR, int U>
 __device__ __forceinline__ void q4_rows_dot(const uint8_t *const (&rows)[NR], const uint16_t *const (&sc)[NR],
-                                            const __half *xs, int K, int lane, float (&acc)[NR]) {
+                                            const uint8_t *st, int K, int lane, float (&acc)[NR]) {
+  const int nb = q4_pad(K) / 32;
 #pragma unroll
   for (int r = 0; r < NR; ++r) acc[r] = 0.f;
   for (int c0 = lane * 32; c0 < K; c0 += 1024 * U) {
@@ -178,11 +184,8 @@ __device__ __forceinline__ void q4_rows_dot(const uint8_t *const (&rows)[NR], co
     for (int u = 0; u < U; ++u) {
       const int c = c0 + u * 1024;
       if (c < K) {
-        const int j = c >> 10;
-        const uint4 *xb = reinterpret_cast<const uint4 *>(xs) + (j * 4) * 32 + lane;
-        const uint4 xq[4] = {xb[0], xb[32], xb[64], xb[96]};
 #pragma unroll
-        for (int r = 0; r < NR; ++r) acc[r] = fmaf(s[r][u], q4_dot32(w[r][u], xq), acc[r]);
+        for (int r = 0; r < NR; ++r) acc[r] = fmaf(s[r][u], q4_dot32(w[r][u], st, nb, c / 32), acc[r]);
       }
     }
   }
@@ -199,14 +202,12 @@ struct Q4GemvParams {
 };
 
 template <int MR>
-__global__ void __launch_bounds__(256) ffn1_q4_kernel(const __grid_constant__ Q4GemvParams p) {
-  extern __shared__ __align__(16) __half xs1[];  // [MR][H]
+__global__ void __launch_bounds__(256, 4) ffn1_q4_kernel(const __grid_constant__ Q4GemvParams p) {
+  extern __shared__ __align__(16) uint8_t xs1[];  // [MR][q4_stage_bytes(H)]
   const int g = blockIdx.x / p.bpg, cid = blockIdx.x % p.bpg;
   const int M = p.row_count[g], rb = p.row_begin[g], H = p.H, I = p.I;
-  float down[MR];
-#pragma unroll
-  const int Hp = q4_pad(H);
-  for (int m = 0; m < MR; ++m) down[m] = m < M ? stage_x_h2(p.xp + static_cast<size_t>(rb + m) * H, H, xs1 + m * Hp) : 1.f;
+  const int Hs = q4_stage_bytes(H);
+  for (int m = 0; m < M; ++m) stage_x_q8(p.xp + static_cast<size_t>(rb + m) * H, H, xs1 + m * Hs);
   __syncthreads();
   const Q4Layout L = q4_layout(H, I);
   const uint8_t *img = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_bytes;
@@ -223,9 +224,9 @@ __global__ void __launch_bounds__(256) ffn1_q4_kernel(const __grid_constant__ Q4
     for (int m = 0; m < MR; ++m) {
       if (m < M) {
         float a[2];
-        q4_rows_dot<2, 4>(rows, scs, xs1 + m * Hp, H, lane, a);
-        const float gs = down[m] * dev::warp_sum(a[0]);
-        const float us = down[m] * dev::warp_sum(a[1]);
+        q4_rows_dot<2, 4>(rows, scs, xs1 + m * Hs, H, lane, a);
+        const float gs = dev::warp_sum(a[0]);
+        const float us = dev::warp_sum(a[1]);
         if (lane == 0) p.h[static_cast<size_t>(rb + m) * I + i] = dev::f2bf(dev::silu(gs) * us);
       }
     }
@@ -233,14 +234,12 @@ __global__ void __launch_bounds__(256) ffn1_q4_kernel(const __grid_constant__ Q4
 }
 
 template <int MR>
-__global__ void __launch_bounds__(256) ffn2_q4_kernel(const __grid_constant__ Q4GemvParams p) {
-  extern __shared__ __align__(16) __half hs2[];  // [MR][I]
+__global__ void __launch_bounds__(256, 4) ffn2_q4_kernel(const __grid_constant__ Q4GemvParams p) {
+  extern __shared__ __align__(16) uint8_t hs2[];  // [MR][q4_stage_bytes(I)]
   const int g = blockIdx.x / p.bpg, cid = blockIdx.x % p.bpg;
   const int M = p.row_count[g], rb = p.row_begin[g], H = p.H, I = p.I;
-  float down[MR];
-#pragma unroll
-  const int Ip = q4_pad(I);
-  for (int m = 0; m < MR; ++m) down[m] = m < M ? stage_x_h2(p.h + static_cast<size_t>(rb + m) * I, I, hs2 + m * Ip) : 1.f;
+  const int Is = q4_stage_bytes(I);
+  for (int m = 0; m < M; ++m) stage_x_q8(p.h + static_cast<size_t>(rb + m) * I, I, hs2 + m * Is);
   __syncthreads();
   const Q4Layout L = q4_layout(H, I);
   const uint8_t *img = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_bytes;
@@ -257,8 +256,8 @@ __global__ void __launch_bounds__(256) ffn2_q4_kernel(const __grid_constant__ Q4
     for (int m = 0; m < MR; ++m) {
       if (m < M) {
         float a[1];
-        q4_rows_dot<1, 4>(rows, scs, hs2 + m * Ip, I, lane, a);
-        const float s = down[m] * dev::warp_sum(a[0]);
+        q4_rows_dot<1, 4>(rows, scs, hs2 + m * Is, I, lane, a);
+        const float s = dev::warp_sum(a[0]);
         if (lane == 0) p.out[static_cast<size_t>(rb + m) * H + j] = s;
       }
     }
@@ -305,7 +304,7 @@ void launch_q4_gemv(const uint8_t *pool, size_t slot_bytes, int H, int I, const 
   static const int c2 = [] { const char *e = std::getenv("HM_Q4_CHUNK2"); return e ? std::atoi(e) : 32; }();
   p.chunk = std::max(c1, static_cast<int>((static_cast<long>(G) * I + target - 1) / target + 7) / 8 * 8);
   p.bpg = (I + p.chunk - 1) / p.chunk;
-  int smem = mr * q4_pad(H) * 2;
+  int smem = mr * q4_stage_bytes(H);
   switch (mr) {
     case 1: q4_smem(ffn1_q4_kernel<1>, smem); ffn1_q4_kernel<1><<<G * p.bpg, 256, smem, st>>>(p); break;
     case 2: q4_smem(ffn1_q4_kernel<2>, smem); ffn1_q4_kernel<2><<<G * p.bpg, 256, smem, st>>>(p); break;
@@ -316,7 +315,7 @@ void launch_q4_gemv(const uint8_t *pool, size_t slot_bytes, int H, int I, const 
   // h row, which at 8 rows per block cost as much traffic as the weights
   p.chunk = std::max(c2, static_cast<int>((static_cast<long>(G) * H + target - 1) / target + 7) / 8 * 8);
   p.bpg = (H + p.chunk - 1) / p.chunk;
-  smem = mr * q4_pad(I) * 2;
+  smem = mr * q4_stage_bytes(I);
   switch (mr) {
     case 1: q4_smem(ffn2_q4_kernel<1>, smem); ffn2_q4_kernel<1><<<G * p.bpg, 256, smem, st>>>(p); break;
     case 2: q4_smem(ffn2_q4_kernel<2>, smem); ffn2_q4_kernel<2><<<G * p.bpg, 256, smem, st>>>(p); break;
