@@ -22,7 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # CPython fp64, one rounding per operation.
 CXXFLAGS = ["-std=c++17", "-O2", "-fPIC", "-ffp-contract=off", "-fno-fast-math",
             "-Wall", "-Wextra", "-Wno-unused-parameter", "-pthread"]
-HOST_ISA = ["-mavx512f", "-mavx512bw", "-mavx512vl", "-mavx512bf16", "-mavx512dq", "-mfma", "-mamx-tile",
+HOST_ISA = ["-mavx512f", "-mavx512bw", "-mavx512vl", "-mavx512bf16", "-mavx512dq", "-mavx512vnni", "-mfma", "-mamx-tile",
             "-mamx-bf16"]
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

@@ -584,82 +584,90 @@ inline Q4View q4_view(const uint8_t *img, int H, int I) {
   return v;
 }
 
-// x (bf16 [K]) -> even / odd elements in fp32 and, per 128-group, the lane-wise
-// partial sums of x (so that sum_k (n_k - 8) x_k = sum_k n_k x_k - 8 sum_k x_k).
+// x (bf16 [K]) for the int4 GEMV: per 128-group g, scale sx = max|x|/127 and
+// two int8 digits per element, x ~= sx * (hi + lo/256) (|error| <= sx/512),
+// split into even / odd elements so that VNNI (vpdpbusd: u8 x s8, 4 per int32
+// lane) multiplies the low nibbles (even elements) and the high nibbles (odd)
+// of a weight byte vector with the matching digits.  sq = sum(hi) + sum(lo)/256.
 struct Q4X {
-  std::vector<float> xe, xo, sx;  // [K/2], [K/2], [K/128][16]
+  std::vector<int8_t> d;   // [K/128][4][64]: even hi | odd hi | even lo | odd lo
+  std::vector<float> sx, sq;
 };
-inline void q4_prep_x(const uint16_t *x, int K, Q4X &q) {
-  q.xe.resize(K / 2);
-  q.xo.resize(K / 2);
-  q.sx.assign(static_cast<size_t>(K / 128) * 16, 0.0f);
-  for (int k = 0; k < K / 2; ++k) {
-    q.xe[k] = bf2f(x[2 * k]);
-    q.xo[k] = bf2f(x[2 * k + 1]);
-  }
-  for (int g = 0; g < K / 128; ++g)
-    for (int c = 0; c < 4; ++c)
-      for (int l = 0; l < 16; ++l) q.sx[g * 16 + l] += q.xe[g * 64 + c * 16 + l] + q.xo[g * 64 + c * 16 + l];
+inline void q4_alloc_x(int K, Q4X &q) {
+  const int ng = K / 128;
+  q.d.resize(static_cast<size_t>(ng) * 256);
+  q.sx.resize(ng);
+  q.sq.resize(ng);
 }
-
-// out[r] = sum_k w[r][k] x[k] for n 4-bit rows (K/2 bytes, K/128 scales each)
-inline void dot_rows_q4(const uint8_t *nib, const uint16_t *sc, int n, int K, const Q4X &q, float *out) {
-  const __m512i m15 = _mm512_set1_epi32(15);
-  const __m512 eight = _mm512_set1_ps(8.0f);
-  for (int r = 0; r < n; ++r) {
-    const uint8_t *row = nib + static_cast<size_t>(r) * (K / 2);
-    const uint16_t *srow = sc + static_cast<size_t>(r) * (K / 128);
-    _mm_prefetch(reinterpret_cast<const char *>(row + 16 * (K / 2)), _MM_HINT_T1);
-    __m512 acc = _mm512_setzero_ps();
-    for (int g = 0; g < K / 128; ++g) {
-      __m512 d0 = _mm512_setzero_ps(), d1 = _mm512_setzero_ps();
-      for (int c = 0; c < 4; ++c) {  // 16 bytes = 32 weights
-        const __m512i b = _mm512_cvtepu8_epi32(_mm_loadu_si128(reinterpret_cast<const __m128i *>(row + g * 64 + c * 16)));
-        const __m512 lo = _mm512_cvtepi32_ps(_mm512_and_epi32(b, m15));
-        const __m512 hi = _mm512_cvtepi32_ps(_mm512_srli_epi32(b, 4));
-        d0 = _mm512_fmadd_ps(lo, _mm512_loadu_ps(&q.xe[g * 64 + c * 16]), d0);
-        d1 = _mm512_fmadd_ps(hi, _mm512_loadu_ps(&q.xo[g * 64 + c * 16]), d1);
-      }
-      const __m512 dg = _mm512_fnmadd_ps(eight, _mm512_loadu_ps(&q.sx[g * 16]), _mm512_add_ps(d0, d1));
-      acc = _mm512_fmadd_ps(_mm512_set1_ps(bf2f(srow[g])), dg, acc);
+// groups [g0, g1) of x (q already sized by q4_alloc_x)
+inline void q4_prep_groups(const uint16_t *x, Q4X &q, int g0, int g1) {
+  for (int g = g0; g < g1; ++g) {
+    float m = 0.f;
+    for (int i = 0; i < 128; ++i) m = std::max(m, std::fabs(bf2f(x[g * 128 + i])));
+    const float s = m > 0.f ? m / 127.f : 1.f, inv = 1.f / s;
+    int sh = 0, sl = 0;
+    int8_t *d = q.d.data() + static_cast<size_t>(g) * 256;
+    for (int i = 0; i < 128; ++i) {
+      const float t = bf2f(x[g * 128 + i]) * inv;
+      const float hi = std::nearbyint(t);
+      const int lo = std::max(-127, std::min(127, static_cast<int>(std::nearbyint((t - hi) * 256.f))));
+      d[(i & 1) * 64 + (i >> 1)] = static_cast<int8_t>(hi);
+      d[128 + (i & 1) * 64 + (i >> 1)] = static_cast<int8_t>(lo);
+      sh += static_cast<int>(hi);
+      sl += lo;
     }
-    out[r] = _mm512_reduce_add_ps(acc);
+    q.sx[g] = s;
+    q.sq[g] = static_cast<float>(sh) + static_cast<float>(sl) * (1.f / 256.f);
   }
 }
+inline void q4_prep_x(const uint16_t *x, int K, Q4X &q) {
+  q4_alloc_x(K, q);
+  q4_prep_groups(x, q, 0, K / 128);
+}
 
-// Up to 4 tokens at once: the nibbles of each 128-group are decoded once and
-// reused for every token.  out[t * ldo + r].
+// Up to 4 tokens at once: each 128-group's 64 nibble bytes are split into
+// low / high nibble vectors once and multiplied with every token's digits
+// (4 vpdpbusd per token and group).  out[t * ldo + r].
 template <int MT>
 inline void dot_rows_q4_mt(const uint8_t *nib, const uint16_t *sc, int n, int K, const Q4X *const *q, float *out,
                            size_t ldo) {
-  const __m512i m15 = _mm512_set1_epi32(15);
-  const __m512 eight = _mm512_set1_ps(8.0f);
+  const __m512i m15 = _mm512_set1_epi8(15);
+  const __m512 inv256 = _mm512_set1_ps(1.f / 256.f);
+  const int ng = K / 128;
   for (int r = 0; r < n; ++r) {
     const uint8_t *row = nib + static_cast<size_t>(r) * (K / 2);
     const uint16_t *srow = sc + static_cast<size_t>(r) * (K / 128);
     _mm_prefetch(reinterpret_cast<const char *>(row + 16 * (K / 2)), _MM_HINT_T1);
     __m512 acc[MT];
-    for (int t = 0; t < MT; ++t) acc[t] = _mm512_setzero_ps();
-    for (int g = 0; g < K / 128; ++g) {
-      __m512 lo[4], hi[4];
-      for (int c = 0; c < 4; ++c) {
-        const __m512i b = _mm512_cvtepu8_epi32(_mm_loadu_si128(reinterpret_cast<const __m128i *>(row + g * 64 + c * 16)));
-        lo[c] = _mm512_cvtepi32_ps(_mm512_and_epi32(b, m15));
-        hi[c] = _mm512_cvtepi32_ps(_mm512_srli_epi32(b, 4));
-      }
-      const __m512 sv = _mm512_set1_ps(bf2f(srow[g]));
+    float corr[MT];
+    for (int t = 0; t < MT; ++t) {
+      acc[t] = _mm512_setzero_ps();
+      corr[t] = 0.f;
+    }
+    for (int g = 0; g < ng; ++g) {
+      const __m512i wb = _mm512_loadu_si512(row + g * 64);
+      const __m512i lo = _mm512_and_si512(wb, m15);
+      const __m512i hi = _mm512_and_si512(_mm512_srli_epi16(wb, 4), m15);
+      const float sw = bf2f(srow[g]);
       for (int t = 0; t < MT; ++t) {
-        __m512 d0 = _mm512_setzero_ps(), d1 = _mm512_setzero_ps();
-        for (int c = 0; c < 4; ++c) {
-          d0 = _mm512_fmadd_ps(lo[c], _mm512_loadu_ps(&q[t]->xe[g * 64 + c * 16]), d0);
-          d1 = _mm512_fmadd_ps(hi[c], _mm512_loadu_ps(&q[t]->xo[g * 64 + c * 16]), d1);
-        }
-        const __m512 dg = _mm512_fnmadd_ps(eight, _mm512_loadu_ps(&q[t]->sx[g * 16]), _mm512_add_ps(d0, d1));
-        acc[t] = _mm512_fmadd_ps(sv, dg, acc[t]);
+        const int8_t *d = q[t]->d.data() + static_cast<size_t>(g) * 256;
+        __m512i ah = _mm512_dpbusd_epi32(_mm512_setzero_si512(), lo, _mm512_loadu_si512(d));
+        ah = _mm512_dpbusd_epi32(ah, hi, _mm512_loadu_si512(d + 64));
+        __m512i al = _mm512_dpbusd_epi32(_mm512_setzero_si512(), lo, _mm512_loadu_si512(d + 128));
+        al = _mm512_dpbusd_epi32(al, hi, _mm512_loadu_si512(d + 192));
+        const __m512 f = _mm512_fmadd_ps(_mm512_cvtepi32_ps(al), inv256, _mm512_cvtepi32_ps(ah));
+        const float c = sw * q[t]->sx[g];
+        acc[t] = _mm512_fmadd_ps(_mm512_set1_ps(c), f, acc[t]);
+        corr[t] += c * q[t]->sq[g];
       }
     }
-    for (int t = 0; t < MT; ++t) out[static_cast<size_t>(t) * ldo + r] = _mm512_reduce_add_ps(acc[t]);
+    for (int t = 0; t < MT; ++t) out[static_cast<size_t>(t) * ldo + r] = _mm512_reduce_add_ps(acc[t]) - 8.f * corr[t];
   }
+}
+
+inline void dot_rows_q4(const uint8_t *nib, const uint16_t *sc, int n, int K, const Q4X &q, float *out) {
+  const Q4X *qp[1] = {&q};
+  dot_rows_q4_mt<1>(nib, sc, n, K, qp, out, 0);
 }
 
 inline void dot_rows_q4_tokens(const uint8_t *nib, const uint16_t *sc, int n, int K, const Q4X *const *q, int mt,
@@ -699,8 +707,11 @@ void cpu_experts_decode_q4(ThreadPool &pool, const uint8_t *const *imgs, const u
   if (n <= 0) return;
   hbuf.resize(static_cast<size_t>(n) * I);
   uint16_t *h = hbuf.data();
-  std::vector<Q4X> qx(n);
-  for (int e = 0; e < n; ++e) q4_prep_x(xs[e], H, qx[e]);
+  std::vector<Q4X> qx(n), hx(n);
+  for (int e = 0; e < n; ++e) {
+    q4_prep_x(xs[e], H, qx[e]);
+    q4_alloc_x(I, hx[e]);
+  }
   pool.run([&](int tid, int nt) {
     // phase 1: 16-pair units over the flat (expert, pair) space, gate and up rows
     const long nu = static_cast<long>(n) * I / 16;
@@ -714,17 +725,19 @@ void cpu_experts_decode_q4(ThreadPool &pool, const uint8_t *const *imgs, const u
       for (int i = 0; i < 16; ++i) h[static_cast<size_t>(e) * I + i0 + i] = f2bf(silu(g[i]) * u[i]);
     }
     pool.barrier();
-    Q4X hx;
-    int he = -1;
+    {  // h -> int8 digits, groups split over the threads (once, not per thread)
+      const long ng = static_cast<long>(n) * (I / 128);
+      for (long q = ng * tid / nt; q < ng * (tid + 1) / nt; ++q) {
+        const int e = static_cast<int>(q / (I / 128)), gq = static_cast<int>(q % (I / 128));
+        q4_prep_groups(h + static_cast<size_t>(e) * I, hx[e], gq, gq + 1);
+      }
+    }
+    pool.barrier();
     const long r1 = static_cast<long>(n) * H / 16;
     for (long q = r1 * tid / nt; q < r1 * (tid + 1) / nt; ++q) {
       const int e = static_cast<int>(q / (H / 16)), j0 = static_cast<int>(q % (H / 16)) * 16;
-      if (e != he) {
-        q4_prep_x(h + static_cast<size_t>(e) * I, I, hx);
-        he = e;
-      }
       const Q4View v = q4_view(imgs[e], H, I);
-      dot_rows_q4(v.n2 + static_cast<size_t>(j0) * (I / 2), v.s2 + static_cast<size_t>(j0) * (I / 128), 16, I, hx,
+      dot_rows_q4(v.n2 + static_cast<size_t>(j0) * (I / 2), v.s2 + static_cast<size_t>(j0) * (I / 128), 16, I, hx[e],
                   outs[e] + j0);
     }
   });
@@ -750,6 +763,8 @@ void cpu_expert_q4(ThreadPool &pool, const uint8_t *img, int H, int I, const uin
     }
     scratch.resize(static_cast<size_t>(M) * I);
     uint16_t *hh = scratch.data();
+    std::vector<Q4X> hxs(M);
+    for (int t = 0; t < M; ++t) q4_alloc_x(I, hxs[t]);
     const Q4View v = q4_view(img, H, I);
     pool.run([&](int tid, int nt) {
       const int nu = I / 16;
@@ -763,12 +778,14 @@ void cpu_expert_q4(ThreadPool &pool, const uint8_t *img, int H, int I, const uin
           for (int i = 0; i < 16; ++i) hh[static_cast<size_t>(t) * I + i0 + i] = f2bf(silu(g[t * 16 + i]) * u[t * 16 + i]);
       }
       pool.barrier();
-      std::vector<Q4X> hx(M);
-      const Q4X *hp[4];
-      for (int t = 0; t < M; ++t) {
-        q4_prep_x(hh + static_cast<size_t>(t) * I, I, hx[t]);
-        hp[t] = &hx[t];
+      const long ng = static_cast<long>(M) * (I / 128);
+      for (long q = ng * tid / nt; q < ng * (tid + 1) / nt; ++q) {
+        const int t = static_cast<int>(q / (I / 128)), gq = static_cast<int>(q % (I / 128));
+        q4_prep_groups(hh + static_cast<size_t>(t) * I, hxs[t], gq, gq + 1);
       }
+      pool.barrier();
+      const Q4X *hp[4];
+      for (int t = 0; t < M; ++t) hp[t] = &hxs[t];
       const int nr = H / 16;
       for (int q = nr * tid / nt; q < nr * (tid + 1) / nt; ++q)
         dot_rows_q4_tokens(v.n2 + static_cast<size_t>(q * 16) * (I / 2), v.s2 + static_cast<size_t>(q * 16) * (I / 128),
