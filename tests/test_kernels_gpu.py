@@ -270,3 +270,30 @@ def test_q4_quantize_and_ffn(H, I, rows):
         gq, uq, dq = ref.q4_expert(q[s].cpu().numpy(), H, I)
         want = ref.expert(xs[r0:r0 + m], gq, uq, dq)
         assert rel_err(o[r0:r0 + m], want) <= TOL, (s, m, rel_err(o[r0:r0 + m], want))
+
+
+def test_expert_ffn_many_groups_and_empty_groups():
+    """More groups than one launch takes (kMaxGroups = 96: split into several
+    launches), empty groups interleaved, on both paths."""
+    H, I = 256, 256
+    n_slots = 8
+    pool, experts = make_pool(n_slots, H, I, 21)
+    groups, rb = [], 0
+    for gi in range(110):
+        c = 0 if gi % 9 == 4 else (1 + gi % 3 if gi % 2 else 5 + gi % 4)
+        groups.append((gi % n_slots, rb, c))
+        rb += c
+    x = torch.randn((rb, H), device="cuda").to(torch.bfloat16)
+    h = torch.empty((rb, I), dtype=torch.bfloat16, device="cuda")
+    out = torch.zeros((rb, H), device="cuda")
+    K.expert_ffn(pool, n_slots, H, I, groups, x, h, out, _lib.FFN_AUTO)
+    torch.cuda.synchronize()
+    xn, on = bf16_numpy(x), out.cpu().numpy()
+    for slot, b, c in groups:
+        if c:
+            assert rel_err(on[b:b + c], ref.expert(xn[b:b + c], *experts[slot])) <= TOL, (slot, b, c)
+
+
+@pytest.mark.parametrize("counts,path", [([1, 2, 4], _lib.FFN_GEMV), ([96, 33], _lib.FFN_GEMM)])
+def test_expert_ffn_deepseek_shape(counts, path):
+    _ffn_case(2048, 1408, counts, path)
