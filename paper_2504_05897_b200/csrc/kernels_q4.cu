@@ -91,32 +91,47 @@ __global__ void q4_dequantize_kernel(const uint8_t *__restrict__ q, int H, int I
 // and two int8 digits per element, x ~= sx * (hi + lo/256) (|error| <= sx/512,
 // i.e. ~1e-5 of the block max), split into even / odd elements so that the
 // DP4A against a nibble word's low (even elements) and high (odd) nibbles
-// multiplies matching pairs.  Per block in shared memory: 4 x 16 int8 (even
-// hi, odd hi, even lo, odd lo) = 64 bytes, then sx and sq = sum(hi) + sum(lo)/256.
-// Lane L reads block j*32 + L: consecutive lanes, consecutive 16-byte words.
+// multiplies matching pairs.  Shared memory: four planes of 16 int8 per block
+// (even hi | odd hi | even lo | odd lo, each plane [nb][16]), then sx[nb] and
+// sq[nb] = sum(hi) + sum(lo)/256.  Lane L reads block j*32 + L of each plane:
+// consecutive lanes, consecutive 16-byte words (a [nb][64] layout put lanes
+// 64 B apart and cost 4-way bank conflicts on every load).
 __host__ __device__ inline int q4_pad(int K) { return (K + 1023) / 1024 * 1024; }
 __host__ __device__ inline int q4_stage_bytes(int K) { return q4_pad(K) / 32 * 72; }
 
 __device__ void stage_x_q8(const uint16_t *__restrict__ x, int K, uint8_t *st) {
   const int nb = q4_pad(K) / 32;
-  int8_t *q = reinterpret_cast<int8_t *>(st);
+  int4 *planes = reinterpret_cast<int4 *>(st);  // plane p, block b: planes[p * nb + b]
   float *sx = reinterpret_cast<float *>(st + static_cast<size_t>(nb) * 64);
   float *sq = sx + nb;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-    int8_t *d = q + static_cast<size_t>(b) * 64;
     if (b * 32 >= K) {  // padding block: zeros
-      for (int i = 0; i < 64; ++i) d[i] = 0;
+      const int4 z = make_int4(0, 0, 0, 0);
+      planes[b] = planes[nb + b] = planes[2 * nb + b] = planes[3 * nb + b] = z;
       sx[b] = 0.f;
       sq[b] = 0.f;
       continue;
     }
     float v[32], m = 0.f;
+    const uint4 *src = reinterpret_cast<const uint4 *>(x + static_cast<size_t>(b) * 32);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      v[i] = dev::bf2f(x[b * 32 + i]);
-      m = fmaxf(m, fabsf(v[i]));
+    for (int c = 0; c < 4; ++c) {  // 4 x 16-byte loads = 32 bf16
+      const uint4 u = src[c];
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        v[c * 8 + 2 * j] = dev::bf_lo(w[j]);
+        v[c * 8 + 2 * j + 1] = dev::bf_hi(w[j]);
+      }
     }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) m = fmaxf(m, fabsf(v[i]));
     const float s = m > 0.f ? m / 127.f : 1.f, inv = 1.f / s;
+    uint32_t pk[4][4];  // [plane][word]
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int w = 0; w < 4; ++w) pk[p][w] = 0u;
     int sh = 0, sl = 0;
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
@@ -124,11 +139,16 @@ __device__ void stage_x_q8(const uint16_t *__restrict__ x, int K, uint8_t *st) {
       const float hi = rintf(t);
       const int lo = max(-127, min(127, __float2int_rn((t - hi) * 256.f)));
       const int hq = static_cast<int>(hi);
-      d[(i & 1) * 16 + (i >> 1)] = static_cast<int8_t>(hq);       // even / odd hi
-      d[32 + (i & 1) * 16 + (i >> 1)] = static_cast<int8_t>(lo);  // even / odd lo
+      const int k = i >> 1, word = k >> 2, sh8 = (k & 3) * 8;  // byte k of the plane
+      pk[i & 1][word] |= (static_cast<uint32_t>(hq) & 0xFFu) << sh8;        // even / odd hi
+      pk[2 + (i & 1)][word] |= (static_cast<uint32_t>(lo) & 0xFFu) << sh8;  // even / odd lo
       sh += hq;
       sl += lo;
     }
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+      planes[p * nb + b] = make_int4(static_cast<int>(pk[p][0]), static_cast<int>(pk[p][1]),
+                                     static_cast<int>(pk[p][2]), static_cast<int>(pk[p][3]));
     sx[b] = s;
     sq[b] = static_cast<float>(sh) + static_cast<float>(sl) * (1.f / 256.f);
   }
@@ -137,8 +157,8 @@ __device__ void stage_x_q8(const uint16_t *__restrict__ x, int K, uint8_t *st) {
 // 32 weights (one 16-byte nibble load) of a row against staged block b ->
 // sum_k (n_k - 8) x_k in fp32
 __device__ __forceinline__ float q4_dot32(const uint4 w, const uint8_t *st, int nb, int b) {
-  const int4 *blk = reinterpret_cast<const int4 *>(st + static_cast<size_t>(b) * 64);
-  const int4 eh = blk[0], oh = blk[1], el = blk[2], ol = blk[3];
+  const int4 *pl = reinterpret_cast<const int4 *>(st) + b;
+  const int4 eh = pl[0], oh = pl[nb], el = pl[2 * nb], ol = pl[3 * nb];
   const float sx = reinterpret_cast<const float *>(st + static_cast<size_t>(nb) * 64)[b];
   const float sq = reinterpret_cast<const float *>(st + static_cast<size_t>(nb) * 64)[nb + b];
   const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
@@ -301,7 +321,7 @@ void launch_q4_gemv(const uint8_t *pool, size_t slot_bytes, int H, int I, const 
   }
   const int target = sm_count() * 4, G = p.n_groups;
   static const int c1 = [] { const char *e = std::getenv("HM_Q4_CHUNK1"); return e ? std::atoi(e) : 8; }();
-  static const int c2 = [] { const char *e = std::getenv("HM_Q4_CHUNK2"); return e ? std::atoi(e) : 32; }();
+  static const int c2 = [] { const char *e = std::getenv("HM_Q4_CHUNK2"); return e ? std::atoi(e) : 8; }();
   p.chunk = std::max(c1, static_cast<int>((static_cast<long>(G) * I + target - 1) / target + 7) / 8 * 8);
   p.bpg = (I + p.chunk - 1) / p.chunk;
   int smem = mr * q4_stage_bytes(H);
@@ -311,8 +331,6 @@ void launch_q4_gemv(const uint8_t *pool, size_t slot_bytes, int H, int I, const 
     default: q4_smem(ffn1_q4_kernel<4>, smem); ffn1_q4_kernel<4><<<G * p.bpg, 256, smem, st>>>(p); break;
   }
   HM_LAUNCH_CHECK();
-  // W2 rows: at least 32 per block -- every block stages (and scans) the whole
-  // h row, which at 8 rows per block cost as much traffic as the weights
   p.chunk = std::max(c2, static_cast<int>((static_cast<long>(G) * H + target - 1) / target + 7) / 8 * 8);
   p.bpg = (H + p.chunk - 1) / p.chunk;
   smem = mr * q4_stage_bytes(I);
