@@ -16,10 +16,13 @@ from paper_2504_05897_b200 import _lib  # noqa: E402
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 shapes = {"mixtral": (4096, 14336), "deepseek": (2048, 1408), "qwen2": (3584, 2560)}
+if len(sys.argv) > 2:  # shape filter, e.g. `deepseek`
+    shapes = {k: v for k, v in shapes.items() if k in sys.argv[2].split(",")}
+counts = tuple(int(c) for c in sys.argv[3].split(",")) if len(sys.argv) > 3 else (1, 2, 4, 8)
 res = {}
 for name, (H, I) in shapes.items():
     eb = 3 * H * I * 2
-    for n in (1, 2, 4, 8):
+    for n in counts:
         n_slots = min(max(2 * n, int(4 * 126e6 // eb) + n), max(2 * n, int(24e9 // eb)))
         pool = (torch.randn((n_slots, 3 * H * I), device="cuda") * 0.02).to(torch.bfloat16)
         x = torch.randn((n, H), device="cuda").to(torch.bfloat16)
