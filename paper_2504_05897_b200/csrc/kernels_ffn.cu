@@ -126,34 +126,56 @@ __global__ void __launch_bounds__(256) ffn2_gemv_kernel(const __grid_constant__ 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint16_t *w2 = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_elems + static_cast<size_t>(2) * I * H;
   const int j_end = min(H, (cid + 1) * p.chunk);
-  for (int j = cid * p.chunk + wid; j < j_end; j += nw) {
-    const uint16_t *wr = w2 + static_cast<size_t>(j) * I;
-    float acc[MR];
+  // two rows per warp at a time (rows j and j + nw): twice the loads in flight
+  // per warp -- small-I experts (DeepSeek: 2.8 KB rows) were latency-bound
+  constexpr int RW = 2;
+  for (int j0 = cid * p.chunk + wid; j0 < j_end; j0 += nw * RW) {
+    const uint16_t *wr[RW];
+    bool live[RW];
 #pragma unroll
-    for (int m = 0; m < MR; ++m) acc[m] = 0.f;
+    for (int r = 0; r < RW; ++r) {
+      live[r] = j0 + r * nw < j_end;
+      wr[r] = w2 + static_cast<size_t>(live[r] ? j0 + r * nw : j0) * I;
+    }
+    float acc[MR][RW];
+#pragma unroll
+    for (int m = 0; m < MR; ++m)
+#pragma unroll
+      for (int r = 0; r < RW; ++r) acc[m][r] = 0.f;
     constexpr int U = 4;
     for (int c0 = lane * 8; c0 < I; c0 += 256 * U) {
-      uint4 wv[U];
+      uint4 wv[RW][U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int c = c0 + u * 256;
-        if (c < I) wv[u] = dev::ld_stream(wr + c);
-      }
+      for (int r = 0; r < RW; ++r)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int c = c0 + u * 256;
+          if (c < I && live[r]) wv[r][u] = dev::ld_stream(wr[r] + c);
+        }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int c = c0 + u * 256;
         if (c < I) {
 #pragma unroll
           for (int m = 0; m < MR; ++m)
-            if (m < M) acc[m] += dev::dot8(wv[u], *reinterpret_cast<const uint4 *>(hs + m * I + c));
+            if (m < M) {
+              const uint4 hv = *reinterpret_cast<const uint4 *>(hs + m * I + c);
+#pragma unroll
+              for (int r = 0; r < RW; ++r)
+                if (live[r]) acc[m][r] += dev::dot8(wv[r][u], hv);
+            }
         }
       }
     }
 #pragma unroll
     for (int m = 0; m < MR; ++m) {
       if (m < M) {
-        const float s = dev::warp_sum(acc[m]);
-        if (lane == 0) p.out[static_cast<size_t>(rb + m) * H + j] = s;
+#pragma unroll
+        for (int r = 0; r < RW; ++r) {
+          if (!live[r]) continue;
+          const float s = dev::warp_sum(acc[m][r]);
+          if (lane == 0) p.out[static_cast<size_t>(rb + m) * H + j0 + r * nw] = s;
+        }
       }
     }
   }
