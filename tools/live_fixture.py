@@ -1,0 +1,73 @@
+"""Live-run decision fixture (run on the GPU box; commits tests/golden/live_*.json).
+
+A tiny HybriMoE stack runs in MODEL MODE on the B200: every layer's router
+logits are x . W_g computed on the GPU from that layer's live input, so the
+LayerRequests come from this implementation's kernels, not from the
+reference's trace generator.  The runtime's per-layer LayerRequests are
+written in the reference's trace format (tracegen.save_trace, byte-identical
+to the reference writer) together with the SHA-256 of the runtime's decision
+stream.  tests/test_live_fixture.py replays the trace through the UNMODIFIED
+reference run_trace (build container) and through the native decision core,
+and requires the same stream: decision parity on a live B200 run.
+
+    python tools/live_fixture.py
+"""
+from __future__ import annotations
+
+import json
+import sys
+import tempfile
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests" / "golden"))
+
+import paper_2504_05897_b200.core as mcore  # noqa: E402
+import paper_2504_05897_b200.costs as mcost  # noqa: E402
+import paper_2504_05897_b200.engine as me  # noqa: E402
+from paper_2504_05897_b200.moe import SHAPES, HybridMoE  # noqa: E402
+from paper_2504_05897_b200.tracegen import save_trace  # noqa: E402
+from stream import digest, from_records  # noqa: E402
+
+
+def run(policy_name: str, seed: int) -> dict:
+    cfg = SHAPES["tiny"]
+    eb = mcore.expert_bytes(cfg)
+    prof = mcost.HardwareProfile(gpu_time_per_expert=1.0, cpu_slope=2.0, transfer_bandwidth=eb / 0.5,
+                                 cpu_first_expert_penalty=1.4)
+    policy = me.EnginePolicy(cache_policy=policy_name, prefetch=False)
+    ratio = 0.5
+    moe = HybridMoE(cfg, "tiny", policy, ratio, prof, max_tokens=64)
+    moe.init_random_weights(seed)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    passes, recs = [], []
+    stages = [("prefill", 48)] + [("decode", 1)] * 12
+    for stage, T in stages:
+        x = torch.randn((T, moe.H), generator=g, device="cuda").to(torch.bfloat16)
+        _, info = moe.forward_pass(x, None, decision_log=True)  # model mode: logits = x . W_g per layer
+        torch.cuda.synchronize()
+        recs.extend(info["records"])
+        layers = tuple(mcore.make_layer_request(l, loads.tolist(), scores.tolist())
+                       for l, (loads, scores) in enumerate(info["requests"]))
+        passes.append(mcore.ForwardPass(stage, T, layers))
+    trace = mcore.Trace(cfg, tuple(passes), {"source": "live B200 run, model-mode routing"})
+    with tempfile.TemporaryDirectory() as d:
+        p = Path(d) / "t.jsonl"
+        save_trace(trace, p)
+        text = p.read_text()
+    return {"policy": policy_name, "prefetch": False, "ratio": ratio, "seed": 2,
+            "profile": {k: getattr(prof, k) for k in prof.__dataclass_fields__},
+            "trace_jsonl": text, "runtime_stream_sha256": digest(from_records(recs, policy_name == "mrs")),
+            "gpu": torch.cuda.get_device_name(0)}
+
+
+if __name__ == "__main__":
+    out = {p: run(p, 5 + i) for i, p in enumerate(("mrs", "lru", "lfu"))}
+    dst = ROOT / "gpurun_out" / "live_fixture.json"
+    dst.parent.mkdir(exist_ok=True)
+    dst.write_text(json.dumps(out))
+    print(dst, {k: v["runtime_stream_sha256"][:16] for k, v in out.items()})
