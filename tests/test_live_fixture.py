@@ -27,9 +27,9 @@ def test_live_run_replays_through_decision_core(policy, tmp_path):
     p.write_text(case["trace_jsonl"])
     trace = load_trace(p)
     assert trace.metadata.get("source", "").startswith("live B200 run")
-    m = me.run_trace(trace, me.EnginePolicy(cache_policy=policy, prefetch=case["prefetch"]), case["ratio"],
+    m = me.run_trace(trace, me.EnginePolicy(cache_policy=case["policy"], prefetch=case["prefetch"]), case["ratio"],
                      mcost.HardwareProfile(**case["profile"]), case["seed"], decision_log=True)
-    assert digest(from_records(m.decisions, policy == "mrs")) == case["runtime_stream_sha256"]
+    assert digest(from_records(m.decisions, case["policy"] == "mrs")) == case["runtime_stream_sha256"]
 
 
 @pytest.mark.reference
@@ -45,6 +45,6 @@ def test_live_run_replays_through_reference(policy, moesim, tmp_path):
     p.write_text(case["trace_jsonl"])
     trace = rtrace.load_trace(str(p))
     with mg.Recorder() as rec:
-        reng.run_trace(trace, reng.EnginePolicy(cache_policy=policy, prefetch=case["prefetch"]), case["ratio"],
+        reng.run_trace(trace, reng.EnginePolicy(cache_policy=case["policy"], prefetch=case["prefetch"]), case["ratio"],
                        rcost.HardwareProfile(**case["profile"]), case["seed"])
     assert digest(rec.stream) == case["runtime_stream_sha256"]

@@ -65,8 +65,54 @@ def run(policy_name: str, seed: int) -> dict:
             "gpu": torch.cuda.get_device_name(0)}
 
 
+def run_prefetch(seed: int) -> dict:
+    """Impact-driven prefetch on live routing: phase 1 runs the stack in model
+    mode and keeps every layer's GPU-computed logits; phase 2 (a fresh stack,
+    same weights) runs trace mode on exactly those logits with prefetch on and
+    the reference's prediction model fed with the phase-1 loads, so its
+    decisions must equal the reference replaying the recorded trace."""
+    from paper_2504_05897_b200.moe import TracePredictor
+    cfg = SHAPES["tiny"]
+    eb = mcore.expert_bytes(cfg)
+    prof = mcost.HardwareProfile(gpu_time_per_expert=1.0, cpu_slope=2.0, transfer_bandwidth=eb / 0.5,
+                                 cpu_first_expert_penalty=1.4)
+    stages = [("prefill", 48)] + [("decode", 1)] * 12
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    xs = [torch.randn((T, cfg.routed_expert_dims[0]), generator=g, device="cuda").to(torch.bfloat16)
+          for _, T in stages]
+    moe = HybridMoE(cfg, "tiny", me.EnginePolicy(), 0.5, prof, max_tokens=64)
+    moe.init_seeded_weights(seed)
+    passes, logits = [], []
+    for (stage, T), x in zip(stages, xs):
+        _, info = moe.forward_pass(x, None, decision_log=True, keep_layers=True)
+        torch.cuda.synchronize()
+        logits.append([lg.clone() for _, lg, _ in info["layers"]])
+        passes.append(mcore.ForwardPass(stage, T, tuple(mcore.make_layer_request(l, lo.tolist(), sc.tolist())
+                                                         for l, (lo, sc) in enumerate(info["requests"]))))
+    trace = mcore.Trace(cfg, tuple(passes), {"source": "live B200 run, model-mode routing"})
+    del moe
+    policy = me.EnginePolicy(cache_policy="mrs", prefetch=True)
+    moe2 = HybridMoE(cfg, "tiny", policy, 0.5, prof, max_tokens=64)
+    moe2.init_seeded_weights(seed)
+    recs, pseed = [], 2
+    for p, x in enumerate(xs):
+        _, info = moe2.forward_pass(x, logits[p], predict=TracePredictor(trace, p, pseed), decision_log=True)
+        torch.cuda.synchronize()
+        recs.extend(info["records"])
+        assert [list(lo) for lo, _ in info["requests"]] == [list(r.loads) for r in trace.passes[p].layers]
+    with tempfile.TemporaryDirectory() as d:
+        f = Path(d) / "t.jsonl"
+        save_trace(trace, f)
+        text = f.read_text()
+    return {"policy": "mrs", "prefetch": True, "ratio": 0.5, "seed": pseed,
+            "profile": {k: getattr(prof, k) for k in prof.__dataclass_fields__},
+            "trace_jsonl": text, "runtime_stream_sha256": digest(from_records(recs, True)),
+            "gpu": torch.cuda.get_device_name(0)}
+
+
 if __name__ == "__main__":
     out = {p: run(p, 5 + i) for i, p in enumerate(("mrs", "lru", "lfu"))}
+    out["mrs_prefetch"] = run_prefetch(9)
     dst = ROOT / "gpurun_out" / "live_fixture.json"
     dst.parent.mkdir(exist_ok=True)
     dst.write_text(json.dumps(out))
