@@ -75,6 +75,11 @@ __global__ void router_topk_kernel(const float *__restrict__ logits, int T, int 
         bi = oi;
       }
     }
+    if (bi >= N) {  // non-finite logits (NaN compares false): take the lowest free index, never write out of range
+      bi = 0;
+      while (bi < N && __shfl_sync(0xffffffffu, ((taken >> (bi >> 5)) & 1u), bi & 31)) ++bi;
+      bv = m;
+    }
     if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
     float p = expf(bv - m) * inv;
     psel[k] = p;
@@ -176,6 +181,11 @@ __global__ void __launch_bounds__(256) router_fused_small_kernel(
           bv = ov;
           bi = oi;
         }
+      }
+      if (bi >= N) {  // non-finite logits: lowest free index (as router_topk_kernel)
+        bi = 0;
+        while (bi < N && __shfl_sync(0xffffffffu, ((taken >> (bi >> 5)) & 1u), bi & 31)) ++bi;
+        bv = m;
       }
       if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
       const float p = expf(bv - m) * inv;

@@ -297,3 +297,19 @@ def test_expert_ffn_many_groups_and_empty_groups():
 @pytest.mark.parametrize("counts,path", [([1, 2, 4], _lib.FFN_GEMV), ([96, 33], _lib.FFN_GEMM)])
 def test_expert_ffn_deepseek_shape(counts, path):
     _ffn_case(2048, 1408, counts, path)
+
+
+def test_router_survives_non_finite_logits():
+    """NaN / inf logits (a diverged hidden state) never select an out-of-range
+    expert: every token still gets K distinct valid experts."""
+    T, N, Kk = 64, 64, 6
+    lg = torch.randn((T, N), device="cuda")
+    lg[3] = float("nan")
+    lg[5, :7] = float("nan")
+    lg[9, 10] = float("inf")
+    sel, w, probs, counts = K.router_topk(lg, N, Kk, False)
+    torch.cuda.synchronize()
+    s = sel.cpu().numpy()
+    assert ((s >= 0) & (s < N)).all()
+    assert all(len(set(r)) == Kk for r in s.tolist())
+    assert int(counts.sum()) == T * Kk

@@ -27,6 +27,7 @@ def test_live_run_replays_through_decision_core(policy, tmp_path):
     p.write_text(case["trace_jsonl"])
     trace = load_trace(p)
     assert trace.metadata.get("source", "").startswith("live B200 run")
+    assert trace.config.num_routed in (8, 64)
     m = me.run_trace(trace, me.EnginePolicy(cache_policy=case["policy"], prefetch=case["prefetch"]), case["ratio"],
                      mcost.HardwareProfile(**case["profile"]), case["seed"], decision_log=True)
     assert digest(from_records(m.decisions, case["policy"] == "mrs")) == case["runtime_stream_sha256"]

@@ -110,9 +110,52 @@ def run_prefetch(seed: int) -> dict:
             "gpu": torch.cuda.get_device_name(0)}
 
 
+def run_shape(shape: str, seed: int, ratio: float, n_decode: int, prefill: int) -> dict:
+    """A full-size shape (DeepSeek: 64 experts, top-6 + 2 shared) planned with
+    the profile the bench calibrated on a B200 box.  The logits come from the
+    reference's trace generator (the MoE-only stack has no normalisation, so a
+    26-layer model-mode residual stream diverges); the LayerRequests -- counts
+    and fp64 score sums -- are the GPU router's."""
+    from paper_2504_05897_b200.moe import with_shared_time
+    from paper_2504_05897_b200.tracegen import GenParams, generate_router_logits
+    cfg = SHAPES[shape]
+    base = json.loads((ROOT / "profiles" / "r01c_configs" / f"{shape}_25.json").read_text())["profile"]
+    prof = with_shared_time(mcost.HardwareProfile(**base), cfg)
+    policy = me.EnginePolicy(cache_policy="mrs", prefetch=False)
+    moe = HybridMoE(cfg, shape, policy, ratio, prof, max_tokens=prefill, host_images=64)
+    moe.init_random_weights(seed)
+    gen, logits = generate_router_logits(cfg, GenParams(seed=seed), prefill, n_decode)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    passes, recs = [], []
+    for p, fwd in enumerate(gen.passes):
+        lg = []
+        for l in range(cfg.num_layers):
+            a = logits[p][l].astype(np.float32)
+            if moe.family.shared_gate:
+                a = np.concatenate([a, np.zeros((a.shape[0], 1), np.float32)], axis=1)
+            lg.append(torch.from_numpy(np.ascontiguousarray(a)).cuda())
+        x = torch.randn((fwd.token_count, moe.H), generator=g, device="cuda").to(torch.bfloat16)
+        _, info = moe.forward_pass(x, lg, decision_log=True)
+        torch.cuda.synchronize()
+        recs.extend(info["records"])
+        passes.append(mcore.ForwardPass(fwd.stage, fwd.token_count,
+                                        tuple(mcore.make_layer_request(l, lo.tolist(), sc.tolist())
+                                              for l, (lo, sc) in enumerate(info["requests"]))))
+    trace = mcore.Trace(cfg, tuple(passes), {"source": "live B200 run, GPU router on generator logits"})
+    with tempfile.TemporaryDirectory() as d:
+        f = Path(d) / "t.jsonl"
+        save_trace(trace, f)
+        text = f.read_text()
+    return {"policy": "mrs", "prefetch": False, "ratio": ratio, "seed": 2,
+            "profile": {k: getattr(prof, k) for k in prof.__dataclass_fields__},
+            "trace_jsonl": text, "runtime_stream_sha256": digest(from_records(recs, True)),
+            "gpu": torch.cuda.get_device_name(0)}
+
+
 if __name__ == "__main__":
     out = {p: run(p, 5 + i) for i, p in enumerate(("mrs", "lru", "lfu"))}
     out["mrs_prefetch"] = run_prefetch(9)
+    out["deepseek_mrs"] = run_shape("deepseek", 11, 0.25, 6, 256)
     dst = ROOT / "gpurun_out" / "live_fixture.json"
     dst.parent.mkdir(exist_ok=True)
     dst.write_text(json.dumps(out))
