@@ -49,3 +49,38 @@ def test_live_run_replays_through_reference(policy, moesim, tmp_path):
         reng.run_trace(trace, reng.EnginePolicy(cache_policy=case["policy"], prefetch=case["prefetch"]), case["ratio"],
                        rcost.HardwareProfile(**case["profile"]), case["seed"])
     assert digest(rec.stream) == case["runtime_stream_sha256"]
+
+
+LIVE_EP = json.loads((Path(__file__).resolve().parent / "golden" / "live_ep.json").read_text())
+
+
+@pytest.mark.parametrize("rank", sorted(LIVE_EP))
+def test_live_ep_rank_replays_through_decision_core(rank, tmp_path):
+    """Per-rank parity on a live two-rank run: the rank's own
+    masked LayerRequests at its share of the global budget."""
+    case = LIVE_EP[rank]
+    p = tmp_path / "live.jsonl"
+    p.write_text(case["trace_jsonl"])
+    trace = load_trace(p)
+    m = me.run_trace(trace, me.EnginePolicy(cache_policy=case["policy"], prefetch=case["prefetch"]), case["ratio"],
+                     mcost.HardwareProfile(**case["profile"]), case["seed"], decision_log=True)
+    assert digest(from_records(m.decisions, True)) == case["runtime_stream_sha256"]
+
+
+@pytest.mark.reference
+@pytest.mark.parametrize("rank", sorted(LIVE_EP))
+def test_live_ep_rank_replays_through_reference(rank, moesim, tmp_path):
+    import make_golden as mg
+    import moesim.costs as rcost
+    import moesim.engine as reng
+    import moesim.tracegen as rtrace
+
+    case = LIVE_EP[rank]
+    p = tmp_path / "live.jsonl"
+    p.write_text(case["trace_jsonl"])
+    trace = rtrace.load_trace(str(p))
+    assert reng.cache_capacity(trace.config, case["ratio"]) == case["capacity"]
+    with mg.Recorder() as rec:
+        reng.run_trace(trace, reng.EnginePolicy(cache_policy=case["policy"], prefetch=case["prefetch"]), case["ratio"],
+                       rcost.HardwareProfile(**case["profile"]), case["seed"])
+    assert digest(rec.stream) == case["runtime_stream_sha256"]
