@@ -625,6 +625,15 @@ inline void q4_prep_x(const uint16_t *x, int K, Q4X &q) {
   q4_prep_groups(x, q, 0, K / 128);
 }
 
+// Software-prefetch distance of the 4-bit decode stream (HM_Q4_PF bytes, 0 = off).
+inline int q4_pf_dist() {
+  static const int d = [] {
+    const char *e = std::getenv("HM_Q4_PF");
+    return e ? std::atoi(e) : 16384;
+  }();
+  return d;
+}
+
 // Up to 4 tokens at once: each 128-group's 64 nibble bytes are split into
 // low / high nibble vectors once and multiplied with every token's digits
 // (4 vpdpbusd per token and group).  out[t * ldo + r].
@@ -645,6 +654,8 @@ inline void dot_rows_q4_mt(const uint8_t *nib, const uint16_t *sc, int n, int K,
       corr[t] = 0.f;
     }
     for (int g = 0; g < ng; ++g) {
+      // rows of a unit are contiguous: keep the stream q4_pf_dist() bytes ahead
+      _mm_prefetch(reinterpret_cast<const char *>(row + g * 64) + q4_pf_dist(), _MM_HINT_T1);
       const __m512i wb = _mm512_loadu_si512(row + g * 64);
       const __m512i lo = _mm512_and_si512(wb, m15);
       const __m512i hi = _mm512_and_si512(_mm512_srli_epi16(wb, 4), m15);
