@@ -312,8 +312,8 @@ def run_ours(args) -> None:
     from paper_2504_05897_b200.moe import TracePredictor
     predictors = [TracePredictor(trace, p, args.seed) for p in range(len(trace.passes))]
 
-    def predictor(p):  # the reference's prediction model on this pass, native
-        return predictors[p]
+    def predictor(p):  # the reference's prediction model on this pass, native -- or the live look-ahead
+        return "live" if args.predict == "live" else predictors[p]
 
     st = torch.cuda.current_stream()
     # ---- prefill: 1k tokens, cold cache (the reference's TTFT, engine.py:465-466)
@@ -474,7 +474,7 @@ def run_ours(args) -> None:
                        "shape": args.shape, "layers": cfg.num_layers, "experts": cfg.num_routed,
                        "top_k": cfg.num_activated, "hidden": H, "inter": I, "cache_slots": moe.capacity,
                        "host_images": moe.host_images, "policy": args.policy, "prefetch": args.prefetch,
-                       "scheduling": args.scheduling,
+                       "predict": args.predict, "scheduling": args.scheduling,
                        "l2": f"each step streams {cfg.num_layers * cfg.num_activated} expert evaluations x "
                              f"{image_bytes / 1e6:.1f} MB of weights (>> 126 MB L2); no flush needed",
                        "parallelism": f"ep{world}" if world > 1 else "single", "weight_bits": args.bits,
@@ -527,6 +527,9 @@ def main() -> None:
     ap.add_argument("--scheduling", default="hybrid",
                     choices=["hybrid", "static_layer_split", "fixed_frequency_map", "gpu_ondemand"])
     ap.add_argument("--prefetch", action="store_true")
+    ap.add_argument("--predict", default="trace", choices=["trace", "live"],
+                    help="prefetch predictions: the reference's trace-mode model, or the live gate look-ahead "
+                         "(future layers' gates on the current hidden state, one kernel per layer)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--host-images", type=int, default=None)
     ap.add_argument("--cpu-threads", type=int, default=0)

@@ -392,6 +392,13 @@ long long hm_launch_count(void);
  * fp64 with explicit round-to-nearest mul/add (bit-identical to the host core). */
 int hm_mrs_update_dev(double *S, const double *scores, int layer, int N, int p,
                       double alpha, void *stream);
+/* Live look-ahead prediction: for future layers
+ * first_layer .. first_layer+hz-1, the gate rows gate_w[layer][0..N) (bf16,
+ * [L][ld][H]) applied to the current hidden state x [T, H] and counted through
+ * the router's top-K rule -> counts [hz][N] int32 (device); host_counts (device
+ * view of mapped memory, int64 [hz][N], optional) receives a fenced copy. */
+int hm_lookahead(const uint16_t *x, const uint16_t *gate_w, int first_layer, int hz, int T, int N,
+                 int ld, int K, int H, int32_t *counts, int64_t *host_counts, void *stream);
 /* Hold `stream` until the host stores `seq` into *flag (device view of mapped
  * pinned memory): lets CUDA events time a group of kernels without the host's
  * launch latency in between (kernel-timing mode of the runtime). */
@@ -473,7 +480,11 @@ int hm_runtime_buffers(hm_runtime *rt, void **pool, void **host_store, size_t *s
 int hm_runtime_image_of(const hm_runtime *rt, int layer, int expert, int64_t *image);
 int hm_runtime_shared_slot(const hm_runtime *rt, int layer, int chunk, int64_t *slot);
 /* One MoE layer: y[T, H] = x + sum_k w E_k(x) for router logits [T, ld],
- * executing the decision core's plan for this layer (engine.py:288-389). */
+ * executing the decision core's plan for this layer (engine.py:288-389).
+ * Predictions for the prefetch decision: n_pred LayerRequests (pred_layers
+ * [n_pred], pred_loads [n_pred][N], host), or n_pred == HM_PREDICT_LIVE for
+ * the live look-ahead on x (hm_runtime_set_lookahead). */
+#define HM_PREDICT_LIVE (-1)
 int hm_runtime_forward_layer(hm_runtime *rt, int layer, const uint16_t *x, const float *logits,
                              int T, int ld, uint16_t *y, const int32_t *pred_layers,
                              const int64_t *pred_loads, int n_pred, void *stream,
@@ -481,7 +492,8 @@ int hm_runtime_forward_layer(hm_runtime *rt, int layer, const uint16_t *x, const
 /* A whole pass (all L layers, one call): begin_pass, forward_layer per layer
  * (ping-pong between buf0/buf1; *y_out receives the final buffer), end_pass.
  * logits: L device pointers [T, ld].  pass_loads (HOST, [L*N], optional):
- * the pass's loads for the trace-mode prediction model (hm_predict_layers).
+ * the pass's loads for the trace-mode prediction model (hm_predict_layers);
+ * without them (and prefetch on) the live look-ahead predicts, if set.
  * stats: optional [L] array.  Under expert parallelism it needs the peer-memory
  * exchange (hm_runtime_set_ep_exchange). */
 int hm_runtime_forward_pass(hm_runtime *rt, const uint16_t *x, const float *const *logits, int T,
@@ -544,6 +556,11 @@ int hm_ep_dispatch_rows(hm_ep *ep, const uint16_t *xp, const int32_t *sel, const
 int hm_ep_return_rows(hm_ep *ep, const float *out, int rows, void *stream);
 /* Device pointers of this rank's received-rows (bf16) and returned-rows (fp32) buffers. */
 int hm_ep_dispatch_buffers(hm_ep *ep, uint16_t **xrecv, float **ret);
+/* Live prediction: gate_w [L][ld][H] bf16
+ * (device; NULL disables) -- layer l's input through the gates of layers
+ * l+1..l+horizon gives the predicted loads of forward_layer(n_pred =
+ * HM_PREDICT_LIVE) and of forward_pass without pass_loads (prefetch on). */
+int hm_runtime_set_lookahead(hm_runtime *rt, const uint16_t *gate_w, int ld, int horizon);
 /* Run forward_layer token-sharded through `ep` (dispatch mode enabled): x and
  * logits hold this rank's tokens only (T may be 0). */
 int hm_runtime_set_ep_dispatch(hm_runtime *rt, hm_ep *ep);

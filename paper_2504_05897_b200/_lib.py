@@ -18,6 +18,7 @@ from .errors import CalibrationError, EvictionError, PlanInvariantError
 _LIB_PATH = Path(__file__).resolve().parent / "libhybrimoe.so"
 
 HM_OK, HM_EVALUE, HM_EEVICTION, HM_EPLAN, HM_ERUNTIME, HM_ECALIBRATION, HM_EASSERT, HM_ECUDA = range(8)
+HM_PREDICT_LIVE = -1  # forward_layer n_pred: the runtime's live look-ahead predicts
 DEV_CPU, DEV_GPU, DEV_PCIE = 0, 1, 2
 KIND_COMPUTE, KIND_TRANSFER = 0, 1
 ASSIGN_CPU, ASSIGN_GPU_CACHED, ASSIGN_GPU_TRANSFER = 0, 1, 2
@@ -347,6 +348,8 @@ for _name, (_args, _res) in {
     "hm_ep_enable_dispatch": ([vp, C.c_int, C.c_int, C.c_int, C.c_char_p], C.c_int),
     "hm_ep_open_peer_dispatch": ([vp, C.c_int, C.c_char_p], C.c_int),
     "hm_runtime_set_ep_dispatch": ([vp, vp], C.c_int),
+    "hm_runtime_set_lookahead": ([vp, vp, C.c_int, C.c_int], C.c_int),
+    "hm_lookahead": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp], C.c_int),
 }.items():
     _f = getattr(lib, _name)
     _f.argtypes = _args

@@ -541,6 +541,74 @@ __global__ void __launch_bounds__(kTailThreads) combine_tail_kernel(const __grid
   *reinterpret_cast<uint2 *>(c.y + static_cast<size_t>(t) * c.H + col) = o2;
 }
 
+// Live look-ahead prediction (N9): the gates of layers l+1..l+hz
+// applied to the CURRENT hidden state x [T, H]; per future layer the top-K of
+// each token's logits (value desc, index asc, like router_topk_kernel) are
+// counted into counts[f][N] (the predicted loads).  One block per (future
+// layer, token); warps split the N dot products, summed in router_logits_kernel's
+// order, so the logits -- and the selection -- are bit-identical to
+// router_logits + router_topk on the same gate.
+__global__ void __launch_bounds__(256) lookahead_kernel(const uint16_t *__restrict__ x,
+                                                        const uint16_t *__restrict__ gate_w, int first_layer,
+                                                        int hz, int T, int N, int ld, int K, int H,
+                                                        int32_t *__restrict__ counts) {
+  __shared__ float s_lg[256];
+  const int f = blockIdx.x / max(T, 1), t = blockIdx.x % max(T, 1);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint16_t *xr = x + static_cast<size_t>(t) * H;
+  const uint16_t *wl = gate_w + static_cast<size_t>(first_layer + f) * ld * H;
+  for (int e = wid; e < N; e += nw) {
+    const uint16_t *wr = wl + static_cast<size_t>(e) * H;
+    float acc = 0.f;
+    for (int c = lane * 8; c < H; c += 256)
+      acc += dev::dot8(*reinterpret_cast<const uint4 *>(wr + c), *reinterpret_cast<const uint4 *>(xr + c));
+    acc = dev::warp_sum(acc);
+    if (lane == 0) s_lg[e] = acc;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    float v[kMaxPerLane];
+#pragma unroll
+    for (int j = 0; j < kMaxPerLane; ++j) {
+      const int e = lane + 32 * j;
+      v[j] = e < N ? s_lg[e] : -FLT_MAX;
+    }
+    uint32_t taken = 0;
+    for (int k = 0; k < K; ++k) {
+      float bv = -FLT_MAX;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int j = 0; j < kMaxPerLane; ++j) {
+        const int e = lane + 32 * j;
+        if (e < N && !((taken >> j) & 1u) && (v[j] > bv || (v[j] == bv && e < bi))) {
+          bv = v[j];
+          bi = e;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (bi >= N) {  // non-finite logits: lowest free index
+        bi = 0;
+        while (bi < N && __shfl_sync(0xffffffffu, ((taken >> (bi >> 5)) & 1u), bi & 31)) ++bi;
+      }
+      if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+      if (lane == 0) atomicAdd(&counts[f * N + bi], 1);
+    }
+  }
+}
+
+__global__ void lookahead_publish_kernel(const int32_t *__restrict__ counts, int n, int64_t *host_counts) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) host_counts[i] = counts[i];
+  __threadfence_system();
+}
+
 // One thread spins until the host writes `seq` into a mapped flag: holds the
 // stream while the host enqueues the kernels to be timed, so the CUDA events
 // around them measure GPU time, not host launch latency (bench roofline).
@@ -756,6 +824,25 @@ int hm_combine_tail(const float *out, const float *host_out, const uint64_t *hos
   const long blocks = static_cast<long>(T) * cs + (S ? 1 : 0);
   if (blocks > 0) {
     hm::combine_tail_kernel<<<static_cast<unsigned>(blocks), hm::kTailThreads, 0, static_cast<cudaStream_t>(stream)>>>(c);
+    HM_LAUNCH_CHECK();
+  }
+  HM_API_END
+}
+
+int hm_lookahead(const uint16_t *x, const uint16_t *gate_w, int first_layer, int hz, int T, int N, int ld, int K,
+                 int H, int32_t *counts, int64_t *host_counts, void *stream) {
+  HM_API_BEGIN
+  HM_REQUIRE(N >= 1 && N <= 256 && K >= 1 && K <= N && ld >= N && H % 8 == 0 && hz >= 0 && T >= 0, HM_EVALUE,
+             "look-ahead shape out of range");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (hz == 0) return HM_OK;
+  HM_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * hz * N, st));
+  if (T > 0) {
+    hm::lookahead_kernel<<<hz * T, 256, 0, st>>>(x, gate_w, first_layer, hz, T, N, ld, K, H, counts);
+    HM_LAUNCH_CHECK();
+  }
+  if (host_counts) {
+    hm::lookahead_publish_kernel<<<1, 256, 0, st>>>(counts, hz * N, host_counts);
     HM_LAUNCH_CHECK();
   }
   HM_API_END

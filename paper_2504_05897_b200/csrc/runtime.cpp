@@ -39,6 +39,7 @@ int hm_predict_layers(const int64_t *, int, int, int64_t, int, int64_t, int, dou
 int hm_router_fused_small(const float *, int, int, int, int, int, int, int, const uint16_t *, int, int32_t *,
                           float *, int32_t *, int32_t *, uint16_t *, int32_t *, double *, void *);
 int hm_combine_f32(const float *, const int32_t *, const float *, int, int, int, float *, void *);
+int hm_lookahead(const uint16_t *, const uint16_t *, int, int, int, int, int, int, int, int32_t *, int64_t *, void *);
 int hm_router_fused_mirror(const float *, int, int, int, int, int, int, int, const uint16_t *, int, int32_t *, float *,
                            int32_t *, int32_t *, uint16_t *, int32_t *, double *, int32_t *, double *, uint16_t *,
                            uint32_t *, uint32_t, void *);
@@ -134,6 +135,14 @@ struct Runtime {
   float *dv_h_out = nullptr;
   uint32_t *h_flag = nullptr, *dv_flag = nullptr;
   uint32_t seq = 0, gate_seq = 0;  // h_flag[0]: router flag; h_flag[8]: kernel-timing gate
+  // live look-ahead prediction (hm_runtime_set_lookahead): gates [L][la_ld][H]
+  // of the model, applied to each layer's input for layers l+1..l+la_hz; the
+  // predicted loads land in pinned memory (mapped: written by the kernel)
+  const uint16_t *la_gate = nullptr;
+  int la_ld = 0, la_hz = 0;
+  int32_t *la_counts = nullptr;
+  int64_t *la_host = nullptr, *la_dv = nullptr;
+  std::vector<int32_t> la_layers;
   std::unique_ptr<ThreadPool> workers;
   std::vector<uint16_t> hbuf;
   std::vector<int64_t> loads;
@@ -298,6 +307,8 @@ struct Runtime {
     if (lcounts) cudaFree(lcounts);
     if (q4_scratch) cudaFree(q4_scratch);
     if (lsums) cudaFree(lsums);
+    if (la_counts) cudaFree(la_counts);
+    if (la_host) cudaFreeHost(la_host);
     for (void *p : {static_cast<void *>(pool), static_cast<void *>(sel), static_cast<void *>(w),
                     static_cast<void *>(probs), dmeta, static_cast<void *>(pos), static_cast<void *>(row_src),
                     static_cast<void *>(xp), static_cast<void *>(h), static_cast<void *>(out),
@@ -396,6 +407,21 @@ struct Runtime {
     // rows) into mapped host memory and raises a flag the host spins on
     const bool mirror = fused && zero_copy;
     const bool mirror_rows = mirror && static_cast<size_t>(T) * K * H * 2 <= (512u << 10);
+    // live prediction: launched ahead of the router so the predicted loads are
+    // on the host when the LayerRequest is (same flag / same event)
+    if (n_pred == HM_PREDICT_LIVE) {
+      HM_REQUIRE(la_gate != nullptr, HM_EVALUE, "live prediction needs hm_runtime_set_lookahead");
+      HM_REQUIRE(!disp, HM_EVALUE, "live prediction is not available in token-sharded dispatch mode");
+      n_pred = std::max(0, std::min(layer + la_hz, L - 1) - layer);
+      if (n_pred > 0) {
+        // the publish kernel stores the int64 loads into mapped memory: stream
+        // order puts it before the router's flag / event
+        ok(hm_lookahead(x, la_gate, layer + 1, n_pred, T, N, la_ld, K, H, la_counts, la_dv, vs));
+      }
+      for (int d = 0; d < n_pred; ++d) la_layers[d] = layer + 1 + d;
+      pred_layers = la_layers.data();
+      pred_loads = la_host;
+    }
     if (mirror) {
       ++seq;
       ok(hm_router_fused_mirror(logits, T, N, ld, K, cfg.renormalize, S, cfg.shared_gate_col, x, H, sel, w, pos,
@@ -659,12 +685,13 @@ int hm_runtime_forward_pass(hm_runtime *rt, const uint16_t *x, const float *cons
   HM_REQUIRE(r->W == 1 || r->ep, HM_EVALUE,
              "expert-parallel passes need the peer-memory exchange (hm_runtime_set_ep_exchange) or forward_layer");
   const bool predicting = pass_loads != nullptr && r->engine->cfg.prefetch;
+  const bool live = pass_loads == nullptr && r->engine->cfg.prefetch && r->la_gate != nullptr;
   std::vector<int32_t> pl(static_cast<size_t>(horizon > 0 ? horizon : 1));
   std::vector<int64_t> pload(static_cast<size_t>(horizon > 0 ? horizon : 1) * r->N);
   r->engine->begin_pass();
   const uint16_t *cur = x;
   for (int l = 0; l < r->L; ++l) {
-    int n_pred = 0;
+    int n_pred = live ? HM_PREDICT_LIVE : 0;
     if (predicting) {
       const int rc = hm_predict_layers(pass_loads, r->L, r->N, pass_index, l, seed, horizon, accuracy, pl.data(),
                                        pload.data(), &n_pred);
@@ -715,6 +742,29 @@ int hm_runtime_preload(hm_runtime *rt, const uint32_t *refs, int n) {
 int hm_runtime_set_ep_output(hm_runtime *rt, float *y32) {
   HM_API_BEGIN
   reinterpret_cast<hm::Runtime *>(rt)->y32 = y32;
+  HM_API_END
+}
+
+int hm_runtime_set_lookahead(hm_runtime *rt, const uint16_t *gate_w, int ld, int horizon) {
+  HM_API_BEGIN
+  auto *r = reinterpret_cast<hm::Runtime *>(rt);
+  HM_REQUIRE(gate_w == nullptr || (ld >= r->N && horizon >= 0 && r->H % 8 == 0 && r->N <= 256), HM_EVALUE,
+             "look-ahead gate shape out of range");
+  RT_CUDA(cudaDeviceSynchronize());
+  if (r->la_counts) cudaFree(r->la_counts);
+  if (r->la_host) cudaFreeHost(r->la_host);
+  r->la_counts = nullptr;
+  r->la_host = r->la_dv = nullptr;
+  r->la_gate = gate_w;
+  r->la_ld = ld;
+  r->la_hz = gate_w ? horizon : 0;
+  const size_t n = static_cast<size_t>(std::max(1, r->la_hz)) * r->N;
+  if (gate_w) {
+    RT_CUDA(cudaMalloc(&r->la_counts, n * 4));
+    RT_CUDA(cudaHostAlloc(&r->la_host, n * 8, cudaHostAllocMapped));
+    RT_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&r->la_dv), r->la_host, 0));
+    r->la_layers.assign(std::max(1, r->la_hz), 0);
+  }
   HM_API_END
 }
 

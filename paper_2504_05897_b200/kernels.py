@@ -59,6 +59,17 @@ def router_logits(x: torch.Tensor, wg: torch.Tensor, stream=None) -> torch.Tenso
     return out
 
 
+def lookahead(x: torch.Tensor, gate_w: torch.Tensor, first_layer: int, horizon: int, n_routed: int, k: int,
+              stream=None) -> torch.Tensor:
+    """Predicted loads [horizon, N] int32 of layers first_layer.. for hidden state
+    x: the gates gate_w [L, ld, H] through the router's top-K (hm_lookahead)."""
+    T, H = x.shape
+    counts = torch.empty((max(1, horizon), n_routed), dtype=torch.int32, device=x.device)
+    check(lib.hm_lookahead(_p(x), _p(gate_w), first_layer, horizon, T, n_routed, gate_w.shape[1], k, H, _p(counts),
+                           None, _stream(stream)))
+    return counts[:horizon]
+
+
 def offsets(counts: torch.Tensor, stream=None) -> torch.Tensor:
     E = counts.shape[0]
     out = torch.empty((E + 1,), dtype=torch.int32, device=counts.device)

@@ -324,8 +324,11 @@ class HybridMoE:
             raise ValueError(f"T={T} exceeds max_tokens={self.max_tokens}")
         st = stream if stream is not None else torch.cuda.current_stream()
         a, b = self._ping_pong(T)
+        live = predict == "live" and self.policy.prefetch
+        if live:
+            self._set_lookahead()
         if ((self.ep_world == 1 or self._ep is not None) and logits is not None and not decision_log and not keep_layers
-                and (predict is None or isinstance(predict, TracePredictor) or not self.policy.prefetch)):
+                and (predict is None or isinstance(predict, TracePredictor) or live or not self.policy.prefetch)):
             return self._forward_pass_native(x, logits, predict, a, b, st)
         cur = x
         stats, records, layers_io, requests = [], [], [], []
@@ -346,10 +349,12 @@ class HybridMoE:
                                             float(self.policy.prediction.accuracy), _lib.ptr(pl, C.c_int32),
                                             _lib.ptr(pload, C.c_int64), C.byref(npred)))
                 pl = pl[: npred.value]
+            elif live:  # native look-ahead, launched ahead of this layer's router
+                pl, pload = np.zeros(1, np.int32), np.zeros((1, self.N), np.int64)
             else:
                 if not self.policy.prefetch:
                     preds = []
-                elif predict == "live":  # gate look-ahead on the current hidden state
+                elif predict == "live_py":  # the same look-ahead through the Python kernels (checker)
                     preds = self.lookahead(cur, l, stream=st)
                 else:
                     preds = predict(l) if predict is not None else []
@@ -361,7 +366,8 @@ class HybridMoE:
             out = a if (l % 2 == 0) else b
             check(lib.hm_runtime_forward_layer(self._rt, l, cur.data_ptr(), lg.data_ptr(), T, lg.shape[1],
                                                out.data_ptr(), _lib.ptr(pl, C.c_int32), _lib.ptr(pload, C.c_int64),
-                                               len(pl), st.cuda_stream, C.byref(ls)))
+                                               _lib.HM_PREDICT_LIVE if live else len(pl), st.cuda_stream,
+                                               C.byref(ls)))
             if self.ep_world > 1 and self._ep is None:  # all-reduce the ranks' partials, then the residual
                 import torch.distributed as dist
                 part = self.y32[:T]
@@ -396,6 +402,8 @@ class HybridMoE:
         res = _lib.PassResult()
         yp = C.c_void_p()
         pl = predict if isinstance(predict, TracePredictor) and self.policy.prefetch else None
+        if pl is None and predict != "live":
+            self._set_lookahead(off=True)
         check(lib.hm_runtime_forward_pass(
             self._rt, x.data_ptr(), lgp, T, logits[0].shape[1], a.data_ptr(), b.data_ptr(),
             _lib.ptr(pl.pass_loads, C.c_int64) if pl is not None else None, pl.pass_index if pl else 0,
@@ -403,6 +411,15 @@ class HybridMoE:
             st.cuda_stream, stats, C.byref(res), C.byref(yp)))
         y = a if yp.value == a.data_ptr() else b
         return y, {"stats_raw": stats, "records": [], "requests": [], "layers": [], "pass": res}
+
+    def _set_lookahead(self, off: bool = False) -> None:
+        """Point the runtime's live predictor at the gate weights (or detach it)."""
+        want = None if off or self.gate_w is None else (self.gate_w.data_ptr(), self.policy.prediction.horizon)
+        if want is None and not off:
+            raise RuntimeError("live prediction needs gate weights (init_random_weights)")
+        if getattr(self, "_la", None) != want:
+            check(lib.hm_runtime_set_lookahead(self._rt, want[0] if want else None, self.ld, want[1] if want else 0))
+            self._la = want
 
     def lookahead(self, x: torch.Tensor, layer: int, horizon: int | None = None, stream=None):
         """Live-mode prediction: the gates of layers

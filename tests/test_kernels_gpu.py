@@ -299,6 +299,23 @@ def test_expert_ffn_deepseek_shape(counts, path):
     _ffn_case(2048, 1408, counts, path)
 
 
+@pytest.mark.parametrize("T,N,ld,Kk,H", [(1, 8, 8, 2, 256), (7, 64, 64, 6, 2048), (32, 64, 65, 4, 3584),
+                                          (3, 256, 256, 8, 512)])
+def test_lookahead_equals_router_on_future_gates(T, N, ld, Kk, H):
+    """hm_lookahead == router_logits + router_topk counts, per future layer
+    (bit-exact: same dot-product order, same tie-break)."""
+    from paper_2504_05897_b200.kernels import lookahead, router_logits
+    L = 5
+    g = torch.Generator(device="cuda").manual_seed(T * 7 + N)
+    gate = (torch.randn((L, ld, H), generator=g, device="cuda") / H ** 0.5).to(torch.bfloat16)
+    x = torch.randn((T, H), generator=g, device="cuda").to(torch.bfloat16)
+    got = lookahead(x, gate, 1, 3, N, Kk)
+    for f in range(3):
+        _, _, _, c = K.router_topk(router_logits(x, gate[1 + f]), N, Kk, True)
+        assert torch.equal(got[f].cpu(), c.cpu()), f
+    assert int(got.sum()) == 3 * T * Kk
+
+
 def test_router_survives_non_finite_logits():
     """NaN / inf logits (a diverged hidden state) never select an out-of-range
     expert: every token still gets K distinct valid experts."""

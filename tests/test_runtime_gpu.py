@@ -134,6 +134,52 @@ def test_live_lookahead_prefetch_model_mode():
     assert torch.isfinite(x.float()).all()
 
 
+@pytest.mark.parametrize("zero_copy", ["1", "0"])
+def test_native_live_lookahead_matches_python_lookahead(monkeypatch, zero_copy):
+    """The runtime's live predictor (one look-ahead kernel ahead of the router,
+    loads published with the LayerRequest) makes the same decisions as the
+    Python look-ahead (router_logits + router_topk per future layer): model
+    mode per layer, and the one-call native pass in trace mode."""
+    monkeypatch.setenv("HM_ZERO_COPY", zero_copy)
+    cfg = SHAPES["tiny"]
+    prof = stress_profile(cfg)
+    policy = me.EnginePolicy(prefetch=True)
+    trace, logits = generate_router_logits(cfg, GenParams(seed=8), 24, 4)
+    runs = {}
+    for mode in ("live_py", "live", "live_native_pass"):
+        moe = HybridMoE(cfg, "tiny", policy, 0.5, prof, max_tokens=64)
+        moe.init_seeded_weights(6)
+        g = torch.Generator(device="cuda").manual_seed(2)
+        recs, ys, res = [], [], []
+        for p, fwd in enumerate(trace.passes):  # model mode: logits from each layer's live input
+            x = torch.randn((fwd.token_count, moe.H), generator=g, device="cuda").to(torch.bfloat16)
+            y, info = moe.forward_pass(x, None, predict=mode.replace("_native_pass", ""), decision_log=True)
+            recs.extend(info["records"])
+            ys.append(y.float().cpu().numpy())
+            r = info["pass"]
+            res.append((r.latency, r.lookups, r.hits, r.inserts, r.evictions, r.prefetch_issued))
+        g = torch.Generator(device="cuda").manual_seed(3)
+        for p, fwd in enumerate(trace.passes):  # trace mode, per layer vs one native call
+            lg = [torch.from_numpy(np.ascontiguousarray(logits[p][l], dtype=np.float32)).cuda()
+                  for l in range(cfg.num_layers)]
+            x = torch.randn((fwd.token_count, moe.H), generator=g, device="cuda").to(torch.bfloat16)
+            pred = "live" if mode == "live_native_pass" else mode
+            y, info = moe.forward_pass(x, lg, predict=pred, decision_log=mode != "live_native_pass")
+            torch.cuda.synchronize()
+            ys.append(y.float().cpu().numpy())
+            r = info["pass"]
+            res.append((r.latency, r.lookups, r.hits, r.inserts, r.evictions, r.prefetch_issued))
+        runs[mode] = (digest(from_records(recs, True)), ys, res)
+    assert runs["live_py"][0] == runs["live"][0] == runs["live_native_pass"][0]
+    assert runs["live_py"][2] == runs["live"][2]
+    assert runs["live_py"][2] == runs["live_native_pass"][2]
+    assert sum(r[-1] for r in runs["live"][2]) > 0  # the predictions drove prefetches
+    for a, b in zip(runs["live_py"][1], runs["live"][1]):
+        assert np.array_equal(a, b)
+    for a, b in zip(runs["live_py"][1], runs["live_native_pass"][1]):
+        assert np.array_equal(a, b)
+
+
 def test_native_trace_predictor_matches_python_predictor():
     """forward_pass with the native prediction model makes the same decisions
     as with the Python (numpy) prediction model."""
