@@ -78,8 +78,8 @@ def _run(rank: int, world: int, port: int, q, exchange: str = "p2p") -> None:
             dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("exchange", ["p2p", "allreduce"])
-def test_two_ranks_equal_one_rank(exchange):
+@pytest.mark.parametrize("exchange,world", [("p2p", 2), ("allreduce", 2), ("p2p", 4)])
+def test_ranks_equal_one_rank(exchange, world):
     ctx = torch.multiprocessing.get_context("spawn")
     q = ctx.Queue()
     single = ctx.Process(target=_run, args=(0, 1, 0, q))
@@ -87,27 +87,27 @@ def test_two_ranks_equal_one_rank(exchange):
     ref = q.get(timeout=300)  # drain the queue before joining (large items block the child's exit)
     single.join(timeout=60)
     port = _free_port()
-    procs = [ctx.Process(target=_run, args=(r, 2, port, q, exchange)) for r in range(2)]
+    procs = [ctx.Process(target=_run, args=(r, world, port, q, exchange)) for r in range(world)]
     for p in procs:
         p.start()
-    got = dict((r[0], r) for r in (q.get(timeout=300), q.get(timeout=300)))
+    got = dict((r[0], r) for r in (q.get(timeout=300) for _ in range(world)))
     for p in procs:
         p.join(timeout=60)
     assert single.exitcode == 0 and all(p.exitcode == 0 for p in procs)
     _, _, ref_outs, ref_loads, ref_cap, _ = ref
-    assert got[0][4] + got[1][4] == ref_cap                      # global budget split across ranks
-    for r in (0, 1):
+    assert sum(got[r][4] for r in range(world)) == ref_cap      # global budget split across ranks
+    for r in range(world):
         for p, (o_ref, o) in enumerate(zip(ref_outs, got[r][2])):
             err = np.abs(o - o_ref).max() / np.abs(o_ref).max()
             assert err <= 1e-2, (r, p, err)
         for o, o_py in zip(got[r][5], got[r][2]):  # native pass == per-layer pass, bit for bit
             assert np.array_equal(o, o_py)
-        if exchange == "p2p":  # the fused exchange sums in rank order: both ranks hold identical y
-            for a, b in zip(got[0][2], got[1][2]):
+        if exchange == "p2p":  # the fused exchange sums in rank order: every rank holds identical y
+            for a, b in zip(got[0][2], got[r][2]):
                 assert np.array_equal(a, b)
         for p in range(len(ref_loads)):
             for l, full in enumerate(ref_loads[p]):
-                masked = [v if e % 2 == r else 0 for e, v in enumerate(full)]
+                masked = [v if e % world == r else 0 for e, v in enumerate(full)]
                 assert got[r][3][p][l] == masked
 
 
@@ -158,7 +158,8 @@ def _run_dispatch(rank: int, world: int, port: int, q) -> None:
         dist.destroy_process_group()
 
 
-def test_token_sharded_dispatch_equals_one_rank():
+@pytest.mark.parametrize("world", [2, 4])
+def test_token_sharded_dispatch_equals_one_rank(world):
     ctx = torch.multiprocessing.get_context("spawn")
     q = ctx.Queue()
     single = ctx.Process(target=_run, args=(0, 1, 0, q))
@@ -166,15 +167,15 @@ def test_token_sharded_dispatch_equals_one_rank():
     ref = q.get(timeout=300)
     single.join(timeout=60)
     port = _free_port()
-    procs = [ctx.Process(target=_run_dispatch, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_run_dispatch, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got = dict(q.get(timeout=300) for _ in range(2))
+    got = dict(q.get(timeout=300) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
     assert single.exitcode == 0 and all(p.exitcode == 0 for p in procs)
     _, _, ref_outs, ref_loads, _, _ = ref
-    for r in (0, 1):
+    for r in range(world):
         outs, loads = got[r][False]
         n_outs, _ = got[r][True]
         for p, ((a, b, o), (_, _, o_nat)) in enumerate(zip(outs, n_outs)):
@@ -187,7 +188,7 @@ def test_token_sharded_dispatch_equals_one_rank():
                 assert o.shape[0] == 0
         for p in range(len(ref_loads)):                          # global, rank-masked LayerRequests
             for l, full in enumerate(ref_loads[p]):
-                assert loads[p][l] == [v if e % 2 == r else 0 for e, v in enumerate(full)]
+                assert loads[p][l] == [v if e % world == r else 0 for e, v in enumerate(full)]
 
 
 def _run_dispatch_shared(rank: int, world: int, port: int, q) -> None:
