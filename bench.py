@@ -460,7 +460,7 @@ def run_ours(args) -> None:
 
     # ---- CPU baseline: the oracle port on this host, bounded sample
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # rank 0 at N=1 only
         per_tok, sample = cpu_oracle_decode(args.shape, args.ref_layers)
         cpu = {"value": 1.0 / per_tok, "unit": "tok/s", "cores": os.cpu_count(), "kind": "port", "sample": sample}
 

@@ -61,7 +61,8 @@ def expert(x: np.ndarray, gate: np.ndarray, up: np.ndarray, down: np.ndarray) ->
     """SwiGLU expert in fp32: x [M, H], gate/up [I, H], down [H, I] (fp32 arrays)."""
     g = x @ gate.T
     u = x @ up.T
-    h = g / (1.0 + np.exp(-g)) * u
+    with np.errstate(over="ignore"):  # exp(-g) -> inf for very negative g: silu -> -0, as intended
+        h = g / (1.0 + np.exp(-g)) * u
     return h @ down.T
 
 
