@@ -102,28 +102,39 @@ void check_plan(const Plan &plan) {
       if (evs[i + 1]->start < evs[i]->end)
         raise(HM_EPLAN, "overlap on device: " + ev_str(*evs[i]) + " vs " + ev_str(*evs[i + 1]));
   }
-  std::unordered_map<uint32_t, const Event *> computed;
-  for (const Event &ev : plan.events) {
-    if (ev.kind != HM_KIND_COMPUTE) continue;
-    if (computed.count(ev.ref)) raise(HM_EPLAN, "expert computed twice: " + ref_str(ev.ref));
-    computed[ev.ref] = &ev;
-  }
-  std::unordered_set<uint32_t> assigned;
-  for (auto &a : plan.assign) assigned.insert(a.first);
-  bool same = assigned.size() == computed.size();
-  if (same)
-    for (auto &kv : computed)
-      if (!assigned.count(kv.first)) same = false;
-  if (!same) raise(HM_EPLAN, "assignment and compute events cover different experts");
-  std::unordered_map<uint32_t, double> transfer_end;
+  // the per-layer plans are small (tens of experts): sorted vectors instead of
+  // hash containers keep this check off the allocator on the decision path
+  std::vector<std::pair<uint32_t, const Event *>> computed;
+  computed.reserve(plan.events.size());
   for (const Event &ev : plan.events)
-    if (ev.kind == HM_KIND_TRANSFER) transfer_end[ev.ref] = ev.end;
+    if (ev.kind == HM_KIND_COMPUTE) computed.emplace_back(ev.ref, &ev);
+  std::stable_sort(computed.begin(), computed.end(),
+                   [](const std::pair<uint32_t, const Event *> &a, const std::pair<uint32_t, const Event *> &b) {
+                     return a.first < b.first;
+                   });
+  for (size_t i = 0; i + 1 < computed.size(); ++i)
+    if (computed[i].first == computed[i + 1].first)
+      raise(HM_EPLAN, "expert computed twice: " + ref_str(computed[i].first));
+  std::vector<uint32_t> assigned;
+  assigned.reserve(plan.assign.size());
+  for (auto &a : plan.assign) assigned.push_back(a.first);
+  std::sort(assigned.begin(), assigned.end());
+  assigned.erase(std::unique(assigned.begin(), assigned.end()), assigned.end());
+  bool same = assigned.size() == computed.size();
+  for (size_t i = 0; same && i < assigned.size(); ++i) same = assigned[i] == computed[i].first;
+  if (!same) raise(HM_EPLAN, "assignment and compute events cover different experts");
+  auto compute_of = [&](uint32_t r) {
+    auto it = std::lower_bound(computed.begin(), computed.end(), r,
+                               [](const std::pair<uint32_t, const Event *> &a, uint32_t v) { return a.first < v; });
+    return it->second;
+  };
   for (auto &a : plan.assign) {
     if (a.second != HM_ASSIGN_GPU_TRANSFER) continue;
-    auto it = transfer_end.find(a.first);
-    if (it == transfer_end.end())
-      raise(HM_EPLAN, ref_str(a.first) + " marked gpu_after_transfer but has no transfer");
-    if (computed[a.first]->start < it->second)
+    const Event *tr = nullptr;  // the last transfer event of the expert (dict overwrite order)
+    for (const Event &ev : plan.events)
+      if (ev.kind == HM_KIND_TRANSFER && ev.ref == a.first) tr = &ev;
+    if (!tr) raise(HM_EPLAN, ref_str(a.first) + " marked gpu_after_transfer but has no transfer");
+    if (compute_of(a.first)->start < tr->end)
       raise(HM_EPLAN, ref_str(a.first) + " computed before its transfer ends");
   }
   if (!plan.events.empty()) {
@@ -463,14 +474,17 @@ double Evaluator::makespan(std::vector<int64_t> c, std::vector<int64_t> u) {
 // -------------------------------------------------------------- caching.py
 std::vector<double> top_p_filter(const double *s, int n, int p) {
   // caching.py:58-62: keep the p largest by (-score, index)
+  // (-score, index) is a total order, so partial selection of the first p
+  // gives exactly the stable sort's prefix
   std::vector<int> order(n);
   for (int i = 0; i < n; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+  const int keep = std::min(n, std::max(p, 0));
+  std::partial_sort(order.begin(), order.begin() + keep, order.end(), [&](int a, int b) {
     if (s[a] != s[b]) return s[a] > s[b];
     return a < b;
   });
   std::vector<double> out(n, 0.0);
-  for (int k = 0; k < n && k < p; ++k) out[order[k]] = s[order[k]];
+  for (int k = 0; k < keep; ++k) out[order[k]] = s[order[k]];
   return out;
 }
 
