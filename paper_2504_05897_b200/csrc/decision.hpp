@@ -59,6 +59,7 @@ struct Evaluator {
   hm_profile profile;
   double expert_bytes;
   std::unordered_map<std::string, double> memo;
+  std::string kbuf;  // reused lookup key (no allocation on a memo hit)
   double makespan(std::vector<int64_t> cached, std::vector<int64_t> uncached);
 };
 
