@@ -309,7 +309,8 @@ int hm_router_fused_small(const float *logits, int T, int N, int ld, int K, int 
                           double *meta_d, void *stream);
 /* hm_router_fused_small plus a mirror in mapped pinned host memory (device
  * views of cudaHostAlloc(..., cudaHostAllocMapped) buffers): the meta block,
- * optionally the routed rows of xp (host_xp may be NULL), then *host_flag =
+ * optionally the routed rows of xp (host_xp may be NULL; with T == 1 only row
+ * 0 -- every routed row is that token), then *host_flag =
  * seq after a system-scope fence -- the host spins on the flag instead of a
  * D2H copy + event wait (the LayerRequest hand-off of engine.py:288-306). */
 int hm_router_fused_mirror(const float *logits, int T, int N, int ld, int K, int renormalize,

@@ -121,6 +121,9 @@ struct HostMirror {
 constexpr int kFusedMaxRows = 1024;
 constexpr int kFusedMaxE = 320;
 
+// PL = experts per lane, ceil(N / 32) rounded up to a power of two: the top-K
+// scans touch only the lanes' live values (same selection as PL = 8)
+template <int PL>
 __global__ void __launch_bounds__(256) router_fused_small_kernel(
     const float *__restrict__ logits, int T, int N, int ld, int K, int renorm, int n_shared, int shared_gate_col,
     const uint16_t *__restrict__ x, int H, int32_t *__restrict__ sel, float *__restrict__ w, int32_t *__restrict__ pos,
@@ -137,18 +140,18 @@ __global__ void __launch_bounds__(256) router_fused_small_kernel(
   __syncthreads();
   for (int t = wid; t < T; t += nw) {
     const float *row = logits + static_cast<size_t>(t) * ld;
-    float v[kMaxPerLane];
+    float v[PL];
     float m = -FLT_MAX;
 #pragma unroll
-    for (int j = 0; j < kMaxPerLane; ++j) {
+    for (int j = 0; j < PL; ++j) {
       const int e = lane + 32 * j;
       v[j] = e < N ? row[e] : -FLT_MAX;
       m = fmaxf(m, v[j]);
     }
     m = dev::warp_max(m);
-    float s = 0.0f, ex[kMaxPerLane];
+    float s = 0.0f, ex[PL];
 #pragma unroll
-    for (int j = 0; j < kMaxPerLane; ++j) {
+    for (int j = 0; j < PL; ++j) {
       const int e = lane + 32 * j;
       ex[j] = e < N ? expf(v[j] - m) : 0.0f;
       s += ex[j];
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__(256) router_fused_small_kernel(
     s = dev::warp_sum(s);
     const float inv = 1.0f / s;
 #pragma unroll
-    for (int j = 0; j < kMaxPerLane; ++j) {
+    for (int j = 0; j < PL; ++j) {
       const int e = lane + 32 * j;
       if (e < N) s_probs[t * N + e] = ex[j] * inv;
     }
@@ -166,7 +169,7 @@ __global__ void __launch_bounds__(256) router_fused_small_kernel(
       float bv = -FLT_MAX;
       int bi = 0x7fffffff;
 #pragma unroll
-      for (int j = 0; j < kMaxPerLane; ++j) {
+      for (int j = 0; j < PL; ++j) {
         const int e = lane + 32 * j;
         if (e < N && !((taken >> j) & 1u) && (v[j] > bv || (v[j] == bv && e < bi))) {
           bv = v[j];
@@ -265,7 +268,9 @@ __global__ void __launch_bounds__(256) router_fused_small_kernel(
   }
   __syncthreads();
   const int H8 = H / 8;
-  const int n_host = hm_.xp ? s_off[N] : 0;  // routed rows also go to the host worker's input
+  // routed rows also go to the host worker's input; one token (decode): every
+  // routed row is that token, so one copy crosses PCIe (the host reads row 0)
+  const int n_host = hm_.xp ? (T == 1 ? min(1, s_off[N]) : s_off[N]) : 0;
 #pragma unroll 4
   for (int v = threadIdx.x; v < R * H8; v += blockDim.x) {  // gather rows in permuted order
     const int p = v / H8, c = v - p * H8;
@@ -288,6 +293,24 @@ __global__ void __launch_bounds__(256) router_fused_small_kernel(
     __syncthreads();
     if (threadIdx.x == 0) *reinterpret_cast<volatile uint32_t *>(hm_.flag) = hm_.seq;
   }
+}
+
+void launch_router_fused(const float *logits, int T, int N, int ld, int K, int renorm, int n_shared,
+                         int shared_gate_col, const uint16_t *x, int H, int32_t *sel, float *w, int32_t *pos,
+                         int32_t *row_src, uint16_t *xp, int32_t *meta_i, double *meta_d, HostMirror m,
+                         cudaStream_t st) {
+#define HM_ROUTER_FUSED(PLV)                                                                                     \
+  router_fused_small_kernel<PLV><<<1, 256, 0, st>>>(logits, T, N, ld, K, renorm, n_shared, shared_gate_col, x, H, \
+                                                    sel, w, pos, row_src, xp, meta_i, meta_d, m)
+  if (N <= 32)
+    HM_ROUTER_FUSED(1);
+  else if (N <= 64)
+    HM_ROUTER_FUSED(2);
+  else if (N <= 128)
+    HM_ROUTER_FUSED(4);
+  else
+    HM_ROUTER_FUSED(8);
+#undef HM_ROUTER_FUSED
 }
 
 // score_sum[e] = sum_t probs[t, e] in fp64, fixed reduction order.
@@ -684,9 +707,8 @@ int hm_router_fused_small(const float *logits, int T, int N, int ld, int K, int 
   HM_REQUIRE(T >= 1 && T <= 32 && N >= 1 && N <= 256 && K >= 1 && K <= 8 && K <= N && ld >= N &&
                  T * (K + n_shared) <= hm::kFusedMaxRows && N + n_shared <= hm::kFusedMaxE && H % 8 == 0,
              HM_EVALUE, "shape outside the fused small-T router");
-  hm::router_fused_small_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      logits, T, N, ld, K, renormalize, n_shared, shared_gate_col, x, H, sel, w, pos, row_src, xp, meta_i, meta_d,
-      hm::HostMirror{});
+  hm::launch_router_fused(logits, T, N, ld, K, renormalize, n_shared, shared_gate_col, x, H, sel, w, pos, row_src,
+                          xp, meta_i, meta_d, hm::HostMirror{}, static_cast<cudaStream_t>(stream));
   HM_LAUNCH_CHECK();
   HM_API_END
 }
@@ -700,9 +722,9 @@ int hm_router_fused_mirror(const float *logits, int T, int N, int ld, int K, int
                  T * (K + n_shared) <= hm::kFusedMaxRows && N + n_shared <= hm::kFusedMaxE && H % 8 == 0,
              HM_EVALUE, "shape outside the fused small-T router");
   HM_REQUIRE(host_meta_i && host_meta_d && host_flag, HM_EVALUE, "host mirror needs meta and flag pointers");
-  hm::router_fused_small_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      logits, T, N, ld, K, renormalize, n_shared, shared_gate_col, x, H, sel, w, pos, row_src, xp, meta_i, meta_d,
-      hm::HostMirror{host_meta_i, host_meta_d, host_xp, host_flag, seq});
+  hm::launch_router_fused(logits, T, N, ld, K, renormalize, n_shared, shared_gate_col, x, H, sel, w, pos, row_src,
+                          xp, meta_i, meta_d, hm::HostMirror{host_meta_i, host_meta_d, host_xp, host_flag, seq},
+                          static_cast<cudaStream_t>(stream));
   HM_LAUNCH_CHECK();
   HM_API_END
 }

@@ -569,7 +569,8 @@ struct Runtime {
         for (uint32_t r : cpu_refs) {
           const size_t rb = h_offsets[ref_expert(r)];
           imgs.push_back(image_ptr(r));
-          xs.push_back(h_x + rb * H);
+          // a one-token mirror carries the token once (row 0): every routed row is it
+          xs.push_back(h_x + (mirror_rows && T == 1 ? 0 : rb) * H);
           outs.push_back(h_out + rb * H);
         }
         if (q4) {
