@@ -50,3 +50,14 @@ def test_runtime_config_layout_matches_header():
     """The ctypes mirror of hm_runtime_config has the header's size (the
     weight_bits field was appended with explicit padding)."""
     assert ctypes.sizeof(_lib.RuntimeConfig) == 8 * 4 + 2 * 8 + 8 * 4  # 8 int32, 2 int64, 8 int32
+
+
+def test_lookahead_rejects_bad_shapes_without_touching_the_device():
+    """hm_lookahead (live prediction) validates its shape before any launch."""
+    f = _lib.lib.hm_lookahead
+    assert f(None, None, 1, 3, 1, 0, 8, 2, 256, None, None, None) == _lib.HM_EVALUE      # N = 0
+    assert f(None, None, 1, 3, 1, 8, 4, 2, 256, None, None, None) == _lib.HM_EVALUE      # ld < N
+    assert f(None, None, 1, 3, 1, 8, 8, 9, 256, None, None, None) == _lib.HM_EVALUE      # K > N
+    assert f(None, None, 1, 3, 1, 8, 8, 2, 100, None, None, None) == _lib.HM_EVALUE      # H % 8
+    assert "look-ahead shape" in _lib.last_error()
+    assert f(None, None, 1, 0, 1, 8, 8, 2, 256, None, None, None) == _lib.HM_OK          # horizon 0: nothing to do
