@@ -246,26 +246,35 @@ def test_model_mode_runs_and_is_deterministic():
     assert torch.isfinite(y1.float()).all()
 
 
-def test_zero_copy_path_equals_copy_path(monkeypatch):
+@pytest.mark.parametrize("family", ["tiny", "deepseek", "qwen2"])
+def test_zero_copy_path_equals_copy_path(monkeypatch, family):
     """The zero-copy decode path (router mirrors the LayerRequest and the routed
     rows into mapped host memory, host spins on a flag; the combine reads the
     host worker's rows over PCIe and folds the MRS update into the same launch)
-    gives bit-identical outputs, decisions and MRS table to the copy path."""
+    gives bit-identical outputs, decisions and MRS table to the copy path --
+    also with 64 routed experts and shared experts (DeepSeek / Qwen2 families)."""
     from paper_2504_05897_b200.moe import TracePredictor
-    cfg = SHAPES["tiny"]
+    if family == "tiny":
+        cfg = SHAPES["tiny"]
+    else:
+        n_shared, k = (2, 6) if family == "deepseek" else (1, 8)
+        cfg = mcore.ModelConfig(num_layers=3, num_routed=64, num_shared=n_shared, num_activated=k,
+                                routed_expert_dims=(256, 256),
+                                shared_expert_dims=(256, 256 if family == "deepseek" else 4 * 256),
+                                bytes_per_weight=2)
     prof = stress_profile(cfg)
     policy = me.EnginePolicy(prefetch=True)
     trace, logits = generate_router_logits(cfg, GenParams(seed=8), 24, 6)
     outs = []
     for zc in ("0", "1"):
         monkeypatch.setenv("HM_ZERO_COPY", zc)
-        moe = HybridMoE(cfg, "tiny", policy, 0.5, prof, max_tokens=64)
+        moe = HybridMoE(cfg, family, policy, 0.5, prof, max_tokens=64)
         moe.init_seeded_weights(6)
         g = torch.Generator(device="cuda").manual_seed(5)
         ys, recs, ncpu = [], [], 0
         for p, fwd in enumerate(trace.passes):
-            lg = [torch.from_numpy(np.ascontiguousarray(logits[p][l], dtype=np.float32)).cuda()
-                  for l in range(cfg.num_layers)]
+            lg = [torch.from_numpy(np.ascontiguousarray(np.pad(logits[p][l], ((0, 0), (0, moe.ld - moe.N))),
+                                                        dtype=np.float32)).cuda() for l in range(cfg.num_layers)]
             x = torch.randn((fwd.token_count, moe.H), generator=g, device="cuda").to(torch.bfloat16)
             y, info = moe.forward_pass(x, lg, predict=TracePredictor(trace, p, 5), decision_log=True)
             torch.cuda.synchronize()
