@@ -27,6 +27,17 @@ def stress_profile(cfg):
                                  cpu_first_expert_penalty=1.4)
 
 
+def family_cfg(family: str):
+    """The tiny stack, or a 3-layer stack of 64 routed experts with the family's
+    shared experts (DeepSeek: 2 chunk-sized, top-6; Qwen2: 1 four-chunk, top-8)."""
+    if family == "tiny":
+        return SHAPES["tiny"]
+    n_shared, k = (2, 6) if family == "deepseek" else (1, 8)
+    return mcore.ModelConfig(num_layers=3, num_routed=64, num_shared=n_shared, num_activated=k,
+                             routed_expert_dims=(256, 256),
+                             shared_expert_dims=(256, 256 if family == "deepseek" else 4 * 256), bytes_per_weight=2)
+
+
 def bf(t: torch.Tensor) -> np.ndarray:
     return ref.bf16_to_f32(t.view(torch.int16).cpu().numpy().view(np.uint16))
 
@@ -134,20 +145,20 @@ def test_live_lookahead_prefetch_model_mode():
     assert torch.isfinite(x.float()).all()
 
 
-@pytest.mark.parametrize("zero_copy", ["1", "0"])
-def test_native_live_lookahead_matches_python_lookahead(monkeypatch, zero_copy):
+@pytest.mark.parametrize("zero_copy,family", [("1", "tiny"), ("0", "tiny"), ("1", "deepseek"), ("1", "qwen2")])
+def test_native_live_lookahead_matches_python_lookahead(monkeypatch, zero_copy, family):
     """The runtime's live predictor (one look-ahead kernel ahead of the router,
     loads published with the LayerRequest) makes the same decisions as the
     Python look-ahead (router_logits + router_topk per future layer): model
     mode per layer, and the one-call native pass in trace mode."""
     monkeypatch.setenv("HM_ZERO_COPY", zero_copy)
-    cfg = SHAPES["tiny"]
+    cfg = family_cfg(family)
     prof = stress_profile(cfg)
     policy = me.EnginePolicy(prefetch=True)
     trace, logits = generate_router_logits(cfg, GenParams(seed=8), 24, 4)
     runs = {}
     for mode in ("live_py", "live", "live_native_pass"):
-        moe = HybridMoE(cfg, "tiny", policy, 0.5, prof, max_tokens=64)
+        moe = HybridMoE(cfg, family, policy, 0.5, prof, max_tokens=64)
         moe.init_seeded_weights(6)
         g = torch.Generator(device="cuda").manual_seed(2)
         recs, ys, res = [], [], []
@@ -160,8 +171,8 @@ def test_native_live_lookahead_matches_python_lookahead(monkeypatch, zero_copy):
             res.append((r.latency, r.lookups, r.hits, r.inserts, r.evictions, r.prefetch_issued))
         g = torch.Generator(device="cuda").manual_seed(3)
         for p, fwd in enumerate(trace.passes):  # trace mode, per layer vs one native call
-            lg = [torch.from_numpy(np.ascontiguousarray(logits[p][l], dtype=np.float32)).cuda()
-                  for l in range(cfg.num_layers)]
+            lg = [torch.from_numpy(np.ascontiguousarray(np.pad(logits[p][l], ((0, 0), (0, moe.ld - moe.N))),
+                                                        dtype=np.float32)).cuda() for l in range(cfg.num_layers)]
             x = torch.randn((fwd.token_count, moe.H), generator=g, device="cuda").to(torch.bfloat16)
             pred = "live" if mode == "live_native_pass" else mode
             y, info = moe.forward_pass(x, lg, predict=pred, decision_log=mode != "live_native_pass")
@@ -254,14 +265,7 @@ def test_zero_copy_path_equals_copy_path(monkeypatch, family):
     gives bit-identical outputs, decisions and MRS table to the copy path --
     also with 64 routed experts and shared experts (DeepSeek / Qwen2 families)."""
     from paper_2504_05897_b200.moe import TracePredictor
-    if family == "tiny":
-        cfg = SHAPES["tiny"]
-    else:
-        n_shared, k = (2, 6) if family == "deepseek" else (1, 8)
-        cfg = mcore.ModelConfig(num_layers=3, num_routed=64, num_shared=n_shared, num_activated=k,
-                                routed_expert_dims=(256, 256),
-                                shared_expert_dims=(256, 256 if family == "deepseek" else 4 * 256),
-                                bytes_per_weight=2)
+    cfg = family_cfg(family)
     prof = stress_profile(cfg)
     policy = me.EnginePolicy(prefetch=True)
     trace, logits = generate_router_logits(cfg, GenParams(seed=8), 24, 6)
