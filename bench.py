@@ -426,8 +426,9 @@ def run_ours(args) -> None:
     # (tools/profile_round.sh): measured bytes for that launch beside its
     # algorithmic bytes -- traffic ~ algorithmic means weights are read once
     traffic = {}
-    tp = ROOT / "profiles" / "r01b_traffic.json"
-    if tp.exists() and args.shape == "mixtral" and args.bits == 16:
+    tp = {"mixtral": ROOT / "profiles" / "r01b_traffic.json",
+          "deepseek": ROOT / "profiles" / "r01d_traffic_deepseek.json"}.get(args.shape)
+    if tp is not None and tp.exists() and args.bits == 16:
         traffic = json.loads(tp.read_text())
     tg = traffic.get("decode_gemv", {})
     roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
