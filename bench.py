@@ -426,10 +426,11 @@ def run_ours(args) -> None:
     # (tools/profile_round.sh): measured bytes for that launch beside its
     # algorithmic bytes -- traffic ~ algorithmic means weights are read once
     traffic = {}
-    tp = {"mixtral": ROOT / "profiles" / "r01b_traffic.json",
-          "deepseek": ROOT / "profiles" / "r01d_traffic_deepseek.json"}.get(args.shape)
-    if tp is not None and tp.exists() and args.bits == 16:
-        traffic = json.loads(tp.read_text())
+    tp = {("mixtral", 16): "r01b_traffic.json", ("deepseek", 16): "r01d_traffic_deepseek.json",
+          ("qwen2", 16): "r01d_traffic_qwen2.json", ("mixtral", 4): "r01d_traffic_mixtral_q4.json"}.get(
+        (args.shape, args.bits))
+    if tp is not None and (ROOT / "profiles" / tp).exists():
+        traffic = json.loads((ROOT / "profiles" / tp).read_text())
     tg = traffic.get("decode_gemv", {})
     roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved_gbs / hbm_peak, "traffic": tg.get("dram_bytes"),
