@@ -80,70 +80,185 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- reference arm / cpu baseline
-def cpu_oracle_decode(shape: str, n_layers_sample: int, n_distinct: int = 2, seed: int = 0, threads: int | None = None):
-    """The reference's CPU path, ported: per layer the oracle's plan (all experts
-    uncached -> the decision restatement) + fp32 numpy SwiGLU experts on the CPU
-    (plan_all_cpu semantics, scheduling.py:273-284) for one decode token.
-    Returns (seconds per token scaled to all L layers, sample description)."""
-    from oracle import decisions as od
-    from oracle import moe_ref as ref
-    from paper_2504_05897_b200.moe import SHAPES, FAMILIES, shared_chunks
-    from paper_2504_05897_b200.tracegen import GenParams, generate_router_logits
+# The reference's own CPU path for this hot path: every
+# expert of every layer on the host cores under plan_all_cpu semantics
+# (scheduling.py:273-284), bf16 expert weights with fp32 accumulation
+# (torch CPU / oneDNN, AMX where present) on all host threads, routing from the
+# reference's own trace generator (fp32 logits frozen from the unmodified
+# moesim.tracegen by tests/golden/make_router_golden.py), the router and the
+# plan from the oracle restatement.  Nothing here imports the product package.
+REF_SHAPES = {  # L, N, K, (H, I), shared chunks of (H, I), renormalise, shared gate
+    "tiny": (4, 8, 2, (256, 256), 0, True, False),
+    "mixtral": (32, 8, 2, (4096, 14336), 0, True, False),
+    "deepseek": (26, 64, 6, (2048, 1408), 2, False, False),
+    "qwen2": (28, 64, 8, (3584, 2560), 8, False, True),
+}
+REF_POOL_BYTES = 16 << 30   # distinct expert images (aliased modulo their count): >> host LLC
 
-    cfg = SHAPES[shape]
-    fam = FAMILIES[shape]
-    H, I = cfg.routed_expert_dims
-    S = shared_chunks(cfg)
-    rng = np.random.default_rng(seed)
-    experts = [tuple((rng.standard_normal(sh, dtype=np.float32) * 0.02) for sh in ((I, H), (I, H), (H, I)))
-               for _ in range(n_distinct)]
-    _, logits = generate_router_logits(cfg, GenParams(seed=seed), 0, 1)
+
+def host_info() -> dict:
+    out = {"cpu_count": os.cpu_count()}
+    try:
+        txt = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {ln.split(":", 1)[0].strip(): ln.split(":", 1)[1].strip() for ln in txt.splitlines() if ":" in ln}
+        out.update(model=kv.get("Model name"), sockets=kv.get("Socket(s)"), numa_nodes=kv.get("NUMA node(s)"),
+                   l3=kv.get("L3 cache"))
+    except Exception:
+        pass
+    return out
+
+
+class CpuMoE:
+    """The all-CPU MoE stack of one shape: bf16 expert images on the host."""
+
+    def __init__(self, shape: str, threads: int | None = None, pool_bytes: int = REF_POOL_BYTES) -> None:
+        import torch
+        self.torch = torch
+        L, N, K, (H, I), S, renorm, sgate = REF_SHAPES[shape]
+        self.L, self.N, self.K, self.H, self.I, self.S, self.renorm, self.sgate = L, N, K, H, I, S, renorm, sgate
+        self.threads = threads or os.cpu_count() or 1
+        torch.set_num_threads(self.threads)
+        n = 3 * H * I
+        total = L * (N + S)
+        self.n_images = int(min(total, max(8, pool_bytes // (2 * n))))
+        g = torch.Generator().manual_seed(0)
+        base = (torch.randn(n, generator=g) * 0.02).to(torch.bfloat16)
+        self.images = torch.empty((self.n_images, n), dtype=torch.bfloat16)
+        for i in range(self.n_images):  # distinct images: base rotated by a per-image offset
+            o = (i * 7919 * 64) % n
+            self.images[i, : n - o].copy_(base[o:])
+            self.images[i, n - o:].copy_(base[:o])
+        self.logits = np.load(ROOT / "oracle" / "fixtures" / f"decode_logits_{shape}.npy")
+        self.image_bytes = 2 * n
+        from oracle import cpu_moe
+        self.scratch = cpu_moe.Scratch()
+
+    def expert(self, l: int, e: int, x):
+        """SwiGLU on rows x [M, H] bf16, fp32 accumulation: decode-sized row
+        groups through the plain-C oracle (oracle/cpu_moe.c, weight streaming
+        on all threads), prefill-sized ones through torch CPU (oneDNN / AMX
+        GEMM).  Image layout: W13 rows [gate | up] x H, then W2 [H][I]."""
+        torch = self.torch
+        img = self.images[(l * (self.N + self.S) + e) % self.n_images]
+        H, I = self.H, self.I
+        if x.shape[0] <= 8:
+            from oracle import cpu_moe
+            xc = x.contiguous()
+            out = torch.empty((x.shape[0], H), dtype=torch.float32)
+            cpu_moe.expert(img.data_ptr(), img.data_ptr() + 4 * H * I, H, I, xc.data_ptr(), x.shape[0],
+                           out.data_ptr(), self.scratch)
+            return out
+        F = torch.nn.functional
+        gu = F.linear(x, img[: 2 * H * I].view(2 * I, H)).float()
+        h = (F.silu(gu[:, :I]) * gu[:, I:]).to(torch.bfloat16)
+        return F.linear(h, img[2 * H * I:].view(H, I)).float()
+
+    def layer(self, l: int, x, logits: np.ndarray):
+        """One MoE layer on x [T, H] bf16 with fp32 logits [T, N]: oracle router,
+        plan_all_cpu, experts in plan order, weighted sum + residual."""
+        from oracle import decisions as od
+        from oracle import moe_ref as ref
+        torch = self.torch
+        lg = logits
+        if self.sgate:
+            lg = np.concatenate([lg, np.zeros((lg.shape[0], 1), np.float32)], axis=1)
+        sel, w, _, counts, _ = ref.router(lg, self.N, self.K, self.renorm, self.S, self.N if self.sgate else -1)
+        tasks = [((l, e), int(counts[e])) for e in range(self.N + self.S) if counts[e] > 0]
+        events, _, _ = od.all_cpu(tasks, self.prof)
+        y = torch.zeros((x.shape[0], self.H), dtype=torch.float32)
+        selt, wt = torch.from_numpy(sel), torch.from_numpy(w)
+        for ev in events:  # plan CPU order
+            e = ev[1][1]
+            rows, slot = (selt == e).nonzero(as_tuple=True)
+            out = self.expert(l, e, x[rows])
+            y.index_add_(0, rows, out * wt[rows, slot][:, None])
+        return (x.float() + y).to(torch.bfloat16)
+
     prof = dict(gpu_time_per_expert=1.0, cpu_slope=1.0, transfer_bandwidth=1e9, transfer_latency=0.0,
                 gpu_saturation_load=256, gpu_slope=0.0, cpu_first_expert_penalty=1.0, shared_expert_time=0.0,
                 non_expert_time=0.0)
-    x = rng.standard_normal((1, H), dtype=np.float32)
-    L = min(n_layers_sample, cfg.num_layers)
-    t0 = time.perf_counter()
-    for l in range(L):
-        lg = logits[0][l].astype(np.float32)
-        if fam.shared_gate:
-            lg = np.concatenate([lg, np.zeros((1, 1), np.float32)], axis=1)
-        sel, w, _, counts, _ = ref.router(lg, cfg.num_routed, cfg.num_activated, fam.renormalize, S,
-                                          cfg.num_routed if fam.shared_gate else -1)
-        tasks = [((l, e), int(counts[e])) for e in range(cfg.num_routed) if counts[e] > 0]
-        od.best_plan([], tasks, prof, 3.0 * H * I * 2)
-        y = np.zeros_like(x)
-        for k in range(sel.shape[1]):
-            e = int(sel[0, k])
-            y += w[0, k] * ref.expert(x, *experts[(l * 7 + e) % n_distinct])
-        x = x + y
-    dt = time.perf_counter() - t0
-    per_token = dt * cfg.num_layers / L
-    return per_token, f"{L} of {cfg.num_layers} layers of one decode token, fp32 numpy experts " \
-                      f"({n_distinct} distinct weight sets aliased), scaled to {cfg.num_layers} layers"
+
+    def decode_token(self, p: int, x):
+        for l in range(self.L):
+            x = self.layer(l, x, self.logits[p % len(self.logits), l][None, :])
+        return x
+
+    def prefill(self, T: int, seed: int = 0):
+        rng = np.random.default_rng(seed)
+        x = self.torch.randn((T, self.H), generator=self.torch.Generator().manual_seed(seed)).to(self.torch.bfloat16)
+        for l in range(self.L):
+            x = self.layer(l, x, rng.standard_normal((T, self.N)).astype(np.float32))
+        return x
+
+
+def cpu_reference_decode(shape: str, steps: int, warmup: int, prefill: int = 0, threads: int | None = None):
+    """Timed all-CPU decode (and optionally one prefill): returns the cpu_baseline dict."""
+    import torch
+    t_setup = time.perf_counter()
+    m = CpuMoE(shape, threads)
+    setup = time.perf_counter() - t_setup
+    x = torch.randn((1, m.H), generator=torch.Generator().manual_seed(1)).to(torch.bfloat16)
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        x = m.decode_token(i, x)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    ms = 1e3 * statistics.mean(times)
+    out = {"value": 1e3 / ms, "unit": "tok/s", "cores": m.threads, "kind": "port", "ms_per_token": ms,
+           "sample": f"{steps} decode tokens x all {m.L} layers (after {warmup} warm-up), every expert on the host: "
+                     f"bf16 weights, fp32 accumulation (plain-C oracle oracle/cpu_moe.c, OpenMP, {m.threads} "
+                     f"threads; prefill GEMMs torch CPU/oneDNN), oracle router + "
+                     f"plan_all_cpu; routing = fp32 logits frozen from the unmodified reference generator; "
+                     f"{m.n_images} distinct {m.image_bytes / 1e6:.1f} MB expert images aliased modulo their count "
+                     f"({m.n_images * m.image_bytes / 1e9:.1f} GB >> LLC)",
+           "setup_s": setup, "host": host_info()}
+    if prefill:
+        t0 = time.perf_counter()
+        m.prefill(prefill)
+        out["prefill_ms"] = 1e3 * (time.perf_counter() - t0)
+        out["prefill_tokens"] = prefill
+    return out
 
 
 def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cores = os.cpu_count()
-    times = []
-    sample = ""
-    for i in range(args.warmup + args.steps):
-        dt, sample = cpu_oracle_decode(args.shape, args.ref_layers, seed=i)
-        if i >= args.warmup:
-            times.append(dt)
-    ms = 1e3 * statistics.mean(times)
-    tok_s = 1e3 / ms  # one sequence on the host cores
+    cb = cpu_reference_decode(args.shape, args.steps, args.warmup, prefill=args.prefill if args.ref_prefill else 0)
+    tok_s = cb["value"]
     line = {"impl": "reference", "metric": "decode tok/s at 25% expert-cache budget", "value": tok_s,
-            "unit": "tok/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (reference trace generator routing, random-init weights)",
-            "config": {"workload": f"{args.shape}-shaped MoE decode, batch 1, CPU oracle port", "shape": args.shape},
-            "cpu_baseline": {"value": tok_s, "unit": "tok/s", "cores": cores, "kind": "port", "sample": sample},
+            "unit": "tok/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": cb["ms_per_token"], "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16 weights, fp32 accumulation (CPU)",
+            "data": "synthetic (reference trace-generator routing frozen from the reference, random-init weights)",
+            "config": {"workload": f"{args.shape}-shaped MoE decode, batch 1, all experts on the host CPU "
+                                   f"(the reference's CPU path, plan_all_cpu)", "shape": args.shape},
+            "cpu_baseline": cb,
             "e2e": {"value": tok_s, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if "prefill_ms" in cb:
+        line["prefill"] = {"tokens": cb["prefill_tokens"], "ms": cb["prefill_ms"]}
     print(json.dumps(line), flush=True)
+
+
+def reference_decision_path(passes, cfg, profile, capacity: int, policy: str, prefetch: bool) -> dict:
+    """the reference's decision path (oracle restatement of
+    run_pass, engine.py:288-486; one Python thread) on the same LayerRequests
+    and calibrated profile the runtime planned with: microseconds per layer."""
+    from oracle import decisions as od
+    prof = {k: getattr(profile, k) for k in ("gpu_time_per_expert", "cpu_slope", "transfer_bandwidth",
+                                              "transfer_latency", "gpu_saturation_load", "gpu_slope",
+                                              "cpu_first_expert_penalty", "shared_expert_time", "non_expert_time")}
+    H, I = cfg.routed_expert_dims
+    nbytes = 3.0 * H * I * cfg.bytes_per_weight
+    t0 = time.perf_counter()
+    od.run(passes, cfg.num_layers, cfg.num_routed, cfg.num_activated, nbytes, prof, capacity, policy, False)
+    dt = time.perf_counter() - t0
+    n_layers = sum(len(layers) for _, layers in passes)
+    return {"us_per_layer": 1e6 * dt / max(1, n_layers), "layers": n_layers, "threads": 1, "kind": "port",
+            "what": "oracle restatement of the reference run_pass decisions (lookup, select_plan, inserts, MRS) on "
+                    "the runtime's own LayerRequests (the timed decode passes) with the calibrated profile"}
 
 
 # --------------------------------------------------------------------------- our arm
@@ -186,13 +301,14 @@ def run_ours(args) -> None:
     from paper_2504_05897_b200 import _lib
     from paper_2504_05897_b200.calibration import calibrate_shape
     from paper_2504_05897_b200.engine import EnginePolicy
-    from paper_2504_05897_b200.moe import FAMILIES, SHAPES, HybridMoE, layer_stats, with_shared_time
-    from paper_2504_05897_b200.prefetch import predict_layers
+    from paper_2504_05897_b200.moe import SHAPES, HybridMoE, layer_stats, with_shared_time
     from paper_2504_05897_b200.tracegen import GenParams, generate_router_logits
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}: one rank per GPU is required")
     # HM_SAME_GPU=1: every rank on cuda:0 with a gloo control plane -- only to
     # exercise the multi-rank harness on a one-GPU box (timings meaningless:
     # the ranks' contexts time-slice the GPU)
@@ -217,33 +333,30 @@ def run_ours(args) -> None:
     t_setup = time.time()
     from paper_2504_05897_b200.costs import load_profile, save_profile
     # Stage-calibrated profiles: the reference's cost model is linear in load
-    # (costs.py:68-88), but the host worker is DRAM-bound at decode loads (1-4
-    # tokens) and compute-bound (AMX) at prefill loads, so one fit cannot serve
-    # both; the decode profile is fitted at decode loads, the prefill profile
-    # at prefill loads, and each pass is planned with its stage's profile.
+    # (costs.py:68-88), but the host worker is DRAM-bound at decode loads and
+    # compute-bound (AMX) at prefill loads, so one fit cannot serve both.  The
+    # decode profile is fitted at the load decode plans with -- one token per
+    # expert at batch 1 -- so a host expert is rated at its streaming time, not
+    # at a slope through loads 1-4 (which under-rated it 1.8x in round 1); the
+    # prefill profile at prefill loads.  Each pass is planned with its stage's profile.
     if args.profile_file:  # e.g. for runs under a profiler, where warm-up timings are distorted
         base_profile = load_profile(args.profile_file)
         prefill_profile = load_profile(args.prefill_profile_file) if args.prefill_profile_file else base_profile
     else:
-        # decode profile at decode loads on every device (the GPU's flat cost
-        # is the GEMV's, not an average with prefill-sized GEMMs)
-        base_profile = calibrate_shape(H, I, weight_bits=args.bits, gpu_loads=(1, 2, 3, 4))[0].profile
+        base_profile = calibrate_shape(H, I, weight_bits=args.bits, gpu_loads=(1, 2, 3, 4), cpu_loads=(1,),
+                                       cpu_bursts=4)[0].profile
         prefill_profile = base_profile
-        if args.stage_profiles:
+        if args.stage_profiles and not args.live_fixture:  # a fixture replays with ONE profile
             prefill_profile = calibrate_shape(H, I, cpu_loads=(64, 128, 256), cpu_bursts=1,
                                               gpu_loads=(64, 128, 256, 384, 512), weight_bits=args.bits)[0].profile
         if args.save_profile and rank == 0:
             save_profile(base_profile, args.save_profile)
             save_profile(prefill_profile, args.save_profile + ".prefill")
-
-    class _Cal:
-        profile = base_profile
-    cal = _Cal()
-    prof = with_shared_time(cal.profile, cfg)
+    prof = with_shared_time(base_profile, cfg)
     prof_prefill = with_shared_time(prefill_profile, cfg)
     policy = EnginePolicy(scheduling=args.scheduling, cache_policy=args.policy, prefetch=args.prefetch)
-    # expert parallelism over the ranks of this box: one replicated sequence, each
-    # rank homes experts e % world, host bytes and worker cores split by rank
+    # expert parallelism over the ranks of this box: each rank homes experts
+    # e % world, host bytes and worker cores split by rank
     image_bytes = 3 * H * I * 2 if args.bits == 16 else 3 * H * I // 2 + 3 * H * I // 64
     total_bytes = cfg.num_layers * cfg.num_routed * image_bytes // world
     host_images = args.host_images
@@ -261,16 +374,19 @@ def run_ours(args) -> None:
         moe = HybridMoE(cfg, args.shape, policy, args.ratio, prof, host_images=host_images,
                         max_tokens=max(args.prefill, 1), cpu_threads=threads, ep_rank=rank, ep_world=world,
                         exchange=args.exchange, weight_bits=args.bits)
-    except PeerMemoryUnavailable as e:  # every rank sees the same verdict: use the NCCL all-reduce exchange
-        if args.exchange == "dispatch":
+    except PeerMemoryUnavailable as e:  # every rank sees the same verdict: use the NCCL exchange instead
+        if args.exchange not in ("p2p", "dispatch"):
             raise
-        exchange_note = f"p2p unavailable ({e}); NCCL all-reduce used"
+        fallback = "nccl_a2a" if args.exchange == "dispatch" else "allreduce"
+        exchange_note = f"p2p unavailable ({e}); NCCL {fallback} used"
         moe = HybridMoE(cfg, args.shape, policy, args.ratio, prof, host_images=host_images,
                         max_tokens=max(args.prefill, 1), cpu_threads=threads, ep_rank=rank, ep_world=world,
-                        exchange="allreduce", weight_bits=args.bits)
+                        exchange=fallback, weight_bits=args.bits)
     moe.init_random_weights(seed=args.seed + rank)
     n_dec = args.warmup + args.steps
-    trace, logits = generate_router_logits(cfg, GenParams(seed=args.seed), args.prefill, 2 * n_dec + 1)
+    # passes: prefill | warm-up | timed | instrumented (kernel timing) | e2e
+    n_pass = 1 + n_dec + args.steps + n_dec
+    trace, logits = generate_router_logits(cfg, GenParams(seed=args.seed), args.prefill, n_pass - 1)
     dev_logits = []
     for p in range(len(trace.passes)):
         layer_logits = []
@@ -280,17 +396,13 @@ def run_ours(args) -> None:
                 lg = np.concatenate([lg, np.zeros((lg.shape[0], 1), np.float32)], axis=1)
             layer_logits.append(torch.from_numpy(np.ascontiguousarray(lg)).cuda())
         dev_logits.append(layer_logits)
-    # fixed residency of the comparison baselines (engine.py:423-434), executed for real
-    if args.scheduling == "static_layer_split":
-        split = int(args.ratio * cfg.num_layers)
-        moe.preload([(l, e) for l in range(split) for e in range(cfg.num_routed) if e % world == rank])
-    elif args.scheduling == "fixed_frequency_map":
+    if args.scheduling == "fixed_frequency_map":  # kTransformers-like pinned set (engine.py:195-231)
         from paper_2504_05897_b200.engine import compute_fixed_pinned_set
         fixed = compute_fixed_pinned_set(trace, moe.capacity * world, policy.calibration_prefix_fraction, None)
         moe.set_fixed_gpu_set(sorted(r for r in fixed if r[1] % world == rank)[: moe.capacity])
     g = torch.Generator(device="cuda").manual_seed(1234)  # replicated hidden state on every rank
     xs = [torch.randn((f.token_count, H), generator=g, device="cuda").to(torch.bfloat16) for f in trace.passes]
-    if world > 1 and args.exchange == "dispatch":  # token-sharded: rank r keeps tokens [r*T/G, (r+1)*T/G)
+    if world > 1 and moe.exchange in ("dispatch", "nccl_a2a"):  # token-sharded: rank r keeps tokens [r*T/G, (r+1)*T/G)
         def shard(t):
             T = t.shape[0]
             return t[rank * T // world:(rank + 1) * T // world].contiguous()
@@ -312,25 +424,30 @@ def run_ours(args) -> None:
     from paper_2504_05897_b200.moe import TracePredictor
     predictors = [TracePredictor(trace, p, args.seed) for p in range(len(trace.passes))]
 
-    def predictor(p):  # the reference's prediction model on this pass, native -- or the live look-ahead
+    def predictor(p):  # the reference's prediction model on this pass, natively -- or the live look-ahead
         return "live" if args.predict == "live" else predictors[p]
 
+    lib = _lib.lib
     st = torch.cuda.current_stream()
+    live_fixture = bool(args.live_fixture)
+    fixture_records, fixture_requests = [], []
     # ---- prefill: 1k tokens, cold cache (the reference's TTFT, engine.py:465-466)
-    _trace('prefill')
+    _trace("prefill")
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    _lib.lib.hm_runtime_set_copy_timing(moe._rt, 1)
-    ev0.record(st)
+    lib.hm_runtime_set_copy_timing(moe._rt, 1)
     moe.set_profile(prof_prefill)
-    _, pinfo = moe.forward_pass(xs[0], dev_logits[0], predict=predictor(0))
-    moe.set_profile(prof)
+    ev0.record(st)
+    _, pinfo = moe.forward_pass(xs[0], dev_logits[0], predict=predictor(0), decision_log=live_fixture)
     ev1.record(st)
     ev1.synchronize()
+    moe.set_profile(prof)
     prefill_ms = ev0.elapsed_time(ev1)
-    import ctypes as C
+    if live_fixture:
+        fixture_records.extend(pinfo["records"])
+        fixture_requests.append(pinfo["requests"])
     cms, cby, cn, cmx = C.c_double(), C.c_int64(), C.c_int64(), C.c_double()
-    _lib.check(_lib.lib.hm_runtime_copy_times(moe._rt, C.byref(cms), C.byref(cby), C.byref(cn), C.byref(cmx)))
-    _lib.lib.hm_runtime_set_copy_timing(moe._rt, 0)
+    _lib.check(lib.hm_runtime_copy_times(moe._rt, C.byref(cms), C.byref(cby), C.byref(cn), C.byref(cmx)))
+    lib.hm_runtime_set_copy_timing(moe._rt, 0)
     # PCIe roofline of the prefill's expert copies (CUDA events on the copy stream)
     h2d_roofline = {"bound": "pcie", "copies": cn.value, "bytes": cby.value, "copy_ms": cms.value,
                     "achieved_gbs": cby.value / (cms.value / 1e3) / 1e9 if cms.value > 0 else None,
@@ -338,26 +455,28 @@ def run_ours(args) -> None:
                     "frac_of_gen5": (cby.value / (cms.value / 1e3) / 1e9 / 64.0) if cms.value > 0 else None,
                     "link_busy_frac_of_prefill": cms.value / prefill_ms if prefill_ms > 0 else None}
     pst = layer_stats(pinfo)
+    predicted_ttft_ms = 1e3 * pinfo["pass"].latency
 
     # ---- decode: W warm-up passes (recorded for the parity block), then K timed passes
-    _trace('decode')
+    _trace("decode")
     warm_records, warm_requests = [], []
     for p in range(1, 1 + args.warmup):
-        _trace(f"warm-up pass {p}")
         _, winfo = moe.forward_pass(xs[p], dev_logits[p], predict=predictor(p), decision_log=True)
         warm_records.extend(winfo["records"])
         warm_requests.append(winfo["requests"])
     torch.cuda.synchronize()
+    if live_fixture:
+        fixture_records.extend(warm_records)
+        fixture_requests.extend(warm_requests)
     parity = warm_parity(cfg, trace, warm_requests, warm_records, moe, policy, args)
-    lib = _lib.lib
-    lib.hm_runtime_set_kernel_timing(moe._rt, 1)
     launches0 = lib.hm_launch_count()
-    stats_all = []
+    stats_all, predicted = [], []
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    # HM_NCU_TIMED=1: bracket the timed region for `ncu --profile-from-start off`
-    ncu_timed = os.environ.get("HM_NCU_TIMED") == "1"  # (the runtime drops its timing gate under ncu)
+    # the timed region runs the runtime exactly as e2e does: no kernel-timing
+    # events, no timing gate (those run in a separate instrumented pass below)
+    ncu_timed = os.environ.get("HM_NCU_TIMED") == "1"  # bracket for `ncu --profile-from-start off`
     with ClockSampler(local) as clocks:
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if ncu_timed:
@@ -365,7 +484,6 @@ def run_ours(args) -> None:
         t0.record(st)
         for k in range(args.steps):
             p = 1 + args.warmup + k
-            _trace(f"timed pass {p}")
             _, info = moe.forward_pass(xs[p], dev_logits[p], predict=predictor(p))
             stats_all.append(info)
         t1.record(st)
@@ -376,12 +494,9 @@ def run_ours(args) -> None:
     if dist:
         dist.barrier()
     launches = lib.hm_launch_count() - launches0
+    predicted = [1e3 * info["pass"].latency for info in stats_all]
     stats_all = [s for info in stats_all for s in layer_stats(info)]
     ms_total = t0.elapsed_time(t1)
-    import ctypes as C
-    kms, kbytes, kn, kmax = C.c_double(), C.c_int64(), C.c_int64(), C.c_double()
-    lib.hm_runtime_kernel_times(moe._rt, C.byref(kms), C.byref(kbytes), C.byref(kn), C.byref(kmax))
-    lib.hm_runtime_set_kernel_timing(moe._rt, 0)
     if dist:
         t = torch.tensor([ms_total], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -389,45 +504,62 @@ def run_ours(args) -> None:
     ms_step = ms_total / args.steps
     tok_s = 1e3 / ms_step  # one sequence, experts sharded: tokens of the whole job per second
 
+    # ---- instrumented passes (outside the timed region): CUDA events around
+    # every expert-FFN launch for the dominant kernel's roofline
+    _trace("instrumented")
+    lib.hm_runtime_set_kernel_timing(moe._rt, 1)
+    i0 = 1 + n_dec
+    for k in range(args.steps):
+        p = i0 + k
+        moe.forward_pass(xs[p], dev_logits[p], predict=predictor(p))
+    torch.cuda.synchronize()
+    kms, kbytes, kn, kmax = C.c_double(), C.c_int64(), C.c_int64(), C.c_double()
+    lib.hm_runtime_kernel_times(moe._rt, C.byref(kms), C.byref(kbytes), C.byref(kn), C.byref(kmax))
+    lib.hm_runtime_set_kernel_timing(moe._rt, 0)
+
     # ---- e2e: host buffers through the public API, copies inside the timed region
-    _trace('e2e')
-    e2e_passes = range(1 + n_dec, 1 + 2 * n_dec)
+    _trace("e2e")
+    e2e_passes = list(range(1 + n_dec + args.steps, 1 + 2 * n_dec + args.steps))
     host_x = [xs[p].cpu().pin_memory() for p in e2e_passes]
     host_lg = [torch.stack([t.cpu() for t in dev_logits[p]]).pin_memory() for p in e2e_passes]
     y_host = torch.empty((host_x[0].shape[0], H), dtype=torch.bfloat16).pin_memory()
     dx = torch.empty_like(host_x[0], device="cuda")
     dlg = torch.empty_like(host_lg[0], device="cuda")
     for i in range(args.warmup):
-        p = list(e2e_passes)[i]
         dx.copy_(host_x[i], non_blocking=True)
         dlg.copy_(host_lg[i], non_blocking=True)
-        y, _ = moe.forward_pass(dx, list(dlg), predict=predictor(p))
+        y, _ = moe.forward_pass(dx, list(dlg), predict=predictor(e2e_passes[i]))
         y_host.copy_(y, non_blocking=True)
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     for i in range(args.warmup, n_dec):
-        p = list(e2e_passes)[i]
         dx.copy_(host_x[i], non_blocking=True)
         dlg.copy_(host_lg[i], non_blocking=True)
-        y, _ = moe.forward_pass(dx, list(dlg), predict=predictor(p))
+        y, _ = moe.forward_pass(dx, list(dlg), predict=predictor(e2e_passes[i]))
         y_host.copy_(y, non_blocking=True)
     e1.record(st)
     e1.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / args.steps
+    e2e_total = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([e2e_total], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_ms = e2e_total / args.steps
     h2d = host_x[0].numel() * 2 + host_lg[0].numel() * 4
     d2h = y_host.numel() * 2
 
     # ---- roofline of the dominant GPU kernel (decode expert FFN, HBM-bound)
-    _trace('roofline of the dominant GPU kernel (decode expert FFN, HBM-bound)')
     achieved_gbs = kbytes.value / (kms.value / 1e3) / 1e9 if kms.value > 0 else 0.0
     hbm_peak = float(pk["hbm_gbs"])
     # DRAM traffic of the same kernels from the committed ncu --set full capture
     # (tools/profile_round.sh): measured bytes for that launch beside its
     # algorithmic bytes -- traffic ~ algorithmic means weights are read once
     traffic = {}
-    tp = {("mixtral", 16): "r01b_traffic.json", ("deepseek", 16): "r01d_traffic_deepseek.json",
-          ("qwen2", 16): "r01d_traffic_qwen2.json", ("mixtral", 4): "r01d_traffic_mixtral_q4.json"}.get(
+    tp = {("mixtral", 16): "r02_traffic_mixtral.json", ("deepseek", 16): "r02_traffic_deepseek.json",
+          ("qwen2", 16): "r02_traffic_qwen2.json", ("mixtral", 4): "r01d_traffic_mixtral_q4.json"}.get(
         (args.shape, args.bits))
     if tp is not None and (ROOT / "profiles" / tp).exists():
         traffic = json.loads((ROOT / "profiles" / tp).read_text())
@@ -436,13 +568,15 @@ def run_ours(args) -> None:
                 "frac": achieved_gbs / hbm_peak, "traffic": tg.get("dram_bytes"),
                 "traffic_launch": tg.get("launch"), "traffic_algorithmic_bytes": tg.get("algorithmic_bytes"),
                 "traffic_source": traffic.get("source"),
-                "kernel": "decode expert FFN (ffn1_gemv + ffn2_gemv, weights streamed once)" if args.bits == 16 else
+                "kernel": "decode expert FFN (fused GEMV, weights streamed once)" if args.bits == 16 else
                           "decode expert FFN on 4-bit images (ffn1_q4 + ffn2_q4)",
                 "launches": kn.value, "avg_launch_us": 1e3 * kms.value / max(1, kn.value),
-                "bytes_per_launch": kbytes.value / max(1, kn.value), "peak_kind": pk_kind}
+                "bytes_per_launch": kbytes.value / max(1, kn.value), "peak_kind": pk_kind,
+                "timed_in": "separate instrumented passes (CUDA events around each expert-FFN launch), "
+                            "not the headline timed region"}
     # plan-conditional roofline of the whole step: max(B_gpu/BW_hbm, B_cpu/BW_host, B_h2d/BW_pcie) per layer
     bw_host = host_bw_gbs * 1e9
-    bw_pcie = cal.profile.transfer_bandwidth  # bytes / s, fitted at warm-up
+    bw_pcie = base_profile.transfer_bandwidth  # bytes / s, fitted at warm-up
     bound_s = sum(max(s.bytes_gpu / (hbm_peak * 1e9), s.bytes_cpu / bw_host, s.bytes_h2d / bw_pcie)
                   for s in stats_all)
     n_cpu = sum(s.n_cpu for s in stats_all) / args.steps
@@ -460,27 +594,54 @@ def run_ours(args) -> None:
                      "kernel": "expert_gemm_kernel (ffn1 SwiGLU + ffn2), 256 tokens x 8 experts",
                      "ms": gb["ms"], "hbm_gbs": gb["hbm_gbs"]}
 
-    # ---- CPU baseline: the oracle port on this host, bounded sample
+    # ---- BASELINE.md §5 A (decision path) and C (simulator prediction vs measured)
+    decision_baseline = None
+    if rank == 0 and not args.no_cpu_baseline:
+        dpasses = [("decode", [(l, list(lo), list(sc)) for l, (lo, sc) in enumerate(reqs)])
+                   for reqs in warm_requests]
+        decision_baseline = reference_decision_path(dpasses, cfg, prof, moe.capacity, args.policy, False)
+        decision_baseline["native_us_per_layer"] = statistics.mean(s.t_decide_us for s in stats_all)
+        decision_baseline["speedup"] = decision_baseline["us_per_layer"] / max(1e-9,
+                                                                              decision_baseline["native_us_per_layer"])
+    model_check = {"what": "simulator (the reference's cost model, the decision core's own pass latency) with the "
+                           "calibrated profiles vs measured",
+                   "predicted_tbt_ms": statistics.mean(predicted), "measured_tbt_ms": ms_step,
+                   "tbt_ratio_measured_over_predicted": ms_step / max(1e-9, statistics.mean(predicted)),
+                   "predicted_ttft_ms": predicted_ttft_ms, "measured_ttft_ms": prefill_ms,
+                   "ttft_ratio_measured_over_predicted": prefill_ms / max(1e-9, predicted_ttft_ms)}
+
+    # ---- CPU baseline: the reference's all-CPU path on this host, bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # rank 0 at N=1 only
-        per_tok, sample = cpu_oracle_decode(args.shape, args.ref_layers)
-        cpu = {"value": 1.0 / per_tok, "unit": "tok/s", "cores": os.cpu_count(), "kind": "port", "sample": sample}
+        del moe  # release the pinned store first (host memory)
+        torch.cuda.synchronize()
+        cpu = cpu_reference_decode(args.shape, args.cpu_baseline_steps, 1, prefill=0)
+
+    # ---- per-rank parity, gathered
+    if dist:
+        allp = [None] * world
+        dist.all_gather_object(allp, parity)
+        parity = {"per_rank": allp}
+    if live_fixture and rank == 0:
+        write_live_fixture(args, cfg, prof, fixture_records, fixture_requests, trace)
 
     if rank == 0:
         line = {
             "metric": "decode tok/s at 25% expert-cache budget", "value": tok_s, "unit": "tok/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16" if args.bits == 16 else "int4 weights, bf16 activations",
-            "data": "synthetic (reference trace-generator routing GenParams(1.0,0.85,0.6), random-init N(0,0.02^2) bf16 weights)",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16" if args.bits == 16 else "int4 weights, bf16 activations",
+            "data": "synthetic (reference trace-generator routing GenParams(1.0,0.85,0.6), random-init N(0,0.02^2) "
+                    "bf16 weights)",
             "config": {"workload": f"{args.shape}-shaped MoE decode, batch 1, {args.ratio:.0%} expert-cache budget",
                        "shape": args.shape, "layers": cfg.num_layers, "experts": cfg.num_routed,
-                       "top_k": cfg.num_activated, "hidden": H, "inter": I, "cache_slots": moe.capacity,
-                       "host_images": moe.host_images, "policy": args.policy, "prefetch": args.prefetch,
+                       "top_k": cfg.num_activated, "hidden": H, "inter": I, "cache_slots": moe_capacity(cfg, args),
+                       "host_images": host_images, "policy": args.policy, "prefetch": args.prefetch,
                        "predict": args.predict, "scheduling": args.scheduling,
                        "l2": f"each step streams {cfg.num_layers * cfg.num_activated} expert evaluations x "
                              f"{image_bytes / 1e6:.1f} MB of weights (>> 126 MB L2); no flush needed",
                        "parallelism": f"ep{world}" if world > 1 else "single", "weight_bits": args.bits,
-                       "ep_exchange": moe.exchange if exchange_note is None else exchange_note},
+                       "ep_exchange": (exchange_note or args.exchange) if world > 1 else "none"},
             "prefill": {"tokens": args.prefill, "ms": prefill_ms, "cold_cache": True,
                         "gpu_experts": sum(s.n_gpu for s in pst), "cpu_experts": sum(s.n_cpu for s in pst),
                         "transfers": sum(s.n_transfer for s in pst)},
@@ -497,17 +658,71 @@ def run_ours(args) -> None:
                          "host_decide_us_per_layer": statistics.mean(s.t_decide_us for s in stats_all),
                          "host_wait_router_us_per_layer": statistics.mean(s.t_wait_router_us for s in stats_all),
                          "cpu_worker_ms": sum(s.t_cpu_us for s in stats_all) / 1e3 / args.steps},
-            "profile": {k: getattr(cal.profile, k) for k in ("gpu_time_per_expert", "cpu_slope", "transfer_bandwidth",
-                                                              "transfer_latency", "gpu_slope",
-                                                              "cpu_first_expert_penalty")},
+            "profile": {k: getattr(base_profile, k) for k in ("gpu_time_per_expert", "cpu_slope",
+                                                               "transfer_bandwidth", "transfer_latency", "gpu_slope",
+                                                               "cpu_first_expert_penalty")},
             "prefill_profile": {k: getattr(prefill_profile, k) for k in ("gpu_time_per_expert", "cpu_slope",
                                                                           "gpu_slope", "cpu_first_expert_penalty")},
+            "model_vs_measured": model_check,
+            "decision_path_baseline": decision_baseline,
             "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks.summary(), "parity": parity,
             "setup_s": setup_s,
         }
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def moe_capacity(cfg, args) -> int:
+    from paper_2504_05897_b200.engine import cache_capacity
+    return cache_capacity(cfg, args.ratio)
+
+
+def write_live_fixture(args, cfg, prof, records, requests, trace) -> None:
+    """Live-run decision fixture of THIS bench configuration: the prefill and
+    warm-up decode passes' LayerRequests (from the GPU router) in the
+    reference's trace format, the profile the runtime planned with, and the
+    SHA-256 of the runtime's decision stream (tests/test_live_fixture.py
+    replays it through the unmodified reference run_trace)."""
+    import tempfile
+
+    sys.path.insert(0, str(ROOT / "tests" / "golden"))
+    from stream import digest, from_records
+
+    from paper_2504_05897_b200 import core as mcore
+    from paper_2504_05897_b200.tracegen import save_trace
+    passes = []
+    for i, reqs in enumerate(requests):
+        fwd = trace.passes[i]
+        passes.append(mcore.ForwardPass(fwd.stage, fwd.token_count, tuple(
+            mcore.make_layer_request(l, list(map(int, lo)), list(map(float, sc))) for l, (lo, sc) in enumerate(reqs))))
+    live = mcore.Trace(cfg, tuple(passes), {"source": f"live B200 run, bench.py --shape {args.shape} "
+                                                      f"--ratio {args.ratio} (GPU router on generator logits)"})
+    with tempfile.TemporaryDirectory() as d:
+        f = Path(d) / "t.jsonl"
+        save_trace(live, f)
+        text = f.read_text()
+    import torch
+    out = {"policy": args.policy, "prefetch": args.prefetch, "ratio": args.ratio, "seed": args.seed,
+           "profile": {k: getattr(prof, k) for k in prof.__dataclass_fields__}, "trace_jsonl": text,
+           "runtime_stream_sha256": digest(from_records(records, args.policy == "mrs")),
+           "gpu": torch.cuda.get_device_name(0)}
+    Path(args.live_fixture).parent.mkdir(parents=True, exist_ok=True)
+    Path(args.live_fixture).write_text(json.dumps(out))
+
+
+def spawn_ranks(argv: list[str], n: int) -> int:
+    """`bench.py --gpus N` launched without torchrun: start N ranks (one per GPU) itself."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # NCCL's init log (communicator ranks) on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + argv
+    return subprocess.call(cmd, env=env)
 
 
 def main() -> None:
@@ -520,10 +735,10 @@ def main() -> None:
     ap.add_argument("--ratio", type=float, default=0.25)
     ap.add_argument("--bits", type=int, default=16, choices=[16, 4],
                     help="expert weights: bf16 (BASELINE config) or the paper's 4-bit (int4 g128)")
-    ap.add_argument("--exchange", default="p2p", choices=["p2p", "dispatch", "allreduce"],
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "dispatch", "nccl_a2a", "allreduce"],
                     help="expert parallelism: replicated tokens + fused peer-memory reduce (p2p), token-sharded "
-                         "all-to-all dispatch/return over peer memory (dispatch), or replicated + process-group "
-                         "all-reduce (allreduce)")
+                         "all-to-all dispatch/return over peer memory (dispatch) or over NCCL grouped send/recv "
+                         "(nccl_a2a), or replicated + NCCL all-reduce (allreduce)")
     ap.add_argument("--prefill", type=int, default=1024)
     ap.add_argument("--policy", default="mrs", choices=["mrs", "lru", "lfu"])
     ap.add_argument("--scheduling", default="hybrid",
@@ -536,8 +751,13 @@ def main() -> None:
     ap.add_argument("--host-images", type=int, default=None)
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--host-bw-gbs", type=float, default=0.0, help="<= 0: measure")
-    ap.add_argument("--ref-layers", type=int, default=4)
+    ap.add_argument("--cpu-baseline-steps", type=int, default=3,
+                    help="decode tokens of the bounded CPU-baseline sample in our arm's line")
+    ap.add_argument("--ref-prefill", action=argparse.BooleanOptionalAction, default=True,
+                    help="reference arm: also time one all-CPU prefill of --prefill tokens")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--live-fixture", default=None,
+                    help="write a live-run decision fixture (prefill + warm-up passes) to this path")
     ap.add_argument("--profile-file", default=None, help="HardwareProfile key=value file instead of calibrating")
     ap.add_argument("--save-profile", default=None, help="write the calibrated HardwareProfile here")
     ap.add_argument("--prefill-profile-file", default=None)
@@ -548,6 +768,8 @@ def main() -> None:
         raise SystemExit("--warmup must be >= 3")
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(sys.argv[1:], args.gpus))
     else:
         run_ours(args)
 

@@ -14,6 +14,7 @@
 // same layer, engine.py:318-330), and a kernel waits for its slot's copy.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdlib>
@@ -113,7 +114,7 @@ struct Runtime {
   std::vector<cudaEvent_t> use_ev;
   int64_t use_seq = 0, copy_waited_seq = 0;
   cudaStream_t last_compute = nullptr;
-  cudaEvent_t ev_req = nullptr, ev_rows = nullptr;
+  cudaEvent_t ev_req = nullptr, ev_rows = nullptr, ev_switch = nullptr;
   // device scratch
   int32_t *sel = nullptr, *counts = nullptr, *offsets = nullptr, *pos = nullptr, *row_src = nullptr;
   float *w = nullptr, *probs = nullptr, *out = nullptr;
@@ -226,7 +227,11 @@ struct Runtime {
       slot_bytes = static_cast<size_t>(3) * H * I * 2;
     }
     slot_elems = slot_bytes / 2;
-    n_slots = c.capacity + static_cast<int64_t>(L) * S;
+    // [0, capacity) cache slots, then the shared chunks, then one staging slot
+    // for transfers that enter no cache slot (capacity 0, e.g. a small budget
+    // or an expert-parallel rank whose share rounds to 0: the plan still
+    // copies and computes them on the GPU, they are just not kept)
+    n_slots = c.capacity + static_cast<int64_t>(L) * S + 1;
     if (n_slots > 0) RT_CUDA(cudaMalloc(&pool, static_cast<size_t>(n_slots) * slot_bytes));
     RT_CUDA(cudaHostAlloc(&store, static_cast<size_t>(c.host_images) * slot_bytes, cudaHostAllocPortable));
     RT_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
@@ -242,6 +247,7 @@ struct Runtime {
     }
     RT_CUDA(cudaEventCreateWithFlags(&ev_req, cudaEventDisableTiming));
     RT_CUDA(cudaEventCreateWithFlags(&ev_rows, cudaEventDisableTiming));
+    RT_CUDA(cudaEventCreateWithFlags(&ev_switch, cudaEventDisableTiming));
     const size_t T = static_cast<size_t>(c.max_tokens);
     const size_t rows = T * Kp;
     RT_CUDA(cudaMalloc(&sel, rows * 4));
@@ -303,6 +309,7 @@ struct Runtime {
     }
     if (ev_req) cudaEventDestroy(ev_req);
     if (ev_rows) cudaEventDestroy(ev_rows);
+    if (ev_switch) cudaEventDestroy(ev_switch);
     if (copy) cudaStreamDestroy(copy);
     if (lcounts) cudaFree(lcounts);
     if (q4_scratch) cudaFree(q4_scratch);
@@ -326,6 +333,7 @@ struct Runtime {
     return (static_cast<int64_t>(layer) * n_home + expert / W) % cfg.host_images;
   }
   int64_t shared_slot(int layer, int chunk) const { return cfg.capacity + static_cast<int64_t>(layer) * S + chunk; }
+  int64_t staging_slot() const { return n_slots - 1; }
   uint16_t *slot_ptr(int64_t s) const { return pool + static_cast<size_t>(s) * slot_elems; }
   const uint16_t *image_ptr(uint32_t ref) const {
     return store + static_cast<size_t>(image_of(ref_layer(ref), ref_expert(ref))) * slot_elems;
@@ -385,6 +393,34 @@ struct Runtime {
     for (int i = 0; i < n; ++i) slot_use_seq[g[i].slot] = use_seq;
   }
 
+  // The fixed-residency baselines plan GPU experts as already cached
+  // (engine.py:171-205): their experts must have been preloaded into slots.
+  // Checked before the engine mutates any state, with a clear message.
+  void check_fixed_residency(int layer) const {
+    const int sch = engine->cfg.scheduling;
+    if (sch != HM_SCHED_STATIC_SPLIT && sch != HM_SCHED_FIXED_MAP) return;
+    for (int e = 0; e < N; ++e) {
+      if (loads[e] <= 0) continue;
+      const uint32_t r = pack_ref(layer, e);
+      const bool gpu = sch == HM_SCHED_STATIC_SPLIT ? layer < engine->cfg.split_point
+                                                    : engine->fixed_pinned.count(r) > 0;
+      if (!gpu) continue;
+      auto it = engine->cache.resident.find(r);
+      HM_REQUIRE(it != engine->cache.resident.end() && it->second.slot >= 0 && it->second.slot < cfg.capacity,
+                 HM_EVALUE,
+                 std::string(sch == HM_SCHED_STATIC_SPLIT ? "static_layer_split" : "fixed_frequency_map") +
+                     " plans expert (" + std::to_string(layer) + ", " + std::to_string(e) +
+                     ") on the GPU but it is not preloaded into an HBM slot (HybridMoE.preload)");
+    }
+  }
+
+  int64_t checked_slot(uint32_t ref, int64_t slot) const {
+    HM_REQUIRE(slot >= 0 && slot < cfg.capacity, HM_EVALUE,
+               "expert (" + std::to_string(ref_layer(ref)) + ", " + std::to_string(ref_expert(ref)) +
+                   ") has no HBM slot (resident beyond the cache capacity)");
+    return slot;
+  }
+
   void forward_layer(int layer, const uint16_t *x, const float *logits, int T, int ld, uint16_t *y,
                      const int32_t *pred_layers, const int64_t *pred_loads, int n_pred, cudaStream_t st,
                      hm_layer_stats *stats) {
@@ -394,8 +430,16 @@ struct Runtime {
     hm_layer_stats s{};
     void *vs = static_cast<void *>(st);
     const int rows = T * Kp;
-    if (st != last_compute) {  // a new compute stream: order it after every expert kernel so far
-      if (use_seq > 0) RT_CUDA(cudaStreamWaitEvent(st, use_ev[use_seq % kUseRing], 0));
+    if (st != last_compute) {
+      // a new compute stream: order it after ALL work of the previous one (the
+      // combine / MRS launches still read out, pos, w, scores_dev and the
+      // mapped h_out that this layer's router and host worker overwrite)
+      if (last_compute != nullptr) {
+        RT_CUDA(cudaEventRecord(ev_switch, last_compute));
+        RT_CUDA(cudaStreamWaitEvent(st, ev_switch, 0));
+      } else if (use_seq > 0) {
+        RT_CUDA(cudaStreamWaitEvent(st, use_ev[use_seq % kUseRing], 0));
+      }
       last_compute = st;
     }
     // (0) router, LayerRequest, permutation -- all on the compute stream; the
@@ -474,6 +518,7 @@ struct Runtime {
       scores[e] = tot > 0.0 ? h_score_sum[e] / tot : 0.0;  // == the fused kernel's scores, bit for bit
       h_scores[e] = scores[e];
     }
+    check_fixed_residency(layer);
     engine->run_layer(layer, loads.data(), scores.data(), N, pred_layers, pred_loads, n_pred);
     const LayerRecord &rec = engine->rec;
     s.makespan_planned = rec.plan.makespan;
@@ -507,7 +552,7 @@ struct Runtime {
     for (const Event &ev : rec.plan.events) {
       if (ev.device != HM_DEV_GPU || assign_of(ev.ref) != HM_ASSIGN_GPU_CACHED) continue;
       const int e = ref_expert(ev.ref);
-      const int64_t slot = engine->cache.resident.at(ev.ref).slot;
+      const int64_t slot = checked_slot(ev.ref, engine->cache.resident.at(ev.ref).slot);
       wait_ready(slot, st);  // a prefetch may still be in flight
       batch.push_back(hm_group{static_cast<int32_t>(slot), h_offsets[e], h_counts[e], 0});
     }
@@ -537,11 +582,29 @@ struct Runtime {
       }
     };
     for (size_t i = 0; i < rec.demand.size(); ++i) {
-      copy_and_maybe_compute(rec.demand[i].first, rec.demand_slots[i], true);
+      copy_and_maybe_compute(rec.demand[i].first, checked_slot(rec.demand[i].first, rec.demand_slots[i]), true);
       ++s.n_transfer;
     }
+    // transfers that entered no cache slot (capacity 0: engine.py:318 inserts
+    // only when capacity > 0) still run where the plan put them: through the
+    // staging slot, one at a time (each copy waits for the previous reader)
+    if (rec.demand.size() < static_cast<size_t>(std::count_if(
+                                rec.plan.events.begin(), rec.plan.events.end(),
+                                [](const Event &e) { return e.kind == HM_KIND_TRANSFER; }))) {
+      std::vector<const Event *> xf;
+      for (const Event &e : rec.plan.events)
+        if (e.kind == HM_KIND_TRANSFER) xf.push_back(&e);
+      std::stable_sort(xf.begin(), xf.end(), [](const Event *a, const Event *b) { return a->start < b->start; });
+      for (const Event *e : xf) {
+        bool inserted = false;
+        for (auto &d : rec.demand) inserted = inserted || d.first == e->ref;
+        if (inserted) continue;
+        copy_and_maybe_compute(e->ref, staging_slot(), true);
+        ++s.n_transfer;
+      }
+    }
     for (size_t i = 0; i < rec.chosen.size(); ++i) {
-      copy_and_maybe_compute(rec.chosen[i].first, rec.chosen_slots[i], false);
+      copy_and_maybe_compute(rec.chosen[i].first, checked_slot(rec.chosen[i].first, rec.chosen_slots[i]), false);
       ++s.n_prefetch;
     }
 

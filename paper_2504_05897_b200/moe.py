@@ -201,6 +201,17 @@ class HybridMoE:
         self.gate_w: torch.Tensor | None = None
         self.max_tokens = max_tokens
         self._bufs: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
+        # fixed residency of the baseline schedulings: static_layer_split keeps
+        # the layers below the split on the GPU (engine.py:185-192); those
+        # experts (this rank's home share) are copied into slots once weights exist
+        self._fixed_refs: list[tuple[int, int]] = []
+        self._weights_ready = False
+        if policy.scheduling == "static_layer_split":
+            refs = [(l, e) for l in range(split) for e in range(self.N) if e % self.ep_world == self.ep_rank]
+            if len(refs) > self.capacity:
+                raise ValueError(f"static_layer_split keeps {len(refs)} experts of layers < {split} on this GPU, "
+                                 f"more than its {self.capacity} cache slots")
+            self._fixed_refs = refs
 
     def __del__(self) -> None:
         if getattr(self, "_rt", None):
@@ -242,6 +253,8 @@ class HybridMoE:
         self.gate_w = (torch.randn((self.L, self.ld, self.H), generator=g, device="cuda") / math.sqrt(self.H)).to(
             torch.bfloat16)
         torch.cuda.synchronize()
+        self._weights_ready = True
+        self._apply_residency()
 
     def init_seeded_weights(self, base_seed: int = 0) -> None:
         """Per-expert seeded init (torch.Generator seed 1000*layer +
@@ -263,6 +276,13 @@ class HybridMoE:
         self.gate_w = (torch.randn((self.L, self.ld, self.H), generator=g, device="cuda") / math.sqrt(self.H)).to(
             torch.bfloat16)
         torch.cuda.synchronize()
+        self._weights_ready = True
+        self._apply_residency()
+
+    def _apply_residency(self) -> None:
+        """(Re)copy the fixed-residency experts into their slots (after weights change)."""
+        if self._fixed_refs and self._weights_ready:
+            self.preload(self._fixed_refs)
 
     def set_profile(self, profile: HardwareProfile) -> None:
         """Plan the following passes with another calibrated profile (e.g. the
@@ -281,10 +301,13 @@ class HybridMoE:
 
     def set_fixed_gpu_set(self, refs) -> None:
         """fixed_frequency_map's GPU-pinned set (engine.py:195-231), made resident."""
-        refs = list(refs)
-        arr = (C.c_uint32 * max(1, len(refs)))(*[(int(l) << 16) | int(e) for l, e in refs])
+        refs = [(int(l), int(e)) for l, e in refs]
+        if len(refs) > self.capacity:
+            raise ValueError(f"fixed GPU set of {len(refs)} experts exceeds the {self.capacity} cache slots")
+        arr = (C.c_uint32 * max(1, len(refs)))(*[(l << 16) | e for l, e in refs])
         check(lib.hm_engine_set_fixed_pinned(self.engine._h, arr, len(refs)))
-        self.preload(refs)
+        self._fixed_refs = refs
+        self._apply_residency()
 
     def image_of(self, layer: int, expert: int) -> int:
         v = C.c_int64()
