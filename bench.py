@@ -574,7 +574,12 @@ def run_ours(args) -> None:
                 "bytes_per_launch": kbytes.value / max(1, kn.value), "peak_kind": pk_kind,
                 "timed_in": "separate instrumented passes (CUDA events around each expert-FFN launch), "
                             "not the headline timed region"}
-    # plan-conditional roofline of the whole step: max(B_gpu/BW_hbm, B_cpu/BW_host, B_h2d/BW_pcie) per layer
+    # plan-conditional roofline of the whole step: max(B_gpu/BW_hbm, B_cpu/BW_host, B_h2d/BW_pcie) per layer;
+    # host bandwidth = the better of the read probe and what the worker itself streamed in the step
+    cpu_us = sum(s.t_cpu_us for s in stats_all)
+    worker_gbs = sum(s.bytes_cpu for s in stats_all) / (cpu_us * 1e-6) / 1e9 if cpu_us > 0 else 0.0
+    host_probe_gbs = host_bw_gbs
+    host_bw_gbs = max(host_bw_gbs, worker_gbs)
     bw_host = host_bw_gbs * 1e9
     bw_pcie = base_profile.transfer_bandwidth  # bytes / s, fitted at warm-up
     bound_s = sum(max(s.bytes_gpu / (hbm_peak * 1e9), s.bytes_cpu / bw_host, s.bytes_h2d / bw_pcie)
@@ -653,6 +658,7 @@ def run_ours(args) -> None:
             "step_roofline": {"bound": "plan-conditional max(B_gpu/HBM, B_cpu/host DRAM, B_h2d/PCIe)",
                               "bound_ms_per_step": 1e3 * bound_s / args.steps,
                               "frac": (1e3 * bound_s / args.steps) / ms_step, "host_bw_gbs": host_bw_gbs,
+                              "host_read_probe_gbs": host_probe_gbs, "host_worker_gbs": worker_gbs,
                               "pcie_gbs": bw_pcie / 1e9},
             "per_step": {"gpu_experts": n_gpu, "cpu_experts": n_cpu, "transfers": n_xfer,
                          "host_decide_us_per_layer": statistics.mean(s.t_decide_us for s in stats_all),

@@ -5,9 +5,12 @@ Measures the three resources the decision core plans with and fits a
 costs.py:134-219), all in seconds, for one expert of shape (H, I):
 
   gpu   one expert through ``hm_expert_ffn`` at loads 1..512 tokens (CUDA events)
-  cpu   one expert on the AVX-512 host worker at decode loads 1..4, in bursts of
-        three after an idle gap: position 0 is the cold first expert of a
-        burst (the reference's first-expert penalty, Fig. 3e)
+  cpu   one expert on the AVX-512 host worker, in bursts of three after an idle
+        gap: position 0 is the cold first expert of a burst (the reference's
+        first-expert penalty, Fig. 3e).  At decode (every load 1) through the
+        worker's decode entry (hm_cpu_experts_decode, the call the runtime
+        makes per layer) after a gap like the step's router wait, so the
+        fitted slope is the per-expert time the step actually pays.
   pcie  pinned H2D copies of 1/4, 1/2 and 1 expert image (CUDA events)
 """
 from __future__ import annotations
@@ -34,6 +37,9 @@ def measure_samples(H: int, I: int, gpu_loads=(1, 2, 4, 8, 32, 128, 256, 384, 51
 
     q4 = weight_bits == 4
     elems = 3 * H * I
+    # host images well beyond the last-level cache (small experts would
+    # otherwise be served from a 60-300 MB LLC and look faster than in the step)
+    n_images = max(n_images, -(-(512 << 20) // (elems * (1 if q4 else 2))))
     slot_elems = elems
     if q4:
         nb = C.c_size_t()
@@ -85,14 +91,22 @@ def measure_samples(H: int, I: int, gpu_loads=(1, 2, 4, 8, 32, 128, 256, 384, 51
     try:
         xs = np.ascontiguousarray(x[: max(cpu_loads)].view(torch.int16).cpu().numpy().view(np.uint16))
         outs = np.empty((max(cpu_loads), H), dtype=np.float32)
+        decode = all(m == 1 for m in cpu_loads)
         for m in cpu_loads:
             for burst in range(cpu_bursts):
-                time.sleep(0.02)
+                time.sleep(1e-4 if decode else 0.02)
                 for pos in range(3):
                     img = host[(burst * 3 + pos) % n_images]
-                    t0 = time.perf_counter()
-                    fn = lib.hm_cpu_expert_q4 if q4 else lib.hm_cpu_expert
-                    check(fn(cpool, img.data_ptr(), H, I, xs.ctypes.data, m, outs.ctypes.data))
+                    if decode:
+                        ip, xp_, op = (C.c_void_p * 1)(img.data_ptr()), (C.c_void_p * 1)(xs.ctypes.data), \
+                            (C.c_void_p * 1)(outs.ctypes.data)
+                        fn = lib.hm_cpu_experts_decode_q4 if q4 else lib.hm_cpu_experts_decode
+                        t0 = time.perf_counter()
+                        check(fn(cpool, ip, xp_, 1, H, I, op))
+                    else:
+                        fn = lib.hm_cpu_expert_q4 if q4 else lib.hm_cpu_expert
+                        t0 = time.perf_counter()
+                        check(fn(cpool, img.data_ptr(), H, I, xs.ctypes.data, m, outs.ctypes.data))
                     samples.append(CalibrationSample("cpu", float(m), pos, time.perf_counter() - t0))
     finally:
         lib.hm_cpu_pool_destroy(cpool)
