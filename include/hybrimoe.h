@@ -347,6 +347,7 @@ typedef struct hm_group {
 #define HM_FFN_AUTO 0 /* <= 4 rows: weight-streaming GEMV; larger: tcgen05 GEMM */
 #define HM_FFN_GEMV 1
 #define HM_FFN_GEMM 2
+#define HM_FFN_GEMV_SPLIT 3 /* the two-launch ffn1 -> ffn2 GEMV pair (A/B of the fused persistent GEMV) */
 /* out[rows of g] = W2_g (silu(Wg_g x) * (Wu_g x)) for every group (groups is
  * a HOST array).  h [total_rows, I] bf16 scratch, out [total_rows, H] fp32. */
 int hm_expert_ffn(const uint16_t *pool, int n_slots, int H, int I, const hm_group *groups,
@@ -557,6 +558,34 @@ int hm_ep_dispatch_rows(hm_ep *ep, const uint16_t *xp, const int32_t *sel, const
 int hm_ep_return_rows(hm_ep *ep, const float *out, int rows, void *stream);
 /* Device pointers of this rank's received-rows (bf16) and returned-rows (fp32) buffers. */
 int hm_ep_dispatch_buffers(hm_ep *ep, uint16_t **xrecv, float **ret);
+/* NCCL transport of the token-sharded mode (grouped
+ * ncclSend/ncclRecv): the baseline of, and the fallback for, the peer-memory
+ * kernels when CUDA IPC between the ranks is unavailable.  Rank 0 makes the
+ * 128-byte ncclUniqueId, the caller distributes it (control plane), every rank
+ * creates its exchange with dispatch mode enabled.  Then, per layer,
+ * hm_ep_dispatch_meta = pack + in-place ncclAllGather of the [counts | sums]
+ * slots + the same table kernel (its count matrix also mirrored to mapped host
+ * memory); hm_ep_dispatch_rows / hm_ep_return_rows = one NCCL group of
+ * per-(expert, peer) sends and receives planned on the host from that matrix
+ * (hm_ep_a2a_plan), so they must be called after the meta flag was raised.
+ * libnccl.so.2 is loaded at run time. */
+int hm_ep_nccl_unique_id(void *id128);
+int hm_ep_create_nccl(int rank, int world, int max_rows, int H, const void *id128, int n_experts_total,
+                      int n_routed, int Kp, hm_ep **out);
+int hm_ep_uses_nccl(const hm_ep *ep);
+/* One rank's all-to-all(v) schedule from the all-gathered count matrix
+ * counts_all [world][n_experts_total] (direction 0: dispatch, local permuted
+ * rows -> home layouts; 1: return).  Ops in issue order; src_row / dst_row are
+ * row indices in the sender's / receiver's buffer.  ops = NULL: count only. */
+#define HM_A2A_SEND 0
+#define HM_A2A_RECV 1
+#define HM_A2A_COPY 2
+typedef struct hm_a2a_op {
+  int32_t kind, peer;
+  int64_t src_row, dst_row, rows;
+} hm_a2a_op;
+int hm_ep_a2a_plan(const int32_t *counts_all, int world, int n_experts_total, int n_routed, int rank,
+                   int direction, hm_a2a_op *ops, int max_ops, int *n_ops);
 /* Live prediction: gate_w [L][ld][H] bf16
  * (device; NULL disables) -- layer l's input through the gates of layers
  * l+1..l+horizon gives the predicted loads of forward_layer(n_pred =

@@ -255,7 +255,7 @@ for _name, (_args, _res) in _DEV_SIGS.items():
     _f = getattr(lib, _name)
     _f.argtypes = _args
     _f.restype = _res
-FFN_AUTO, FFN_GEMV, FFN_GEMM = 0, 1, 2
+FFN_AUTO, FFN_GEMV, FFN_GEMM, FFN_GEMV_SPLIT = 0, 1, 2, 3
 
 _HOST_SIGS = {
     "hm_cpu_pool_create": ([C.c_int, P(vp)], C.c_int),
@@ -348,9 +348,23 @@ for _name, (_args, _res) in {
     "hm_ep_enable_dispatch": ([vp, C.c_int, C.c_int, C.c_int, C.c_char_p], C.c_int),
     "hm_ep_open_peer_dispatch": ([vp, C.c_int, C.c_char_p], C.c_int),
     "hm_runtime_set_ep_dispatch": ([vp, vp], C.c_int),
+    "hm_ep_nccl_unique_id": ([C.c_char_p], C.c_int),
+    "hm_ep_create_nccl": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_int, C.c_int, C.c_int, P(vp)],
+                          C.c_int),
+    "hm_ep_uses_nccl": ([vp], C.c_int),
+    "hm_ep_a2a_plan": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, P(C.c_int)], C.c_int),
     "hm_runtime_set_lookahead": ([vp, vp, C.c_int, C.c_int], C.c_int),
     "hm_lookahead": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp], C.c_int),
 }.items():
     _f = getattr(lib, _name)
     _f.argtypes = _args
     _f.restype = _res
+
+
+class A2aOp(C.Structure):
+    """hm_a2a_op: one step of a rank's all-to-all(v) schedule (include/hybrimoe.h)."""
+    _fields_ = [("kind", C.c_int32), ("peer", C.c_int32), ("src_row", C.c_int64), ("dst_row", C.c_int64),
+                ("rows", C.c_int64)]
+
+
+HM_A2A_SEND, HM_A2A_RECV, HM_A2A_COPY = 0, 1, 2

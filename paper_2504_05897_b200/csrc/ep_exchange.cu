@@ -19,9 +19,13 @@
 // deadlock-free.  Inbox and flags are double-buffered by the parity of the
 // call sequence number: a rank can run at most one exchange ahead of a peer.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
+#include <string>
 #include <vector>
 
 #include "device.cuh"
@@ -202,11 +206,17 @@ __device__ void all_to_all_handshake(const DispParams &p, size_t off_flags, int 
   if (threadIdx.x == 0) *done = 0;
 }
 
+// GATHERED: the slots [par][*] of this rank's region were already filled by an
+// NCCL all-gather (NCCL transport), so step 1 (peer stores + flags) is skipped
+// and the [world][E] count matrix is also mirrored to the host (host_counts),
+// which sizes the grouped ncclSend/ncclRecv of the row all-to-alls.
+template <bool GATHERED>
 __global__ void __launch_bounds__(256) ep_meta_kernel(const __grid_constant__ DispParams p,
                                                       const int32_t *__restrict__ counts,
                                                       const double *__restrict__ score_sum, int32_t *dev_meta_i,
                                                       double *dev_meta_d, int32_t *host_meta_i, double *host_meta_d,
-                                                      uint32_t *host_flag, uint32_t host_seq) {
+                                                      uint32_t *host_flag, uint32_t host_seq,
+                                                      int32_t *host_counts) {
   __shared__ int32_t s_cnt[kEpMaxWorld][kDispMaxE];
   __shared__ double s_sum[kEpMaxWorld][256];
   __shared__ int32_t s_gc[kDispMaxE], s_rb[kDispMaxE];
@@ -214,6 +224,7 @@ __global__ void __launch_bounds__(256) ep_meta_kernel(const __grid_constant__ Di
   __shared__ double s_tot;
   const int par = static_cast<int>(p.seq & 1u), E = p.E, N = p.N, G = p.world;
   // 1. my counts and score sums into every rank's slot [par][me]
+  if (!GATHERED) {
   for (int r = 0; r < G; ++r) {
     char *slot = p.region[r] + p.off_meta + (static_cast<size_t>(par) * G + p.rank) * p.meta_slot;
     for (int e = threadIdx.x; e < E; e += blockDim.x) reinterpret_cast<int32_t *>(slot)[e] = counts[e];
@@ -228,6 +239,7 @@ __global__ void __launch_bounds__(256) ep_meta_kernel(const __grid_constant__ Di
     const uint32_t *f = reinterpret_cast<const uint32_t *>(p.region[p.rank] + p.off_mflags) + par * G + threadIdx.x;
     while (static_cast<int32_t>(ld_acquire_sys(f) - p.seq) < 0) {  // reached (wrap-safe)
     }
+  }
   }
   __syncthreads();
   // 2. gather every rank's slot from my own region
@@ -245,6 +257,7 @@ __global__ void __launch_bounds__(256) ep_meta_kernel(const __grid_constant__ Di
       p.src_base[s * E + e] = run;
       run += s_cnt[s][e];
       p.counts_all[s * E + e] = s_cnt[s][e];
+      if (GATHERED) host_counts[s * E + e] = s_cnt[s][e];
     }
     p.src_base[G * E + e] = run;
     c = run;
@@ -309,6 +322,17 @@ __global__ void __launch_bounds__(256) ep_meta_kernel(const __grid_constant__ Di
   }
 }
 
+// NCCL transport: this rank's counts and score sums into its own slot [par][rank]
+// (the in-place send buffer of the all-gather)
+__global__ void ep_pack_meta_kernel(const __grid_constant__ DispParams p, const int32_t *__restrict__ counts,
+                                    const double *__restrict__ score_sum) {
+  const int par = static_cast<int>(p.seq & 1u);
+  char *slot = p.region[p.rank] + p.off_meta + (static_cast<size_t>(par) * p.world + p.rank) * p.meta_slot;
+  for (int e = threadIdx.x; e < p.E; e += blockDim.x) reinterpret_cast<int32_t *>(slot)[e] = counts[e];
+  double *d = reinterpret_cast<double *>(slot + (static_cast<size_t>(p.E) * 4 + 7) / 8 * 8);
+  for (int e = threadIdx.x; e < p.N; e += blockDim.x) d[e] = score_sum[e];
+}
+
 // one block per 256 (row, 16-byte column) items of the local permuted rows
 __global__ void __launch_bounds__(256) ep_dispatch_kernel(const __grid_constant__ DispParams p,
                                                           const uint16_t *__restrict__ xp,
@@ -342,6 +366,116 @@ __global__ void __launch_bounds__(256) ep_return_kernel(const __grid_constant__ 
 
 }  // namespace
 
+// ---------------------------------------------------------------- NCCL transport
+// The token-sharded all-to-alls over NCCL (grouped ncclSend /
+// ncclRecv), the baseline and the fallback of the peer-memory kernels when
+// CUDA IPC between the ranks is unavailable.  libnccl is loaded at run time
+// (the copy torch already mapped into the process when there is one), so the
+// library has no link-time NCCL dependency.
+struct Nccl {
+  ncclResult_t (*get_unique_id)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*all_gather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  const char *(*error_string)(ncclResult_t) = nullptr;
+};
+
+const Nccl &nccl() {
+  static Nccl n;
+  static std::string err;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      err = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return;
+    }
+    auto sym = [&](const char *name) {
+      void *f = dlsym(h, name);
+      if (!f && err.empty()) err = std::string("libnccl lacks ") + name;
+      return f;
+    };
+    n.get_unique_id = reinterpret_cast<decltype(n.get_unique_id)>(sym("ncclGetUniqueId"));
+    n.comm_init_rank = reinterpret_cast<decltype(n.comm_init_rank)>(sym("ncclCommInitRank"));
+    n.comm_destroy = reinterpret_cast<decltype(n.comm_destroy)>(sym("ncclCommDestroy"));
+    n.all_gather = reinterpret_cast<decltype(n.all_gather)>(sym("ncclAllGather"));
+    n.send = reinterpret_cast<decltype(n.send)>(sym("ncclSend"));
+    n.recv = reinterpret_cast<decltype(n.recv)>(sym("ncclRecv"));
+    n.group_start = reinterpret_cast<decltype(n.group_start)>(sym("ncclGroupStart"));
+    n.group_end = reinterpret_cast<decltype(n.group_end)>(sym("ncclGroupEnd"));
+    n.error_string = reinterpret_cast<decltype(n.error_string)>(sym("ncclGetErrorString"));
+  });
+  if (!err.empty()) raise(HM_ECUDA, err);
+  return n;
+}
+
+#define HM_NCCL(call)                                                                                  \
+  do {                                                                                                 \
+    const ncclResult_t r_ = (call);                                                                    \
+    if (r_ != ncclSuccess) hm::raise(HM_ECUDA, std::string("NCCL: ") + hm::nccl().error_string(r_) + \
+                                                   " (" #call ")");                                  \
+  } while (0)
+
+// The all-to-all(v) schedule of one layer from the all-gathered [world][E]
+// count matrix -- the same layout the peer-memory kernels write (home layout:
+// experts in index order, inside an expert rows by source rank then source
+// order; a source's own rows stay in its expert-contiguous permuted order).
+// Between any two ranks the sends and the receives are both issued in expert
+// index order, so NCCL's in-order pairing of p2p operations matches them.
+void a2a_plan(const int32_t *cnt, int world, int E, int N, int rank, int direction, std::vector<hm_a2a_op> &ops) {
+  ops.clear();
+  const size_t SE = static_cast<size_t>(E);
+  std::vector<int64_t> loff(world * SE), sbase(world * SE), rbase(E);
+  std::vector<int64_t> run_home(world, 0);
+  auto home = [&](int e) { return (e < N ? e : e - N) % world; };
+  auto c = [&](int s, int e) { return static_cast<int64_t>(cnt[s * SE + e]); };
+  for (int s = 0; s < world; ++s) {
+    int64_t run = 0;
+    for (int e = 0; e < E; ++e) {
+      loff[s * SE + e] = run;
+      run += c(s, e);
+    }
+  }
+  for (int e = 0; e < E; ++e) {
+    int64_t run = 0;
+    for (int s = 0; s < world; ++s) {
+      sbase[s * SE + e] = run;
+      run += c(s, e);
+    }
+    rbase[e] = run_home[home(e)];
+    run_home[home(e)] += run;
+  }
+  if (direction == 0) {  // dispatch: local permuted rows -> home layouts
+    for (int e = 0; e < E; ++e) {
+      const int64_t n = c(rank, e), h = home(e);
+      if (n) ops.push_back(hm_a2a_op{h == rank ? HM_A2A_COPY : HM_A2A_SEND, static_cast<int32_t>(h),
+                                     loff[rank * SE + e], rbase[e] + sbase[rank * SE + e], n});
+    }
+    for (int e = 0; e < E; ++e)
+      if (home(e) == rank)
+        for (int s = 0; s < world; ++s)
+          if (s != rank && c(s, e))
+            ops.push_back(hm_a2a_op{HM_A2A_RECV, s, loff[s * SE + e], rbase[e] + sbase[s * SE + e], c(s, e)});
+  } else {  // return: home-layout output rows -> their sources' permuted positions
+    for (int e = 0; e < E; ++e)
+      if (home(e) == rank)
+        for (int s = 0; s < world; ++s)
+          if (c(s, e))
+            ops.push_back(hm_a2a_op{s == rank ? HM_A2A_COPY : HM_A2A_SEND, s, rbase[e] + sbase[s * SE + e],
+                                    loff[s * SE + e], c(s, e)});
+    for (int e = 0; e < E; ++e) {
+      const int h = home(e);
+      if (h != rank && c(rank, e))
+        ops.push_back(hm_a2a_op{HM_A2A_RECV, h, rbase[e] + sbase[rank * SE + e], loff[rank * SE + e], c(rank, e)});
+    }
+  }
+}
+
 struct EpExchange {
   int rank, world, max_rows, H, cs, max_tiles;
   size_t inbox_stride;
@@ -362,6 +496,30 @@ struct EpExchange {
          region_bytes = 0;
   int32_t *tables = nullptr;  // counts_all | recv_base | src_base | local_off | gcount | ret_map | done
   uint32_t dseq = 0;
+  // NCCL transport (hm_ep_create_nccl): no IPC, the region is private
+  bool use_nccl = false;
+  ncclComm_t comm = nullptr;
+  int32_t *h_counts = nullptr;   // mapped pinned [world][E]: the all-gathered count matrix
+  int32_t *dv_counts = nullptr;  // its device alias
+  std::vector<hm_a2a_op> plan;
+
+  // The rows of `plan` through grouped ncclSend/ncclRecv (local rows by a D2D
+  // copy); src/dst are the row bases, row_bytes the bytes of one row.
+  void run_plan(const char *src, char *dst, size_t row_bytes, cudaStream_t st) {
+    const Nccl &n = nccl();
+    for (const hm_a2a_op &o : plan)
+      if (o.kind == HM_A2A_COPY)
+        HM_CUDA(cudaMemcpyAsync(dst + o.dst_row * row_bytes, src + o.src_row * row_bytes, o.rows * row_bytes,
+                                cudaMemcpyDeviceToDevice, st));
+    HM_NCCL(n.group_start());
+    for (const hm_a2a_op &o : plan) {
+      if (o.kind == HM_A2A_SEND)
+        HM_NCCL(n.send(src + o.src_row * row_bytes, o.rows * row_bytes, ncclUint8, o.peer, comm, st));
+      else if (o.kind == HM_A2A_RECV)
+        HM_NCCL(n.recv(dst + o.dst_row * row_bytes, o.rows * row_bytes, ncclUint8, o.peer, comm, st));
+    }
+    HM_NCCL(n.group_end());
+  }
 
   static size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 
@@ -392,6 +550,8 @@ struct EpExchange {
     HM_CUDA(cudaMemset(region, 0, off_xrecv));  // metadata and flags
     peer_region[rank] = region;
     region_opened[rank] = true;
+    if (use_nccl)
+      for (int q = 0; q < world; ++q) region_opened[q] = true;  // no peer mappings: NCCL moves the rows
     const size_t nt = static_cast<size_t>(world) * E + E + (world + 1ull) * E + world * (E + 1ull) + E +
                       static_cast<size_t>(max_rows) * Kp + 2;
     HM_CUDA(cudaMalloc(&tables, nt * 4));
@@ -434,9 +594,18 @@ struct EpExchange {
     return p;
   }
 
-  EpExchange(int r, int w, int rows, int h) : rank(r), world(w), max_rows(rows), H(h) {
+  EpExchange(int r, int w, int rows, int h, const ncclUniqueId *nccl_id = nullptr)
+      : rank(r), world(w), max_rows(rows), H(h) {
     HM_REQUIRE(w >= 1 && w <= kEpMaxWorld && r >= 0 && r < w, HM_EVALUE, "expert-parallel world must be 1..8");
     HM_REQUIRE(rows >= 1 && h % 4 == 0, HM_EVALUE, "bad exchange shape");
+    if (nccl_id) {  // NCCL transport: a communicator instead of IPC inboxes
+      use_nccl = true;
+      HM_NCCL(nccl().comm_init_rank(&comm, world, *nccl_id, rank));
+      HM_CUDA(cudaHostAlloc(&h_counts, static_cast<size_t>(world) * kDispMaxE * 4, cudaHostAllocMapped));
+      HM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dv_counts), h_counts, 0));
+      for (int q = 0; q < world; ++q) opened[q] = true;
+      return;
+    }
     cs = (H + 4 * kEpThreads - 1) / (4 * kEpThreads);
     max_tiles = max_rows * cs;
     inbox_stride = static_cast<size_t>(max_rows) * H;
@@ -465,6 +634,8 @@ struct EpExchange {
     if (flags) cudaFree(flags);
     if (region) cudaFree(region);
     if (tables) cudaFree(tables);
+    if (h_counts) cudaFreeHost(h_counts);
+    if (comm) nccl().comm_destroy(comm);
   }
 };
 
@@ -549,8 +720,9 @@ int hm_ep_combine_allreduce(hm_ep *ep, const float *out, const float *host_out, 
 int hm_ep_enable_dispatch(hm_ep *ep, int n_experts_total, int n_routed, int Kp, void *region_handle) {
   HM_API_BEGIN
   auto *e = reinterpret_cast<hm::EpExchange *>(ep);
-  e->enable_dispatch(n_experts_total, n_routed, Kp);
   HM_REQUIRE(region_handle, HM_EVALUE, "null handle buffer");
+  HM_REQUIRE(!e->use_nccl, HM_EVALUE, "the NCCL transport enables dispatch at creation (hm_ep_create_nccl)");
+  e->enable_dispatch(n_experts_total, n_routed, Kp);
   HM_CUDA(cudaIpcGetMemHandle(static_cast<cudaIpcMemHandle_t *>(region_handle), e->region));
   HM_API_END
 }
@@ -577,9 +749,20 @@ int hm_ep_dispatch_meta(hm_ep *ep, const int32_t *counts, const double *score_su
   HM_REQUIRE(e->disp, HM_EVALUE, "dispatch mode not enabled");
   for (int r = 0; r < e->world; ++r) HM_REQUIRE(e->region_opened[r], HM_EVALUE, "dispatch peers not opened");
   ++e->dseq;
-  hm::ep_meta_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(e->params(), counts, score_sum, dev_meta_i,
-                                                                      dev_meta_d, host_meta_i, host_meta_d,
-                                                                      host_flag, host_seq);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const hm::DispParams p = e->params();
+  if (e->use_nccl) {  // pack my slot, in-place ncclAllGather of the slots, then the tables
+    hm::ep_pack_meta_kernel<<<1, 256, 0, st>>>(p, counts, score_sum);
+    HM_LAUNCH_CHECK();
+    char *slots = e->region + e->off_meta + static_cast<size_t>(e->dseq & 1u) * e->world * e->meta_slot;
+    HM_NCCL(hm::nccl().all_gather(slots + static_cast<size_t>(e->rank) * e->meta_slot, slots, e->meta_slot,
+                                  ncclUint8, e->comm, st));
+    hm::ep_meta_kernel<true><<<1, 256, 0, st>>>(p, counts, score_sum, dev_meta_i, dev_meta_d, host_meta_i,
+                                                host_meta_d, host_flag, host_seq, e->dv_counts);
+  } else {
+    hm::ep_meta_kernel<false><<<1, 256, 0, st>>>(p, counts, score_sum, dev_meta_i, dev_meta_d, host_meta_i,
+                                                 host_meta_d, host_flag, host_seq, nullptr);
+  }
   HM_LAUNCH_CHECK();
   HM_API_END
 }
@@ -589,9 +772,19 @@ int hm_ep_dispatch_rows(hm_ep *ep, const uint16_t *xp, const int32_t *sel, const
   HM_API_BEGIN
   auto *e = reinterpret_cast<hm::EpExchange *>(ep);
   HM_REQUIRE(e->disp && rows >= 0 && rows <= e->max_rows * e->Kp, HM_EVALUE, "bad dispatch");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (e->use_nccl) {  // the host holds the count matrix (after the meta flag): grouped send/recv
+    hm::a2a_plan(e->h_counts, e->world, e->E, e->N, e->rank, 0, e->plan);
+    int64_t recv = 0;
+    for (const hm_a2a_op &o : e->plan)
+      if (o.kind != HM_A2A_SEND) recv = std::max(recv, o.dst_row + o.rows);
+    HM_REQUIRE(recv <= static_cast<int64_t>(e->max_rows) * e->Kp, HM_EVALUE, "received rows exceed the buffer");
+    e->run_plan(reinterpret_cast<const char *>(xp), e->region + e->off_xrecv, static_cast<size_t>(e->H) * 2, st);
+    return HM_OK;
+  }
   const long items = static_cast<long>(rows) * (e->H / 8);
   const int grid = static_cast<int>(std::max<long>(1, (items + 255) / 256));
-  hm::ep_dispatch_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(e->params(), xp, sel, row_src, rows);
+  hm::ep_dispatch_kernel<<<grid, 256, 0, st>>>(e->params(), xp, sel, row_src, rows);
   HM_LAUNCH_CHECK();
   HM_API_END
 }
@@ -600,8 +793,55 @@ int hm_ep_return_rows(hm_ep *ep, const float *out, int rows, void *stream) {
   HM_API_BEGIN
   auto *e = reinterpret_cast<hm::EpExchange *>(ep);
   HM_REQUIRE(e->disp && rows >= 0 && rows <= e->max_rows * e->Kp, HM_EVALUE, "bad return");
-  hm::ep_return_kernel<<<std::max(1, rows), 256, 0, static_cast<cudaStream_t>(stream)>>>(e->params(), out, rows);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (e->use_nccl) {
+    hm::a2a_plan(e->h_counts, e->world, e->E, e->N, e->rank, 1, e->plan);
+    e->run_plan(reinterpret_cast<const char *>(out), e->region + e->off_ret, static_cast<size_t>(e->H) * 4, st);
+    return HM_OK;
+  }
+  hm::ep_return_kernel<<<std::max(1, rows), 256, 0, st>>>(e->params(), out, rows);
   HM_LAUNCH_CHECK();
+  HM_API_END
+}
+
+int hm_ep_nccl_unique_id(void *id) {
+  HM_API_BEGIN
+  HM_REQUIRE(id, HM_EVALUE, "null id buffer");
+  HM_NCCL(hm::nccl().get_unique_id(static_cast<ncclUniqueId *>(id)));
+  HM_API_END
+}
+
+int hm_ep_create_nccl(int rank, int world, int max_rows, int H, const void *id, int n_experts_total, int n_routed,
+                      int Kp, hm_ep **out) {
+  HM_API_BEGIN
+  HM_REQUIRE(out && id, HM_EVALUE, "null argument");
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof uid);
+  auto *e = new hm::EpExchange(rank, world, max_rows, H, &uid);
+  try {
+    e->enable_dispatch(n_experts_total, n_routed, Kp);
+  } catch (...) {
+    delete e;
+    throw;
+  }
+  *out = reinterpret_cast<hm_ep *>(e);
+  HM_API_END
+}
+
+int hm_ep_uses_nccl(const hm_ep *ep) { return reinterpret_cast<const hm::EpExchange *>(ep)->use_nccl ? 1 : 0; }
+
+int hm_ep_a2a_plan(const int32_t *counts_all, int world, int n_experts_total, int n_routed, int rank, int direction,
+                   hm_a2a_op *ops, int max_ops, int *n_ops) {
+  HM_API_BEGIN
+  HM_REQUIRE(counts_all && n_ops && world >= 1 && rank >= 0 && rank < world && n_routed >= 1 &&
+                 n_routed <= n_experts_total && (direction == 0 || direction == 1),
+             HM_EVALUE, "bad all-to-all plan arguments");
+  for (int i = 0; i < world * n_experts_total; ++i) HM_REQUIRE(counts_all[i] >= 0, HM_EVALUE, "negative count");
+  std::vector<hm_a2a_op> v;
+  hm::a2a_plan(counts_all, world, n_experts_total, n_routed, rank, direction, v);
+  *n_ops = static_cast<int>(v.size());
+  HM_REQUIRE(!ops || static_cast<int>(v.size()) <= max_ops, HM_EVALUE, "plan exceeds max_ops");
+  if (ops) std::copy(v.begin(), v.end(), ops);
   HM_API_END
 }
 

@@ -181,6 +181,182 @@ __global__ void __launch_bounds__(256) ffn2_gemv_kernel(const __grid_constant__ 
   }
 }
 
+// ------------------------------------------------------------ fused decode GEMV
+// ONE persistent launch per layer for ffn1 -> ffn2 (instead of two short
+// launches that each pay a ramp and a tail; DeepSeek's 4-6 small experts ran
+// at 3.7 TB/s that way).  Work items, claimed dynamically by warps:
+//   phase 1 item (g, i):   gate row i and up row i of group g's W13 (2 rows of
+//                          H), h[r, i] = bf16(silu(gate.x_r) * (up.x_r));
+//                          then done1[g] += 1 (release)
+//   phase 2 item (g, j..): NR2 rows of W2 (I columns), out[r, j] = W2[j].h_r;
+//                          the item's first weight loads are issued BEFORE
+//                          waiting for done1[g] == I (acquire), so the
+//                          phase boundary overlaps with DRAM streaming.
+// A warp moves to phase 2 only after the phase-1 counter is exhausted, i.e.
+// every phase-1 item is held by a running warp that never waits: no deadlock
+// whatever the residency.  Per lane, columns are accumulated in the same order
+// as ffn1/ffn2_gemv_kernel (c = lane*8 + 256k, k increasing), so the outputs
+// are bit-identical to the two-launch path.  The last warp to exit resets the
+// counters for the next launch on the stream.
+struct FusedGemvParams {
+  const uint16_t *pool;
+  size_t slot_elems;
+  int H, I, n_groups;
+  int n1, n2, items2_per_group;  // phase-1 items (= G*I), phase-2 items, per group
+  int total_warps;
+  const uint16_t *xp;
+  uint16_t *h;
+  float *out;
+  int32_t *ctr;  // [0] phase-1 claims, [1] phase-2 claims, [2] exits, [4 ..] done1[g]
+  int32_t slot[kMaxGroups];
+  int32_t row_begin[kMaxGroups];
+  int32_t row_count[kMaxGroups];
+};
+
+__device__ __forceinline__ int ld_acquire_gpu(const int32_t *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int MR, int NR2>
+__global__ void __launch_bounds__(256, MR == 1 ? 4 : 2) ffn_decode_fused_kernel(const __grid_constant__ FusedGemvParams p) {
+  const int lane = threadIdx.x & 31;
+  const int H = p.H, I = p.I;
+  int32_t *done1 = p.ctr + 4;
+  // ---------------- phase 1
+  for (;;) {
+    int it = 0;
+    if (lane == 0) it = atomicAdd(p.ctr, 1);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= p.n1) break;
+    const int g = it / I, i = it - g * I;
+    const int M = p.row_count[g], rb = p.row_begin[g];
+    const uint16_t *w13 = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_elems;
+    const size_t grow = static_cast<size_t>((i / kIlv) * 2 * kIlv + (i % kIlv));
+    const uint16_t *wg = w13 + grow * H;
+    const uint16_t *wu = wg + static_cast<size_t>(kIlv) * H;
+    const uint16_t *x = p.xp + static_cast<size_t>(rb) * H;
+    float ag[MR], au[MR];
+#pragma unroll
+    for (int m = 0; m < MR; ++m) ag[m] = au[m] = 0.f;
+    constexpr int U = 4;
+    for (int c0 = lane * 8; c0 < H; c0 += 256 * U) {
+      uint4 gv[U], uv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + u * 256;
+        if (c < H) {
+          gv[u] = dev::ld_stream(wg + c);
+          uv[u] = dev::ld_stream(wu + c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + u * 256;
+        if (c < H) {
+#pragma unroll
+          for (int m = 0; m < MR; ++m) {
+            if (m < M) {
+              const uint4 xv = __ldg(reinterpret_cast<const uint4 *>(x + static_cast<size_t>(m) * H + c));
+              ag[m] += dev::dot8(gv[u], xv);
+              au[m] += dev::dot8(uv[u], xv);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MR; ++m) {
+      if (m < M) {
+        const float gs = dev::warp_sum(ag[m]), us = dev::warp_sum(au[m]);
+        if (lane == 0) p.h[static_cast<size_t>(rb + m) * I + i] = dev::f2bf(dev::silu(gs) * us);
+      }
+    }
+    if (lane == 0) {
+      __threadfence();
+      atomicAdd(done1 + g, 1);
+    }
+  }
+  // ---------------- phase 2
+  constexpr int U2 = 8 / NR2;
+  for (;;) {
+    int it = 0;
+    if (lane == 0) it = atomicAdd(p.ctr + 1, 1);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= p.n2) break;
+    const int g = it / p.items2_per_group, j0 = (it - g * p.items2_per_group) * NR2;
+    const int M = p.row_count[g], rb = p.row_begin[g];
+    const uint16_t *w2 = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_elems + static_cast<size_t>(2) * I * H;
+    bool live[NR2];
+    const uint16_t *wr[NR2];
+#pragma unroll
+    for (int r = 0; r < NR2; ++r) {
+      live[r] = j0 + r < H;
+      wr[r] = w2 + static_cast<size_t>(live[r] ? j0 + r : j0) * I;
+    }
+    float acc[MR][NR2];
+#pragma unroll
+    for (int m = 0; m < MR; ++m)
+#pragma unroll
+      for (int r = 0; r < NR2; ++r) acc[m][r] = 0.f;
+    const uint16_t *hrow = p.h + static_cast<size_t>(rb) * I;
+    bool ready = false;
+    for (int c0 = lane * 8; c0 < I; c0 += 256 * U2) {
+      uint4 wv[NR2][U2];
+#pragma unroll
+      for (int r = 0; r < NR2; ++r)
+#pragma unroll
+        for (int u = 0; u < U2; ++u) {
+          const int c = c0 + u * 256;
+          if (c < I && live[r]) wv[r][u] = dev::ld_stream(wr[r] + c);
+        }
+      if (!ready) {  // h of group g complete? (the loads above are already in flight)
+        if (lane == 0)
+          while (ld_acquire_gpu(done1 + g) < I) __nanosleep(64);
+        __syncwarp();
+        ready = true;
+      }
+#pragma unroll
+      for (int u = 0; u < U2; ++u) {
+        const int c = c0 + u * 256;
+        if (c < I) {
+#pragma unroll
+          for (int m = 0; m < MR; ++m)
+            if (m < M) {
+              const uint4 hv = __ldcg(reinterpret_cast<const uint4 *>(hrow + static_cast<size_t>(m) * I + c));
+#pragma unroll
+              for (int r = 0; r < NR2; ++r)
+                if (live[r]) acc[m][r] += dev::dot8(wv[r][u], hv);
+            }
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MR; ++m) {
+      if (m < M) {
+#pragma unroll
+        for (int r = 0; r < NR2; ++r) {
+          if (!live[r]) continue;
+          const float s = dev::warp_sum(acc[m][r]);
+          if (lane == 0) p.out[static_cast<size_t>(rb + m) * H + j0 + r] = s;
+        }
+      }
+    }
+  }
+  // ---------------- the last warp out resets the counters
+  if (lane == 0) {
+    __threadfence();
+    if (atomicAdd(p.ctr + 2, 1) == p.total_warps - 1) {
+      p.ctr[0] = 0;
+      p.ctr[1] = 0;
+      for (int g = 0; g < p.n_groups; ++g) done1[g] = 0;
+      __threadfence();
+      p.ctr[2] = 0;
+    }
+  }
+}
+
 // ------------------------------------------------------------ tcgen05 GEMM
 constexpr int BM = 128, BK = 64, STAGES = 4;
 
@@ -469,9 +645,95 @@ void launch_pdl(K kernel, int grid, int smem, cudaStream_t st, const GemvParams 
   HM_LAUNCH_CHECK();
 }
 
+// HM_GEMV_FUSED=0 selects the two-launch ffn1/ffn2 pair (A/B and tests).
+bool gemv_fused_enabled() {
+  static const bool on = [] {
+    const char *e = std::getenv("HM_GEMV_FUSED");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+// Claim/completion counters of the fused GEMV, one zeroed set per stream
+// (the kernel's last warp re-zeroes them, so launches on one stream reuse it).
+int32_t *fused_counters(cudaStream_t st) {
+  static std::mutex mu;
+  static std::vector<std::pair<cudaStream_t, int32_t *>> sets;
+  std::lock_guard<std::mutex> g(mu);
+  for (auto &kv : sets)
+    if (kv.first == st) return kv.second;
+  int32_t *c = nullptr;
+  HM_CUDA(cudaMalloc(&c, (4 + kMaxGroups) * sizeof(int32_t)));
+  HM_CUDA(cudaMemset(c, 0, (4 + kMaxGroups) * sizeof(int32_t)));
+  HM_CUDA(cudaDeviceSynchronize());
+  sets.emplace_back(st, c);
+  return c;
+}
+
+template <int MR, int NR2>
+void launch_fused_one(const FusedGemvParams &p0, cudaStream_t st) {
+  static int per_sm = 0;
+  if (!per_sm) {
+    HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ffn_decode_fused_kernel<MR, NR2>, 256, 0));
+    per_sm = std::max(1, std::min(per_sm, 4));
+  }
+  FusedGemvParams p = p0;
+  const long warps_needed = static_cast<long>(p.n1);
+  const int grid = static_cast<int>(std::max<long>(1, std::min<long>(static_cast<long>(num_sms()) * per_sm,
+                                                                     (warps_needed + 7) / 8)));
+  p.total_warps = grid * 8;
+  ffn_decode_fused_kernel<MR, NR2><<<grid, 256, 0, st>>>(p);
+  HM_LAUNCH_CHECK();
+}
+
+void launch_gemv_fused(const uint16_t *pool, size_t slot_elems, int H, int I, const std::vector<hm_group> &gs,
+                       const uint16_t *xp, uint16_t *h, float *out, cudaStream_t st) {
+  FusedGemvParams p{};
+  p.pool = pool;
+  p.slot_elems = slot_elems;
+  p.H = H;
+  p.I = I;
+  p.n_groups = static_cast<int>(gs.size());
+  p.xp = xp;
+  p.h = h;
+  p.out = out;
+  p.ctr = fused_counters(st);
+  int mr = 1;
+  for (size_t g = 0; g < gs.size(); ++g) {
+    p.slot[g] = gs[g].slot;
+    p.row_begin[g] = gs[g].row_begin;
+    p.row_count[g] = gs[g].row_count;
+    mr = std::max(mr, gs[g].row_count);
+  }
+  // long W2 rows (Mixtral, I = 14336): one row per item, 8 loads in flight per
+  // lane; short rows (DeepSeek 1408, Qwen2 2560): two rows per item
+  const bool one = I >= 4096;
+  const int nr2 = one ? 1 : 2;
+  p.n1 = p.n_groups * I;
+  p.items2_per_group = (H + nr2 - 1) / nr2;
+  p.n2 = p.n_groups * p.items2_per_group;
+  switch (mr * 2 + (one ? 1 : 0)) {
+    case 2: launch_fused_one<1, 2>(p, st); break;
+    case 3: launch_fused_one<1, 1>(p, st); break;
+    case 4: launch_fused_one<2, 2>(p, st); break;
+    case 5: launch_fused_one<2, 1>(p, st); break;
+    default:
+      if (one)
+        launch_fused_one<4, 1>(p, st);
+      else
+        launch_fused_one<4, 2>(p, st);
+  }
+}
+
 void launch_gemv(const uint16_t *pool, size_t slot_elems, int H, int I, const std::vector<hm_group> &gs,
-                 const uint16_t *xp, uint16_t *h, float *out, cudaStream_t st) {
+                 const uint16_t *xp, uint16_t *h, float *out, cudaStream_t st, bool split = false) {
   if (gs.empty()) return;
+  if (!split && gemv_fused_enabled()) {
+    HM_REQUIRE(static_cast<int>(gs.size()) <= kMaxGroups, HM_EVALUE, "too many expert groups in one launch");
+    HM_REQUIRE(H % 8 == 0 && I % 8 == 0 && I % kIlv == 0, HM_EVALUE, "GEMV needs H % 8 == 0 and I % 128 == 0");
+    launch_gemv_fused(pool, slot_elems, H, I, gs, xp, h, out, st);
+    return;
+  }
   HM_REQUIRE(static_cast<int>(gs.size()) <= kMaxGroups, HM_EVALUE, "too many expert groups in one launch");
   HM_REQUIRE(H % 8 == 0 && I % 8 == 0 && I % kIlv == 0, HM_EVALUE, "GEMV needs H % 8 == 0 and I % 128 == 0");
   GemvParams p{};
@@ -635,7 +897,8 @@ int hm_expert_ffn(const uint16_t *pool, int n_slots, int H, int I, const hm_grou
                    gr.row_begin + gr.row_count <= total_rows,
                HM_EVALUE, "expert group outside the pool or the row range");
     if (gr.row_count == 0) continue;
-    const bool gemv = path == HM_FFN_GEMV || (path == HM_FFN_AUTO && gr.row_count <= hm::kGemvMaxRows);
+    const bool gemv = path == HM_FFN_GEMV || path == HM_FFN_GEMV_SPLIT ||
+                      (path == HM_FFN_AUTO && gr.row_count <= hm::kGemvMaxRows);
     if (gemv) {
       HM_REQUIRE(gr.row_count <= hm::kGemvMaxRows, HM_EVALUE, "GEMV path takes at most 4 rows per expert");
       small.push_back(gr);
@@ -646,7 +909,7 @@ int hm_expert_ffn(const uint16_t *pool, int n_slots, int H, int I, const hm_grou
   const size_t slot_elems = static_cast<size_t>(3) * H * I;
   for (size_t b = 0; b < small.size(); b += hm::kMaxGroups) {
     std::vector<hm_group> part(small.begin() + b, small.begin() + std::min(small.size(), b + hm::kMaxGroups));
-    hm::launch_gemv(pool, slot_elems, H, I, part, xp, h, out, st);
+    hm::launch_gemv(pool, slot_elems, H, I, part, xp, h, out, st, path == HM_FFN_GEMV_SPLIT);
   }
   for (size_t b = 0; b < big.size(); b += hm::kMaxGroups) {
     std::vector<hm_group> part(big.begin() + b, big.begin() + std::min(big.size(), b + hm::kMaxGroups));

@@ -55,6 +55,7 @@ int hm_ep_dispatch_meta(hm_ep *, const int32_t *, const double *, int32_t *, dou
 int hm_ep_dispatch_rows(hm_ep *, const uint16_t *, const int32_t *, const int32_t *, int, void *);
 int hm_ep_return_rows(hm_ep *, const float *, int, void *);
 int hm_ep_dispatch_buffers(hm_ep *, uint16_t **, float **);
+int hm_ep_uses_nccl(const hm_ep *);
 int hm_combine_tail(const float *, const float *, const uint64_t *, const int32_t *, const float *, int, int, int,
                     const uint16_t *, uint16_t *, double *, const double *, int, int, int, double, void *);
 }
@@ -488,7 +489,9 @@ struct Runtime {
       ++seq;
       ok(hm_ep_dispatch_meta(ep, lcounts, lsums, counts, score_sum, static_cast<int32_t *>(dv_hmeta),
                              reinterpret_cast<double *>(static_cast<char *>(dv_hmeta) + meta_ioff), dv_flag, seq, vs));
-      ok(hm_ep_dispatch_rows(ep, xp, sel, row_src, rows, vs));
+      // peer memory: the row all-to-all is a kernel sized on the device; NCCL
+      // sizes its sends on the host, after the meta flag (below)
+      if (!hm_ep_uses_nccl(ep)) ok(hm_ep_dispatch_rows(ep, xp, sel, row_src, rows, vs));
     } else {
       ok(hm_router_topk(logits, T, N, ld, K, cfg.renormalize, S, cfg.shared_gate_col, sel, w, probs, counts, vs));
       if (W > 1) ok(hm_mask_nonhome(sel, w, T * Kp, N, R, W, vs));
@@ -502,6 +505,7 @@ struct Runtime {
     double t0 = now_us();
     if (mirror || disp) {
       wait_flag(st);
+      if (disp && hm_ep_uses_nccl(ep)) ok(hm_ep_dispatch_rows(ep, xp, sel, row_src, rows, vs));
     } else {
       RT_CUDA(cudaEventSynchronize(ev_req));
     }

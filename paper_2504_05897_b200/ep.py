@@ -16,12 +16,18 @@ residual, pushing partials into the peers' inboxes over NVLink through CUDA
 IPC mappings -- or, as the baseline, by an all-reduce on the process group
 (NCCL on the GPUs; gloo in the CPU tests) followed by the residual add.
 
-Token-sharded mode (``exchange="dispatch"``): every rank holds and routes only
+Token-sharded mode (``exchange="dispatch"`` over peer memory, ``"nccl_a2a"``
+over NCCL grouped send/recv): every rank holds and routes only
 its own tokens; the global LayerRequest comes from an all-gather of the ranks'
 counts and score sums (rank-order sums, identical everywhere), token rows go
 to their experts' home ranks by an all-to-all over peer memory and the expert
 outputs come back by the reverse all-to-all before the local combine
-(csrc/ep_exchange.cu: ep_meta / ep_dispatch / ep_return kernels).
+(csrc/ep_exchange.cu: ep_meta / ep_dispatch / ep_return kernels).  With
+``NcclExchange`` the same three steps run as an ncclAllGather of the per-rank
+count/score slots followed by one NCCL group of per-(expert, peer) sends and
+receives each way, planned on the host from the gathered count matrix
+(``a2a_plan``, the native hm_ep_a2a_plan) -- the baseline of the peer-memory
+kernels and their fallback where CUDA IPC is unavailable.
 """
 from __future__ import annotations
 
@@ -111,6 +117,59 @@ class P2PExchange:
             raise PeerMemoryUnavailable("; ".join(bad))
         dist.barrier(group=group)
         self.rank, self.world, self.dispatch = rank, world, dispatch is not None
+
+    @property
+    def handle(self) -> int:
+        return self._h
+
+    def close(self) -> None:
+        from . import _lib
+        if getattr(self, "_h", None):
+            _lib.lib.hm_ep_destroy(self._h)
+            self._h = None
+
+
+def a2a_plan(counts_all, world: int, n_total: int, n_routed: int, rank: int, direction: int) -> list[tuple]:
+    """One rank's all-to-all(v) schedule (hm_ep_a2a_plan): (kind, peer, src_row,
+    dst_row, rows) in issue order; kind 0 send, 1 recv, 2 local copy;
+    direction 0 dispatch (local permuted rows -> home layouts), 1 return."""
+    import ctypes as C
+
+    import numpy as np
+
+    from . import _lib
+    cnt = np.ascontiguousarray(counts_all, dtype=np.int32).reshape(world, n_total)
+    n = C.c_int()
+    _lib.check(_lib.lib.hm_ep_a2a_plan(_lib.ptr(cnt, C.c_int32), world, n_total, n_routed, rank, direction, None, 0,
+                                       C.byref(n)))
+    ops = (_lib.A2aOp * max(1, n.value))()
+    _lib.check(_lib.lib.hm_ep_a2a_plan(_lib.ptr(cnt, C.c_int32), world, n_total, n_routed, rank, direction, ops,
+                                       n.value, C.byref(n)))
+    return [(o.kind, o.peer, o.src_row, o.dst_row, o.rows) for o in ops[: n.value]]
+
+
+class NcclExchange:
+    """Token-sharded exchange of one rank over NCCL (include/hybrimoe.h,
+    hm_ep_create_nccl).  Collective constructor: rank 0 makes the ncclUniqueId,
+    the process group distributes it (control plane only), every rank joins the
+    communicator with dispatch mode enabled."""
+
+    def __init__(self, rank: int, world: int, max_rows: int, hidden: int, dispatch: tuple[int, int, int],
+                 group=None) -> None:
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from . import _lib
+        uid = C.create_string_buffer(128)
+        if rank == 0:
+            _lib.check(_lib.lib.hm_ep_nccl_unique_id(uid))
+        box = [uid.raw if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        h = C.c_void_p()
+        _lib.check(_lib.lib.hm_ep_create_nccl(rank, world, max_rows, hidden, box[0], *dispatch, C.byref(h)))
+        self._h = h.value
+        self.rank, self.world, self.dispatch = rank, world, True
 
     @property
     def handle(self) -> int:

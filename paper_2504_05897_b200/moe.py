@@ -178,11 +178,16 @@ class HybridMoE:
                 self._ep = P2PExchange(self.ep_rank, self.ep_world, max_tokens, H, process_group,
                                        dispatch=(self.N + self.S, self.N, self.K + self.S))
                 check(lib.hm_runtime_set_ep_dispatch(self._rt, self._ep.handle))
+            elif exchange == "nccl_a2a":  # token-sharded over NCCL grouped send/recv (baseline / fallback)
+                from .ep import NcclExchange
+                self._ep = NcclExchange(self.ep_rank, self.ep_world, max_tokens, H,
+                                        (self.N + self.S, self.N, self.K + self.S), process_group)
+                check(lib.hm_runtime_set_ep_dispatch(self._rt, self._ep.handle))
             elif exchange == "allreduce":  # baseline: partials all-reduced on the process group
                 self.y32 = torch.empty((max_tokens, H), dtype=torch.float32, device="cuda")
                 check(lib.hm_runtime_set_ep_output(self._rt, self.y32.data_ptr()))
             else:
-                raise ValueError(f"unknown expert-parallel exchange {exchange!r} (p2p | dispatch | allreduce)")
+                raise ValueError(f"unknown expert-parallel exchange {exchange!r} (p2p | dispatch | nccl_a2a | allreduce)")
         pool, store, sb, ns = C.c_void_p(), C.c_void_p(), C.c_size_t(), C.c_int64()
         check(lib.hm_runtime_buffers(self._rt, C.byref(pool), C.byref(store), C.byref(sb), C.byref(ns)))
         self.slot_bytes, self.n_slots = sb.value, ns.value

@@ -237,3 +237,82 @@ def test_gloo_world2_token_sharded_dispatch_equals_full_layer():
     assert all(p.exitcode == 0 for p in procs)
     for r, (err, ok_counts, dsum) in res.items():
         assert ok_counts and err < 1e-5 and dsum < 1e-12, (r, err, ok_counts, dsum)
+
+
+def _a2a_worker(rank, world, port, q):
+    """The NCCL transport's schedule (native hm_ep_a2a_plan) executed with gloo
+    point-to-point ops in the same issue order: every rank's rows must land in
+    the home layout the peer-memory kernels write, and come back."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        N, S, Hs = 10, 2, 3
+        E = N + S
+        rng = np.random.default_rng(100 + world)
+        counts = rng.integers(0, 4, size=(world, E)).astype(np.int32)   # same draw on every rank
+        counts[world - 1] = 0                                            # one rank holds no tokens
+        mine = torch.from_numpy(counts[rank].copy())
+        gathered = [torch.zeros(E, dtype=torch.int32) for _ in range(world)]
+        dist.all_gather(gathered, mine)                                  # the all-gathered count matrix
+        cnt = torch.stack(gathered).numpy()
+        assert (cnt == counts).all()
+        home = lambda e: (e if e < N else e - N) % world                # noqa: E731
+        # local permuted rows: expert-contiguous, value = (rank, expert, index)
+        local = np.array([[rank, e, i] for e in range(E) for i in range(cnt[rank, e])], dtype=np.float32)
+        local = torch.from_numpy(local.reshape(-1, Hs))
+
+        def run(plan, src, n_dst):
+            dst = torch.full((n_dst, Hs), -1.0)
+            reqs = []
+            for kind, peer, s0, d0, n in plan:
+                if kind == 2:
+                    dst[d0:d0 + n] = src[s0:s0 + n]
+                elif kind == 0:
+                    reqs.append(dist.isend(src[s0:s0 + n].contiguous(), peer))
+                else:
+                    buf = torch.empty((n, Hs))
+                    reqs.append((dist.irecv(buf, peer), buf, d0, n))
+            for r in reqs:
+                if isinstance(r, tuple):
+                    r[0].wait()
+                    dst[r[2]:r[2] + r[3]] = r[1]
+                else:
+                    r.wait()
+            return dst
+
+        # dispatch: home layout = my experts in index order, rows by source rank then source order
+        want = np.array([[s, e, i] for e in range(E) if home(e) == rank for s in range(world)
+                         for i in range(cnt[s, e])], dtype=np.float32).reshape(-1, Hs)
+        recv = run(ep.a2a_plan(cnt, world, E, N, rank, 0), local, len(want))
+        assert np.array_equal(recv.numpy(), want)
+        # "experts" on the home rank, then the return all-to-all to the source positions
+        back = run(ep.a2a_plan(cnt, world, E, N, rank, 1), recv * 2 + 1, local.shape[0])
+        assert torch.equal(back, local * 2 + 1)
+        q.put((rank, True))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_nccl_a2a_schedule_moves_rows_to_home_layout_and_back(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_a2a_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    assert all(p.exitcode == 0 for p in procs)
+    assert dict(q.get(timeout=5) for _ in range(world)) == {r: True for r in range(world)}
+
+
+def test_a2a_plan_validates_and_counts():
+    cnt = np.array([[1, 0, 2], [0, 3, 1]], dtype=np.int32)
+    ops0 = ep.a2a_plan(cnt, 2, 3, 3, 0, 0)
+    # rank 0: expert 0 (home 0) local copy, expert 2 (home 0) local copy; receives expert 2 from rank 1
+    assert ops0 == [(2, 0, 0, 0, 1), (2, 0, 1, 1, 2), (1, 1, 3, 3, 1)]
+    from paper_2504_05897_b200 import _lib
+    with pytest.raises(ValueError):
+        ep.a2a_plan(-cnt, 2, 3, 3, 0, 0)
+    assert "negative" in _lib.last_error()

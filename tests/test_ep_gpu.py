@@ -111,7 +111,7 @@ def test_ranks_equal_one_rank(exchange, world):
                 assert got[r][3][p][l] == masked
 
 
-def _run_dispatch(rank: int, world: int, port: int, q) -> None:
+def _run_dispatch(rank: int, world: int, port: int, q, exchange: str = "dispatch") -> None:
     """Token-sharded expert parallelism: rank r holds tokens [r*T/G, (r+1)*T/G)
     of every pass (a decode token lives on rank 0; rank 1 has none)."""
     import sys
@@ -135,8 +135,14 @@ def _run_dispatch(rank: int, world: int, port: int, q) -> None:
         trace, logits = generate_router_logits(cfg, GenParams(seed=3), 32, 3)
         res = {}
         for native in (False, True):
-            moe = HybridMoE(cfg, "tiny", EnginePolicy(), 0.5, prof, max_tokens=48, ep_rank=rank, ep_world=world,
-                            cpu_threads=2, exchange="dispatch")
+            try:
+                moe = HybridMoE(cfg, "tiny", EnginePolicy(), 0.5, prof, max_tokens=48, ep_rank=rank, ep_world=world,
+                                cpu_threads=2, exchange=exchange)
+            except RuntimeError as e:  # NCCL refuses two ranks on one device ("Duplicate GPU")
+                if exchange == "nccl_a2a" and "NCCL" in str(e):
+                    q.put((rank, ("unavailable", str(e))))
+                    return
+                raise
             moe.init_seeded_weights(7)
             g = torch.Generator(device="cuda").manual_seed(5)
             outs, loads = [], []
@@ -158,8 +164,8 @@ def _run_dispatch(rank: int, world: int, port: int, q) -> None:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_token_sharded_dispatch_equals_one_rank(world):
+@pytest.mark.parametrize("world,exchange", [(2, "dispatch"), (4, "dispatch"), (2, "nccl_a2a")])
+def test_token_sharded_dispatch_equals_one_rank(world, exchange):
     ctx = torch.multiprocessing.get_context("spawn")
     q = ctx.Queue()
     single = ctx.Process(target=_run, args=(0, 1, 0, q))
@@ -167,12 +173,15 @@ def test_token_sharded_dispatch_equals_one_rank(world):
     ref = q.get(timeout=300)
     single.join(timeout=60)
     port = _free_port()
-    procs = [ctx.Process(target=_run_dispatch, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_run_dispatch, args=(r, world, port, q, exchange)) for r in range(world)]
     for p in procs:
         p.start()
     got = dict(q.get(timeout=300) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
+    bad = [v[1] for v in got.values() if isinstance(v, tuple) and v[0] == "unavailable"]
+    if bad:  # the NCCL transport needs one GPU per rank; this box has one GPU
+        pytest.skip(bad[0])
     assert single.exitcode == 0 and all(p.exitcode == 0 for p in procs)
     _, _, ref_outs, ref_loads, _, _ = ref
     for r in range(world):
