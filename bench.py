@@ -354,6 +354,17 @@ def run_ours(args) -> None:
             save_profile(prefill_profile, args.save_profile + ".prefill")
     prof = with_shared_time(base_profile, cfg)
     prof_prefill = with_shared_time(prefill_profile, cfg)
+    # non-expert (attention block) time per layer, measured on this GPU at the
+    # family's attention shapes (costs.py:45, engine.py:307): reported as the
+    # reference's end-to-end what-if; the planning profile keeps the
+    # reference's default 0 (SPEC.md: speedups isolate expert handling), which
+    # no decision depends on
+    from paper_2504_05897_b200.calibration import measure_non_expert_time
+    non_expert = {"decode_us_per_layer": 1e6 * measure_non_expert_time(args.shape, 1, args.prefill),
+                  "prefill_us_per_layer": 1e6 * measure_non_expert_time(args.shape, args.prefill, 0, reps=5),
+                  "context": args.prefill,
+                  "what": "RMSNorm + QKV/O projections + SDPA over the KV cache, bf16 (cuBLAS/SDPA library calls, "
+                          "calibration input only, not executed in the timed step)"}
     policy = EnginePolicy(scheduling=args.scheduling, cache_policy=args.policy, prefetch=args.prefetch)
     # expert parallelism over the ranks of this box: each rank homes experts
     # e % world, host bytes and worker cores split by rank
@@ -670,6 +681,11 @@ def run_ours(args) -> None:
             "prefill_profile": {k: getattr(prefill_profile, k) for k in ("gpu_time_per_expert", "cpu_slope",
                                                                           "gpu_slope", "cpu_first_expert_penalty")},
             "model_vs_measured": model_check,
+            "non_expert": dict(non_expert, **{
+                "tbt_ms_with_non_expert": ms_step + cfg.num_layers * non_expert["decode_us_per_layer"] / 1e3,
+                "ttft_ms_with_non_expert": prefill_ms + cfg.num_layers * non_expert["prefill_us_per_layer"] / 1e3,
+                "predicted_tbt_ms_with_non_expert": statistics.mean(predicted)
+                + cfg.num_layers * non_expert["decode_us_per_layer"] / 1e3}),
             "decision_path_baseline": decision_baseline,
             "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks.summary(), "parity": parity,
             "setup_s": setup_s,

@@ -133,3 +133,62 @@ def calibrate_shape(H: int, I: int, gpu_saturation_load: int = 256, **kw):
     options (e.g. weight_bits=4)."""
     samples = measure_samples(H, I, **kw)
     return calibrate(samples, gpu_saturation_load=gpu_saturation_load), samples
+
+
+# Attention blocks of the named models (the non-expert part of one decoder
+# layer): (hidden, query heads, kv heads, head dim) of the released configs;
+# DeepSeek-V2-Lite's MLA (q 16 x 192, compressed kv 512 + 64 rope, kv_b up-
+# projection) is costed by its projection shapes with 128-wide heads.
+ATTENTION_SHAPES = {
+    "tiny": dict(H=256, nh=4, nkv=4, hd=64, proj=None),
+    "mixtral": dict(H=4096, nh=32, nkv=8, hd=128, proj=None),
+    "qwen2": dict(H=3584, nh=28, nkv=4, hd=128, proj=None),
+    "deepseek": dict(H=2048, nh=16, nkv=16, hd=128, proj=[(2048, 16 * 192), (2048, 576), (512, 16 * 256),
+                                                         (16 * 128, 2048)]),
+}
+
+
+def measure_non_expert_time(family: str, tokens: int, context: int, reps: int = 20, seed: int = 0) -> float:
+    """Seconds per layer of the non-expert work the reference folds into
+    ``non_expert_time`` (costs.py:45, engine.py:307; SPEC.md: "attention etc.,
+    default 0"): RMSNorm, the QKV / O projections and attention over a KV cache
+    of ``context`` positions for ``tokens`` new tokens, at the family's shapes,
+    bf16.  Calibration input only -- these are cuBLAS / SDPA library calls, not
+    the MoE hot path; weights of several layers rotate so the projections stream
+    from HBM as in a real step."""
+    import torch.nn.functional as F
+
+    a = ATTENTION_SHAPES[family]
+    H, nh, nkv, hd = a["H"], a["nh"], a["nkv"], a["hd"]
+    proj = a["proj"] or [(H, (nh + 2 * nkv) * hd), (nh * hd, H)]
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    per_layer = sum(i * o for i, o in proj) * 2
+    n_layers = max(2, -(-(512 << 20) // per_layer))  # > 4x the 126 MB L2
+    ws = [[(torch.randn((o, i), generator=g, device="cuda") * 0.02).to(torch.bfloat16) for i, o in proj]
+          for _ in range(n_layers)]
+    kc = torch.randn((1, nkv, context + tokens, hd), generator=g, device="cuda").to(torch.bfloat16)
+    vc = torch.randn_like(kc)
+    x = torch.randn((tokens, H), generator=g, device="cuda").to(torch.bfloat16)
+    norm_w = torch.ones(H, device="cuda", dtype=torch.bfloat16)
+
+    def layer(w) -> torch.Tensor:
+        hn = F.rms_norm(x, (H,), norm_w)
+        t = hn
+        for m in w[:-1]:  # q/kv projections (DeepSeek: the chain of its MLA projections, shapes only)
+            t = F.linear(hn if m.shape[1] == H else t[:, : m.shape[1]], m)
+        qh = t[:, : nh * hd].reshape(tokens, nh, hd).transpose(0, 1).unsqueeze(0) if t.shape[1] >= nh * hd else \
+            hn[:, : nh * hd].reshape(tokens, nh, hd).transpose(0, 1).unsqueeze(0)
+        o = F.scaled_dot_product_attention(qh, kc, vc, is_causal=context == 0, enable_gqa=nh != nkv)
+        o = o.squeeze(0).transpose(0, 1).reshape(tokens, nh * hd)
+        return x + F.linear(o, w[-1])
+
+    for i in range(n_layers):
+        layer(ws[i])
+    st = torch.cuda.current_stream()
+    a0, b0 = _events()
+    a0.record(st)
+    for r in range(reps):
+        layer(ws[r % n_layers])
+    b0.record(st)
+    b0.synchronize()
+    return a0.elapsed_time(b0) / 1e3 / reps

@@ -184,177 +184,199 @@ __global__ void __launch_bounds__(256) ffn2_gemv_kernel(const __grid_constant__ 
 // ------------------------------------------------------------ fused decode GEMV
 // ONE persistent launch per layer for ffn1 -> ffn2 (instead of two short
 // launches that each pay a ramp and a tail; DeepSeek's 4-6 small experts ran
-// at 3.7 TB/s that way).  Work items, claimed dynamically by warps:
+// at 3.7 TB/s that way).  Work items, statically strided over the warps of a
+// cooperative (co-resident) grid -- warp w takes items w, w + W, w + 2W, ...:
 //   phase 1 item (g, i):   gate row i and up row i of group g's W13 (2 rows of
-//                          H), h[r, i] = bf16(silu(gate.x_r) * (up.x_r));
-//                          then done1[g] += 1 (release)
+//                          H), h[r, i] = bf16(silu(gate.x_r) * (up.x_r)); a
+//                          warp publishes its count of finished items of g
+//                          with one release-add on sub-counter done[g][w % 32]
 //   phase 2 item (g, j..): NR2 rows of W2 (I columns), out[r, j] = W2[j].h_r;
-//                          the item's first weight loads are issued BEFORE
-//                          waiting for done1[g] == I (acquire), so the
+//                          the item's first weight loads are issued BEFORE the
+//                          warp waits (lane k acquires sub-counter k, the warp
+//                          sums them) for group g's I phase-1 items, so the
 //                          phase boundary overlaps with DRAM streaming.
-// A warp moves to phase 2 only after the phase-1 counter is exhausted, i.e.
-// every phase-1 item is held by a running warp that never waits: no deadlock
-// whatever the residency.  Per lane, columns are accumulated in the same order
-// as ffn1/ffn2_gemv_kernel (c = lane*8 + 256k, k increasing), so the outputs
-// are bit-identical to the two-launch path.  The last warp to exit resets the
-// counters for the next launch on the stream.
+// All phase-1 items precede all phase-2 items in the item order, and the grid
+// is co-resident (cooperative launch), so every wait is on a running warp.
+// The 32 sub-counters per group sit on separate 128-byte lines (a single
+// counter serialised the adds of thousands of warps); they are never reset:
+// they only grow, and the host passes each group's running total at launch
+// (bases, tracked per stream) so the target is base + I.  Per
+// lane, columns are accumulated in the same order as ffn1/ffn2_gemv_kernel
+// (c = lane*8 + 256k, k increasing): outputs bit-identical to the pair.
+constexpr int kDoneStride = 32;  // ints: one 128-byte line per counter
+
 struct FusedGemvParams {
   const uint16_t *pool;
   size_t slot_elems;
   int H, I, n_groups;
-  int n1, n2, items2_per_group;  // phase-1 items (= G*I), phase-2 items, per group
-  int total_warps;
+  int n1, n2, items2_per_group, total_warps;
   const uint16_t *xp;
   uint16_t *h;
   float *out;
-  int32_t *ctr;  // [0] phase-1 claims, [1] phase-2 claims, [2] exits, [4 ..] done1[g]
+  uint32_t *done;  // [kMaxGroups][32 counters][kDoneStride]
+  uint32_t base[kMaxGroups];
   int32_t slot[kMaxGroups];
   int32_t row_begin[kMaxGroups];
   int32_t row_count[kMaxGroups];
 };
 
-__device__ __forceinline__ int ld_acquire_gpu(const int32_t *p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void red_release_gpu(uint32_t *p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
-template <int MR, int NR2>
-__global__ void __launch_bounds__(256, MR == 1 ? 4 : 2) ffn_decode_fused_kernel(const __grid_constant__ FusedGemvParams p) {
-  const int lane = threadIdx.x & 31;
+template <int MR, int U>
+__device__ __forceinline__ void fused_phase1(const FusedGemvParams &p, int it, int lane) {
   const int H = p.H, I = p.I;
-  int32_t *done1 = p.ctr + 4;
-  // ---------------- phase 1
-  for (;;) {
-    int it = 0;
-    if (lane == 0) it = atomicAdd(p.ctr, 1);
-    it = __shfl_sync(0xffffffffu, it, 0);
-    if (it >= p.n1) break;
-    const int g = it / I, i = it - g * I;
-    const int M = p.row_count[g], rb = p.row_begin[g];
-    const uint16_t *w13 = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_elems;
-    const size_t grow = static_cast<size_t>((i / kIlv) * 2 * kIlv + (i % kIlv));
-    const uint16_t *wg = w13 + grow * H;
-    const uint16_t *wu = wg + static_cast<size_t>(kIlv) * H;
-    const uint16_t *x = p.xp + static_cast<size_t>(rb) * H;
-    float ag[MR], au[MR];
+  const int g = it / I, i = it - g * I;
+  const int M = p.row_count[g], rb = p.row_begin[g];
+  const uint16_t *w13 = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_elems;
+  const size_t grow = static_cast<size_t>((i / kIlv) * 2 * kIlv + (i % kIlv));
+  const uint16_t *wg = w13 + grow * H;
+  const uint16_t *wu = wg + static_cast<size_t>(kIlv) * H;
+  const uint16_t *x = p.xp + static_cast<size_t>(rb) * H;
+  float ag[MR], au[MR];
 #pragma unroll
-    for (int m = 0; m < MR; ++m) ag[m] = au[m] = 0.f;
-    constexpr int U = 4;
-    for (int c0 = lane * 8; c0 < H; c0 += 256 * U) {
-      uint4 gv[U], uv[U];
+  for (int m = 0; m < MR; ++m) ag[m] = au[m] = 0.f;
+  for (int c0 = lane * 8; c0 < H; c0 += 256 * U) {
+    uint4 gv[U], uv[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int c = c0 + u * 256;
-        if (c < H) {
-          gv[u] = dev::ld_stream(wg + c);
-          uv[u] = dev::ld_stream(wu + c);
-        }
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u * 256;
+      if (c < H) {
+        gv[u] = dev::ld_stream(wg + c);
+        uv[u] = dev::ld_stream(wu + c);
       }
+    }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int c = c0 + u * 256;
-        if (c < H) {
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u * 256;
+      if (c < H) {
 #pragma unroll
-          for (int m = 0; m < MR; ++m) {
-            if (m < M) {
-              const uint4 xv = __ldg(reinterpret_cast<const uint4 *>(x + static_cast<size_t>(m) * H + c));
-              ag[m] += dev::dot8(gv[u], xv);
-              au[m] += dev::dot8(uv[u], xv);
-            }
+        for (int m = 0; m < MR; ++m) {
+          if (m < M) {
+            const uint4 xv = __ldg(reinterpret_cast<const uint4 *>(x + static_cast<size_t>(m) * H + c));
+            ag[m] += dev::dot8(gv[u], xv);
+            au[m] += dev::dot8(uv[u], xv);
           }
         }
       }
     }
+  }
 #pragma unroll
-    for (int m = 0; m < MR; ++m) {
-      if (m < M) {
-        const float gs = dev::warp_sum(ag[m]), us = dev::warp_sum(au[m]);
-        if (lane == 0) p.h[static_cast<size_t>(rb + m) * I + i] = dev::f2bf(dev::silu(gs) * us);
-      }
-    }
-    if (lane == 0) {
-      __threadfence();
-      atomicAdd(done1 + g, 1);
+  for (int m = 0; m < MR; ++m) {
+    if (m < M) {
+      const float gs = dev::warp_sum(ag[m]), us = dev::warp_sum(au[m]);
+      if (lane == 0) p.h[static_cast<size_t>(rb + m) * I + i] = dev::f2bf(dev::silu(gs) * us);
     }
   }
-  // ---------------- phase 2
-  constexpr int U2 = 8 / NR2;
-  for (;;) {
-    int it = 0;
-    if (lane == 0) it = atomicAdd(p.ctr + 1, 1);
-    it = __shfl_sync(0xffffffffu, it, 0);
-    if (it >= p.n2) break;
-    const int g = it / p.items2_per_group, j0 = (it - g * p.items2_per_group) * NR2;
-    const int M = p.row_count[g], rb = p.row_begin[g];
-    const uint16_t *w2 = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_elems + static_cast<size_t>(2) * I * H;
-    bool live[NR2];
-    const uint16_t *wr[NR2];
+}
+
+template <int MR, int NR2, int U2>
+__device__ __forceinline__ void fused_phase2(const FusedGemvParams &p, int it2, int lane) {
+  const int H = p.H, I = p.I;
+  const int g = it2 / p.items2_per_group, j0 = (it2 - g * p.items2_per_group) * NR2;
+  const int M = p.row_count[g], rb = p.row_begin[g];
+  const uint16_t *w2 = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_elems + static_cast<size_t>(2) * I * H;
+  bool live[NR2];
+  const uint16_t *wr[NR2];
 #pragma unroll
-    for (int r = 0; r < NR2; ++r) {
-      live[r] = j0 + r < H;
-      wr[r] = w2 + static_cast<size_t>(live[r] ? j0 + r : j0) * I;
-    }
-    float acc[MR][NR2];
+  for (int r = 0; r < NR2; ++r) {
+    live[r] = j0 + r < H;
+    wr[r] = w2 + static_cast<size_t>(live[r] ? j0 + r : j0) * I;
+  }
+  float acc[MR][NR2];
 #pragma unroll
-    for (int m = 0; m < MR; ++m)
+  for (int m = 0; m < MR; ++m)
 #pragma unroll
-      for (int r = 0; r < NR2; ++r) acc[m][r] = 0.f;
-    const uint16_t *hrow = p.h + static_cast<size_t>(rb) * I;
-    bool ready = false;
-    for (int c0 = lane * 8; c0 < I; c0 += 256 * U2) {
-      uint4 wv[NR2][U2];
+    for (int r = 0; r < NR2; ++r) acc[m][r] = 0.f;
+  const uint16_t *hrow = p.h + static_cast<size_t>(rb) * I;
+  bool ready = false;
+  for (int c0 = lane * 8; c0 < I; c0 += 256 * U2) {
+    uint4 wv[NR2][U2];
 #pragma unroll
-      for (int r = 0; r < NR2; ++r)
-#pragma unroll
-        for (int u = 0; u < U2; ++u) {
-          const int c = c0 + u * 256;
-          if (c < I && live[r]) wv[r][u] = dev::ld_stream(wr[r] + c);
-        }
-      if (!ready) {  // h of group g complete? (the loads above are already in flight)
-        if (lane == 0)
-          while (ld_acquire_gpu(done1 + g) < I) __nanosleep(64);
-        __syncwarp();
-        ready = true;
-      }
+    for (int r = 0; r < NR2; ++r)
 #pragma unroll
       for (int u = 0; u < U2; ++u) {
         const int c = c0 + u * 256;
-        if (c < I) {
-#pragma unroll
-          for (int m = 0; m < MR; ++m)
-            if (m < M) {
-              const uint4 hv = __ldcg(reinterpret_cast<const uint4 *>(hrow + static_cast<size_t>(m) * I + c));
-#pragma unroll
-              for (int r = 0; r < NR2; ++r)
-                if (live[r]) acc[m][r] += dev::dot8(wv[r][u], hv);
-            }
-        }
+        if (c < I && live[r]) wv[r][u] = dev::ld_stream(wr[r] + c);
       }
+    if (!ready) {  // h of group g complete?  (the loads above are already in flight)
+      const uint32_t *d = p.done + (static_cast<size_t>(g) * 32 + lane) * kDoneStride;
+      const uint32_t target = p.base[g] + static_cast<uint32_t>(I);
+      for (;;) {  // every lane acquires its own sub-counter; the warp sums them
+        uint32_t v = ld_acquire_gpu(d);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (static_cast<int32_t>(v - target) >= 0) break;
+        __nanosleep(32);
+      }
+      __syncwarp();
+      ready = true;
     }
 #pragma unroll
-    for (int m = 0; m < MR; ++m) {
-      if (m < M) {
+    for (int u = 0; u < U2; ++u) {
+      const int c = c0 + u * 256;
+      if (c < I) {
 #pragma unroll
-        for (int r = 0; r < NR2; ++r) {
-          if (!live[r]) continue;
-          const float s = dev::warp_sum(acc[m][r]);
-          if (lane == 0) p.out[static_cast<size_t>(rb + m) * H + j0 + r] = s;
-        }
+        for (int m = 0; m < MR; ++m)
+          if (m < M) {
+            const uint4 hv = __ldcg(reinterpret_cast<const uint4 *>(hrow + static_cast<size_t>(m) * I + c));
+#pragma unroll
+            for (int r = 0; r < NR2; ++r)
+              if (live[r]) acc[m][r] += dev::dot8(wv[r][u], hv);
+          }
       }
     }
   }
-  // ---------------- the last warp out resets the counters
-  if (lane == 0) {
-    __threadfence();
-    if (atomicAdd(p.ctr + 2, 1) == p.total_warps - 1) {
-      p.ctr[0] = 0;
-      p.ctr[1] = 0;
-      for (int g = 0; g < p.n_groups; ++g) done1[g] = 0;
-      __threadfence();
-      p.ctr[2] = 0;
+#pragma unroll
+  for (int m = 0; m < MR; ++m) {
+    if (m < M) {
+#pragma unroll
+      for (int r = 0; r < NR2; ++r) {
+        if (!live[r]) continue;
+        const float s = dev::warp_sum(acc[m][r]);
+        if (lane == 0) p.out[static_cast<size_t>(rb + m) * H + j0 + r] = s;
+      }
     }
   }
+}
+
+// MINB resident CTAs per SM.  Phase-1 items go to the first total_warps warps
+// in warp-major order (spread over the SMs), a count chosen so that each does
+// the same number of items (a plain stride left a last round running a few
+// percent of the warps while all phase-2 warps waited); phase-2 items are
+// strided over all warps of the grid.
+template <int MR, int NR2, int MINB>
+__global__ void __launch_bounds__(256, MINB) ffn_decode_fused_kernel(const __grid_constant__ FusedGemvParams p) {
+  constexpr int U1 = 4;
+  constexpr int U2 = (MINB >= 4 ? 4 : 8) / NR2;
+  const int lane = threadIdx.x & 31;
+  const int w0 = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  const int all = gridDim.x * (blockDim.x >> 5);
+  // phase 1; completions are published once per group this warp worked on
+  // (one release-add on the warp's own sub-counter), not per item: a release
+  // per item stalled the warp's next loads
+  int cur_g = -1;
+  uint32_t n_done = 0;
+  for (int it = w0; w0 < p.total_warps && it < p.n1; it += p.total_warps) {
+    const int g = it / p.I;
+    if (g != cur_g) {
+      if (cur_g >= 0 && lane == 0)
+        red_release_gpu(p.done + (static_cast<size_t>(cur_g) * 32 + (w0 & 31)) * kDoneStride, n_done);
+      cur_g = g;
+      n_done = 0;
+    }
+    fused_phase1<MR, U1>(p, it, lane);
+    ++n_done;
+  }
+  if (cur_g >= 0 && lane == 0)
+    red_release_gpu(p.done + (static_cast<size_t>(cur_g) * 32 + (w0 & 31)) * kDoneStride, n_done);
+  for (int it2 = w0; it2 < p.n2; it2 += all) fused_phase2<MR, NR2, U2>(p, it2, lane);
 }
 
 // ------------------------------------------------------------ tcgen05 GEMM
@@ -645,44 +667,63 @@ void launch_pdl(K kernel, int grid, int smem, cudaStream_t st, const GemvParams 
   HM_LAUNCH_CHECK();
 }
 
-// HM_GEMV_FUSED=0 selects the two-launch ffn1/ffn2 pair (A/B and tests).
+// HM_GEMV_FUSED=1 selects the persistent one-launch kernel; the default is
+// the two-launch ffn1/ffn2 pair, which measured faster at every decode shape
+// (tools/gemv_lib_bench.py).
 bool gemv_fused_enabled() {
   static const bool on = [] {
     const char *e = std::getenv("HM_GEMV_FUSED");
-    return !e || std::atoi(e) != 0;
+    return e && std::atoi(e) != 0;
   }();
   return on;
 }
 
-// Claim/completion counters of the fused GEMV, one zeroed set per stream
-// (the kernel's last warp re-zeroes them, so launches on one stream reuse it).
-int32_t *fused_counters(cudaStream_t st) {
+// Completion counters of the fused GEMV, one set per stream, with the host's
+// running count of the increments every counter received (the kernel never
+// resets them; each launch waits for base + I/32 per counter of its groups).
+struct FusedCounters {
+  cudaStream_t st;
+  uint32_t *dev;
+  uint32_t base[kMaxGroups];
+};
+FusedCounters &fused_counters(cudaStream_t st) {
   static std::mutex mu;
-  static std::vector<std::pair<cudaStream_t, int32_t *>> sets;
+  static std::vector<FusedCounters *> sets;
   std::lock_guard<std::mutex> g(mu);
-  for (auto &kv : sets)
-    if (kv.first == st) return kv.second;
-  int32_t *c = nullptr;
-  HM_CUDA(cudaMalloc(&c, (4 + kMaxGroups) * sizeof(int32_t)));
-  HM_CUDA(cudaMemset(c, 0, (4 + kMaxGroups) * sizeof(int32_t)));
+  for (auto *c : sets)
+    if (c->st == st) return *c;
+  auto *c = new FusedCounters{st, nullptr, {}};
+  const size_t bytes = static_cast<size_t>(kMaxGroups) * 32 * kDoneStride * sizeof(uint32_t);
+  HM_CUDA(cudaMalloc(&c->dev, bytes));
+  HM_CUDA(cudaMemset(c->dev, 0, bytes));
   HM_CUDA(cudaDeviceSynchronize());
-  sets.emplace_back(st, c);
-  return c;
+  sets.push_back(c);
+  return *c;
 }
 
-template <int MR, int NR2>
-void launch_fused_one(const FusedGemvParams &p0, cudaStream_t st) {
+template <int MR, int NR2, int MINB>
+void launch_fused_one(FusedGemvParams &p, cudaStream_t st) {
   static int per_sm = 0;
   if (!per_sm) {
-    HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ffn_decode_fused_kernel<MR, NR2>, 256, 0));
+    HM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ffn_decode_fused_kernel<MR, NR2, MINB>, 256, 0));
     per_sm = std::max(1, std::min(per_sm, 4));
   }
-  FusedGemvParams p = p0;
-  const long warps_needed = static_cast<long>(p.n1);
-  const int grid = static_cast<int>(std::max<long>(1, std::min<long>(static_cast<long>(num_sms()) * per_sm,
-                                                                     (warps_needed + 7) / 8)));
-  p.total_warps = grid * 8;
-  ffn_decode_fused_kernel<MR, NR2><<<grid, 256, 0, st>>>(p);
+  // the whole co-resident grid; phase 1 in whole rounds over total_warps of it
+  const int grid = num_sms() * per_sm;
+  const long wmax = static_cast<long>(grid) * 8;
+  const long rounds = (static_cast<long>(p.n1) + wmax - 1) / wmax;
+  p.total_warps = static_cast<int>((p.n1 + rounds - 1) / rounds);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency: phase-2 warps wait on phase-1 warps
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  HM_CUDA(cudaLaunchKernelEx(&cfg, ffn_decode_fused_kernel<MR, NR2, MINB>, p));
   HM_LAUNCH_CHECK();
 }
 
@@ -697,12 +738,15 @@ void launch_gemv_fused(const uint16_t *pool, size_t slot_elems, int H, int I, co
   p.xp = xp;
   p.h = h;
   p.out = out;
-  p.ctr = fused_counters(st);
+  FusedCounters &fc = fused_counters(st);
+  p.done = fc.dev;
   int mr = 1;
   for (size_t g = 0; g < gs.size(); ++g) {
     p.slot[g] = gs[g].slot;
     p.row_begin[g] = gs[g].row_begin;
     p.row_count[g] = gs[g].row_count;
+    p.base[g] = fc.base[g];
+    fc.base[g] += static_cast<uint32_t>(I);  // what this launch adds to group g's 32 sub-counters together
     mr = std::max(mr, gs[g].row_count);
   }
   // long W2 rows (Mixtral, I = 14336): one row per item, 8 loads in flight per
@@ -712,23 +756,28 @@ void launch_gemv_fused(const uint16_t *pool, size_t slot_elems, int H, int I, co
   p.n1 = p.n_groups * I;
   p.items2_per_group = (H + nr2 - 1) / nr2;
   p.n2 = p.n_groups * p.items2_per_group;
+  static const int minb = [] {  // HM_GEMV_MINB=3|4 (A/B); default 4
+    const char *e = std::getenv("HM_GEMV_MINB");
+    return e && std::atoi(e) == 3 ? 3 : 4;
+  }();
   switch (mr * 2 + (one ? 1 : 0)) {
-    case 2: launch_fused_one<1, 2>(p, st); break;
-    case 3: launch_fused_one<1, 1>(p, st); break;
-    case 4: launch_fused_one<2, 2>(p, st); break;
-    case 5: launch_fused_one<2, 1>(p, st); break;
+    case 2: minb == 4 ? launch_fused_one<1, 2, 4>(p, st) : launch_fused_one<1, 2, 3>(p, st); break;
+    case 3: minb == 4 ? launch_fused_one<1, 1, 4>(p, st) : launch_fused_one<1, 1, 3>(p, st); break;
+    case 4: launch_fused_one<2, 2, 2>(p, st); break;
+    case 5: launch_fused_one<2, 1, 2>(p, st); break;
     default:
       if (one)
-        launch_fused_one<4, 1>(p, st);
+        launch_fused_one<4, 1, 2>(p, st);
       else
-        launch_fused_one<4, 2>(p, st);
+        launch_fused_one<4, 2, 2>(p, st);
   }
 }
 
+// path HM_FFN_GEMV: HM_GEMV_FUSED decides; HM_FFN_GEMV_SPLIT / _FUSED force one
 void launch_gemv(const uint16_t *pool, size_t slot_elems, int H, int I, const std::vector<hm_group> &gs,
-                 const uint16_t *xp, uint16_t *h, float *out, cudaStream_t st, bool split = false) {
+                 const uint16_t *xp, uint16_t *h, float *out, cudaStream_t st, int path) {
   if (gs.empty()) return;
-  if (!split && gemv_fused_enabled()) {
+  if (path == HM_FFN_GEMV_FUSED || (path != HM_FFN_GEMV_SPLIT && gemv_fused_enabled())) {
     HM_REQUIRE(static_cast<int>(gs.size()) <= kMaxGroups, HM_EVALUE, "too many expert groups in one launch");
     HM_REQUIRE(H % 8 == 0 && I % 8 == 0 && I % kIlv == 0, HM_EVALUE, "GEMV needs H % 8 == 0 and I % 128 == 0");
     launch_gemv_fused(pool, slot_elems, H, I, gs, xp, h, out, st);
@@ -897,7 +946,7 @@ int hm_expert_ffn(const uint16_t *pool, int n_slots, int H, int I, const hm_grou
                    gr.row_begin + gr.row_count <= total_rows,
                HM_EVALUE, "expert group outside the pool or the row range");
     if (gr.row_count == 0) continue;
-    const bool gemv = path == HM_FFN_GEMV || path == HM_FFN_GEMV_SPLIT ||
+    const bool gemv = path == HM_FFN_GEMV || path == HM_FFN_GEMV_SPLIT || path == HM_FFN_GEMV_FUSED ||
                       (path == HM_FFN_AUTO && gr.row_count <= hm::kGemvMaxRows);
     if (gemv) {
       HM_REQUIRE(gr.row_count <= hm::kGemvMaxRows, HM_EVALUE, "GEMV path takes at most 4 rows per expert");
@@ -909,7 +958,7 @@ int hm_expert_ffn(const uint16_t *pool, int n_slots, int H, int I, const hm_grou
   const size_t slot_elems = static_cast<size_t>(3) * H * I;
   for (size_t b = 0; b < small.size(); b += hm::kMaxGroups) {
     std::vector<hm_group> part(small.begin() + b, small.begin() + std::min(small.size(), b + hm::kMaxGroups));
-    hm::launch_gemv(pool, slot_elems, H, I, part, xp, h, out, st, path == HM_FFN_GEMV_SPLIT);
+    hm::launch_gemv(pool, slot_elems, H, I, part, xp, h, out, st, path);
   }
   for (size_t b = 0; b < big.size(); b += hm::kMaxGroups) {
     std::vector<hm_group> part(big.begin() + b, big.begin() + std::min(big.size(), b + hm::kMaxGroups));

@@ -1,0 +1,6 @@
+set -x
+timeout 600 python -m pytest tests/test_kernels_gpu.py -q -m gpu -p no:cacheprovider -x -k "fused or gemv or deepseek or mixtral" > gpurun_out/r2e_pytest.log 2>&1; echo pytest rc=$?
+tail -5 gpurun_out/r2e_pytest.log
+timeout 600 python tools/gemv_lib_bench.py 40 deepseek,qwen2,mixtral 1,2,4,6,8 > gpurun_out/r2e_gemv_smem.log 2>&1; echo gemv rc=$?
+cat gpurun_out/r2e_gemv_smem.log
+HM_GEMV_FUSED=1 timeout 600 python tools/gemv_lib_bench.py 40 deepseek,qwen2,mixtral 1,2,4,6,8 > gpurun_out/r2e_gemv_reg.log 2>&1; echo gemv rc=$?
