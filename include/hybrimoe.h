@@ -455,7 +455,9 @@ typedef struct hm_runtime_config {
   int64_t host_images;     /* distinct expert images in the pinned master store */
   int32_t cpu_threads;     /* host worker threads (<= 0: all cores) */
   int32_t max_tokens;      /* largest T of one forward_layer call */
-  int32_t gpu_mrs;         /* keep the GPU copy of S updated with hm_mrs_update_dev */
+  int32_t gpu_mrs;         /* zero-copy decode: the router computes the layer's new MRS row on the GPU
+                              (old row read from the engine's mapped table); the decision core takes it
+                              at step (5) instead of its own recurrence */
   int32_t residual;        /* y = x + MoE(x) (1) or y = MoE(x) (0) */
   int32_t ep_rank;         /* expert parallelism: this rank computes experts e with  */
   int32_t ep_world;        /* e % ep_world == ep_rank (shared chunk c: c % ep_world) */
@@ -506,7 +508,8 @@ int hm_runtime_forward_pass(hm_runtime *rt, const uint16_t *x, const float *cons
                             uint16_t **y_out);
 /* The LayerRequest (loads, normalised scores) the router produced last. */
 int hm_runtime_last_request(const hm_runtime *rt, int64_t *loads, double *scores);
-/* GPU copy of the MRS table S [L, N] (synchronises the device). */
+/* The MRS table S [L, N] the decisions use -- one table, mapped into the GPU,
+ * whose decode rows the router computes (synchronises the device). */
 int hm_runtime_device_mrs(hm_runtime *rt, double *host_out);
 int hm_runtime_sync(hm_runtime *rt);
 /* Make experts resident (fixed residency of the baseline policies,

@@ -155,7 +155,7 @@ def measure_non_expert_time(family: str, tokens: int, context: int, reps: int = 
     of ``context`` positions for ``tokens`` new tokens, at the family's shapes,
     bf16.  Calibration input only -- these are cuBLAS / SDPA library calls, not
     the MoE hot path; weights of several layers rotate so the projections stream
-    from HBM as in a real step."""
+    from HBM as in a real step, captured in one CUDA graph and replayed."""
     import torch.nn.functional as F
 
     a = ATTENTION_SHAPES[family]
@@ -182,13 +182,24 @@ def measure_non_expert_time(family: str, tokens: int, context: int, reps: int = 
         o = o.squeeze(0).transpose(0, 1).reshape(tokens, nh * hd)
         return x + F.linear(o, w[-1])
 
-    for i in range(n_layers):
-        layer(ws[i])
+    # one CUDA graph replays the layers back to back: the GPU time of the block,
+    # not PyTorch's per-op launch overhead (~10 ops of a few us each at T = 1)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for i in range(n_layers):
+            layer(ws[i])
+    torch.cuda.current_stream().wait_stream(side)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for i in range(n_layers):
+            layer(ws[i])
+    graph.replay()
     st = torch.cuda.current_stream()
     a0, b0 = _events()
     a0.record(st)
-    for r in range(reps):
-        layer(ws[r % n_layers])
+    for _ in range(reps):
+        graph.replay()
     b0.record(st)
     b0.synchronize()
-    return a0.elapsed_time(b0) / 1e3 / reps
+    return a0.elapsed_time(b0) / 1e3 / (reps * n_layers)

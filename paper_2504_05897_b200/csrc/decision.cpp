@@ -773,7 +773,13 @@ void Engine::run_layer(int layer, const int64_t *loads, const double *scores, in
   }
 
   // (5) score-aware state follows every executed layer
-  if (track && policy == HM_POLICY_MRS && mrs_ != nullptr) mrs_->update(layer, scores, n);
+  if (track && policy == HM_POLICY_MRS && mrs_ != nullptr) {
+    if (gpu_mrs_row)
+      std::copy(gpu_mrs_row, gpu_mrs_row + mrs_->N, mrs_->S.begin() + static_cast<size_t>(layer) * mrs_->N);
+    else
+      mrs_->update(layer, scores, n);
+  }
+  gpu_mrs_row = nullptr;
 
   // (6) prefetch into the plan's idle PCIe time
   if (cfg.prefetch && !static_sched && cache.capacity > 0) {

@@ -6,6 +6,8 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
+#include <new>
 #include <string>
 #include <unordered_map>
 #include <unordered_set>
@@ -64,11 +66,33 @@ struct Evaluator {
 };
 
 // MrsState (caching.py:30-76): dense S table over L x N.
+// Page-aligned, page-padded storage: a runtime maps the MRS table into the GPU
+// (cudaHostRegister) so the router can read the old row; separate tables
+// never share a page.
+template <typename T>
+struct PageAlloc {
+  using value_type = T;
+  PageAlloc() = default;
+  template <typename U>
+  PageAlloc(const PageAlloc<U> &) {}
+  T *allocate(size_t n) {
+    const size_t bytes = (n * sizeof(T) + 4095) / 4096 * 4096;
+    void *p = std::aligned_alloc(4096, bytes ? bytes : 4096);
+    if (!p) throw std::bad_alloc();
+    return static_cast<T *>(p);
+  }
+  void deallocate(T *p, size_t) { std::free(p); }
+  template <typename U>
+  bool operator==(const PageAlloc<U> &) const { return true; }
+  template <typename U>
+  bool operator!=(const PageAlloc<U> &) const { return false; }
+};
+
 struct Mrs {
   int L = 0, N = 0;
   double alpha = 0.5;
   int p = 4;
-  std::vector<double> S;
+  std::vector<double, PageAlloc<double>> S;
   double get(uint32_t ref) const {
     int l = ref_layer(ref), e = ref_expert(ref);
     if (l < L && e < N) return S[static_cast<size_t>(l) * N + e];
@@ -138,6 +162,11 @@ struct Engine {
   std::vector<double> layer_makespans;
   LayerRecord rec;
   double tdur = 0.0;
+  // Step (5)'s new MRS row as computed on the GPU by the layer's router
+  // (runtime zero-copy decode path), consumed instead of the host recurrence
+  // for the next run_layer call only; bit-identical by construction
+  // (tests/test_kernels_gpu.py::test_mrs_update_dev_bit_exact).
+  const double *gpu_mrs_row = nullptr;
 
   Engine(const hm_engine_config &c, const hm_profile &p, Cache *cache, Mrs *mrs, Evaluator *ev);
   void begin_pass();

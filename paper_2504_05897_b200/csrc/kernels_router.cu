@@ -116,6 +116,13 @@ struct HostMirror {
   uint16_t *xp;
   uint32_t *flag;
   uint32_t seq;
+  // optional MRS update of this layer's row (caching.py:65-76) on the GPU:
+  // S = the decision core's [L, N] table (mapped host memory, read only), the
+  // new row goes to mrs_row (mapped) for the decision core's step (5)
+  double *S = nullptr;
+  double *mrs_row = nullptr;
+  int layer = 0, p = 0;
+  double alpha = 0.0;
 };
 
 constexpr int kFusedMaxRows = 1024;
@@ -136,6 +143,10 @@ __global__ void __launch_bounds__(256) router_fused_small_kernel(
   __shared__ float s_probs[32 * 256];  // T <= 32 tokens x N <= 256
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int E = N + n_shared, Kp = K + n_shared, R = T * Kp;
+  // the old MRS row is read from the decision core's mapped table now; the
+  // PCIe round trip overlaps with the routing below
+  double mrs_old = 0.0;
+  if (hm_.S && threadIdx.x < N) mrs_old = __ldcv(hm_.S + static_cast<size_t>(hm_.layer) * N + threadIdx.x);
   for (int e = threadIdx.x; e < E; e += blockDim.x) s_counts[e] = 0;
   __syncthreads();
   for (int t = wid; t < T; t += nw) {
@@ -288,6 +299,18 @@ __global__ void __launch_bounds__(256) router_fused_small_kernel(
       const double tot = s_tot;
       hm_.meta_d[e] = s_sum[e];
       hm_.meta_d[N + e] = tot > 0.0 ? s_sum[e] / tot : 0.0;
+    }
+    if (hm_.S && threadIdx.x < N) {  // this layer's new MRS row, a * TopP(s) + (1 - a) * S (caching.py:65-76)
+      const double tot = s_tot;
+      const int i = threadIdx.x;
+      const double si = tot > 0.0 ? s_sum[i] / tot : 0.0;
+      int rank = 0;
+      for (int j = 0; j < N; ++j) {
+        const double sj = tot > 0.0 ? s_sum[j] / tot : 0.0;
+        rank += (sj > si || (sj == si && j < i)) ? 1 : 0;
+      }
+      const double t = rank < hm_.p ? si : 0.0;
+      hm_.mrs_row[i] = __dadd_rn(__dmul_rn(hm_.alpha, t), __dmul_rn(__dsub_rn(1.0, hm_.alpha), mrs_old));
     }
     __threadfence_system();
     __syncthreads();
@@ -725,6 +748,29 @@ int hm_router_fused_mirror(const float *logits, int T, int N, int ld, int K, int
   hm::launch_router_fused(logits, T, N, ld, K, renormalize, n_shared, shared_gate_col, x, H, sel, w, pos, row_src,
                           xp, meta_i, meta_d, hm::HostMirror{host_meta_i, host_meta_d, host_xp, host_flag, seq},
                           static_cast<cudaStream_t>(stream));
+  HM_LAUNCH_CHECK();
+  HM_API_END
+}
+
+int hm_router_fused_mirror_mrs(const float *logits, int T, int N, int ld, int K, int renormalize, int n_shared,
+                               int shared_gate_col, const uint16_t *x, int H, int32_t *sel, float *w, int32_t *pos,
+                               int32_t *row_src, uint16_t *xp, int32_t *meta_i, double *meta_d, int32_t *host_meta_i,
+                               double *host_meta_d, uint16_t *host_xp, uint32_t *host_flag, uint32_t seq, double *S,
+                               int layer, int mrs_p, double mrs_alpha, double *host_mrs_row, void *stream) {
+  HM_API_BEGIN
+  HM_REQUIRE(T >= 1 && T <= 32 && N >= 1 && N <= 256 && K >= 1 && K <= 8 && K <= N && ld >= N &&
+                 T * (K + n_shared) <= hm::kFusedMaxRows && N + n_shared <= hm::kFusedMaxE && H % 8 == 0,
+             HM_EVALUE, "shape outside the fused small-T router");
+  HM_REQUIRE(host_meta_i && host_meta_d && host_flag && S && host_mrs_row && layer >= 0, HM_EVALUE,
+             "host mirror needs meta, flag, MRS table and row pointers");
+  hm::HostMirror m{host_meta_i, host_meta_d, host_xp, host_flag, seq};
+  m.S = S;
+  m.mrs_row = host_mrs_row;
+  m.layer = layer;
+  m.p = mrs_p;
+  m.alpha = mrs_alpha;
+  hm::launch_router_fused(logits, T, N, ld, K, renormalize, n_shared, shared_gate_col, x, H, sel, w, pos, row_src,
+                          xp, meta_i, meta_d, m, static_cast<cudaStream_t>(stream));
   HM_LAUNCH_CHECK();
   HM_API_END
 }

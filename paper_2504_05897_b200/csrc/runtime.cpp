@@ -56,6 +56,9 @@ int hm_ep_dispatch_rows(hm_ep *, const uint16_t *, const int32_t *, const int32_
 int hm_ep_return_rows(hm_ep *, const float *, int, void *);
 int hm_ep_dispatch_buffers(hm_ep *, uint16_t **, float **);
 int hm_ep_uses_nccl(const hm_ep *);
+int hm_router_fused_mirror_mrs(const float *, int, int, int, int, int, int, int, const uint16_t *, int, int32_t *,
+                               float *, int32_t *, int32_t *, uint16_t *, int32_t *, double *, int32_t *, double *,
+                               uint16_t *, uint32_t *, uint32_t, double *, int, int, double, double *, void *);
 int hm_combine_tail(const float *, const float *, const uint64_t *, const int32_t *, const float *, int, int, int,
                     const uint16_t *, uint16_t *, double *, const double *, int, int, int, double, void *);
 }
@@ -119,7 +122,10 @@ struct Runtime {
   // device scratch
   int32_t *sel = nullptr, *counts = nullptr, *offsets = nullptr, *pos = nullptr, *row_src = nullptr;
   float *w = nullptr, *probs = nullptr, *out = nullptr;
-  double *score_sum = nullptr, *S_dev = nullptr, *scores_dev = nullptr;
+  double *score_sum = nullptr, *scores_dev = nullptr;
+  double *S_dev = nullptr;                   // device alias of the engine's (mapped) MRS table
+  double *h_mrs_row = nullptr, *dv_mrs_row = nullptr;  // the GPU-computed new row (mapped)
+  void *mrs_registered = nullptr;
   void *dmeta = nullptr, *hmeta = nullptr;  // LayerRequest block (device / pinned host)
   size_t meta_ioff = 0, meta_bytes = 0;
   uint16_t *xp = nullptr, *h = nullptr;
@@ -272,9 +278,23 @@ struct Runtime {
     RT_CUDA(cudaMalloc(&xp, rows * H * 2));
     RT_CUDA(cudaMalloc(&h, rows * I * 2));
     RT_CUDA(cudaMalloc(&out, rows * H * 4));
-    RT_CUDA(cudaMalloc(&S_dev, static_cast<size_t>(L) * N * 8));
-    std::vector<double> prior(static_cast<size_t>(L) * N, 1.0 / static_cast<double>(N));
-    RT_CUDA(cudaMemcpy(S_dev, prior.data(), prior.size() * 8, cudaMemcpyHostToDevice));
+    // the decision core's own MRS table, mapped: the zero-copy decode router
+    // reads a layer's old row from it and computes the new row on the GPU
+    // (the decision core consumes that row at step (5)); one table, no copy
+    if (engine->mrs_ && !engine->mrs_->S.empty()) {
+      const size_t bytes = (engine->mrs_->S.size() * 8 + 4095) / 4096 * 4096;
+      const cudaError_t e = cudaHostRegister(engine->mrs_->S.data(), bytes, cudaHostRegisterMapped);
+      if (e == cudaSuccess) {
+        mrs_registered = engine->mrs_->S.data();
+      } else if (e == cudaErrorHostMemoryAlreadyRegistered) {
+        (void)cudaGetLastError();
+      } else {
+        RT_CUDA(e);
+      }
+      RT_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&S_dev), engine->mrs_->S.data(), 0));
+      RT_CUDA(cudaHostAlloc(&h_mrs_row, static_cast<size_t>(N) * 8, cudaHostAllocMapped));
+      RT_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dv_mrs_row), h_mrs_row, 0));
+    }
     RT_CUDA(cudaHostAlloc(&h_scores, N * 8, 0));
     RT_CUDA(cudaHostAlloc(&h_x, rows * H * 2, cudaHostAllocMapped));
     RT_CUDA(cudaHostAlloc(&h_out, rows * H * 4, cudaHostAllocMapped));
@@ -319,9 +339,10 @@ struct Runtime {
     if (la_host) cudaFreeHost(la_host);
     for (void *p : {static_cast<void *>(pool), static_cast<void *>(sel), static_cast<void *>(w),
                     static_cast<void *>(probs), dmeta, static_cast<void *>(pos), static_cast<void *>(row_src),
-                    static_cast<void *>(xp), static_cast<void *>(h), static_cast<void *>(out),
-                    static_cast<void *>(S_dev)})
+                    static_cast<void *>(xp), static_cast<void *>(h), static_cast<void *>(out)})
       if (p) cudaFree(p);
+    if (mrs_registered) cudaHostUnregister(mrs_registered);
+    if (h_mrs_row) cudaFreeHost(h_mrs_row);
     for (void *p : {static_cast<void *>(store), hmeta, static_cast<void *>(h_scores), static_cast<void *>(h_x),
                     static_cast<void *>(h_out), static_cast<void *>(h_flag)})
       if (p) cudaFreeHost(p);
@@ -467,7 +488,17 @@ struct Runtime {
       pred_layers = la_layers.data();
       pred_loads = la_host;
     }
-    if (mirror) {
+    // the MRS row of this layer on the GPU, inside the router (zero-copy decode)
+    const bool gpu_row = mirror && cfg.gpu_mrs && engine->cfg.cache_policy == HM_POLICY_MRS && S_dev != nullptr;
+    if (mirror && gpu_row) {
+      ++seq;
+      ok(hm_router_fused_mirror_mrs(logits, T, N, ld, K, cfg.renormalize, S, cfg.shared_gate_col, x, H, sel, w, pos,
+                                    row_src, xp, counts, score_sum, static_cast<int32_t *>(dv_hmeta),
+                                    reinterpret_cast<double *>(static_cast<char *>(dv_hmeta) + meta_ioff),
+                                    mirror_rows ? dv_h_x : nullptr, dv_flag, seq, S_dev, layer, engine->mrs_->p,
+                                    engine->mrs_->alpha, dv_mrs_row, vs));
+      if (W > 1) ok(hm_mask_nonhome(sel, w, T * Kp, N, R, W, vs));
+    } else if (mirror) {
       ++seq;
       ok(hm_router_fused_mirror(logits, T, N, ld, K, cfg.renormalize, S, cfg.shared_gate_col, x, H, sel, w, pos,
                                 row_src, xp, counts, score_sum, static_cast<int32_t *>(dv_hmeta),
@@ -523,6 +554,7 @@ struct Runtime {
       h_scores[e] = scores[e];
     }
     check_fixed_residency(layer);
+    if (gpu_row) engine->gpu_mrs_row = h_mrs_row;  // step (5) takes the router's row
     engine->run_layer(layer, loads.data(), scores.data(), N, pred_layers, pred_loads, n_pred);
     const LayerRecord &rec = engine->rec;
     s.makespan_planned = rec.plan.makespan;
@@ -674,8 +706,7 @@ struct Runtime {
     if (tail) {
       // one launch: combine (+ residual, host rows zero-copy) and the MRS row
       ok(hm_combine_tail(out, dv_h_out, zc_out && !cpu_refs.empty() ? host_mask : nullptr, pos, w, T, Kp, H,
-                         cfg.residual ? x : nullptr, y, do_mrs ? S_dev : nullptr, scores_dev, layer, N,
-                         do_mrs ? engine->mrs_->p : 0, do_mrs ? engine->mrs_->alpha : 0.0, vs));
+                         cfg.residual ? x : nullptr, y, nullptr, scores_dev, layer, N, 0, 0.0, vs));
       if (stats) *stats = s;
       return;
     }
@@ -691,10 +722,6 @@ struct Runtime {
       ok(hm_combine_f32(out, pos, w, T, Kp, H, y32, vs));  // partial; the caller all-reduces
     } else {
       ok(hm_combine(out, pos, w, T, Kp, H, cfg.residual ? x : nullptr, y, vs));
-    }
-    if (cfg.gpu_mrs && engine->cfg.cache_policy == HM_POLICY_MRS && engine->mrs_) {
-      if (!fused && !disp) RT_CUDA(cudaMemcpyAsync(scores_dev, h_scores, N * 8, cudaMemcpyHostToDevice, st));
-      ok(hm_mrs_update_dev(S_dev, scores_dev, layer, N, engine->mrs_->p, engine->mrs_->alpha, vs));
     }
     if (stats) *stats = s;
   }
@@ -789,7 +816,9 @@ int hm_runtime_device_mrs(hm_runtime *rt, double *host_out) {
   HM_API_BEGIN
   auto *r = reinterpret_cast<hm::Runtime *>(rt);
   RT_CUDA(cudaDeviceSynchronize());
-  RT_CUDA(cudaMemcpy(host_out, r->S_dev, static_cast<size_t>(r->L) * r->N * 8, cudaMemcpyDeviceToHost));
+  HM_REQUIRE(r->engine->mrs_ != nullptr, HM_EVALUE, "the runtime's engine has no MRS table");
+  RT_CUDA(cudaDeviceSynchronize());
+  std::memcpy(host_out, r->engine->mrs_->S.data(), r->engine->mrs_->S.size() * 8);
   HM_API_END
 }
 
