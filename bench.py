@@ -702,9 +702,48 @@ def run_ours(args) -> None:
             "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks.summary(), "parity": parity,
             "setup_s": setup_s,
         }
+        if world == 1 and args.extra_configs:
+            line["configs"] = run_extra_configs(args)
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+EXTRA_CONFIGS = {  # BASELINE.json configs 3-4 (DeepSeek-V2-Lite, Qwen2-57B-A14B) at the 25 % budget
+    "deepseek_25": ["--shape", "deepseek", "--ratio", "0.25"],
+    "qwen2_25": ["--shape", "qwen2", "--ratio", "0.25", "--host-images", "192"],
+}
+
+
+def run_extra_configs(args) -> dict:
+    """The other named configs, each a child bench.py run (own process: the
+    Mixtral run's pinned host store is released), summarised into this line so
+    the driver's record carries them; a failure is recorded, never fatal."""
+    out = {}
+    for name in args.extra_configs.split(","):
+        if name not in EXTRA_CONFIGS:
+            out[name] = {"error": "unknown config"}
+            continue
+        cmd = [sys.executable, str(Path(__file__).resolve()), "--steps", "4", "--warmup", "3", "--no-cpu-baseline",
+               "--extra-configs", ""] + EXTRA_CONFIGS[name]
+        t0 = time.time()
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+            rows = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+            if r.returncode != 0 or not rows:
+                out[name] = {"error": f"rc={r.returncode}: {r.stderr[-300:]}"}
+                continue
+            d = json.loads(rows[-1])
+            out[name] = {"decode_tok_s": d["value"], "e2e_tok_s": d["e2e"]["value"], "ms_per_step": d["ms_per_step"],
+                         "prefill_ms": d["prefill"]["ms"], "prefill_tokens": d["prefill"]["tokens"],
+                         "config": d["config"], "per_step": d["per_step"], "roofline": d["roofline"],
+                         "step_roofline": d["step_roofline"], "model_vs_measured": d["model_vs_measured"],
+                         "parity": d["parity"], "clocks": d["clocks"], "gpu_launches": d["gpu_launches"],
+                         "steps": d["steps"], "warmup": d["warmup"], "wall_s": time.time() - t0,
+                         "argv": EXTRA_CONFIGS[name]}
+        except subprocess.TimeoutExpired:
+            out[name] = {"error": "timeout after 300 s"}
+    return out
 
 
 def refit_cpu_decode(stats, prof) -> dict | None:
@@ -818,6 +857,9 @@ def main() -> None:
     ap.add_argument("--profile-file", default=None, help="HardwareProfile key=value file instead of calibrating")
     ap.add_argument("--save-profile", default=None, help="write the calibrated HardwareProfile here")
     ap.add_argument("--prefill-profile-file", default=None)
+    ap.add_argument("--extra-configs", default="deepseek_25,qwen2_25",
+                    help="comma list of other named configs run as child processes after the headline one "
+                         "and summarised under 'configs' ('' = none)")
     ap.add_argument("--refit", action=argparse.BooleanOptionalAction, default=True,
                     help="refit the host-worker decode cost on the warm-up passes before the timed ones")
     ap.add_argument("--stage-profiles", action=argparse.BooleanOptionalAction, default=True,

@@ -47,6 +47,9 @@ struct GemvParams {
 };
 
 // h[r, i] = silu(gate_i . x_r) * (up_i . x_r) for the rows of one group.
+// The warp's first weight batch is issued before the activations are staged:
+// at decode sizes a warp owns only a few rows, so the kernel is a short chain
+// of DRAM round trips and the staging round trip is taken off it.
 template <int MR>
 __global__ void __launch_bounds__(256) ffn1_gemv_kernel(const __grid_constant__ GemvParams p) {
   extern __shared__ __align__(16) uint16_t xs[];  // [MR][H]
@@ -55,28 +58,48 @@ __global__ void __launch_bounds__(256) ffn1_gemv_kernel(const __grid_constant__ 
   asm volatile("griddepcontrol.launch_dependents;");
   const int g = blockIdx.x / p.bpg, cid = blockIdx.x % p.bpg;
   const int M = p.row_count[g], rb = p.row_begin[g], H = p.H, I = p.I;
-  for (int v = threadIdx.x; v < M * H / 8; v += blockDim.x)
-    reinterpret_cast<uint4 *>(xs)[v] = reinterpret_cast<const uint4 *>(p.xp + static_cast<size_t>(rb) * H)[v];
-  __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint16_t *w13 = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_elems;
   const int i_end = min(I, (cid + 1) * p.chunk);
-  for (int i = cid * p.chunk + wid; i < i_end; i += nw) {
+  constexpr int U = 4;
+  auto rows_of = [&](int i, const uint16_t *&wg, const uint16_t *&wu) {
     const size_t grow = static_cast<size_t>((i / kIlv) * 2 * kIlv + (i % kIlv));
-    const uint16_t *wg = w13 + grow * H;
-    const uint16_t *wu = wg + static_cast<size_t>(kIlv) * H;
+    wg = w13 + grow * H;
+    wu = wg + static_cast<size_t>(kIlv) * H;
+  };
+  // first batch of this warp's first pair, in flight during the staging
+  uint4 gv[U], uv[U];
+  const int i0 = cid * p.chunk + wid;
+  if (i0 < i_end) {
+    const uint16_t *wg, *wu;
+    rows_of(i0, wg, wu);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = lane * 8 + u * 256;
+      if (c < H) {
+        gv[u] = dev::ld_stream(wg + c);
+        uv[u] = dev::ld_stream(wu + c);
+      }
+    }
+  }
+  for (int v = threadIdx.x; v < M * H / 8; v += blockDim.x)
+    reinterpret_cast<uint4 *>(xs)[v] = reinterpret_cast<const uint4 *>(p.xp + static_cast<size_t>(rb) * H)[v];
+  __syncthreads();
+  for (int i = i0; i < i_end; i += nw) {
+    const uint16_t *wg, *wu;
+    rows_of(i, wg, wu);
     float ag[MR], au[MR];
 #pragma unroll
     for (int m = 0; m < MR; ++m) ag[m] = au[m] = 0.f;
-    constexpr int U = 4;
     for (int c0 = lane * 8; c0 < H; c0 += 256 * U) {
-      uint4 gv[U], uv[U];
+      if (i != i0 || c0 != lane * 8) {  // (the first batch is already in gv / uv)
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int c = c0 + u * 256;
-        if (c < H) {
-          gv[u] = dev::ld_stream(wg + c);
-          uv[u] = dev::ld_stream(wu + c);
+        for (int u = 0; u < U; ++u) {
+          const int c = c0 + u * 256;
+          if (c < H) {
+            gv[u] = dev::ld_stream(wg + c);
+            uv[u] = dev::ld_stream(wu + c);
+          }
         }
       }
 #pragma unroll
@@ -104,16 +127,38 @@ __global__ void __launch_bounds__(256) ffn1_gemv_kernel(const __grid_constant__ 
   }
 }
 
-// out[r, j] = W2[j, :] . h[r, :]
+// out[r, j] = W2[j, :] . h[r, :].  The warp's first weight batch is loaded
+// BEFORE waiting for ffn1 (programmatic dependent launch): W2 does not depend
+// on h, so at decode sizes most of a warp's bytes are in flight while ffn1
+// finishes, and the wait + h staging overlap them.
 template <int MR>
 __global__ void __launch_bounds__(256) ffn2_gemv_kernel(const __grid_constant__ GemvParams p) {
   extern __shared__ __align__(16) uint16_t hs[];  // [MR][I]
   const int g = blockIdx.x / p.bpg, cid = blockIdx.x % p.bpg;
   const int M = p.row_count[g], rb = p.row_begin[g], H = p.H, I = p.I;
-  if (p.l2_prefetch) {  // prologue independent of ffn1: pull this block's W2 rows into L2
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint16_t *w2 = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_elems + static_cast<size_t>(2) * I * H;
+  const int j_end = min(H, (cid + 1) * p.chunk);
+  // two rows per warp at a time (rows j and j + nw): twice the loads in flight
+  // per warp -- small-I experts (DeepSeek: 2.8 KB rows) were latency-bound
+  constexpr int RW = 2, U = 4;
+  const int jf = cid * p.chunk + wid;
+  uint4 wv[RW][U];
+  if (jf < j_end) {
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      const bool live = jf + r * nw < j_end;
+      const uint16_t *wr = w2 + static_cast<size_t>(live ? jf + r * nw : jf) * I;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = lane * 8 + u * 256;
+        if (c < I && live) wv[r][u] = dev::ld_stream(wr + c);
+      }
+    }
+  }
+  if (p.l2_prefetch) {  // the rest of this block's W2 rows into L2 (independent of ffn1)
     const int j0 = cid * p.chunk, j1 = min(H, (cid + 1) * p.chunk);
-    const char *base = reinterpret_cast<const char *>(p.pool + static_cast<size_t>(p.slot[g]) * p.slot_elems +
-                                                      static_cast<size_t>(2) * I * H + static_cast<size_t>(j0) * I);
+    const char *base = reinterpret_cast<const char *>(w2 + static_cast<size_t>(j0) * I);
     const size_t bytes = j1 > j0 ? static_cast<size_t>(j1 - j0) * I * 2 : 0;
     for (size_t o = static_cast<size_t>(threadIdx.x) * 128; o < bytes; o += static_cast<size_t>(blockDim.x) * 128)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(base + o));
@@ -123,13 +168,7 @@ __global__ void __launch_bounds__(256) ffn2_gemv_kernel(const __grid_constant__ 
   for (int v = threadIdx.x; v < M * I / 8; v += blockDim.x)
     reinterpret_cast<uint4 *>(hs)[v] = reinterpret_cast<const uint4 *>(p.h + static_cast<size_t>(rb) * I)[v];
   __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const uint16_t *w2 = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_elems + static_cast<size_t>(2) * I * H;
-  const int j_end = min(H, (cid + 1) * p.chunk);
-  // two rows per warp at a time (rows j and j + nw): twice the loads in flight
-  // per warp -- small-I experts (DeepSeek: 2.8 KB rows) were latency-bound
-  constexpr int RW = 2;
-  for (int j0 = cid * p.chunk + wid; j0 < j_end; j0 += nw * RW) {
+  for (int j0 = jf; j0 < j_end; j0 += nw * RW) {
     const uint16_t *wr[RW];
     bool live[RW];
 #pragma unroll
@@ -142,16 +181,16 @@ __global__ void __launch_bounds__(256) ffn2_gemv_kernel(const __grid_constant__ 
     for (int m = 0; m < MR; ++m)
 #pragma unroll
       for (int r = 0; r < RW; ++r) acc[m][r] = 0.f;
-    constexpr int U = 4;
     for (int c0 = lane * 8; c0 < I; c0 += 256 * U) {
-      uint4 wv[RW][U];
+      if (j0 != jf || c0 != lane * 8) {  // (the first batch is already in wv)
 #pragma unroll
-      for (int r = 0; r < RW; ++r)
+        for (int r = 0; r < RW; ++r)
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int c = c0 + u * 256;
-          if (c < I && live[r]) wv[r][u] = dev::ld_stream(wr[r] + c);
-        }
+          for (int u = 0; u < U; ++u) {
+            const int c = c0 + u * 256;
+            if (c < I && live[r]) wv[r][u] = dev::ld_stream(wr[r] + c);
+          }
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int c = c0 + u * 256;
