@@ -154,38 +154,51 @@ __device__ void stage_x_q8(const uint16_t *__restrict__ x, int K, uint8_t *st) {
   }
 }
 
-// 32 weights (one 16-byte nibble load) of a row against staged block b ->
-// sum_k (n_k - 8) x_k in fp32
-__device__ __forceinline__ float q4_dot32(const uint4 w, const uint8_t *st, int nb, int b) {
+// One staged 32-element activation block: the four digit planes + scales.
+struct XChunk {
+  int eh[4], oh[4], el[4], ol[4];
+  float sx, sq;
+};
+__device__ __forceinline__ XChunk load_xchunk(const uint8_t *st, int nb, int b) {
   const int4 *pl = reinterpret_cast<const int4 *>(st) + b;
   const int4 eh = pl[0], oh = pl[nb], el = pl[2 * nb], ol = pl[3 * nb];
-  const float sx = reinterpret_cast<const float *>(st + static_cast<size_t>(nb) * 64)[b];
-  const float sq = reinterpret_cast<const float *>(st + static_cast<size_t>(nb) * 64)[nb + b];
+  const float *f = reinterpret_cast<const float *>(st + static_cast<size_t>(nb) * 64);
+  return XChunk{{eh.x, eh.y, eh.z, eh.w}, {oh.x, oh.y, oh.z, oh.w}, {el.x, el.y, el.z, el.w},
+                {ol.x, ol.y, ol.z, ol.w}, f[b], f[nb + b]};
+}
+
+// 32 weights (one 16-byte nibble load) of a row against a staged block ->
+// sum_k (n_k - 8) x_k in fp32
+__device__ __forceinline__ float q4_dot32(const uint4 w, const XChunk &x) {
   const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-  const int ehv[4] = {eh.x, eh.y, eh.z, eh.w}, ohv[4] = {oh.x, oh.y, oh.z, oh.w};
-  const int elv[4] = {el.x, el.y, el.z, el.w}, olv[4] = {ol.x, ol.y, ol.z, ol.w};
   int ah = 0, al = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int lo = static_cast<int>(ws[q] & 0x0F0F0F0Fu);         // elements 8q + 0, 2, 4, 6
     const int hi = static_cast<int>((ws[q] >> 4) & 0x0F0F0F0Fu);  // elements 8q + 1, 3, 5, 7
-    ah = __dp4a(lo, ehv[q], ah);
-    ah = __dp4a(hi, ohv[q], ah);
-    al = __dp4a(lo, elv[q], al);
-    al = __dp4a(hi, olv[q], al);
+    ah = __dp4a(lo, x.eh[q], ah);
+    ah = __dp4a(hi, x.oh[q], ah);
+    al = __dp4a(lo, x.el[q], al);
+    al = __dp4a(hi, x.ol[q], al);
   }
-  return sx * (static_cast<float>(ah) + static_cast<float>(al) * (1.f / 256.f) - 8.f * sq);
+  return x.sx * (static_cast<float>(ah) + static_cast<float>(al) * (1.f / 256.f) - 8.f * x.sq);
 }
 
-// NR rows (sharing x) dotted with the staged x; each lane handles 32-weight
-// chunks lane*32 + 1024*j, U chunks per row loaded before any is consumed (the
-// memory-level parallelism of the bf16 GEMV).  Returns the lane's partials.
-template <int NR, int U>
+// NR rows (sharing x) dotted with the M staged activation rows; each lane
+// handles 32-weight chunks lane*32 + 1024*j, U chunks per row loaded before
+// any is consumed.  Every weight byte is loaded once for all M rows, and every
+// staged activation block once for all NR rows: shared-memory traffic per
+// weight byte is 4M/NR (it was 4 per row and token -- the kernel was bound by
+// it, not by HBM).  Returns the lane's partials acc[m][r].
+template <int MR, int NR, int U>
 __device__ __forceinline__ void q4_rows_dot(const uint8_t *const (&rows)[NR], const uint16_t *const (&sc)[NR],
-                                            const uint8_t *st, int K, int lane, float (&acc)[NR]) {
+                                            const bool (&live)[NR], const uint8_t *st, int stage_bytes, int M, int K,
+                                            int lane, float (&acc)[MR][NR]) {
   const int nb = q4_pad(K) / 32;
 #pragma unroll
-  for (int r = 0; r < NR; ++r) acc[r] = 0.f;
+  for (int m = 0; m < MR; ++m)
+#pragma unroll
+    for (int r = 0; r < NR; ++r) acc[m][r] = 0.f;
   for (int c0 = lane * 32; c0 < K; c0 += 1024 * U) {
     uint4 w[NR][U];
     float s[NR][U];
@@ -194,7 +207,7 @@ __device__ __forceinline__ void q4_rows_dot(const uint8_t *const (&rows)[NR], co
       const int c = c0 + u * 1024;
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
-        if (c < K) {
+        if (c < K && live[r]) {
           w[r][u] = dev::ld_stream(rows[r] + c / 2);
           s[r][u] = dev::bf2f(sc[r][c / kQG]);
         }
@@ -205,7 +218,14 @@ __device__ __forceinline__ void q4_rows_dot(const uint8_t *const (&rows)[NR], co
       const int c = c0 + u * 1024;
       if (c < K) {
 #pragma unroll
-        for (int r = 0; r < NR; ++r) acc[r] = fmaf(s[r][u], q4_dot32(w[r][u], st, nb, c / 32), acc[r]);
+        for (int m = 0; m < MR; ++m) {
+          if (m < M) {
+            const XChunk x = load_xchunk(st + m * stage_bytes, nb, c / 32);
+#pragma unroll
+            for (int r = 0; r < NR; ++r)
+              if (live[r]) acc[m][r] = fmaf(s[r][u], q4_dot32(w[r][u], x), acc[m][r]);
+          }
+        }
       }
     }
   }
@@ -221,8 +241,10 @@ struct Q4GemvParams {
   int32_t slot[kQ4MaxGroups], row_begin[kQ4MaxGroups], row_count[kQ4MaxGroups];
 };
 
+// two (gate, up) pairs per warp at a time (pairs i and i + nw): four rows
+// share every staged activation block
 template <int MR>
-__global__ void __launch_bounds__(256, 4) ffn1_q4_kernel(const __grid_constant__ Q4GemvParams p) {
+__global__ void __launch_bounds__(256, MR == 1 ? 3 : 2) ffn1_q4_kernel(const __grid_constant__ Q4GemvParams p) {
   extern __shared__ __align__(16) uint8_t xs1[];  // [MR][q4_stage_bytes(H)]
   const int g = blockIdx.x / p.bpg, cid = blockIdx.x % p.bpg;
   const int M = p.row_count[g], rb = p.row_begin[g], H = p.H, I = p.I;
@@ -234,27 +256,43 @@ __global__ void __launch_bounds__(256, 4) ffn1_q4_kernel(const __grid_constant__
   const uint16_t *s13 = reinterpret_cast<const uint16_t *>(img + L.s13_off);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int i_end = min(I, (cid + 1) * p.chunk);
-  for (int i = cid * p.chunk + wid; i < i_end; i += nw) {
-    const size_t grow = static_cast<size_t>((i / kIlvQ) * 2 * kIlvQ + (i % kIlvQ));
-    const uint8_t *wg = img + grow * (H / 2), *wu = wg + static_cast<size_t>(kIlvQ) * (H / 2);
-    const uint16_t *sg = s13 + grow * (H / kQG), *su = sg + static_cast<size_t>(kIlvQ) * (H / kQG);
-    const uint8_t *rows[2] = {wg, wu};
-    const uint16_t *scs[2] = {sg, su};
+  for (int i0 = cid * p.chunk + wid; i0 < i_end; i0 += 2 * nw) {
+    const uint8_t *rows[4];
+    const uint16_t *scs[4];
+    bool live[4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int i = i0 + q * nw;
+      const int ii = i < i_end ? i : i0;
+      const size_t grow = static_cast<size_t>((ii / kIlvQ) * 2 * kIlvQ + (ii % kIlvQ));
+      rows[2 * q] = img + grow * (H / 2);
+      rows[2 * q + 1] = rows[2 * q] + static_cast<size_t>(kIlvQ) * (H / 2);
+      scs[2 * q] = s13 + grow * (H / kQG);
+      scs[2 * q + 1] = scs[2 * q] + static_cast<size_t>(kIlvQ) * (H / kQG);
+      live[2 * q] = live[2 * q + 1] = i < i_end;
+    }
+    float a[MR][4];
+    q4_rows_dot<MR, 4, 2>(rows, scs, live, xs1, Hs, M, H, lane, a);
 #pragma unroll
     for (int m = 0; m < MR; ++m) {
       if (m < M) {
-        float a[2];
-        q4_rows_dot<2, 4>(rows, scs, xs1 + m * Hs, H, lane, a);
-        const float gs = dev::warp_sum(a[0]);
-        const float us = dev::warp_sum(a[1]);
-        if (lane == 0) p.h[static_cast<size_t>(rb + m) * I + i] = dev::f2bf(dev::silu(gs) * us);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (!live[2 * q]) continue;
+          const float gs = dev::warp_sum(a[m][2 * q]);
+          const float us = dev::warp_sum(a[m][2 * q + 1]);
+          if (lane == 0) p.h[static_cast<size_t>(rb + m) * I + i0 + q * nw] = dev::f2bf(dev::silu(gs) * us);
+        }
       }
     }
   }
 }
 
-template <int MR>
-__global__ void __launch_bounds__(256, 4) ffn2_q4_kernel(const __grid_constant__ Q4GemvParams p) {
+// NR W2 rows per warp at a time (j, j + nw, ..): NR = 4 when the layer has
+// rows to spare (every staged block shared by four rows), fewer when a single
+// expert's H rows would leave most warps idle (Mixtral, 1 expert: NR = 1)
+template <int MR, int NR>
+__global__ void __launch_bounds__(256, MR == 1 ? 3 : 2) ffn2_q4_kernel(const __grid_constant__ Q4GemvParams p) {
   extern __shared__ __align__(16) uint8_t hs2[];  // [MR][q4_stage_bytes(I)]
   const int g = blockIdx.x / p.bpg, cid = blockIdx.x % p.bpg;
   const int M = p.row_count[g], rb = p.row_begin[g], H = p.H, I = p.I;
@@ -267,18 +305,30 @@ __global__ void __launch_bounds__(256, 4) ffn2_q4_kernel(const __grid_constant__
   const uint16_t *s2 = reinterpret_cast<const uint16_t *>(img + L.s2_off);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int j_end = min(H, (cid + 1) * p.chunk);
-  for (int j = cid * p.chunk + wid; j < j_end; j += nw) {
-    const uint8_t *wr = w2 + static_cast<size_t>(j) * (I / 2);
-    const uint16_t *sr = s2 + static_cast<size_t>(j) * (I / kQG);
-    const uint8_t *rows[1] = {wr};
-    const uint16_t *scs[1] = {sr};
+  constexpr int U = NR == 1 ? 4 : 2;
+  for (int j0 = cid * p.chunk + wid; j0 < j_end; j0 += NR * nw) {
+    const uint8_t *rows[NR];
+    const uint16_t *scs[NR];
+    bool live[NR];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const int j = j0 + q * nw;
+      live[q] = j < j_end;
+      const int jj = live[q] ? j : j0;
+      rows[q] = w2 + static_cast<size_t>(jj) * (I / 2);
+      scs[q] = s2 + static_cast<size_t>(jj) * (I / kQG);
+    }
+    float a[MR][NR];
+    q4_rows_dot<MR, NR, U>(rows, scs, live, hs2, Is, M, I, lane, a);
 #pragma unroll
     for (int m = 0; m < MR; ++m) {
       if (m < M) {
-        float a[1];
-        q4_rows_dot<1, 4>(rows, scs, hs2 + m * Is, I, lane, a);
-        const float s = dev::warp_sum(a[0]);
-        if (lane == 0) p.out[static_cast<size_t>(rb + m) * H + j] = s;
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+          if (!live[q]) continue;
+          const float s = dev::warp_sum(a[m][q]);
+          if (lane == 0) p.out[static_cast<size_t>(rb + m) * H + j0 + q * nw] = s;
+        }
       }
     }
   }
@@ -319,9 +369,9 @@ void launch_q4_gemv(const uint8_t *pool, size_t slot_bytes, int H, int I, const 
     p.row_count[g] = gs[g].row_count;
     mr = std::max(mr, gs[g].row_count);
   }
-  const int target = sm_count() * 4, G = p.n_groups;
+  const int target = sm_count() * 3, G = p.n_groups;  // 3 resident blocks per SM (80 registers)
   static const int c1 = [] { const char *e = std::getenv("HM_Q4_CHUNK1"); return e ? std::atoi(e) : 8; }();
-  static const int c2 = [] { const char *e = std::getenv("HM_Q4_CHUNK2"); return e ? std::atoi(e) : 8; }();
+  static const int c2 = [] { const char *e = std::getenv("HM_Q4_CHUNK2"); return e ? std::atoi(e) : 0; }();
   p.chunk = std::max(c1, static_cast<int>((static_cast<long>(G) * I + target - 1) / target + 7) / 8 * 8);
   p.bpg = (I + p.chunk - 1) / p.chunk;
   int smem = mr * q4_stage_bytes(H);
@@ -331,14 +381,28 @@ void launch_q4_gemv(const uint8_t *pool, size_t slot_bytes, int H, int I, const 
     default: q4_smem(ffn1_q4_kernel<4>, smem); ffn1_q4_kernel<4><<<G * p.bpg, 256, smem, st>>>(p); break;
   }
   HM_LAUNCH_CHECK();
-  p.chunk = std::max(c2, static_cast<int>((static_cast<long>(G) * H + target - 1) / target + 7) / 8 * 8);
+  // ffn2: rows per warp-iteration from the rows available per resident warp
+  const long rows2 = static_cast<long>(G) * H, warps = static_cast<long>(target) * 8;
+  const int nr = rows2 >= 3 * warps ? 4 : rows2 >= 3 * warps / 2 ? 2 : 1;
+  p.chunk = std::max(c2 > 8 ? c2 : nr, static_cast<int>((rows2 + target - 1) / target + nr - 1) / nr * nr);
   p.bpg = (H + p.chunk - 1) / p.chunk;
   smem = mr * q4_stage_bytes(I);
-  switch (mr) {
-    case 1: q4_smem(ffn2_q4_kernel<1>, smem); ffn2_q4_kernel<1><<<G * p.bpg, 256, smem, st>>>(p); break;
-    case 2: q4_smem(ffn2_q4_kernel<2>, smem); ffn2_q4_kernel<2><<<G * p.bpg, 256, smem, st>>>(p); break;
-    default: q4_smem(ffn2_q4_kernel<4>, smem); ffn2_q4_kernel<4><<<G * p.bpg, 256, smem, st>>>(p); break;
+#define HM_Q4_FFN2(MRV, NRV)                                            \
+  q4_smem(ffn2_q4_kernel<MRV, NRV>, smem);                              \
+  ffn2_q4_kernel<MRV, NRV><<<G * p.bpg, 256, smem, st>>>(p)
+  const int sel = (mr == 1 ? 0 : mr == 2 ? 1 : 2) * 3 + (nr == 4 ? 0 : nr == 2 ? 1 : 2);
+  switch (sel) {
+    case 0: HM_Q4_FFN2(1, 4); break;
+    case 1: HM_Q4_FFN2(1, 2); break;
+    case 2: HM_Q4_FFN2(1, 1); break;
+    case 3: HM_Q4_FFN2(2, 4); break;
+    case 4: HM_Q4_FFN2(2, 2); break;
+    case 5: HM_Q4_FFN2(2, 1); break;
+    case 6: HM_Q4_FFN2(4, 4); break;
+    case 7: HM_Q4_FFN2(4, 2); break;
+    default: HM_Q4_FFN2(4, 1); break;
   }
+#undef HM_Q4_FFN2
   HM_LAUNCH_CHECK();
 }
 
