@@ -620,6 +620,17 @@ def run_ours(args) -> None:
                      "traffic_algorithmic_bytes": tm.get("algorithmic_bytes"), "peak_kind": pk_kind + " burst",
                      "kernel": "expert_gemm_kernel (ffn1 SwiGLU + ffn2), 256 tokens x 8 experts",
                      "ms": gb["ms"], "hbm_gbs": gb["hbm_gbs"]}
+    # 256 tokens per expert is 256 flop per weight byte -- the ridge: the shape's
+    # own roof is min(tensor peak, HBM x intensity); and the same kernel at a
+    # compute-bound shape (1024 tokens per expert) for the tensor-pipe side
+    ai = 256.0
+    shape_roof = min(tc_peak, hbm_peak * ai / 1e3)
+    gemm_roofline.update({"flop_per_weight_byte": ai, "shape_roof_tflops": shape_roof,
+                          "frac_of_shape_roof": gb["tflops"] / shape_roof})
+    gc = gemm_bench(H, I, rows_per_expert=1024, n_experts=4, reps=3)
+    gemm_roofline["compute_bound"] = {"tokens_per_expert": 1024, "experts": 4, "achieved": gc["tflops"],
+                                      "frac": gc["tflops"] / tc_peak, "ms": gc["ms"],
+                                      "ncu_tensor_pipe_active": "85.1 % / 80.9 % (profiles/r02_ncu_gemm_q4.md)"}
 
     # ---- BASELINE.md §5 A (decision path) and C (simulator prediction vs measured)
     decision_baseline = None
