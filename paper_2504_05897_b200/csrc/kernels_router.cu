@@ -509,6 +509,10 @@ struct CombineTail {
   const double *scores;
   int layer, N, p;
   double a;
+  // pre-launched tail: wait until the host worker has published its rows
+  // (*gate reaches gate_seq, mapped host memory) before reading them
+  const uint32_t *gate;
+  uint32_t gate_seq;
 };
 
 __device__ void mrs_row_update(double *__restrict__ S, const double *__restrict__ s, int layer, int N, int p,
@@ -544,6 +548,14 @@ __global__ void __launch_bounds__(kTailThreads) combine_tail_kernel(const __grid
   for (int k = threadIdx.x; k < c.Kp; k += blockDim.x) {
     s_w[k] = c.w[static_cast<size_t>(t) * c.Kp + k];
     s_pos[k] = c.pos[static_cast<size_t>(t) * c.Kp + k];
+  }
+  if (c.gate && threadIdx.x == 0) {  // launched before the host worker ran: wait for its rows
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(c.gate) : "memory");
+      if (static_cast<int32_t>(v - c.gate_seq) >= 0) break;
+      __nanosleep(128);
+    }
   }
   __syncthreads();
   if (col >= c.H) return;
@@ -864,9 +876,22 @@ int hm_residual_add(const float *y32, const uint16_t *residual, int T, int H, ui
   HM_API_END
 }
 
+int hm_combine_tail_gated(const float *out, const float *host_out, const uint64_t *host_mask4, const int32_t *pos,
+                          const float *w, int T, int Kp, int H, const uint16_t *residual, uint16_t *y, double *S,
+                          const double *scores, int layer, int N, int p, double alpha, const uint32_t *gate,
+                          uint32_t gate_seq, void *stream);
+
 int hm_combine_tail(const float *out, const float *host_out, const uint64_t *host_mask4, const int32_t *pos,
                     const float *w, int T, int Kp, int H, const uint16_t *residual, uint16_t *y, double *S,
                     const double *scores, int layer, int N, int p, double alpha, void *stream) {
+  return hm_combine_tail_gated(out, host_out, host_mask4, pos, w, T, Kp, H, residual, y, S, scores, layer, N, p,
+                               alpha, nullptr, 0u, stream);
+}
+
+int hm_combine_tail_gated(const float *out, const float *host_out, const uint64_t *host_mask4, const int32_t *pos,
+                          const float *w, int T, int Kp, int H, const uint16_t *residual, uint16_t *y, double *S,
+                          const double *scores, int layer, int N, int p, double alpha, const uint32_t *gate,
+                          uint32_t gate_seq, void *stream) {
   HM_API_BEGIN
   HM_REQUIRE(H % 4 == 0, HM_EVALUE, "hidden size must be a multiple of 4");
   HM_REQUIRE(!S || (N >= 1 && N <= 256), HM_EVALUE, "MRS row too wide for the fused tail");
@@ -887,6 +912,8 @@ int hm_combine_tail(const float *out, const float *host_out, const uint64_t *hos
   c.N = N;
   c.p = p;
   c.a = alpha;
+  c.gate = gate;
+  c.gate_seq = gate_seq;
   HM_REQUIRE(Kp <= hm::kTailMaxKp, HM_EVALUE, "too many selections per token for the fused tail");
   const int cs = (H + 4 * hm::kTailThreads - 1) / (4 * hm::kTailThreads);
   const long blocks = static_cast<long>(T) * cs + (S ? 1 : 0);

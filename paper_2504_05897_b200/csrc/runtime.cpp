@@ -56,6 +56,9 @@ int hm_ep_dispatch_rows(hm_ep *, const uint16_t *, const int32_t *, const int32_
 int hm_ep_return_rows(hm_ep *, const float *, int, void *);
 int hm_ep_dispatch_buffers(hm_ep *, uint16_t **, float **);
 int hm_ep_uses_nccl(const hm_ep *);
+int hm_combine_tail_gated(const float *, const float *, const uint64_t *, const int32_t *, const float *, int, int, int,
+                          const uint16_t *, uint16_t *, double *, const double *, int, int, int, double,
+                          const uint32_t *, uint32_t, void *);
 int hm_router_fused_mirror_mrs(const float *, int, int, int, int, int, int, int, const uint16_t *, int, int32_t *,
                                float *, int32_t *, int32_t *, uint16_t *, int32_t *, double *, int32_t *, double *,
                                uint16_t *, uint32_t *, uint32_t, double *, int, int, double, double *, void *);
@@ -143,6 +146,7 @@ struct Runtime {
   float *dv_h_out = nullptr;
   uint32_t *h_flag = nullptr, *dv_flag = nullptr;
   uint32_t seq = 0, gate_seq = 0;  // h_flag[0]: router flag; h_flag[8]: kernel-timing gate
+  uint32_t tail_seq = 0;           // h_flag[4]: host worker done (pre-launched combine tail)
   // live look-ahead prediction (hm_runtime_set_lookahead): gates [L][la_ld][H]
   // of the model, applied to each layer's input for layers l+1..l+la_hz; the
   // predicted loads land in pinned memory (mapped: written by the kernel)
@@ -657,6 +661,29 @@ struct Runtime {
       if (rb + rc > 256) zc_out = false;
       for (int q = rb; q < rb + rc && q < 256; ++q) host_mask[q >> 6] |= 1ull << (q & 63);
     }
+    // decode: the combine tail is launched BEFORE the host worker runs, gated on
+    // a mapped flag the host raises when the worker's rows are written -- its
+    // launch latency leaves the serial path (the GPU starts it within a PCIe
+    // poll of the flag); the release is RAII so an exception never leaves the
+    // GPU waiting
+    const bool pre_tail = tail && zc_out && !cpu_refs.empty();
+    struct TailGate {
+      Runtime *r;
+      bool on;
+      void open() {
+        if (!on) return;
+        std::atomic_thread_fence(std::memory_order_release);
+        reinterpret_cast<volatile uint32_t *>(r->h_flag)[4] = r->tail_seq;
+        on = false;
+      }
+      ~TailGate() { open(); }
+    } tail_gate{this, false};
+    if (pre_tail) {
+      ++tail_seq;
+      tail_gate.on = true;
+      ok(hm_combine_tail_gated(out, dv_h_out, host_mask, pos, w, T, Kp, H, cfg.residual ? x : nullptr, y, nullptr,
+                               scores_dev, layer, N, 0, 0.0, dv_flag + 4, tail_seq, vs));
+    }
     if (!cpu_refs.empty()) {
       if (!mirror_rows) RT_CUDA(cudaEventSynchronize(ev_rows));
       const double c0 = now_us();
@@ -703,8 +730,13 @@ struct Runtime {
         }
       }
     }
+    tail_gate.open();
+    if (pre_tail) {
+      if (stats) *stats = s;
+      return;
+    }
     if (tail) {
-      // one launch: combine (+ residual, host rows zero-copy) and the MRS row
+      // one launch: combine (+ residual, host rows zero-copy)
       ok(hm_combine_tail(out, dv_h_out, zc_out && !cpu_refs.empty() ? host_mask : nullptr, pos, w, T, Kp, H,
                          cfg.residual ? x : nullptr, y, nullptr, scores_dev, layer, N, 0, 0.0, vs));
       if (stats) *stats = s;
