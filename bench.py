@@ -720,9 +720,11 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
-EXTRA_CONFIGS = {  # BASELINE.json configs 3-4 (DeepSeek-V2-Lite, Qwen2-57B-A14B) at the 25 % budget
+EXTRA_CONFIGS = {  # BASELINE.json configs 3-4: DeepSeek-V2-Lite at 25 %, Qwen2-57B-A14B budget sweep 10/25/50 %
     "deepseek_25": ["--shape", "deepseek", "--ratio", "0.25"],
     "qwen2_25": ["--shape", "qwen2", "--ratio", "0.25", "--host-images", "192"],
+    "qwen2_10": ["--shape", "qwen2", "--ratio", "0.10", "--host-images", "192"],
+    "qwen2_50": ["--shape", "qwen2", "--ratio", "0.50", "--host-images", "192"],
 }
 
 
@@ -750,6 +752,7 @@ def run_extra_configs(args) -> dict:
                          "config": d["config"], "per_step": d["per_step"], "roofline": d["roofline"],
                          "step_roofline": d["step_roofline"], "model_vs_measured": d["model_vs_measured"],
                          "parity": d["parity"], "clocks": d["clocks"], "gpu_launches": d["gpu_launches"],
+                         "decode_refit": d.get("decode_refit"), "h2d_roofline": d.get("h2d_roofline"),
                          "steps": d["steps"], "warmup": d["warmup"], "wall_s": time.time() - t0,
                          "argv": EXTRA_CONFIGS[name]}
         except subprocess.TimeoutExpired:
@@ -868,7 +871,7 @@ def main() -> None:
     ap.add_argument("--profile-file", default=None, help="HardwareProfile key=value file instead of calibrating")
     ap.add_argument("--save-profile", default=None, help="write the calibrated HardwareProfile here")
     ap.add_argument("--prefill-profile-file", default=None)
-    ap.add_argument("--extra-configs", default="deepseek_25,qwen2_25",
+    ap.add_argument("--extra-configs", default="deepseek_25,qwen2_10,qwen2_25,qwen2_50",
                     help="comma list of other named configs run as child processes after the headline one "
                          "and summarised under 'configs' ('' = none)")
     ap.add_argument("--refit", action=argparse.BooleanOptionalAction, default=True,

@@ -439,6 +439,9 @@ int hm_cpu_experts_decode(hm_cpu_pool *pool, const uint16_t *const *imgs, const 
 /* Best-of-reps host DRAM read bandwidth (GB/s) over `bytes` at p (64-byte aligned). */
 /* Decode split granularity in gate/up pairs (0: whole 128-pair blocks); tuning knob. */
 int hm_cpu_set_decode_grain(int grain);
+/* Bytes of its phase-2 (W2) rows each decode thread prefetches toward the LLC
+ * while it waits at the phase-1 barrier (0 disables, the default: measured neutral). */
+int hm_cpu_set_decode_bridge(int kbytes);
 int hm_host_read_bw(hm_cpu_pool *pool, const void *p, size_t bytes, int reps, double *gbs);
 
 typedef struct hm_runtime hm_runtime;

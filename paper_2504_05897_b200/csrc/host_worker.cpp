@@ -90,14 +90,21 @@ void ThreadPool::run(const std::function<void(int, int)> &fn) {
   wait_until([&] { return pending_.load(std::memory_order_acquire) == 0; });
 }
 
-void ThreadPool::barrier() {
+void ThreadPool::barrier() { wait(arrive()); }
+
+uint32_t ThreadPool::arrive() {
   const uint32_t sense = bar_sense_.load(std::memory_order_acquire);
   if (bar_count_.fetch_add(1, std::memory_order_acq_rel) == n_ - 1) {
     bar_count_.store(0, std::memory_order_relaxed);
     bar_sense_.store(sense + 1, std::memory_order_release);
-  } else {
-    wait_until([&] { return bar_sense_.load(std::memory_order_acquire) != sense; });
   }
+  return sense;
+}
+
+bool ThreadPool::passed(uint32_t token) const { return bar_sense_.load(std::memory_order_acquire) != token; }
+
+void ThreadPool::wait(uint32_t token) {
+  wait_until([&] { return passed(token); });
 }
 
 // ------------------------------------------------------------ kernels
@@ -293,6 +300,17 @@ int &decode_grain() {
     return s ? std::atoi(s) : 16;
   }();
   return g;
+}
+
+// Bytes of its phase-2 rows a decode thread may prefetch while waiting at the
+// phase barrier (HM_DECODE_BRIDGE_KB; default 0 = off: an interleaved A/B on
+// the GPU boxes, tools/host_bridge_ab.py, measured it neutral within 3 %).
+size_t &decode_bridge_bytes() {
+  static size_t b = [] {
+    const char *s = std::getenv("HM_DECODE_BRIDGE_KB");
+    return static_cast<size_t>(s ? std::atol(s) : 0) << 10;
+  }();
+  return b;
 }
 
 // ------------------------------------------------------------ AMX (prefill)
@@ -956,8 +974,29 @@ void cpu_experts_decode(ThreadPool &pool, const uint16_t *const *imgs, const uin
         q += i1 - i0;
       }
     }
-    pool.barrier();
+    // h is complete only when every thread has finished phase 1; a thread that
+    // arrives early pulls the head of its phase-2 rows (W2 does not depend on
+    // h) toward the LLC until the last one arrives, so DRAM stays busy through
+    // the phase-1 imbalance instead of idling at the barrier
+    const uint32_t token = pool.arrive();
     const long r1 = static_cast<long>(n) * H;
+    {
+      const size_t cap = decode_bridge_bytes();
+      size_t done = 0;
+      for (long u = r1 * tid / nt; u < r1 * (tid + 1) / nt && done < cap && !pool.passed(token);) {
+        const int e = static_cast<int>(u / H), j0 = static_cast<int>(u % H);
+        const int j1 = static_cast<int>(std::min<long>(H, j0 + (r1 * (tid + 1) / nt - u)));
+        const char *p = reinterpret_cast<const char *>(imgs[e] + static_cast<size_t>(2) * I * H +
+                                                       static_cast<size_t>(j0) * I);
+        const size_t len = static_cast<size_t>(j1 - j0) * I * 2;
+        for (size_t o = 0; o < len && done < cap; o += 4096, done += 4096) {
+          if (pool.passed(token)) break;
+          for (size_t l = o; l < std::min(len, o + 4096); l += 64) _mm_prefetch(p + l, _MM_HINT_T2);
+        }
+        u += j1 - j0;
+      }
+    }
+    pool.wait(token);
     for (long u = r1 * tid / nt; u < r1 * (tid + 1) / nt;) {
       const int e = static_cast<int>(u / H), j0 = static_cast<int>(u % H);
       const int j1 = static_cast<int>(std::min<long>(H, j0 + (r1 * (tid + 1) / nt - u)));
@@ -1065,6 +1104,13 @@ int hm_cpu_set_prefetch(int dist, int hint) {
 }
 
 // Tuning knob for the decode split granularity (pairs; 0 = whole 128-pair blocks).
+int hm_cpu_set_decode_bridge(int kbytes) {
+  HM_API_BEGIN
+  HM_REQUIRE(kbytes >= 0, HM_EVALUE, "bad decode bridge size");
+  hm::decode_bridge_bytes() = static_cast<size_t>(kbytes) << 10;
+  HM_API_END
+}
+
 int hm_cpu_set_decode_grain(int grain) {
   HM_API_BEGIN
   HM_REQUIRE(grain >= 0, HM_EVALUE, "bad decode grain");

@@ -24,6 +24,12 @@ class ThreadPool {
   int size() const { return n_; }
   void run(const std::function<void(int, int)> &fn);
   void barrier();
+  // split barrier: arrive() returns the phase token; passed(token) tells
+  // whether every thread has arrived; wait(token) blocks until then.  Lets a
+  // thread do useful work (prefetch its next phase) while it waits.
+  uint32_t arrive();
+  bool passed(uint32_t token) const;
+  void wait(uint32_t token);
 
  private:
   void loop(int tid);

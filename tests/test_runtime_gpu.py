@@ -334,3 +334,46 @@ def test_q4_stack_parity():
         passes.append(mcore.ForwardPass(fwd.stage, fwd.token_count, tuple(layers)))
     m = me.run_trace(mcore.Trace(cfg, tuple(passes)), policy, 0.5, prof, 2, decision_log=True)
     assert digest(from_records(recs, True)) == digest(from_records(m.decisions, True))
+
+
+@pytest.mark.parametrize("family", ["tiny", "deepseek"])
+def test_gpu_mrs_rows_drive_decisions_bit_identically(family):
+    """Score updates on the GPU (zero-copy decode path): the router computes each
+    layer's new MRS row from the decision core's mapped table and the decision
+    core consumes it at step (5).  Against the host recurrence (gpu_mrs=False):
+    identical decision streams, MRS tables and outputs over prefill + decode
+    passes -- and both equal the reference's decisions replayed on the same
+    LayerRequests."""
+    from paper_2504_05897_b200.moe import TracePredictor
+    cfg = family_cfg(family)
+    prof = stress_profile(cfg)
+    policy = me.EnginePolicy(prefetch=True)
+    trace, logits = generate_router_logits(cfg, GenParams(seed=12), 24, 8)
+    outs = []
+    for gpu_mrs in (False, True):
+        moe = HybridMoE(cfg, family, policy, 0.5, prof, max_tokens=64, gpu_mrs=gpu_mrs)
+        moe.init_seeded_weights(4)
+        g = torch.Generator(device="cuda").manual_seed(3)
+        ys, recs, reqs = [], [], []
+        for p, fwd in enumerate(trace.passes):
+            lg = [torch.from_numpy(np.ascontiguousarray(np.pad(logits[p][l], ((0, 0), (0, moe.ld - moe.N))),
+                                                        dtype=np.float32)).cuda() for l in range(cfg.num_layers)]
+            x = torch.randn((fwd.token_count, moe.H), generator=g, device="cuda").to(torch.bfloat16)
+            y, info = moe.forward_pass(x, lg, predict=TracePredictor(trace, p, 5), decision_log=True)
+            torch.cuda.synchronize()
+            ys.append(y.float().cpu().numpy())
+            recs.extend(info["records"])
+            reqs.append([(lo.tolist(), sc.tolist()) for lo, sc in info["requests"]])
+        outs.append((ys, digest(from_records(recs, True)), moe.mrs.table().copy(), reqs))
+        del moe
+    assert outs[0][1] == outs[1][1]
+    assert np.array_equal(outs[0][2].view(np.uint64), outs[1][2].view(np.uint64))
+    for a, b in zip(outs[0][0], outs[1][0]):
+        assert np.array_equal(a, b)
+    # the decision core alone on the runtime's LayerRequests (host recurrence throughout)
+    passes = [mcore.ForwardPass(f.stage, f.token_count, tuple(mcore.make_layer_request(l, lo, sc)
+                                                             for l, (lo, sc) in enumerate(outs[1][3][p])))
+              for p, f in enumerate(trace.passes)]
+    replay = mcore.Trace(cfg, tuple(passes))
+    m = me.run_trace(replay, policy, 0.5, prof, 5, decision_log=True)
+    assert digest(from_records(m.decisions, True)) == outs[1][1]
