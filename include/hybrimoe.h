@@ -580,6 +580,7 @@ int hm_ep_nccl_unique_id(void *id128);
 int hm_ep_create_nccl(int rank, int world, int max_rows, int H, const void *id128, int n_experts_total,
                       int n_routed, int Kp, hm_ep **out);
 int hm_ep_uses_nccl(const hm_ep *ep);
+int hm_ep_world(const hm_ep *ep);
 /* One rank's all-to-all(v) schedule from the all-gathered count matrix
  * counts_all [world][n_experts_total] (direction 0: dispatch, local permuted
  * rows -> home layouts; 1: return).  Ops in issue order; src_row / dst_row are
@@ -599,7 +600,8 @@ int hm_ep_a2a_plan(const int32_t *counts_all, int world, int n_experts_total, in
  * HM_PREDICT_LIVE) and of forward_pass without pass_loads (prefetch on). */
 int hm_runtime_set_lookahead(hm_runtime *rt, const uint16_t *gate_w, int ld, int horizon);
 /* Run forward_layer token-sharded through `ep` (dispatch mode enabled): x and
- * logits hold this rank's tokens only (T may be 0). */
+ * logits hold this rank's tokens only (T may be 0).  The exchange's world must
+ * be the runtime's ep_world; world 1 runs the whole exchange on one rank. */
 int hm_runtime_set_ep_dispatch(hm_runtime *rt, hm_ep *ep);
 /* Route forward_layer's expert-parallel combine through `ep` (NULL: partial
  * to hm_runtime_set_ep_output's buffer for an external all-reduce). */

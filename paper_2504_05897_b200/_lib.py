@@ -353,6 +353,7 @@ for _name, (_args, _res) in {
     "hm_ep_create_nccl": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_int, C.c_int, C.c_int, P(vp)],
                           C.c_int),
     "hm_ep_uses_nccl": ([vp], C.c_int),
+    "hm_ep_world": ([vp], C.c_int),
     "hm_ep_a2a_plan": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, P(C.c_int)], C.c_int),
     "hm_runtime_set_lookahead": ([vp, vp, C.c_int, C.c_int], C.c_int),
     "hm_lookahead": ([vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp], C.c_int),

@@ -830,6 +830,8 @@ int hm_ep_create_nccl(int rank, int world, int max_rows, int H, const void *id, 
 
 int hm_ep_uses_nccl(const hm_ep *ep) { return reinterpret_cast<const hm::EpExchange *>(ep)->use_nccl ? 1 : 0; }
 
+int hm_ep_world(const hm_ep *ep) { return reinterpret_cast<const hm::EpExchange *>(ep)->world; }
+
 int hm_ep_a2a_plan(const int32_t *counts_all, int world, int n_experts_total, int n_routed, int rank, int direction,
                    hm_a2a_op *ops, int max_ops, int *n_ops) {
   HM_API_BEGIN

@@ -56,6 +56,7 @@ int hm_ep_dispatch_rows(hm_ep *, const uint16_t *, const int32_t *, const int32_
 int hm_ep_return_rows(hm_ep *, const float *, int, void *);
 int hm_ep_dispatch_buffers(hm_ep *, uint16_t **, float **);
 int hm_ep_uses_nccl(const hm_ep *);
+int hm_ep_world(const hm_ep *);
 int hm_combine_tail_gated(const float *, const float *, const uint64_t *, const int32_t *, const float *, int, int, int,
                           const uint16_t *, uint16_t *, double *, const double *, int, int, int, double,
                           const uint32_t *, uint32_t, void *);
@@ -652,7 +653,7 @@ struct Runtime {
     // CPU outputs reach the combine either zero-copy (positions < 256, the
     // combine reads the mapped host rows) or by H2D copies into `out`
     const bool do_mrs = cfg.gpu_mrs && engine->cfg.cache_policy == HM_POLICY_MRS && engine->mrs_;
-    const bool tail = W == 1 && (!do_mrs || fused) && N <= 256;  // combine_tail launch
+    const bool tail = W == 1 && !disp && (!do_mrs || fused) && N <= 256;  // combine_tail launch
     bool zc_out = zero_copy && !disp && (tail || (W > 1 && ep));
     uint64_t host_mask[4] = {0, 0, 0, 0};
     for (uint32_t r : cpu_refs) {
@@ -743,7 +744,7 @@ struct Runtime {
       return;
     }
     // combine (Eq. 1) with the residual stream, then the GPU copy of S
-    if (W > 1 && disp) {  // expert outputs back to their source ranks, then the local combine
+    if (disp) {  // expert outputs back to their source ranks, then the local combine
       ok(hm_ep_return_rows(ep, out, rows_used, vs));
       ok(hm_combine(retbuf, pos, w, T, Kp, H, cfg.residual ? x : nullptr, y, vs));
     } else if (W > 1 && ep) {  // combine + cross-rank sum + residual: one kernel over peer memory
@@ -900,7 +901,8 @@ int hm_runtime_set_lookahead(hm_runtime *rt, const uint16_t *gate_w, int ld, int
 int hm_runtime_set_ep_dispatch(hm_runtime *rt, hm_ep *ep) {
   HM_API_BEGIN
   auto *r = reinterpret_cast<hm::Runtime *>(rt);
-  HM_REQUIRE(r->W > 1 && ep, HM_EVALUE, "token-sharded dispatch needs ep_world > 1 and an exchange");
+  HM_REQUIRE(ep && hm_ep_world(ep) == r->W, HM_EVALUE,
+             "token-sharded dispatch needs an exchange of the runtime's ep_world (1 exercises it on one rank)");
   uint16_t *xr = nullptr;
   float *rb = nullptr;
   const int rc = hm_ep_dispatch_buffers(ep, &xr, &rb);

@@ -272,3 +272,66 @@ def test_token_sharded_dispatch_shared_expert_family():
     assert all(p.exitcode == 0 for p in procs)
     for r, errs in got.items():
         assert max(errs) <= 1e-2, (r, errs)
+
+
+def test_single_rank_exchange_transports_nccl_and_peer_memory():
+    """The token-sharded exchange run on ONE rank (world 1) -- the only way this
+    one-GPU box can execute the NCCL transport (NCCL refuses two ranks on one
+    device): ncclAllGather of the meta slots, the GATHERED table kernel with the
+    host count mirror, the a2a plan (local copies) and the return.  Against the
+    peer-memory kernels on one rank: bit-identical outputs; against the plain
+    single-GPU runtime: the same decision stream, outputs within 1e-2."""
+    import ctypes as C
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from stream import digest, from_records
+
+    import paper_2504_05897_b200.core as mcore
+    import paper_2504_05897_b200.costs as mcost
+    from paper_2504_05897_b200 import _lib
+    from paper_2504_05897_b200.engine import EnginePolicy
+    from paper_2504_05897_b200.moe import SHAPES, HybridMoE
+    from paper_2504_05897_b200.tracegen import GenParams, generate_router_logits
+
+    lib = _lib.lib
+    cfg = SHAPES["tiny"]
+    eb = mcore.expert_bytes(cfg)
+    prof = mcost.HardwareProfile(gpu_time_per_expert=1.0, cpu_slope=2.0, transfer_bandwidth=eb / 0.5)
+    trace, logits = generate_router_logits(cfg, GenParams(seed=3), 32, 4)
+    runs = {}
+    for mode in ("none", "p2p", "nccl"):
+        moe = HybridMoE(cfg, "tiny", EnginePolicy(), 0.5, prof, max_tokens=48, cpu_threads=2)
+        moe.init_seeded_weights(7)
+        ep = C.c_void_p()
+        E, N, Kp = moe.N + moe.S, moe.N, moe.K + moe.S
+        if mode == "p2p":
+            _lib.check(lib.hm_ep_create(0, 1, 48, moe.H, C.byref(ep)))
+            hd = C.create_string_buffer(64)
+            _lib.check(lib.hm_ep_enable_dispatch(ep, E, N, Kp, hd))
+            _lib.check(lib.hm_ep_open_peer_dispatch(ep, 0, hd))
+        elif mode == "nccl":
+            uid = C.create_string_buffer(128)
+            _lib.check(lib.hm_ep_nccl_unique_id(uid))
+            _lib.check(lib.hm_ep_create_nccl(0, 1, 48, moe.H, uid.raw, E, N, Kp, C.byref(ep)))
+            assert lib.hm_ep_uses_nccl(ep) == 1 and lib.hm_ep_world(ep) == 1
+        if mode != "none":
+            _lib.check(lib.hm_runtime_set_ep_dispatch(moe._rt, ep))
+        g = torch.Generator(device="cuda").manual_seed(5)
+        ys, recs = [], []
+        for p, fwd in enumerate(trace.passes):
+            lg = [torch.from_numpy(np.ascontiguousarray(logits[p][l], dtype=np.float32)).cuda()
+                  for l in range(cfg.num_layers)]
+            x = torch.randn((fwd.token_count, moe.H), generator=g, device="cuda").to(torch.bfloat16)
+            y, info = moe.forward_pass(x, lg, decision_log=True)
+            torch.cuda.synchronize()
+            ys.append(y.float().cpu().numpy())
+            recs.extend(info["records"])
+        runs[mode] = (ys, digest(from_records(recs, True)))
+        del moe
+        if ep.value:
+            lib.hm_ep_destroy(ep)
+    assert runs["none"][1] == runs["p2p"][1] == runs["nccl"][1]
+    for a, b, c in zip(runs["p2p"][0], runs["nccl"][0], runs["none"][0]):
+        assert np.array_equal(a, b)
+        assert np.abs(a - c).max() <= 1e-2 * np.abs(c).max()
