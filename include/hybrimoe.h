@@ -439,9 +439,13 @@ int hm_cpu_experts_decode(hm_cpu_pool *pool, const uint16_t *const *imgs, const 
 /* Best-of-reps host DRAM read bandwidth (GB/s) over `bytes` at p (64-byte aligned). */
 /* Decode split granularity in gate/up pairs (0: whole 128-pair blocks); tuning knob. */
 int hm_cpu_set_decode_grain(int grain);
-/* Bytes of its phase-2 (W2) rows each decode thread prefetches toward the LLC
- * while it waits at the phase-1 barrier (0 disables, the default: measured neutral). */
-int hm_cpu_set_decode_bridge(int kbytes);
+/* Decode work balancing: threads that finish their own contiguous range take
+ * chunks from the tails of the others' (default on; 0 = static ranges, A/B). */
+int hm_cpu_set_decode_steal(int on);
+/* Tool hook: enable per-thread phase timestamps of hm_cpu_experts_decode and
+ * copy the last call's [thread][start, phase 1 done, barrier passed, phase 2
+ * done] (ns since the call) into out. */
+int hm_cpu_decode_profile(int enable, int64_t *out, int n_threads);
 int hm_host_read_bw(hm_cpu_pool *pool, const void *p, size_t bytes, int reps, double *gbs);
 
 typedef struct hm_runtime hm_runtime;

@@ -329,7 +329,8 @@ for _name, (_args, _res) in {
     "hm_predict_layers": ([P(i64), C.c_int, C.c_int, i64, C.c_int, i64, C.c_int, f64, P(i32), P(i64),
                            P(C.c_int)], C.c_int),
     "hm_cpu_set_decode_grain": ([C.c_int], C.c_int),
-    "hm_cpu_set_decode_bridge": ([C.c_int], C.c_int),
+    "hm_cpu_set_decode_steal": ([C.c_int], C.c_int),
+    "hm_cpu_decode_profile": ([C.c_int, vp, C.c_int], C.c_int),
     "hm_cpu_expert_q4": ([vp, vp, C.c_int, C.c_int, vp, C.c_int, vp], C.c_int),
     "hm_cpu_experts_decode_q4": ([vp, P(vp), P(vp), C.c_int, C.c_int, C.c_int, P(vp)], C.c_int),
     "hm_cpu_has_amx_bf16": ([], C.c_int),

@@ -38,7 +38,8 @@ static inline void wait_until(Pred done) {
   while (!done()) std::this_thread::yield();
 }
 
-ThreadPool::ThreadPool(int n, int spin_us) : n_(std::max(1, n)), spin_us_(spin_us) {
+ThreadPool::ThreadPool(int n, int spin_us)
+    : n_(std::max(1, n)), spin_us_(spin_us), ranges_(new Range[static_cast<size_t>(2) * std::max(1, n)]) {
   for (int t = 1; t < n_; ++t) threads_.emplace_back([this, t] { loop(t); });
 }
 
@@ -300,17 +301,6 @@ int &decode_grain() {
     return s ? std::atoi(s) : 16;
   }();
   return g;
-}
-
-// Bytes of its phase-2 rows a decode thread may prefetch while waiting at the
-// phase barrier (HM_DECODE_BRIDGE_KB; default 0 = off: an interleaved A/B on
-// the GPU boxes, tools/host_bridge_ab.py, measured it neutral within 3 %).
-size_t &decode_bridge_bytes() {
-  static size_t b = [] {
-    const char *s = std::getenv("HM_DECODE_BRIDGE_KB");
-    return static_cast<size_t>(s ? std::atol(s) : 0) << 10;
-  }();
-  return b;
 }
 
 // ------------------------------------------------------------ AMX (prefill)
@@ -945,65 +935,116 @@ void cpu_expert_amx(ThreadPool &pool, const uint16_t *img, int H, int I, const u
   });
 }
 
+// Run this thread's [front, back) of `rs` in chunks from the front, then
+// steal chunks from the back of the other threads' ranges until all are
+// empty.  process(a, b) handles indices [a, b).  The owner keeps one
+// sequential stream (hardware prefetch); stealing only trims the tails, so a
+// thread slowed by the OS or a busier memory channel no longer holds the
+// phase barrier (measured: the slowest of 16 threads ran phase 1 of a
+// Mixtral expert 1.5x longer than the median one).
+bool &decode_steal() {  // HM_DECODE_STEAL=0 / hm_cpu_set_decode_steal(0): static ranges only (A/B)
+  static bool on = [] {
+    const char *s = std::getenv("HM_DECODE_STEAL");
+    return !s || std::atoi(s) != 0;
+  }();
+  return on;
+}
+
+template <class F>
+void run_ranges(ThreadPool::Range *rs, int tid, int nt, uint32_t chunk, F &&process) {
+  auto take = [&](ThreadPool::Range &r, bool front, uint32_t &a, uint32_t &b) {
+    uint64_t v = r.fb.load(std::memory_order_relaxed);
+    for (;;) {
+      const uint32_t f = static_cast<uint32_t>(v >> 32), k = static_cast<uint32_t>(v);
+      if (f >= k) return false;
+      if (!front && k - f < 2 * chunk) return false;  // leave the owner its last chunk
+      uint32_t nf = f, nk = k;
+      if (front) {
+        nf = std::min(k, f + chunk);
+        a = f;
+        b = nf;
+      } else {
+        nk = k - chunk;
+        a = nk;
+        b = k;
+      }
+      if (r.fb.compare_exchange_weak(v, (static_cast<uint64_t>(nf) << 32) | nk, std::memory_order_acq_rel))
+        return true;
+    }
+  };
+  uint32_t a = 0, b = 0;
+  while (take(rs[tid], true, a, b)) process(a, b);
+  if (!decode_steal()) return;
+  for (int k = 1; k < nt; ++k) {
+    ThreadPool::Range &r = rs[(tid + k) % nt];
+    while (take(r, false, a, b)) process(a, b);
+  }
+}
+
+// Per-thread phase timestamps of the last decode call (hm_cpu_decode_profile):
+// [tid][0] start, [1] phase 1 done, [2] barrier passed, [3] phase 2 done (ns).
+static std::vector<int64_t> g_dec_prof;
+static bool g_dec_prof_on = false;
+static inline int64_t ns_now() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
 void cpu_experts_decode(ThreadPool &pool, const uint16_t *const *imgs, const uint16_t *const *xs, int n, int H,
                         int I, float *const *outs, std::vector<uint16_t> &hbuf) {
+  if (g_dec_prof_on && g_dec_prof.size() < static_cast<size_t>(pool.size()) * 4)
+    g_dec_prof.assign(static_cast<size_t>(pool.size()) * 4, 0);
   // All single-token experts of a layer in one pool run: phase 1 over every
   // (expert, 128-pair block), one barrier, phase 2 over every (expert, row).
   HM_REQUIRE(H % 32 == 0 && I % kIlv == 0, HM_EVALUE, "host worker needs H % 32 == 0 and I % 128 == 0");
   if (n <= 0) return;
   hbuf.resize(static_cast<size_t>(n) * I);
   uint16_t *h = hbuf.data();
-  const int nblk = I / kIlv;
   const int grain = decode_grain();
+  const int64_t t_call = g_dec_prof_on ? ns_now() : 0;
+  // per-thread contiguous ranges (phase 1: pairs in grain units, phase 2:
+  // rows) with stealing from the tails
+  const int nt0 = pool.size();
+  const long np1 = static_cast<long>(n) * I, np2 = static_cast<long>(n) * H;
+  const int g1 = grain > 0 ? grain : kIlv;
+  {
+    const long nu = (np1 + g1 - 1) / g1;
+    ThreadPool::Range *r1 = pool.ranges(0), *r2 = pool.ranges(1);
+    for (int t = 0; t < nt0; ++t) {
+      const uint64_t f1 = static_cast<uint64_t>(std::min(np1, nu * t / nt0 * g1));
+      const uint64_t b1 = static_cast<uint64_t>(std::min(np1, nu * (t + 1) / nt0 * g1));
+      r1[t].fb.store((f1 << 32) | b1, std::memory_order_relaxed);
+      const uint64_t f2 = static_cast<uint64_t>(np2 * t / nt0), b2 = static_cast<uint64_t>(np2 * (t + 1) / nt0);
+      r2[t].fb.store((f2 << 32) | b2, std::memory_order_relaxed);
+    }
+  }
+  // steal units: ~64 KB of weights
+  const uint32_t c1 = static_cast<uint32_t>(std::max<long>(g1, (64L << 10) / (4L * H) / g1 * g1));
+  const uint32_t c2 = static_cast<uint32_t>(std::max<long>(1, (64L << 10) / (2L * I)));
   pool.run([&](int tid, int nt) {
-    if (grain <= 0) {
-      const long u1 = static_cast<long>(n) * nblk;
-      for (long u = u1 * tid / nt; u < u1 * (tid + 1) / nt;) {
-        const int e = static_cast<int>(u / nblk), b0 = static_cast<int>(u % nblk);
-        const int b1 = static_cast<int>(std::min<long>(nblk, b0 + (u1 * (tid + 1) / nt - u)));
-        phase1_stream(imgs[e], H, I, xs[e], h + static_cast<size_t>(e) * I, b0, b1);
-        u += b1 - b0;
-      }
-    } else {  // contiguous pair ranges of `grain`-pair units over the flat (expert, pair) space
-      const long nu = (static_cast<long>(n) * I + grain - 1) / grain;
-      const long p0 = nu * tid / nt * grain, p1 = std::min<long>(static_cast<long>(n) * I, nu * (tid + 1) / nt * grain);
-      for (long q = p0; q < p1;) {
+    int64_t *tp = g_dec_prof_on ? &g_dec_prof[static_cast<size_t>(tid) * 4] : nullptr;
+    if (tp) tp[0] = ns_now() - t_call;
+    run_ranges(pool.ranges(0), tid, nt, c1, [&](uint32_t q0, uint32_t q1) {
+      for (long q = q0; q < static_cast<long>(q1);) {
         const int e = static_cast<int>(q / I), i0 = static_cast<int>(q % I);
-        const int i1 = static_cast<int>(std::min<long>(I, i0 + (p1 - q)));
+        const int i1 = static_cast<int>(std::min<long>(I, i0 + (static_cast<long>(q1) - q)));
         phase1_pairs(imgs[e], H, I, xs[e], h + static_cast<size_t>(e) * I, i0, i1);
         q += i1 - i0;
       }
-    }
-    // h is complete only when every thread has finished phase 1; a thread that
-    // arrives early pulls the head of its phase-2 rows (W2 does not depend on
-    // h) toward the LLC until the last one arrives, so DRAM stays busy through
-    // the phase-1 imbalance instead of idling at the barrier
-    const uint32_t token = pool.arrive();
-    const long r1 = static_cast<long>(n) * H;
-    {
-      const size_t cap = decode_bridge_bytes();
-      size_t done = 0;
-      for (long u = r1 * tid / nt; u < r1 * (tid + 1) / nt && done < cap && !pool.passed(token);) {
+    });
+    if (tp) tp[1] = ns_now() - t_call;
+    pool.barrier();
+    if (tp) tp[2] = ns_now() - t_call;
+    run_ranges(pool.ranges(1), tid, nt, c2, [&](uint32_t u0, uint32_t u1) {
+      for (long u = u0; u < static_cast<long>(u1);) {
         const int e = static_cast<int>(u / H), j0 = static_cast<int>(u % H);
-        const int j1 = static_cast<int>(std::min<long>(H, j0 + (r1 * (tid + 1) / nt - u)));
-        const char *p = reinterpret_cast<const char *>(imgs[e] + static_cast<size_t>(2) * I * H +
-                                                       static_cast<size_t>(j0) * I);
-        const size_t len = static_cast<size_t>(j1 - j0) * I * 2;
-        for (size_t o = 0; o < len && done < cap; o += 4096, done += 4096) {
-          if (pool.passed(token)) break;
-          for (size_t l = o; l < std::min(len, o + 4096); l += 64) _mm_prefetch(p + l, _MM_HINT_T2);
-        }
+        const int j1 = static_cast<int>(std::min<long>(H, j0 + (static_cast<long>(u1) - u)));
+        const uint16_t *w2 = imgs[e] + static_cast<size_t>(2) * I * H;
+        stream_rows(w2 + static_cast<size_t>(j0) * I, j1 - j0, I, h + static_cast<size_t>(e) * I, outs[e] + j0);
         u += j1 - j0;
       }
-    }
-    pool.wait(token);
-    for (long u = r1 * tid / nt; u < r1 * (tid + 1) / nt;) {
-      const int e = static_cast<int>(u / H), j0 = static_cast<int>(u % H);
-      const int j1 = static_cast<int>(std::min<long>(H, j0 + (r1 * (tid + 1) / nt - u)));
-      const uint16_t *w2 = imgs[e] + static_cast<size_t>(2) * I * H;
-      stream_rows(w2 + static_cast<size_t>(j0) * I, j1 - j0, I, h + static_cast<size_t>(e) * I, outs[e] + j0);
-      u += j1 - j0;
-    }
+    });
+    if (tp) tp[3] = ns_now() - t_call;
   });
 }
 
@@ -1104,10 +1145,17 @@ int hm_cpu_set_prefetch(int dist, int hint) {
 }
 
 // Tuning knob for the decode split granularity (pairs; 0 = whole 128-pair blocks).
-int hm_cpu_set_decode_bridge(int kbytes) {
+int hm_cpu_decode_profile(int enable, int64_t *out, int n_threads) {
   HM_API_BEGIN
-  HM_REQUIRE(kbytes >= 0, HM_EVALUE, "bad decode bridge size");
-  hm::decode_bridge_bytes() = static_cast<size_t>(kbytes) << 10;
+  hm::g_dec_prof_on = enable != 0;
+  if (out)
+    for (int i = 0; i < n_threads * 4 && i < static_cast<int>(hm::g_dec_prof.size()); ++i) out[i] = hm::g_dec_prof[i];
+  HM_API_END
+}
+
+int hm_cpu_set_decode_steal(int on) {
+  HM_API_BEGIN
+  hm::decode_steal() = on != 0;
   HM_API_END
 }
 

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <atomic>
+#include <memory>
 #include <condition_variable>
 #include <cstdint>
 #include <functional>
@@ -30,6 +31,13 @@ class ThreadPool {
   uint32_t arrive();
   bool passed(uint32_t token) const;
   void wait(uint32_t token);
+  // Work ranges with stealing (one cache line per thread and phase): thread t
+  // owns [front, back) of some index space, takes chunks from the front;
+  // a thread that ran out takes chunks from the back of the others' ranges.
+  struct alignas(64) Range {
+    std::atomic<uint64_t> fb{0};  // (front << 32) | back
+  };
+  Range *ranges(int phase) { return &ranges_[static_cast<size_t>(phase) * n_]; }
 
  private:
   void loop(int tid);
@@ -44,6 +52,7 @@ class ThreadPool {
   std::atomic<int> bar_count_{0};
   std::atomic<uint32_t> bar_sense_{0};
   std::atomic<bool> stop_{false};
+  std::unique_ptr<Range[]> ranges_;
 };
 
 // AMX path for multi-token experts (prefill); amx_available() requests the

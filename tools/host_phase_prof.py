@@ -1,0 +1,57 @@
+"""Per-thread phase timeline of hm_cpu_experts_decode (hm_cpu_decode_profile):
+start skew, phase-1 spread, barrier wait and phase-2 spread for DeepSeek /
+Mixtral single-token calls on pinned images, medians over many calls.
+
+  python tools/host_phase_prof.py
+"""
+import ctypes as C
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2504_05897_b200 import _lib  # noqa: E402
+
+lib = _lib.lib
+NT = 16
+pool = C.c_void_p()
+lib.hm_cpu_pool_create(NT, C.byref(pool))
+prof = np.zeros((NT, 4), np.int64)
+for name, H, I, n_img, counts, calls in (("deepseek", 2048, 1408, 96, (1, 2), 300), ("mixtral", 4096, 14336, 8, (1,), 30)):
+    elems = 3 * H * I
+    t = torch.empty((n_img, elems), dtype=torch.int16).pin_memory()
+    t.random_(0, 1 << 14)
+    for n in counts:
+        x = np.full((n, H), 0x3F80, np.uint16)
+        out = np.empty((n, H), np.float32)
+        xs = (C.c_void_p * n)(*[x[i:i + 1].ctypes.data for i in range(n)])
+        outs = (C.c_void_p * n)(*[out[i:i + 1].ctypes.data for i in range(n)])
+        imgs = (C.c_void_p * n)()
+        rec, walls = [], []
+        lib.hm_cpu_decode_profile(1, None, 0)
+        k = 0
+        for r in range(calls):
+            for i in range(n):
+                imgs[i] = t[k % n_img].data_ptr()
+                k += 1
+            t0 = time.perf_counter()
+            lib.hm_cpu_experts_decode(pool, imgs, xs, n, H, I, outs)
+            walls.append(time.perf_counter() - t0)
+            lib.hm_cpu_decode_profile(1, prof.ctypes.data, NT)
+            if r >= 3:
+                rec.append(prof.copy())
+            s0 = time.perf_counter() + 40e-6
+            while time.perf_counter() < s0:
+                pass
+        a = np.array(rec) / 1e3  # us
+        med = lambda v: float(np.median(v))  # noqa: E731
+        print(f"{name} n={n}: wall {1e6 * med(walls):.1f} us | start max {med(a[:, :, 0].max(1)):.1f} | "
+              f"phase1 min/med/max {med(a[:, :, 1].min(1)):.1f}/{med(np.median(a[:, :, 1], 1)):.1f}/"
+              f"{med(a[:, :, 1].max(1)):.1f} | barrier passed {med(a[:, :, 2].max(1)):.1f} | "
+              f"phase2 min/med/max {med(a[:, :, 3].min(1)):.1f}/{med(np.median(a[:, :, 3], 1)):.1f}/"
+              f"{med(a[:, :, 3].max(1)):.1f} | GB/s {n * elems * 2 / med(walls) / 1e9:.1f}", flush=True)
+    t = None
+lib.hm_cpu_decode_profile(0, None, 0)
