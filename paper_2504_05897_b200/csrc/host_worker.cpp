@@ -108,6 +108,52 @@ void ThreadPool::wait(uint32_t token) {
   wait_until([&] { return passed(token); });
 }
 
+// Run this thread's [front, back) of `rs` in chunks from the front, then
+// steal chunks from the back of the other threads' ranges until all are
+// empty.  process(a, b) handles indices [a, b).  The owner keeps one
+// sequential stream (hardware prefetch); stealing only trims the tails, so a
+// thread slowed by the OS or a busier memory channel no longer holds the
+// phase barrier (measured: the slowest of 16 threads ran phase 1 of a
+// Mixtral expert 1.5x longer than the median one).
+bool &decode_steal() {  // HM_DECODE_STEAL=0 / hm_cpu_set_decode_steal(0): static ranges only (A/B)
+  static bool on = [] {
+    const char *s = std::getenv("HM_DECODE_STEAL");
+    return !s || std::atoi(s) != 0;
+  }();
+  return on;
+}
+
+template <class F>
+void run_ranges(ThreadPool::Range *rs, int tid, int nt, uint32_t chunk, F &&process) {
+  auto take = [&](ThreadPool::Range &r, bool front, uint32_t &a, uint32_t &b) {
+    uint64_t v = r.fb.load(std::memory_order_relaxed);
+    for (;;) {
+      const uint32_t f = static_cast<uint32_t>(v >> 32), k = static_cast<uint32_t>(v);
+      if (f >= k) return false;
+      if (!front && k - f < 2 * chunk) return false;  // leave the owner its last chunk
+      uint32_t nf = f, nk = k;
+      if (front) {
+        nf = std::min(k, f + chunk);
+        a = f;
+        b = nf;
+      } else {
+        nk = k - chunk;
+        a = nk;
+        b = k;
+      }
+      if (r.fb.compare_exchange_weak(v, (static_cast<uint64_t>(nf) << 32) | nk, std::memory_order_acq_rel))
+        return true;
+    }
+  };
+  uint32_t a = 0, b = 0;
+  while (take(rs[tid], true, a, b)) process(a, b);
+  if (!decode_steal()) return;
+  for (int k = 1; k < nt; ++k) {
+    ThreadPool::Range &r = rs[(tid + k) % nt];
+    while (take(r, false, a, b)) process(a, b);
+  }
+}
+
 // ------------------------------------------------------------ kernels
 namespace {
 
@@ -731,18 +777,29 @@ void cpu_experts_decode_q4(ThreadPool &pool, const uint8_t *const *imgs, const u
     q4_prep_x(xs[e], H, qx[e]);
     q4_alloc_x(I, hx[e]);
   }
+  // 16-pair (phase 1) and 16-row (phase 2) units, per-thread contiguous ranges
+  // with stealing from the tails (as cpu_experts_decode)
+  const int nt0 = pool.size();
+  const long nu1 = static_cast<long>(n) * I / 16, nu2 = static_cast<long>(n) * H / 16;
+  for (int t = 0; t < nt0; ++t) {
+    pool.ranges(0)[t].fb.store((static_cast<uint64_t>(nu1 * t / nt0) << 32) | static_cast<uint64_t>(nu1 * (t + 1) / nt0),
+                               std::memory_order_relaxed);
+    pool.ranges(1)[t].fb.store((static_cast<uint64_t>(nu2 * t / nt0) << 32) | static_cast<uint64_t>(nu2 * (t + 1) / nt0),
+                               std::memory_order_relaxed);
+  }
   pool.run([&](int tid, int nt) {
     // phase 1: 16-pair units over the flat (expert, pair) space, gate and up rows
-    const long nu = static_cast<long>(n) * I / 16;
     float g[16], u[16];
-    for (long q = nu * tid / nt; q < nu * (tid + 1) / nt; ++q) {
-      const int e = static_cast<int>(q / (I / 16)), i0 = static_cast<int>(q % (I / 16)) * 16;
-      const Q4View v = q4_view(imgs[e], H, I);
-      const size_t grow = static_cast<size_t>((i0 / kIlv) * 2 * kIlv + i0 % kIlv);
-      dot_rows_q4(v.n13 + grow * (H / 2), v.s13 + grow * (H / 128), 16, H, qx[e], g);
-      dot_rows_q4(v.n13 + (grow + kIlv) * (H / 2), v.s13 + (grow + kIlv) * (H / 128), 16, H, qx[e], u);
-      for (int i = 0; i < 16; ++i) h[static_cast<size_t>(e) * I + i0 + i] = f2bf(silu(g[i]) * u[i]);
-    }
+    run_ranges(pool.ranges(0), tid, nt, 2, [&](uint32_t q0, uint32_t q1) {
+      for (long q = q0; q < static_cast<long>(q1); ++q) {
+        const int e = static_cast<int>(q / (I / 16)), i0 = static_cast<int>(q % (I / 16)) * 16;
+        const Q4View v = q4_view(imgs[e], H, I);
+        const size_t grow = static_cast<size_t>((i0 / kIlv) * 2 * kIlv + i0 % kIlv);
+        dot_rows_q4(v.n13 + grow * (H / 2), v.s13 + grow * (H / 128), 16, H, qx[e], g);
+        dot_rows_q4(v.n13 + (grow + kIlv) * (H / 2), v.s13 + (grow + kIlv) * (H / 128), 16, H, qx[e], u);
+        for (int i = 0; i < 16; ++i) h[static_cast<size_t>(e) * I + i0 + i] = f2bf(silu(g[i]) * u[i]);
+      }
+    });
     pool.barrier();
     {  // h -> int8 digits, groups split over the threads (once, not per thread)
       const long ng = static_cast<long>(n) * (I / 128);
@@ -752,13 +809,14 @@ void cpu_experts_decode_q4(ThreadPool &pool, const uint8_t *const *imgs, const u
       }
     }
     pool.barrier();
-    const long r1 = static_cast<long>(n) * H / 16;
-    for (long q = r1 * tid / nt; q < r1 * (tid + 1) / nt; ++q) {
-      const int e = static_cast<int>(q / (H / 16)), j0 = static_cast<int>(q % (H / 16)) * 16;
-      const Q4View v = q4_view(imgs[e], H, I);
-      dot_rows_q4(v.n2 + static_cast<size_t>(j0) * (I / 2), v.s2 + static_cast<size_t>(j0) * (I / 128), 16, I, hx[e],
-                  outs[e] + j0);
-    }
+    run_ranges(pool.ranges(1), tid, nt, 2, [&](uint32_t q0, uint32_t q1) {
+      for (long q = q0; q < static_cast<long>(q1); ++q) {
+        const int e = static_cast<int>(q / (H / 16)), j0 = static_cast<int>(q % (H / 16)) * 16;
+        const Q4View v = q4_view(imgs[e], H, I);
+        dot_rows_q4(v.n2 + static_cast<size_t>(j0) * (I / 2), v.s2 + static_cast<size_t>(j0) * (I / 128), 16, I,
+                    hx[e], outs[e] + j0);
+      }
+    });
   });
 }
 
@@ -933,52 +991,6 @@ void cpu_expert_amx(ThreadPool &pool, const uint16_t *img, int H, int I, const u
       }
     }
   });
-}
-
-// Run this thread's [front, back) of `rs` in chunks from the front, then
-// steal chunks from the back of the other threads' ranges until all are
-// empty.  process(a, b) handles indices [a, b).  The owner keeps one
-// sequential stream (hardware prefetch); stealing only trims the tails, so a
-// thread slowed by the OS or a busier memory channel no longer holds the
-// phase barrier (measured: the slowest of 16 threads ran phase 1 of a
-// Mixtral expert 1.5x longer than the median one).
-bool &decode_steal() {  // HM_DECODE_STEAL=0 / hm_cpu_set_decode_steal(0): static ranges only (A/B)
-  static bool on = [] {
-    const char *s = std::getenv("HM_DECODE_STEAL");
-    return !s || std::atoi(s) != 0;
-  }();
-  return on;
-}
-
-template <class F>
-void run_ranges(ThreadPool::Range *rs, int tid, int nt, uint32_t chunk, F &&process) {
-  auto take = [&](ThreadPool::Range &r, bool front, uint32_t &a, uint32_t &b) {
-    uint64_t v = r.fb.load(std::memory_order_relaxed);
-    for (;;) {
-      const uint32_t f = static_cast<uint32_t>(v >> 32), k = static_cast<uint32_t>(v);
-      if (f >= k) return false;
-      if (!front && k - f < 2 * chunk) return false;  // leave the owner its last chunk
-      uint32_t nf = f, nk = k;
-      if (front) {
-        nf = std::min(k, f + chunk);
-        a = f;
-        b = nf;
-      } else {
-        nk = k - chunk;
-        a = nk;
-        b = k;
-      }
-      if (r.fb.compare_exchange_weak(v, (static_cast<uint64_t>(nf) << 32) | nk, std::memory_order_acq_rel))
-        return true;
-    }
-  };
-  uint32_t a = 0, b = 0;
-  while (take(rs[tid], true, a, b)) process(a, b);
-  if (!decode_steal()) return;
-  for (int k = 1; k < nt; ++k) {
-    ThreadPool::Range &r = rs[(tid + k) % nt];
-    while (take(r, false, a, b)) process(a, b);
-  }
 }
 
 // Per-thread phase timestamps of the last decode call (hm_cpu_decode_profile):
