@@ -349,6 +349,7 @@ typedef struct hm_group {
 #define HM_FFN_GEMM 2
 #define HM_FFN_GEMV_SPLIT 3 /* the two-launch ffn1 -> ffn2 GEMV pair, whatever HM_GEMV_FUSED says */
 #define HM_FFN_GEMV_FUSED 4 /* the persistent one-launch ffn1 -> ffn2 GEMV (measured slower; A/B) */
+#define HM_FFN_GEMV_BULK 5  /* the ffn1 -> ffn2 pair with weights staged by the bulk-copy engine */
 /* out[rows of g] = W2_g (silu(Wg_g x) * (Wu_g x)) for every group (groups is
  * a HOST array).  h [total_rows, I] bf16 scratch, out [total_rows, H] fp32. */
 int hm_expert_ffn(const uint16_t *pool, int n_slots, int H, int I, const hm_group *groups,

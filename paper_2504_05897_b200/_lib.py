@@ -255,7 +255,7 @@ for _name, (_args, _res) in _DEV_SIGS.items():
     _f = getattr(lib, _name)
     _f.argtypes = _args
     _f.restype = _res
-FFN_AUTO, FFN_GEMV, FFN_GEMM, FFN_GEMV_SPLIT, FFN_GEMV_FUSED = 0, 1, 2, 3, 4
+FFN_AUTO, FFN_GEMV, FFN_GEMM, FFN_GEMV_SPLIT, FFN_GEMV_FUSED, FFN_GEMV_BULK = 0, 1, 2, 3, 4, 5
 
 _HOST_SIGS = {
     "hm_cpu_pool_create": ([C.c_int, P(vp)], C.c_int),

@@ -220,6 +220,208 @@ __global__ void __launch_bounds__(256) ffn2_gemv_kernel(const __grid_constant__ 
   }
 }
 
+// ------------------------------------------------------------ bulk-copy decode GEMV
+// The same ffn1 -> ffn2 pair with the weights moved by the bulk-copy engine
+// (cp.async.bulk, mbarrier complete_tx) instead of per-lane loads.  Every
+// warp runs its own ring of kBulkMaxStages stage buffers in shared memory and
+// streams a contiguous range of work units through it: lane 0 keeps up to S
+// stages in flight (2 copies per ffn1 stage: gate and up rows; 1..NR rows per
+// ffn2 stage), all lanes wait on the stage's mbarrier, take their dot products
+// from shared memory and hand the stage back.  So each warp has S x 4-8 KB in
+// flight at every instant with no register cost, where the register kernels
+// above hold one 4 KB batch and pay one DRAM round trip per batch: small
+// experts (DeepSeek's 2048 x 1408) were a short chain of such round trips per
+// warp.  Per lane the columns are accumulated in the register kernels' order
+// (c = lane*8 + 256k, k increasing, chunk after chunk): outputs are
+// bit-identical to ffn1/ffn2_gemv_kernel.
+constexpr int kBulkMaxStages = 4;
+constexpr int kBulkWarps = 8;
+
+struct BulkParams {
+  const uint16_t *pool;
+  size_t slot_elems;
+  int H, I;
+  int n_units;      // ffn1: G*I (gate, up) pairs; ffn2: G*ceil(H/nr) row blocks
+  int units_per_group;
+  int ck, nck;      // columns per stage chunk, chunks per unit
+  int nr;           // ffn2: W2 rows per stage (nck == 1 when nr > 1)
+  int stages;       // ring depth per warp (<= kBulkMaxStages)
+  int stage_bytes;  // bytes per stage buffer (multiple of 128)
+  const uint16_t *xp;
+  uint16_t *h;
+  float *out;
+  int32_t slot[kMaxGroups];
+  int32_t row_begin[kMaxGroups];
+  int32_t row_count[kMaxGroups];
+};
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dev::smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(dev::smem_u32(bar))
+      : "memory");
+}
+
+// the warp's contiguous unit range, balanced over all warps of the grid
+__device__ __forceinline__ void bulk_range(int n_units, int &u0, int &u1) {
+  const long W = static_cast<long>(gridDim.x) * kBulkWarps;
+  const long w = static_cast<long>(blockIdx.x) * kBulkWarps + (threadIdx.x >> 5);
+  u0 = static_cast<int>(n_units * w / W);
+  u1 = static_cast<int>(n_units * (w + 1) / W);
+}
+
+// ffn1 step t of unit range [u0, ..): unit u0 + t / nck, column chunk t % nck
+__device__ __forceinline__ void bulk_issue1(const BulkParams &p, int u0, int t, uint16_t *stage, uint64_t *bar) {
+  const int u = u0 + t / p.nck, c = t - (t / p.nck) * p.nck;
+  const int g = u / p.I, i = u - g * p.I;
+  const uint16_t *w13 = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_elems;
+  const size_t grow = static_cast<size_t>((i / kIlv) * 2 * kIlv + (i % kIlv));
+  const int c0 = c * p.ck, cols = min(p.ck, p.H - c0);
+  const uint16_t *wg = w13 + grow * p.H + c0;
+  const uint32_t bytes = static_cast<uint32_t>(cols) * 2;
+  dev::mbar_arrive_expect_tx(bar, 2 * bytes);
+  bulk_g2s(stage, wg, bytes, bar);
+  bulk_g2s(stage + p.ck, wg + static_cast<size_t>(kIlv) * p.H, bytes, bar);
+}
+
+// Activations are read through L1 (__ldg): a warp's unit range can span
+// groups, each with its own rows, and the few KB per group stay L1-resident.
+template <int MR>
+__global__ void __launch_bounds__(kBulkWarps * 32, 1) ffn1_bulk_kernel(const __grid_constant__ BulkParams p) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  __shared__ uint64_t bars[kBulkWarps][kBulkMaxStages];
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int H = p.H, I = p.I, S = p.stages;
+  uint8_t *ring = smem_raw + static_cast<size_t>(wid) * S * p.stage_bytes;
+  auto stage = [&](int s) { return reinterpret_cast<uint16_t *>(ring + static_cast<size_t>(s) * p.stage_bytes); };
+  int u0, u1;
+  bulk_range(p.n_units, u0, u1);
+  const int steps = (u1 - u0) * p.nck;
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) dev::mbar_init(&bars[wid][s], 1);
+    dev::fence_barrier_init();
+    for (int t = 0; t < min(S, steps); ++t) bulk_issue1(p, u0, t, stage(t), &bars[wid][t]);
+  }
+  __syncwarp();
+  float ag[MR], au[MR];
+#pragma unroll
+  for (int m = 0; m < MR; ++m) ag[m] = au[m] = 0.f;
+  for (int t = 0; t < steps; ++t) {
+    const int u = u0 + t / p.nck, c = t - (t / p.nck) * p.nck;
+    const int g = u / I, i = u - g * I;
+    const int M = p.row_count[g], rb = p.row_begin[g];
+    const uint16_t *x = p.xp + static_cast<size_t>(rb) * H;
+    const int s = t % S;
+    dev::mbar_wait(&bars[wid][s], static_cast<uint32_t>((t / S) & 1));
+    const uint16_t *sg = stage(s), *su = sg + p.ck;
+    const int c0 = c * p.ck, cols = min(p.ck, H - c0);
+    for (int k = lane * 8; k < cols; k += 256) {
+      const uint4 wg = *reinterpret_cast<const uint4 *>(sg + k);
+      const uint4 wu = *reinterpret_cast<const uint4 *>(su + k);
+#pragma unroll
+      for (int m = 0; m < MR; ++m) {
+        if (m < M) {
+          const uint4 xv = __ldg(reinterpret_cast<const uint4 *>(x + static_cast<size_t>(m) * H + c0 + k));
+          ag[m] += dev::dot8(wg, xv);
+          au[m] += dev::dot8(wu, xv);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && t + S < steps) bulk_issue1(p, u0, t + S, stage(s), &bars[wid][s]);
+    if (c == p.nck - 1) {
+#pragma unroll
+      for (int m = 0; m < MR; ++m) {
+        if (m < M) {
+          const float gs = dev::warp_sum(ag[m]), us = dev::warp_sum(au[m]);
+          if (lane == 0) p.h[static_cast<size_t>(rb + m) * I + i] = dev::f2bf(dev::silu(gs) * us);
+        }
+        ag[m] = au[m] = 0.f;
+      }
+    }
+  }
+}
+
+// ffn2 step t: unit u0 + t / nck is a block of nr W2 rows (nck == 1) or one
+// row's column chunk t % nck (nr == 1)
+__device__ __forceinline__ void bulk_issue2(const BulkParams &p, int u0, int t, uint16_t *stage, uint64_t *bar) {
+  const int u = u0 + t / p.nck, c = t - (t / p.nck) * p.nck;
+  const int g = u / p.units_per_group, j0 = (u - g * p.units_per_group) * p.nr;
+  const int rows = min(p.nr, p.H - j0);
+  const uint16_t *w2 = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_elems + static_cast<size_t>(2) * p.I * p.H;
+  const int c0 = c * p.ck, cols = min(p.ck, p.I - c0);
+  // nr > 1 only with whole rows (ck == I): the rows are contiguous
+  const uint32_t bytes = static_cast<uint32_t>(rows) * cols * 2;
+  dev::mbar_arrive_expect_tx(bar, bytes);
+  bulk_g2s(stage, w2 + static_cast<size_t>(j0) * p.I + c0, bytes, bar);
+}
+
+// W2's first stages are issued BEFORE the programmatic wait for ffn1: they do
+// not depend on h.  h is read through L1 like the activations above.
+template <int MR, int NR>
+__global__ void __launch_bounds__(kBulkWarps * 32, 1) ffn2_bulk_kernel(const __grid_constant__ BulkParams p) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  __shared__ uint64_t bars[kBulkWarps][kBulkMaxStages];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int H = p.H, I = p.I, S = p.stages;
+  uint8_t *ring = smem_raw + static_cast<size_t>(wid) * S * p.stage_bytes;
+  auto stage = [&](int s) { return reinterpret_cast<uint16_t *>(ring + static_cast<size_t>(s) * p.stage_bytes); };
+  int u0, u1;
+  bulk_range(p.n_units, u0, u1);
+  const int steps = (u1 - u0) * p.nck;
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) dev::mbar_init(&bars[wid][s], 1);
+    dev::fence_barrier_init();
+    for (int t = 0; t < min(S, steps); ++t) bulk_issue2(p, u0, t, stage(t), &bars[wid][t]);
+  }
+  __syncwarp();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  float acc[MR][NR];
+#pragma unroll
+  for (int m = 0; m < MR; ++m)
+#pragma unroll
+    for (int r = 0; r < NR; ++r) acc[m][r] = 0.f;
+  for (int t = 0; t < steps; ++t) {
+    const int u = u0 + t / p.nck, c = t - (t / p.nck) * p.nck;
+    const int g = u / p.units_per_group, j0 = (u - g * p.units_per_group) * p.nr;
+    const int M = p.row_count[g], rb = p.row_begin[g];
+    const int rows = min(p.nr, H - j0);
+    const uint16_t *hr = p.h + static_cast<size_t>(rb) * I;
+    const int s = t % S;
+    dev::mbar_wait(&bars[wid][s], static_cast<uint32_t>((t / S) & 1));
+    const uint16_t *sw = stage(s);
+    const int c0 = c * p.ck, cols = min(p.ck, I - c0);
+    for (int k = lane * 8; k < cols; k += 256) {
+#pragma unroll
+      for (int m = 0; m < MR; ++m) {
+        if (m < M) {
+          const uint4 hv = __ldcg(reinterpret_cast<const uint4 *>(hr + static_cast<size_t>(m) * I + c0 + k));
+#pragma unroll
+          for (int r = 0; r < NR; ++r)
+            if (r < rows) acc[m][r] += dev::dot8(*reinterpret_cast<const uint4 *>(sw + r * cols + k), hv);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && t + S < steps) bulk_issue2(p, u0, t + S, stage(s), &bars[wid][s]);
+    if (c == p.nck - 1) {
+#pragma unroll
+      for (int m = 0; m < MR; ++m) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          if (m < M && r < rows) {
+            const float v = dev::warp_sum(acc[m][r]);
+            if (lane == 0) p.out[static_cast<size_t>(rb + m) * H + j0 + r] = v;
+          }
+          acc[m][r] = 0.f;
+        }
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------ fused decode GEMV
 // ONE persistent launch per layer for ffn1 -> ffn2 (instead of two short
 // launches that each pay a ramp and a tail; DeepSeek's 4-6 small experts ran
@@ -812,10 +1014,117 @@ void launch_gemv_fused(const uint16_t *pool, size_t slot_elems, int H, int I, co
   }
 }
 
+// HM_GEMV_BULK=1 makes the bulk-copy pair the default GEMV (A/B switch);
+// HM_BULK_SMEM_KB sets the ring budget per CTA (default 192: one CTA per SM).
+bool gemv_bulk_enabled() {
+  static const bool on = [] {
+    const char *e = std::getenv("HM_GEMV_BULK");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+int bulk_smem_budget() {
+  static const int kb = [] {
+    const char *e = std::getenv("HM_BULK_SMEM_KB");
+    const int v = e ? std::atoi(e) : 192;
+    return std::max(24, std::min(v, 200));
+  }();
+  return kb * 1024;
+}
+
+template <typename K>
+void launch_bulk(K kernel, int grid, int smem, bool pdl, cudaStream_t st, const BulkParams &p) {
+  set_smem(kernel, smem);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kBulkWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl && pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  HM_CUDA(cudaLaunchKernelEx(&cfg, kernel, p));
+  HM_LAUNCH_CHECK();
+}
+
+void launch_gemv_bulk(const uint16_t *pool, size_t slot_elems, int H, int I, const std::vector<hm_group> &gs,
+                      const uint16_t *xp, uint16_t *h, float *out, cudaStream_t st) {
+  BulkParams p{};
+  p.pool = pool;
+  p.slot_elems = slot_elems;
+  p.H = H;
+  p.I = I;
+  p.xp = xp;
+  p.h = h;
+  p.out = out;
+  int mr = 1;
+  const int G = static_cast<int>(gs.size());
+  for (int g = 0; g < G; ++g) {
+    p.slot[g] = gs[g].slot;
+    p.row_begin[g] = gs[g].row_begin;
+    p.row_count[g] = gs[g].row_count;
+    mr = std::max(mr, gs[g].row_count);
+  }
+  const int budget = bulk_smem_budget();
+  const int per_sm = budget <= 110 * 1024 ? 2 : 1;
+  const int grid = num_sms() * per_sm;
+  auto ring = [&](int stage_bytes) {
+    p.stage_bytes = (stage_bytes + 127) / 128 * 128;
+    p.stages = std::max(1, std::min(kBulkMaxStages, budget / (kBulkWarps * p.stage_bytes)));
+    return kBulkWarps * p.stages * p.stage_bytes;
+  };
+  // ffn1: (gate, up) row pairs, columns in chunks of <= 2048 (8 KB stages)
+  p.nck = (H + 2047) / 2048;
+  p.ck = ((H + p.nck - 1) / p.nck + 7) / 8 * 8;
+  p.nr = 1;
+  p.n_units = G * I;
+  p.units_per_group = I;
+  int smem = ring(2 * p.ck * 2);
+  switch (mr) {
+    case 1: launch_bulk(ffn1_bulk_kernel<1>, grid, smem, false, st, p); break;
+    case 2: launch_bulk(ffn1_bulk_kernel<2>, grid, smem, false, st, p); break;
+    default: launch_bulk(ffn1_bulk_kernel<4>, grid, smem, false, st, p); break;
+  }
+  // ffn2: blocks of whole W2 rows up to 12 KB, or one row in <= 8 KB chunks
+  const int row_bytes = I * 2;
+  if (row_bytes <= 6 * 1024) {
+    p.nck = 1;
+    p.ck = I;
+    p.nr = std::max(1, std::min(4, (12 * 1024) / row_bytes));
+  } else {
+    p.nr = 1;
+    p.nck = (I + 4095) / 4096;
+    p.ck = ((I + p.nck - 1) / p.nck + 7) / 8 * 8;
+  }
+  p.units_per_group = (H + p.nr - 1) / p.nr;
+  p.n_units = G * p.units_per_group;
+  smem = ring(p.nr * p.ck * 2);
+  const int nrk = p.nr == 1 ? 1 : p.nr == 2 ? 2 : 4;
+  switch (mr * 8 + nrk) {
+    case 9: launch_bulk(ffn2_bulk_kernel<1, 1>, grid, smem, true, st, p); break;
+    case 10: launch_bulk(ffn2_bulk_kernel<1, 2>, grid, smem, true, st, p); break;
+    case 12: launch_bulk(ffn2_bulk_kernel<1, 4>, grid, smem, true, st, p); break;
+    case 17: launch_bulk(ffn2_bulk_kernel<2, 1>, grid, smem, true, st, p); break;
+    case 18: launch_bulk(ffn2_bulk_kernel<2, 2>, grid, smem, true, st, p); break;
+    case 20: launch_bulk(ffn2_bulk_kernel<2, 4>, grid, smem, true, st, p); break;
+    case 33: case 25: launch_bulk(ffn2_bulk_kernel<4, 1>, grid, smem, true, st, p); break;
+    case 34: case 26: launch_bulk(ffn2_bulk_kernel<4, 2>, grid, smem, true, st, p); break;
+    default: launch_bulk(ffn2_bulk_kernel<4, 4>, grid, smem, true, st, p); break;
+  }
+}
+
 // path HM_FFN_GEMV: HM_GEMV_FUSED decides; HM_FFN_GEMV_SPLIT / _FUSED force one
 void launch_gemv(const uint16_t *pool, size_t slot_elems, int H, int I, const std::vector<hm_group> &gs,
                  const uint16_t *xp, uint16_t *h, float *out, cudaStream_t st, int path) {
   if (gs.empty()) return;
+  if (path == HM_FFN_GEMV_BULK || ((path == HM_FFN_GEMV || path == HM_FFN_AUTO) && gemv_bulk_enabled())) {
+    HM_REQUIRE(static_cast<int>(gs.size()) <= kMaxGroups, HM_EVALUE, "too many expert groups in one launch");
+    HM_REQUIRE(H % 8 == 0 && I % 8 == 0 && I % kIlv == 0, HM_EVALUE, "GEMV needs H % 8 == 0 and I % 128 == 0");
+    launch_gemv_bulk(pool, slot_elems, H, I, gs, xp, h, out, st);
+    return;
+  }
   if (path == HM_FFN_GEMV_FUSED || (path != HM_FFN_GEMV_SPLIT && gemv_fused_enabled())) {
     HM_REQUIRE(static_cast<int>(gs.size()) <= kMaxGroups, HM_EVALUE, "too many expert groups in one launch");
     HM_REQUIRE(H % 8 == 0 && I % 8 == 0 && I % kIlv == 0, HM_EVALUE, "GEMV needs H % 8 == 0 and I % 128 == 0");
@@ -986,6 +1295,7 @@ int hm_expert_ffn(const uint16_t *pool, int n_slots, int H, int I, const hm_grou
                HM_EVALUE, "expert group outside the pool or the row range");
     if (gr.row_count == 0) continue;
     const bool gemv = path == HM_FFN_GEMV || path == HM_FFN_GEMV_SPLIT || path == HM_FFN_GEMV_FUSED ||
+                      path == HM_FFN_GEMV_BULK ||
                       (path == HM_FFN_AUTO && gr.row_count <= hm::kGemvMaxRows);
     if (gemv) {
       HM_REQUIRE(gr.row_count <= hm::kGemvMaxRows, HM_EVALUE, "GEMV path takes at most 4 rows per expert");

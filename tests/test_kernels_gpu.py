@@ -361,3 +361,35 @@ def test_fused_gemv_bit_identical_to_two_launch_pair(H, I, counts):
     for slot, b, c in groups[:3]:
         want = ref.expert(xn[b:b + c], *experts[slot])
         assert rel_err(on[b:b + c], want) <= TOL, (slot, b, c)
+
+
+@pytest.mark.parametrize("H,I,counts", [(512, 384, [1, 2, 3, 4]), (2048, 1408, [1, 1, 1, 1, 1, 1]),
+                                        (3584, 2560, [1] * 16), (4096, 14336, [1, 2]), (2048, 1408, [4, 2, 3]),
+                                        (256, 256, [1] * 96)])
+def test_bulk_gemv_bit_identical_to_two_launch_pair(H, I, counts):
+    """The bulk-copy ffn1 -> ffn2 pair (per-warp cp.async.bulk rings, unit
+    ranges spanning groups, column chunks for wide rows, multi-row W2 stages
+    for narrow ones) accumulates every column in the register pair's per-lane
+    order: h and out bit-identical, repeated launches included, and within
+    1e-2 of the oracle."""
+    n_slots = min(len(counts), 4) + 1
+    pool, experts = make_pool(n_slots, H, I, 7)
+    rows = sum(counts)
+    x = (torch.randn((rows, H), device="cuda")).to(torch.bfloat16)
+    groups, rb = [], 0
+    for g, c in enumerate(counts):
+        groups.append(((g * 3 + 1) % n_slots, rb, c))
+        rb += c
+    outs = []
+    for path in (_lib.FFN_GEMV_SPLIT, _lib.FFN_GEMV_BULK, _lib.FFN_GEMV_BULK):
+        h = torch.zeros((rows, I), dtype=torch.bfloat16, device="cuda")
+        out = torch.full((rows, H), float("nan"), device="cuda")
+        K.expert_ffn(pool, n_slots, H, I, groups, x, h, out, path)
+        torch.cuda.synchronize()
+        outs.append((h.clone(), out.clone()))
+    for h, out in outs[1:]:
+        assert torch.equal(h, outs[0][0]) and torch.equal(out, outs[0][1])
+    xn, on = bf16_numpy(x), outs[1][1].cpu().numpy()
+    for slot, b, c in groups[:3]:
+        want = ref.expert(xn[b:b + c], *experts[slot])
+        assert rel_err(on[b:b + c], want) <= TOL, (slot, b, c)
