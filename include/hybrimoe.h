@@ -378,6 +378,12 @@ int hm_expert_ffn_q4(const uint8_t *pool, size_t slot_bytes, int n_slots, int H,
 int hm_bench_expert_ffn(const uint16_t *pool, int n_slots, int H, int I, int n_groups,
                         int rows_per_group, const uint16_t *xp, uint16_t *h, float *out, int path,
                         int reps, void *stream, float *ms);
+/* Pure streaming-read floor: back-to-back launches reading `bytes` each from
+ * n_buf rotating buffers at `base` (pair != 0: two dependent launches of 2/3 and
+ * 1/3 of the bytes, the ffn1/ffn2 split); *ms = milliseconds per launch (pair).
+ * The per-size denominator of the decode GEMV's efficiency. */
+int hm_bench_stream_read(const void *base, size_t bytes, int n_buf, int pair, int blocks_per_sm, int reps,
+                         void *stream, float *ms);
 /* y[t] = residual[t] (optional) + sum_k w[t,k] * out[pos[t,k]]  (Eq. 1 combine). */
 int hm_combine(const float *out, const int32_t *pos, const float *w, int T, int Kp, int H,
                const uint16_t *residual, uint16_t *y, void *stream);

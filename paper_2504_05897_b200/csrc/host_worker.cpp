@@ -262,8 +262,9 @@ void phase2(const uint16_t *img, int H, int I, const uint16_t *h, int M, float *
 // prefetch a few KB ahead.  This is the decode (host-DRAM-bound) path.
 // Software-prefetch distance (elements) and hint; HM_PF_DIST / HM_PF_HINT
 // (0 none, 1 T0, 2 T1, 3 NTA) override them for tuning on a new host.
-struct PfCfg {  // tuned on the B200 box's host (tools/host_bench.py): L2 hint, 64 KB ahead -> ~94 % of stream-read
-  int dist = 32768;
+struct PfCfg {  // B200 box host, tools/host_phase_prof.py sweep: L2 hint, 16 KB ahead (64 KB overshot the
+                // per-thread chunks of small experts: DeepSeek 1 expert 104 -> 175 GB/s, Mixtral 184-194 -> 206)
+  int dist = 8192;
   int hint = 2;
 };
 PfCfg &pf_cfg() {

@@ -50,7 +50,7 @@ struct GemvParams {
 // The warp's first weight batch is issued before the activations are staged:
 // at decode sizes a warp owns only a few rows, so the kernel is a short chain
 // of DRAM round trips and the staging round trip is taken off it.
-template <int MR>
+template <int MR, int U = 4>
 __global__ void __launch_bounds__(256) ffn1_gemv_kernel(const __grid_constant__ GemvParams p) {
   extern __shared__ __align__(16) uint16_t xs[];  // [MR][H]
   // let ffn2 (launched with programmatic stream serialization) get scheduled
@@ -61,7 +61,6 @@ __global__ void __launch_bounds__(256) ffn1_gemv_kernel(const __grid_constant__ 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint16_t *w13 = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_elems;
   const int i_end = min(I, (cid + 1) * p.chunk);
-  constexpr int U = 4;
   auto rows_of = [&](int i, const uint16_t *&wg, const uint16_t *&wu) {
     const size_t grow = static_cast<size_t>((i / kIlv) * 2 * kIlv + (i % kIlv));
     wg = w13 + grow * H;
@@ -131,7 +130,7 @@ __global__ void __launch_bounds__(256) ffn1_gemv_kernel(const __grid_constant__ 
 // BEFORE waiting for ffn1 (programmatic dependent launch): W2 does not depend
 // on h, so at decode sizes most of a warp's bytes are in flight while ffn1
 // finishes, and the wait + h staging overlap them.
-template <int MR>
+template <int MR, int RW = 2, int U = 4>
 __global__ void __launch_bounds__(256) ffn2_gemv_kernel(const __grid_constant__ GemvParams p) {
   extern __shared__ __align__(16) uint16_t hs[];  // [MR][I]
   const int g = blockIdx.x / p.bpg, cid = blockIdx.x % p.bpg;
@@ -139,9 +138,8 @@ __global__ void __launch_bounds__(256) ffn2_gemv_kernel(const __grid_constant__ 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint16_t *w2 = p.pool + static_cast<size_t>(p.slot[g]) * p.slot_elems + static_cast<size_t>(2) * I * H;
   const int j_end = min(H, (cid + 1) * p.chunk);
-  // two rows per warp at a time (rows j and j + nw): twice the loads in flight
-  // per warp -- small-I experts (DeepSeek: 2.8 KB rows) were latency-bound
-  constexpr int RW = 2, U = 4;
+  // RW rows per warp at a time (rows j, j + nw, ..): RW x U loads in flight
+  // per lane -- small-I experts (DeepSeek: 2.8 KB rows) were latency-bound
   const int jf = cid * p.chunk + wid;
   uint4 wv[RW][U];
   if (jf < j_end) {
@@ -218,6 +216,32 @@ __global__ void __launch_bounds__(256) ffn2_gemv_kernel(const __grid_constant__ 
       }
     }
   }
+}
+
+// ------------------------------------------------------------ stream-read floor
+// The achievable floor of a weight-streaming launch of a given size: every
+// thread streams 16-byte L1-bypassing loads (U in flight) over a contiguous
+// byte range and folds them into one word per block.  hm_bench_stream_read
+// times it back to back (and as a dependent pair, like ffn1 -> ffn2) so the
+// GEMV's per-size efficiency can be read against what a pure read achieves.
+__global__ void __launch_bounds__(256) stream_read_kernel(const uint4 *src, size_t n16, uint32_t *sink) {
+  constexpr int U = 8;
+  uint32_t acc = 0;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < n16; i += U * stride) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = dev::ld_stream(src + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+  }
+  for (; i < n16; i += stride) {
+    const uint4 v = dev::ld_stream(src + i);
+    acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  acc = __reduce_xor_sync(0xffffffffu, acc);
+  if ((threadIdx.x & 31) == 0 && acc == 0x9e3779b9u) sink[blockIdx.x] = acc;  // keep the loads live
 }
 
 // ------------------------------------------------------------ bulk-copy decode GEMV
@@ -1014,6 +1038,21 @@ void launch_gemv_fused(const uint16_t *pool, size_t slot_elems, int H, int I, co
   }
 }
 
+bool gemv_narrow_enabled() {
+  static const bool on = [] {
+    const char *e = std::getenv("HM_GEMV_NARROW");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+int gemv_narrow_rows_per_warp() {
+  static const int v = [] {
+    const char *e = std::getenv("HM_GEMV_NARROW_RPW");
+    return e ? std::max(1, std::min(8, std::atoi(e))) : 1;
+  }();
+  return v;
+}
+
 // HM_GEMV_BULK=1 makes the bulk-copy pair the default GEMV (A/B switch);
 // HM_BULK_SMEM_KB sets the ring budget per CTA (default 192: one CTA per SM).
 bool gemv_bulk_enabled() {
@@ -1151,31 +1190,61 @@ void launch_gemv(const uint16_t *pool, size_t slot_elems, int H, int I, const st
   }
   const int target = num_sms() * 4;
   const int G = p.n_groups;
+  // narrow experts (a whole W13 row pair / W2 row in one batch of U loads per
+  // lane): every warp's bytes go out in ONE DRAM round trip and the grid is
+  // sized to a fixed number of rows per warp (HM_GEMV_NARROW=1; measured
+  // slower than the 4-load batches at every DeepSeek count, so off;
+  // HM_GEMV_NARROW_RPW: rows per warp)
+  const bool narrow1 = gemv_narrow_enabled() && H <= 2048;
+  const bool narrow2 = gemv_narrow_enabled() && I <= 2048;
+  const int rpw = gemv_narrow_rows_per_warp();
   // ffn1: pairs of (gate, up) rows
   int chunk = static_cast<int>((static_cast<long>(G) * I + target - 1) / target);
   chunk = std::max(8, (chunk + 7) / 8 * 8);
+  if (narrow1) chunk = 8 * rpw;
   p.chunk = chunk;
   p.bpg = (I + chunk - 1) / chunk;
   int smem = mr * H * 2;
   HM_REQUIRE(smem <= 200 * 1024, HM_EVALUE, "decode rows do not fit shared memory");
-  switch (mr) {
-    case 1: set_smem(ffn1_gemv_kernel<1>, smem); ffn1_gemv_kernel<1><<<G * p.bpg, 256, smem, st>>>(p); break;
-    case 2: set_smem(ffn1_gemv_kernel<2>, smem); ffn1_gemv_kernel<2><<<G * p.bpg, 256, smem, st>>>(p); break;
-    default: set_smem(ffn1_gemv_kernel<4>, smem); ffn1_gemv_kernel<4><<<G * p.bpg, 256, smem, st>>>(p); break;
+  auto l1 = [&](auto kern) {
+    set_smem(kern, smem);
+    kern<<<G * p.bpg, 256, smem, st>>>(p);
+  };
+  if (narrow1) {
+    switch (mr) {
+      case 1: l1(ffn1_gemv_kernel<1, 8>); break;
+      case 2: l1(ffn1_gemv_kernel<2, 8>); break;
+      default: l1(ffn1_gemv_kernel<4, 8>); break;
+    }
+  } else {
+    switch (mr) {
+      case 1: l1(ffn1_gemv_kernel<1>); break;
+      case 2: l1(ffn1_gemv_kernel<2>); break;
+      default: l1(ffn1_gemv_kernel<4>); break;
+    }
   }
   HM_LAUNCH_CHECK();
   chunk = static_cast<int>((static_cast<long>(G) * H + target - 1) / target);
   chunk = std::max(8, (chunk + 7) / 8 * 8);
+  if (narrow2) chunk = 8 * rpw;
   p.chunk = chunk;
   p.bpg = (H + chunk - 1) / chunk;
   smem = mr * I * 2;
   HM_REQUIRE(smem <= 200 * 1024, HM_EVALUE, "decode rows do not fit shared memory");
   // warm L2 only while the layer's W2 bytes fit comfortably in the 126 MB L2
-  p.l2_prefetch = static_cast<long>(G) * H * I * 2 <= (64L << 20) ? 1 : 0;
-  switch (mr) {
-    case 1: launch_pdl(ffn2_gemv_kernel<1>, G * p.bpg, smem, st, p); break;
-    case 2: launch_pdl(ffn2_gemv_kernel<2>, G * p.bpg, smem, st, p); break;
-    default: launch_pdl(ffn2_gemv_kernel<4>, G * p.bpg, smem, st, p); break;
+  p.l2_prefetch = !narrow2 && static_cast<long>(G) * H * I * 2 <= (64L << 20) ? 1 : 0;
+  if (narrow2) {
+    switch (mr) {
+      case 1: launch_pdl(ffn2_gemv_kernel<1, 1, 8>, G * p.bpg, smem, st, p); break;
+      case 2: launch_pdl(ffn2_gemv_kernel<2, 1, 8>, G * p.bpg, smem, st, p); break;
+      default: launch_pdl(ffn2_gemv_kernel<4, 1, 8>, G * p.bpg, smem, st, p); break;
+    }
+  } else {
+    switch (mr) {
+      case 1: launch_pdl(ffn2_gemv_kernel<1>, G * p.bpg, smem, st, p); break;
+      case 2: launch_pdl(ffn2_gemv_kernel<2>, G * p.bpg, smem, st, p); break;
+      default: launch_pdl(ffn2_gemv_kernel<4>, G * p.bpg, smem, st, p); break;
+    }
   }
 }
 
@@ -1279,6 +1348,44 @@ int hm_bench_expert_ffn(const uint16_t *pool, int n_slots, int H, int I, int n_g
   *ms /= static_cast<float>(reps);
   cudaEventDestroy(a);
   cudaEventDestroy(b);
+  HM_API_END
+}
+
+// Pure-read floor for a launch of `bytes` (and, pair != 0, two dependent
+// launches of bytes*2/3 and bytes/3 -- the ffn1 / ffn2 split of an expert),
+// over `n_buf` rotating buffers of `bytes` each at `base`.
+int hm_bench_stream_read(const void *base, size_t bytes, int n_buf, int pair, int blocks_per_sm, int reps,
+                         void *stream, float *ms) {
+  HM_API_BEGIN
+  HM_REQUIRE(base && bytes >= 16 && n_buf >= 1 && reps >= 1 && blocks_per_sm >= 1, HM_EVALUE, "bad bench");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint32_t *sink = nullptr;
+  const int grid = hm::num_sms() * blocks_per_sm;
+  HM_CUDA(cudaMallocAsync(&sink, static_cast<size_t>(grid) * 4, st));
+  auto one = [&](int i) {
+    const char *b = static_cast<const char *>(base) + static_cast<size_t>(i % n_buf) * bytes;
+    if (!pair) {
+      hm::stream_read_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4 *>(b), bytes / 16, sink);
+    } else {
+      const size_t a = bytes * 2 / 3 / 16 * 16;
+      hm::stream_read_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4 *>(b), a / 16, sink);
+      hm::stream_read_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4 *>(b + a), (bytes - a) / 16, sink);
+    }
+    HM_LAUNCH_CHECK();
+  };
+  for (int i = 0; i < 3; ++i) one(i);
+  cudaEvent_t e0, e1;
+  HM_CUDA(cudaEventCreate(&e0));
+  HM_CUDA(cudaEventCreate(&e1));
+  HM_CUDA(cudaEventRecord(e0, st));
+  for (int i = 0; i < reps; ++i) one(3 + i);
+  HM_CUDA(cudaEventRecord(e1, st));
+  HM_CUDA(cudaEventSynchronize(e1));
+  HM_CUDA(cudaEventElapsedTime(ms, e0, e1));
+  *ms /= static_cast<float>(reps);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  HM_CUDA(cudaFreeAsync(sink, st));
   HM_API_END
 }
 

@@ -19,7 +19,9 @@ shapes = {"mixtral": (4096, 14336), "deepseek": (2048, 1408), "qwen2": (3584, 25
 if len(sys.argv) > 2:  # shape filter, e.g. `deepseek`
     shapes = {k: v for k, v in shapes.items() if k in sys.argv[2].split(",")}
 counts = tuple(int(c) for c in sys.argv[3].split(",")) if len(sys.argv) > 3 else (1, 2, 4, 8, 16)
-paths = {"split": 3, "bulk": 5}
+import os
+paths = {k: v for k, v in {"split": 3, "bulk": 5, "fused": 4}.items()
+         if k in os.environ.get("GEMV_PATHS", "split").split(",")}
 res = {}
 for name, (H, I) in shapes.items():
     eb = 3 * H * I * 2

@@ -16,13 +16,21 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2504_05897_b200 import _lib  # noqa: E402
 
 lib = _lib.lib
-NT = 16
+import os
+NT = int(os.environ.get("NT", os.cpu_count()))
 pool = C.c_void_p()
 lib.hm_cpu_pool_create(NT, C.byref(pool))
 prof = np.zeros((NT, 4), np.int64)
-for name, H, I, n_img, counts, calls in (("deepseek", 2048, 1408, 96, (1, 2), 300), ("mixtral", 4096, 14336, 8, (1,), 30)):
+CASES = (("deepseek", 2048, 1408, 96, (1, 2, 3, 4), 300), ("mixtral", 4096, 14336, 8, (1,), 30))
+ONLY = os.environ.get("ONLY")  # e.g. deepseek:1,2
+if ONLY:
+    nm, cs = ONLY.split(":")
+    CASES = tuple((c[0], c[1], c[2], c[3], tuple(int(v) for v in cs.split(",")), c[5]) for c in CASES if c[0] == nm)
+for name, H, I, n_img, counts, calls in CASES:
     elems = 3 * H * I
-    t = torch.empty((n_img, elems), dtype=torch.int16).pin_memory()
+    t = torch.empty((n_img, elems), dtype=torch.int16)
+    if torch.cuda.is_available():  # pinned like the runtime's master store
+        t = t.pin_memory()
     t.random_(0, 1 << 14)
     for n in counts:
         x = np.full((n, H), 0x3F80, np.uint16)
