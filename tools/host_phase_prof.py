@@ -26,12 +26,20 @@ ONLY = os.environ.get("ONLY")  # e.g. deepseek:1,2
 if ONLY:
     nm, cs = ONLY.split(":")
     CASES = tuple((c[0], c[1], c[2], c[3], tuple(int(v) for v in cs.split(",")), c[5]) for c in CASES if c[0] == nm)
+Q4 = os.environ.get("Q4") == "1"  # 4-bit images through hm_cpu_experts_decode_q4 (wall time only)
 for name, H, I, n_img, counts, calls in CASES:
     elems = 3 * H * I
+    if Q4:
+        nb = C.c_size_t()
+        lib.hm_q4_image_bytes(H, I, C.byref(nb))
+        elems = nb.value // 2
+        n_img *= 4
     t = torch.empty((n_img, elems), dtype=torch.int16)
     if torch.cuda.is_available():  # pinned like the runtime's master store
         t = t.pin_memory()
     t.random_(0, 1 << 14)
+    if Q4:  # valid bf16 scales (0.01) after the nibbles
+        t.view(torch.uint8)[:, H * I * 3 // 2:].view(torch.int16).fill_(0x3C23)
     for n in counts:
         x = np.full((n, H), 0x3F80, np.uint16)
         out = np.empty((n, H), np.float32)
@@ -46,7 +54,7 @@ for name, H, I, n_img, counts, calls in CASES:
                 imgs[i] = t[k % n_img].data_ptr()
                 k += 1
             t0 = time.perf_counter()
-            lib.hm_cpu_experts_decode(pool, imgs, xs, n, H, I, outs)
+            (lib.hm_cpu_experts_decode_q4 if Q4 else lib.hm_cpu_experts_decode)(pool, imgs, xs, n, H, I, outs)
             walls.append(time.perf_counter() - t0)
             lib.hm_cpu_decode_profile(1, prof.ctypes.data, NT)
             if r >= 3:
