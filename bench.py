@@ -16,6 +16,7 @@ The prefill pass (1024 tokens, cold cache) runs first and is reported as
 from __future__ import annotations
 
 import argparse
+import dataclasses
 from dataclasses import replace
 import json
 import os
@@ -468,6 +469,10 @@ def run_ours(args) -> None:
                     "link_busy_frac_of_prefill": cms.value / prefill_ms if prefill_ms > 0 else None}
     pst = layer_stats(pinfo)
     predicted_ttft_ms = 1e3 * pinfo["pass"].latency
+    if os.environ.get("HM_BENCH_DUMP_PREFILL"):  # per-layer prefill stats (diagnostics)
+        Path(os.environ["HM_BENCH_DUMP_PREFILL"]).write_text(json.dumps(
+            {"prefill_ms": prefill_ms, "predicted_ms": predicted_ttft_ms,
+             "layers": [dataclasses.asdict(x) for x in pst]}, indent=1))
 
     # ---- decode: W warm-up passes (recorded for the parity block), then K timed passes
     _trace("decode")

@@ -350,6 +350,16 @@ int &decode_grain() {
   return g;
 }
 
+// Per-thread phase timestamps of the last decode / AMX call (hm_cpu_decode_profile):
+// AMX: [0] start, [1] activations packed, [2] phase 1 done, [3] phase 2 done (ns);
+// [tid][0] start, [1] phase 1 done, [2] barrier passed, [3] phase 2 done (ns).
+static std::vector<int64_t> g_dec_prof;
+static bool g_dec_prof_on = false;
+static inline int64_t ns_now() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
 // ------------------------------------------------------------ AMX (prefill)
 // Multi-token experts on the AMX tile unit: out^T = W . X^T with A = 16 weight
 // rows x 32 K (row-major, loaded straight from the image) and B = 16 token
@@ -415,11 +425,40 @@ inline void amx_config() {
   done = true;
 }
 
-// VNNI repack: src [M, K] bf16 rows -> dst [K/2][Mpad][2] (zero-padded tokens).
-void vnni_pack(const uint16_t *src, int M, int K, int Mpad, uint16_t *dst) {
-  std::memset(dst, 0, static_cast<size_t>(K) * Mpad * 2);
-  for (int t = 0; t < M; ++t)
-    for (int k = 0; k < K; ++k) dst[(static_cast<size_t>(k >> 1) * Mpad + t) * 2 + (k & 1)] = src[static_cast<size_t>(t) * K + k];
+// VNNI repack: src [M, K] bf16 rows -> dst [K/2][Mpad][2] (zero-padded tokens),
+// i.e. a transpose of the [M][K/2] matrix of 32-bit bf16 pairs.  Rows of
+// k-pairs [kp0, kp1) only: every pool thread packs its own slice (the serial
+// scalar pack was ~40 % of a 64-token DeepSeek expert); 16 tokens per gather.
+void vnni_pack_rows(const uint16_t *src, int M, int K, int Mpad, uint16_t *dst, int kp0, int kp1) {
+  const int *s32 = reinterpret_cast<const int *>(src);
+  uint32_t *d32 = reinterpret_cast<uint32_t *>(dst);
+  const int K2 = K / 2;
+  const __m512i iota = _mm512_set_epi32(15, 14, 13, 12, 11, 10, 9, 8, 7, 6, 5, 4, 3, 2, 1, 0);
+  for (int tb = 0; tb < Mpad; tb += 16) {
+    const int n = M - tb;
+    const __mmask16 live = n >= 16 ? 0xFFFF : n > 0 ? static_cast<__mmask16>((1u << n) - 1u) : 0;
+    const __m512i idx = _mm512_mullo_epi32(_mm512_add_epi32(_mm512_set1_epi32(tb), iota), _mm512_set1_epi32(K2));
+    for (int kp = kp0; kp < kp1; ++kp) {
+      const __m512i v = live ? _mm512_mask_i32gather_epi32(_mm512_setzero_si512(), live, idx, s32 + kp, 4)
+                             : _mm512_setzero_si512();
+      _mm512_storeu_si512(d32 + static_cast<size_t>(kp) * Mpad + tb, v);
+    }
+  }
+}
+// this pool thread's share of the pack, then a barrier (inside pool.run)
+inline void vnni_pack_par(ThreadPool &pool, int tid, int nt, const uint16_t *src, int M, int K, int Mpad,
+                          uint16_t *dst) {
+  const int K2 = K / 2;
+  vnni_pack_rows(src, M, K, Mpad, dst, static_cast<int>(static_cast<long>(K2) * tid / nt),
+                 static_cast<int>(static_cast<long>(K2) * (tid + 1) / nt));
+  pool.barrier();
+}
+// per-thread scratch that persists across calls (a fresh std::vector per call
+// page-faulted and zeroed up to 1 MB per thread per expert)
+template <class T>
+T *tls_buf(std::vector<T> &v, size_t n) {
+  if (v.size() < n) v.resize(n);
+  return v.data();
 }
 
 // C[a][b] (16 rows of A-block a x 16 tokens of B-block b) over the full K for
@@ -475,13 +514,14 @@ AmxCfg &amx_cfg() {
   }();
   return c;
 }
-// 1: cache-blocked, 0: the first kernel, -1 (default): cache-blocked from 256
-// tokens up -- on the box's host the two are within noise below that and the
-// blocked kernel is 15-25 % faster at 256-512 tokens (tools/host_prefill_bench.py).
+// 0 (default): per-unit full-K blocks; 1: cache-blocked; -1: cache-blocked
+// from 256 tokens up.  With dynamic unit claims and vector output transposes
+// in both, the full-K kernel measured faster at every shape and M <= 256 on
+// the box's host (tools/amx_phase_prof.py; Mixtral M=256 11.5 vs 17.6 ms).
 int &amx_algo() {
   static int a = [] {
     const char *e = std::getenv("HM_AMX_ALGO");
-    return e ? std::atoi(e) : -1;
+    return e ? std::atoi(e) : 0;
   }();
   return a;
 }
@@ -561,22 +601,34 @@ void cpu_expert_amx2(ThreadPool &pool, const uint16_t *img, int H, int I, const 
   scratch.resize(static_cast<size_t>(H) * Mpad + static_cast<size_t>(I) * Mpad);
   uint16_t *xv = scratch.data();
   uint16_t *hv = xv + static_cast<size_t>(H) * Mpad;
-  vnni_pack(x, M, H, Mpad, xv);
   const uint16_t *w2 = img + static_cast<size_t>(2) * I * H;
   const int GO = amx_cfg().go;
+  std::atomic<int> next1{0}, next2{0};  // groups of GO units, claimed dynamically
+  if (g_dec_prof_on && g_dec_prof.size() < static_cast<size_t>(pool.size()) * 4)
+    g_dec_prof.assign(static_cast<size_t>(pool.size()) * 4, 0);
+  const int64_t t_call = g_dec_prof_on ? ns_now() : 0;
   pool.run([&](int tid, int nt) {
+    int64_t *tp = g_dec_prof_on ? &g_dec_prof[static_cast<size_t>(tid) * 4] : nullptr;
+    if (tp) tp[0] = ns_now() - t_call;
     amx_config();
-    std::vector<float> cbuf(static_cast<size_t>(GO) * 2 * nbt * 256);
+    vnni_pack_par(pool, tid, nt, x, M, H, Mpad, xv);
+    if (tp) tp[1] = ns_now() - t_call;
+    static thread_local std::vector<float> cvec;
+    struct {
+      float *p;
+      float *data() { return p; }
+    } cbuf{tls_buf(cvec, static_cast<size_t>(GO) * 2 * nbt * 256)};
     // phase 1: unit o = 16 gate rows (block 0) + their 16 up rows (block 1)
     const int ob = I / 16;
-    const int u0 = static_cast<int>(static_cast<long>(ob) * tid / nt), u1 = static_cast<int>(static_cast<long>(ob) * (tid + 1) / nt);
     auto row1 = [&](int o, int which) {
       const int i0 = o * 16;
       const size_t grow = static_cast<size_t>((i0 / kIlv) * 2 * kIlv + i0 % kIlv);
       return img + (grow + (which ? kIlv : 0)) * H;
     };
-    for (int g0 = u0; g0 < u1; g0 += GO) {
-      const int g1 = std::min(u1, g0 + GO);
+    // groups small enough that every thread claims at least two
+    const int GO1 = std::max(1, std::min(GO, ob / (2 * nt)));
+    for (int gi; (gi = next1.fetch_add(1, std::memory_order_relaxed)) * GO1 < ob;) {
+      const int g0 = gi * GO1, g1 = std::min(ob, g0 + GO1);
       amx_gemm_units(row1, g0, g1, static_cast<size_t>(H) * 2, xv, Mpad, H, cbuf.data());
       for (int o = g0; o < g1; ++o) {
         const float *cb = cbuf.data() + static_cast<size_t>(o - g0) * 2 * nbt * 256;
@@ -598,28 +650,30 @@ void cpu_expert_amx2(ThreadPool &pool, const uint16_t *img, int H, int I, const 
         }
       }
     }
+    if (tp) tp[2] = ns_now() - t_call;
     pool.barrier();
     // phase 2: unit q = W2 rows 32q..32q+15 (block 0) and 32q+16..32q+31 (block 1)
     const int pairs = H / 32;
-    const int q0 = static_cast<int>(static_cast<long>(pairs) * tid / nt), q1 = static_cast<int>(static_cast<long>(pairs) * (tid + 1) / nt);
     auto row2 = [&](int q, int which) { return w2 + static_cast<size_t>(q * 32 + which * 16) * I; };
-    for (int g0 = q0; g0 < q1; g0 += GO) {
-      const int g1 = std::min(q1, g0 + GO);
+    const __m512i col = _mm512_set_epi32(240, 224, 208, 192, 176, 160, 144, 128, 112, 96, 80, 64, 48, 32, 16, 0);
+    const int GO2 = std::max(1, std::min(GO, pairs / (2 * nt)));
+    for (int gi; (gi = next2.fetch_add(1, std::memory_order_relaxed)) * GO2 < pairs;) {
+      const int g0 = gi * GO2, g1 = std::min(pairs, g0 + GO2);
       amx_gemm_units(row2, g0, g1, static_cast<size_t>(I) * 2, hv, Mpad, I, cbuf.data());
       for (int q = g0; q < g1; ++q) {
         const float *cb = cbuf.data() + static_cast<size_t>(q - g0) * 2 * nbt * 256;
         for (int a = 0; a < 2; ++a)
           for (int b = 0; b < nbt; ++b) {
             const float *c = cb + (static_cast<size_t>(a) * nbt + b) * 256;
-            for (int t = 0; t < 16; ++t) {
+            for (int t = 0; t < 16; ++t) {  // column t of C = token t's 16 outputs
               const int tok = b * 16 + t;
               if (tok >= M) break;
-              float *o = out + static_cast<size_t>(tok) * H + q * 32 + a * 16;
-              for (int r = 0; r < 16; ++r) o[r] = c[r * 16 + t];
+              _mm512_storeu_ps(out + static_cast<size_t>(tok) * H + q * 32 + a * 16, _mm512_i32gather_ps(col, c + t, 4));
             }
           }
       }
     }
+    if (tp) tp[3] = ns_now() - t_call;
   });
 }
 
@@ -878,14 +932,23 @@ void cpu_expert_q4(ThreadPool &pool, const uint8_t *img, int H, int I, const uin
   scratch.resize(static_cast<size_t>(H) * Mpad + static_cast<size_t>(I) * Mpad);
   uint16_t *xv = scratch.data();
   uint16_t *hv = xv + static_cast<size_t>(H) * Mpad;
-  vnni_pack(x, M, H, Mpad, xv);
   const Q4View v = q4_view(img, H, I);
+  std::atomic<int> next1{0}, next2{0};  // units claimed dynamically
   pool.run([&](int tid, int nt) {
     amx_config();
-    std::vector<float> cbuf(static_cast<size_t>(2) * nbt * 256);
-    std::vector<uint16_t> wbuf(static_cast<size_t>(32) * std::max(H, I));
+    vnni_pack_par(pool, tid, nt, x, M, H, Mpad, xv);
+    static thread_local std::vector<float> cvec;
+    static thread_local std::vector<uint16_t> wvec;
+    struct {
+      float *p;
+      float *data() { return p; }
+    } cbuf{tls_buf(cvec, static_cast<size_t>(2) * nbt * 256)};
+    struct {
+      uint16_t *p;
+      uint16_t *data() { return p; }
+    } wbuf{tls_buf(wvec, static_cast<size_t>(32) * std::max(H, I))};
     const int ob = I / 16;
-    for (int o = ob * tid / nt; o < ob * (tid + 1) / nt; ++o) {
+    for (int o; (o = next1.fetch_add(1, std::memory_order_relaxed)) < ob;) {
       const int i0 = o * 16;
       const size_t grow = static_cast<size_t>((i0 / kIlv) * 2 * kIlv + i0 % kIlv);
       dequant_rows_q4(v.n13 + grow * (H / 2), v.s13 + grow * (H / 128), 16, H, wbuf.data());
@@ -912,7 +975,8 @@ void cpu_expert_q4(ThreadPool &pool, const uint8_t *img, int H, int I, const uin
     }
     pool.barrier();
     const int pairs = H / 32;
-    for (int q = pairs * tid / nt; q < pairs * (tid + 1) / nt; ++q) {
+    const __m512i col = _mm512_set_epi32(240, 224, 208, 192, 176, 160, 144, 128, 112, 96, 80, 64, 48, 32, 16, 0);
+    for (int q; (q = next2.fetch_add(1, std::memory_order_relaxed)) < pairs;) {
       dequant_rows_q4(v.n2 + static_cast<size_t>(q * 32) * (I / 2), v.s2 + static_cast<size_t>(q * 32) * (I / 128),
                       32, I, wbuf.data());
       auto rowp = [&](int, int which) { return wbuf.data() + static_cast<size_t>(which) * 16 * I; };
@@ -920,11 +984,10 @@ void cpu_expert_q4(ThreadPool &pool, const uint8_t *img, int H, int I, const uin
       for (int a = 0; a < 2; ++a)
         for (int b = 0; b < nbt; ++b) {
           const float *c = cbuf.data() + (static_cast<size_t>(a) * nbt + b) * 256;
-          for (int t = 0; t < 16; ++t) {
+          for (int t = 0; t < 16; ++t) {  // column t of C = token t's 16 outputs
             const int tok = b * 16 + t;
             if (tok >= M) break;
-            float *o = out + static_cast<size_t>(tok) * H + q * 32 + a * 16;
-            for (int r = 0; r < 16; ++r) o[r] = c[r * 16 + t];
+            _mm512_storeu_ps(out + static_cast<size_t>(tok) * H + q * 32 + a * 16, _mm512_i32gather_ps(col, c + t, 4));
           }
         }
     }
@@ -943,16 +1006,25 @@ void cpu_expert_amx(ThreadPool &pool, const uint16_t *img, int H, int I, const u
   scratch.resize(static_cast<size_t>(H) * Mpad + static_cast<size_t>(I) * Mpad);
   uint16_t *xv = scratch.data();
   uint16_t *hv = xv + static_cast<size_t>(H) * Mpad;
-  vnni_pack(x, M, H, Mpad, xv);
-  std::memset(hv, 0, static_cast<size_t>(I) * Mpad * 2);
+  // (phase 1 writes every (pair, token block) of hv, padded tokens as zeros)
   const uint16_t *w2 = img + static_cast<size_t>(2) * I * H;
   const int nb = Mpad / 16;
+  if (g_dec_prof_on && g_dec_prof.size() < static_cast<size_t>(pool.size()) * 4)
+    g_dec_prof.assign(static_cast<size_t>(pool.size()) * 4, 0);
+  const int64_t t_call = g_dec_prof_on ? ns_now() : 0;
+  // units are claimed dynamically: with static splits one slowed core held
+  // each phase barrier (measured: phase-1 max 2.5x the median thread)
+  std::atomic<int> next1{0}, next2{0};
   pool.run([&](int tid, int nt) {
+    int64_t *tp = g_dec_prof_on ? &g_dec_prof[static_cast<size_t>(tid) * 4] : nullptr;
+    if (tp) tp[0] = ns_now() - t_call;
     amx_config();
+    vnni_pack_par(pool, tid, nt, x, M, H, Mpad, xv);
+    if (tp) tp[1] = ns_now() - t_call;
     float c[4][16][16];
     // phase 1: 16-output blocks of gate rows with their up rows (128-row interleave)
     const int ob = I / 16;
-    for (int o = ob * tid / nt; o < ob * (tid + 1) / nt; ++o) {
+    for (int o; (o = next1.fetch_add(1, std::memory_order_relaxed)) < ob;) {
       const int i0 = o * 16;
       const size_t grow = static_cast<size_t>((i0 / kIlv) * 2 * kIlv + i0 % kIlv);
       const uint16_t *wg = img + grow * H, *wu = img + (grow + kIlv) * H;
@@ -970,11 +1042,13 @@ void cpu_expert_amx(ThreadPool &pool, const uint16_t *img, int H, int I, const u
         }
       }
     }
+    if (tp) tp[2] = ns_now() - t_call;
     pool.barrier();
     // phase 2: pairs of 16-row blocks of W2
     const int rb = H / 16;
     const int pairs = (rb + 1) / 2;
-    for (int q = pairs * tid / nt; q < pairs * (tid + 1) / nt; ++q) {
+    const __m512i col = _mm512_set_epi32(240, 224, 208, 192, 176, 160, 144, 128, 112, 96, 80, 64, 48, 32, 16, 0);
+    for (int q; (q = next2.fetch_add(1, std::memory_order_relaxed)) < pairs;) {
       const int j0 = q * 32;
       const bool second = j0 + 16 < H;
       const uint16_t *wa0 = w2 + static_cast<size_t>(j0) * I;
@@ -982,25 +1056,20 @@ void cpu_expert_amx(ThreadPool &pool, const uint16_t *img, int H, int I, const u
       for (int b = 0; b < nb; b += 2) {
         const bool two = b + 1 < nb;
         amx_block(wa0, wa1, static_cast<size_t>(I) * 2, hv, Mpad, b * 16, two, I, c);
+        // C is [weight row][token]: token t's 16 outputs are column t -- one
+        // gather and one 64-byte store per token (was 16 scalar stores)
         for (int a = 0; a < (second ? 2 : 1); ++a)
           for (int bb = 0; bb < (two ? 2 : 1); ++bb)
-            for (int r = 0; r < 16; ++r)
-              for (int t = 0; t < 16; ++t) {
-                const int tok = (b + bb) * 16 + t;
-                if (tok < M) out[static_cast<size_t>(tok) * H + j0 + a * 16 + r] = c[a * 2 + bb][r][t];
-              }
+            for (int t = 0; t < 16; ++t) {
+              const int tok = (b + bb) * 16 + t;
+              if (tok >= M) break;
+              _mm512_storeu_ps(out + static_cast<size_t>(tok) * H + j0 + a * 16,
+                               _mm512_i32gather_ps(col, &c[a * 2 + bb][0][t], 4));
+            }
       }
     }
+    if (tp) tp[3] = ns_now() - t_call;
   });
-}
-
-// Per-thread phase timestamps of the last decode call (hm_cpu_decode_profile):
-// [tid][0] start, [1] phase 1 done, [2] barrier passed, [3] phase 2 done (ns).
-static std::vector<int64_t> g_dec_prof;
-static bool g_dec_prof_on = false;
-static inline int64_t ns_now() {
-  return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
-      .count();
 }
 
 void cpu_experts_decode(ThreadPool &pool, const uint16_t *const *imgs, const uint16_t *const *xs, int n, int H,
