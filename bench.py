@@ -523,6 +523,9 @@ def run_ours(args) -> None:
     launches = lib.hm_launch_count() - launches0
     predicted = [1e3 * info["pass"].latency for info in stats_all]
     stats_all = [s for info in stats_all for s in layer_stats(info)]
+    if os.environ.get("HM_BENCH_DUMP_DECODE"):  # per-layer timed-decode stats (diagnostics)
+        Path(os.environ["HM_BENCH_DUMP_DECODE"]).write_text(json.dumps(
+            [dataclasses.asdict(x) for x in stats_all]))
     ms_total = t0.elapsed_time(t1)
     if dist:
         t = torch.tensor([ms_total], device="cuda")

@@ -9,7 +9,7 @@ print("value", round(d["value"], 2), "e2e", round(d["e2e"]["value"], 2), "ms/ste
 print("roofline frac", round(d["roofline"]["frac"], 3), "step_roofline", json.dumps(d["step_roofline"])[:300])
 print("per_step", json.dumps(d["per_step"]))
 print("model_vs_measured", {k: round(v, 3) for k, v in d["model_vs_measured"].items() if isinstance(v, float)})
-print("cpu_baseline", d["cpu_baseline"]["value"], "clocks", d["clocks"])
+print("cpu_baseline", (d.get("cpu_baseline") or {}).get("value"), "clocks", d["clocks"])
 for k, v in d.get("configs", {}).items():
     sr = v.get("step_roofline", {})
     print(f"{k:12s} decode {v.get('decode_tok_s', 0):7.2f} e2e {v.get('e2e_tok_s', 0):7.2f} prefill {v.get('prefill_ms', 0):7.1f}"
