@@ -658,9 +658,15 @@ def run_ours(args) -> None:
 
     # ---- CPU baseline: the reference's all-CPU path on this host, bounded sample
     cpu = None
+    # release the pinned store, the slot pool and the worker threads before the
+    # CPU baseline and the child config runs: explicit, so that a reference
+    # still held elsewhere cannot keep 90 GB of pinned host memory alive
+    torch.cuda.synchronize()
+    if dist:  # every rank's last exchange into a peer's memory has completed
+        dist.barrier()
+    moe.close()
+    del moe
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # rank 0 at N=1 only
-        del moe  # release the pinned store first (host memory)
-        torch.cuda.synchronize()
         cpu = cpu_reference_decode(args.shape, args.cpu_baseline_steps, 1, prefill=0)
 
     # ---- per-rank parity, gathered

@@ -218,6 +218,11 @@ class HybridMoE:
                                  f"more than its {self.capacity} cache slots")
             self._fixed_refs = refs
 
+    def close(self) -> None:
+        """Release the runtime now (HBM slot pool, pinned master store, host
+        worker threads) whatever still references this object; idempotent."""
+        self.__del__()
+
     def __del__(self) -> None:
         if getattr(self, "_rt", None):
             torch.cuda.synchronize()
