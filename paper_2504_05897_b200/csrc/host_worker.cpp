@@ -7,6 +7,8 @@
 // Decode (1 token) is a DRAM-bandwidth-bound GEMV split over all threads;
 // prefill blocks 16 weight rows x 4 tokens so weights are reused from L2.
 #include <immintrin.h>
+#include <pthread.h>
+#include <sched.h>
 #include <sys/syscall.h>
 #include <unistd.h>
 
@@ -38,9 +40,37 @@ static inline void wait_until(Pred done) {
   while (!done()) std::this_thread::yield();
 }
 
+// HM_PIN_THREADS=1: worker t runs on the t-th CPU of the process's affinity
+// mask (the caller, thread 0, is left where it is) -- A/B knob for the
+// in-step straggler variance.
+static void pin_to_nth_cpu(int t) {
+  static const bool on = [] {
+    const char *e = std::getenv("HM_PIN_THREADS");
+    return e && std::atoi(e) != 0;
+  }();
+  if (!on) return;
+  cpu_set_t mask;
+  if (sched_getaffinity(0, sizeof(mask), &mask) != 0) return;
+  int seen = 0;
+  for (int c = 0; c < CPU_SETSIZE; ++c) {
+    if (!CPU_ISSET(c, &mask)) continue;
+    if (seen++ == t) {
+      cpu_set_t one;
+      CPU_ZERO(&one);
+      CPU_SET(c, &one);
+      pthread_setaffinity_np(pthread_self(), sizeof(one), &one);
+      return;
+    }
+  }
+}
+
 ThreadPool::ThreadPool(int n, int spin_us)
     : n_(std::max(1, n)), spin_us_(spin_us), ranges_(new Range[static_cast<size_t>(2) * std::max(1, n)]) {
-  for (int t = 1; t < n_; ++t) threads_.emplace_back([this, t] { loop(t); });
+  for (int t = 1; t < n_; ++t)
+    threads_.emplace_back([this, t] {
+      pin_to_nth_cpu(t);
+      loop(t);
+    });
 }
 
 ThreadPool::~ThreadPool() {

@@ -289,6 +289,54 @@ class HybridMoE:
         self._weights_ready = True
         self._apply_residency()
 
+    # checkpoint loading (e.g. a transformers MoE block's parameters); call
+    # before the first forward pass -- resident HBM copies are not refreshed
+    def _image(self, gate: torch.Tensor, up: torch.Tensor, down: torch.Tensor) -> torch.Tensor:
+        """gate/up [I, H], down [H, I] -> one bf16 slot image [1, 3HI] on the GPU
+        (W13 rows interleaved in 128-row gate/up blocks, include/hybrimoe.h)."""
+        H, I = self.H, self.I
+        if tuple(gate.shape) != (I, H) or tuple(up.shape) != (I, H) or tuple(down.shape) != (H, I):
+            raise ValueError(f"expert weights must be gate/up [{I}, {H}] and down [{H}, {I}]")
+        g = gate.to("cuda", torch.bfloat16).reshape(I // 128, 1, 128, H)
+        u = up.to("cuda", torch.bfloat16).reshape(I // 128, 1, 128, H)
+        w13 = torch.cat([g, u], dim=1).reshape(-1)
+        return torch.cat([w13, down.to("cuda", torch.bfloat16).reshape(-1)]).reshape(1, -1)
+
+    def set_expert_weights(self, layer: int, expert: int, gate: torch.Tensor, up: torch.Tensor,
+                           down: torch.Tensor) -> None:
+        """Routed expert (layer, expert) into the pinned master store (ignored
+        on a rank that is not the expert's home)."""
+        if expert % self.ep_world != self.ep_rank:
+            return
+        n_home = (self.N - self.ep_rank + self.ep_world - 1) // self.ep_world
+        if self.host_images < self.L * n_home:
+            raise ValueError("per-expert weights need one host image per expert (host_images aliases them)")
+        self.store_t[self.image_of(layer, expert)].copy_(self._encode(self._image(gate, up, down))[0])
+        self._weights_ready = True
+
+    def set_shared_weights(self, layer: int, gate: torch.Tensor, up: torch.Tensor, down: torch.Tensor) -> None:
+        """The layer's shared expert(s) as ONE SwiGLU of intermediate size
+        S*I (gate/up [S*I, H], down [H, S*I]: DeepSeek's n_shared experts
+        concatenated, Qwen2's single wide one), split into its S resident chunks."""
+        I = self.I
+        if gate.shape[0] != self.S * I:
+            raise ValueError(f"shared expert intermediate size {gate.shape[0]} != {self.S} chunks x {I}")
+        for c in range(self.S):
+            sl = slice(c * I, (c + 1) * I)
+            self.pool[self.shared_slot(layer, c)].copy_(
+                self._encode(self._image(gate[sl], up[sl], down[:, sl]))[0])
+
+    def set_router_weights(self, layer: int, weight: torch.Tensor, shared_gate: torch.Tensor | None = None) -> None:
+        """Router gate [N, H] (and the Qwen2 shared-expert gate [1, H]) of a layer,
+        for model mode (logits computed on the GPU from the hidden state)."""
+        if self.gate_w is None:
+            self.gate_w = torch.zeros((self.L, self.ld, self.H), dtype=torch.bfloat16, device="cuda")
+        self.gate_w[layer, : self.N] = weight.to("cuda", torch.bfloat16)
+        if self.family.shared_gate:
+            if shared_gate is None:
+                raise ValueError("this family's router needs the shared-expert gate row")
+            self.gate_w[layer, self.N] = shared_gate.reshape(-1).to("cuda", torch.bfloat16)
+
     def _apply_residency(self) -> None:
         """(Re)copy the fixed-residency experts into their slots (after weights change)."""
         if self._fixed_refs and self._weights_ready:
