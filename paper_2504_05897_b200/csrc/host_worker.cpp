@@ -105,8 +105,9 @@ void ThreadPool::loop(int tid) {
   }
 }
 
-void ThreadPool::run(const std::function<void(int, int)> &fn) {
+void ThreadPool::run(const std::function<void(int, int)> &fn, const std::function<void()> *before_self) {
   if (n_ == 1) {
+    if (before_self) (*before_self)();
     fn(0, 1);
     return;
   }
@@ -117,8 +118,19 @@ void ThreadPool::run(const std::function<void(int, int)> &fn) {
     gen_.fetch_add(1, std::memory_order_release);
   }
   cv_.notify_all();
+  // tid 0 must still take part (the job's barriers count it) even if the
+  // caller's own work throws: rethrow only after the job completed
+  std::exception_ptr err;
+  if (before_self) {
+    try {
+      (*before_self)();
+    } catch (...) {
+      err = std::current_exception();
+    }
+  }
   fn(0, n_);
   wait_until([&] { return pending_.load(std::memory_order_acquire) == 0; });
+  if (err) std::rethrow_exception(err);
 }
 
 void ThreadPool::barrier() { wait(arrive()); }
@@ -852,9 +864,13 @@ inline void dequant_rows_q4(const uint8_t *nib, const uint16_t *sc, int n, int K
 }  // namespace
 
 void cpu_experts_decode_q4(ThreadPool &pool, const uint8_t *const *imgs, const uint16_t *const *xs, int n, int H,
-                           int I, float *const *outs, std::vector<uint16_t> &hbuf) {
+                           int I, float *const *outs, std::vector<uint16_t> &hbuf,
+                           const std::function<void()> *before_self) {
   HM_REQUIRE(H % 128 == 0 && I % 128 == 0, HM_EVALUE, "4-bit host worker needs H, I multiples of 128");
-  if (n <= 0) return;
+  if (n <= 0) {
+    if (before_self) (*before_self)();
+    return;
+  }
   hbuf.resize(static_cast<size_t>(n) * I);
   uint16_t *h = hbuf.data();
   std::vector<Q4X> qx(n), hx(n);
@@ -902,7 +918,7 @@ void cpu_experts_decode_q4(ThreadPool &pool, const uint8_t *const *imgs, const u
                     hx[e], outs[e] + j0);
       }
     });
-  });
+  }, before_self);
 }
 
 void cpu_expert_q4(ThreadPool &pool, const uint8_t *img, int H, int I, const uint16_t *x, int M, float *out,
@@ -1103,13 +1119,17 @@ void cpu_expert_amx(ThreadPool &pool, const uint16_t *img, int H, int I, const u
 }
 
 void cpu_experts_decode(ThreadPool &pool, const uint16_t *const *imgs, const uint16_t *const *xs, int n, int H,
-                        int I, float *const *outs, std::vector<uint16_t> &hbuf) {
+                        int I, float *const *outs, std::vector<uint16_t> &hbuf,
+                        const std::function<void()> *before_self) {
   if (g_dec_prof_on && g_dec_prof.size() < static_cast<size_t>(pool.size()) * 4)
     g_dec_prof.assign(static_cast<size_t>(pool.size()) * 4, 0);
   // All single-token experts of a layer in one pool run: phase 1 over every
   // (expert, 128-pair block), one barrier, phase 2 over every (expert, row).
   HM_REQUIRE(H % 32 == 0 && I % kIlv == 0, HM_EVALUE, "host worker needs H % 32 == 0 and I % 128 == 0");
-  if (n <= 0) return;
+  if (n <= 0) {
+    if (before_self) (*before_self)();
+    return;
+  }
   hbuf.resize(static_cast<size_t>(n) * I);
   uint16_t *h = hbuf.data();
   const int grain = decode_grain();
@@ -1157,7 +1177,7 @@ void cpu_experts_decode(ThreadPool &pool, const uint16_t *const *imgs, const uin
       }
     });
     if (tp) tp[3] = ns_now() - t_call;
-  });
+  }, before_self);
 }
 
 void cpu_expert(ThreadPool &pool, const uint16_t *img, int H, int I, const uint16_t *x, int M, float *out,

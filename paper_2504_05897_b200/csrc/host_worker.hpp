@@ -23,7 +23,10 @@ class ThreadPool {
   explicit ThreadPool(int n, int spin_us = 3000);
   ~ThreadPool();
   int size() const { return n_; }
-  void run(const std::function<void(int, int)> &fn);
+  // before_self (optional) runs on the caller after the workers were woken
+  // and before the caller joins as tid 0: host work that overlaps the job's
+  // start (jobs must tolerate a late tid 0, e.g. by stealing its range)
+  void run(const std::function<void(int, int)> &fn, const std::function<void()> *before_self = nullptr);
   void barrier();
   // split barrier: arrive() returns the phase token; passed(token) tells
   // whether every thread has arrived; wait(token) blocks until then.  Lets a
@@ -62,13 +65,16 @@ void cpu_expert_amx(ThreadPool &pool, const uint16_t *img, int H, int I, const u
                     std::vector<uint16_t> &scratch);
 
 // n single-token experts at once (decode): one pool run, one barrier.
+// before_self: see ThreadPool::run.
 void cpu_experts_decode(ThreadPool &pool, const uint16_t *const *imgs, const uint16_t *const *xs, int n, int H,
-                        int I, float *const *outs, std::vector<uint16_t> &hbuf);
+                        int I, float *const *outs, std::vector<uint16_t> &hbuf,
+                        const std::function<void()> *before_self = nullptr);
 
 // 4-bit expert images (include/hybrimoe.h, hm_q4_*): decode GEMV on the
 // nibbles; multi-token groups dequantize 32-row units and run on AMX.
 void cpu_experts_decode_q4(ThreadPool &pool, const uint8_t *const *imgs, const uint16_t *const *xs, int n, int H,
-                           int I, float *const *outs, std::vector<uint16_t> &hbuf);
+                           int I, float *const *outs, std::vector<uint16_t> &hbuf,
+                           const std::function<void()> *before_self = nullptr);
 void cpu_expert_q4(ThreadPool &pool, const uint8_t *img, int H, int I, const uint16_t *x, int M, float *out,
                    std::vector<uint16_t> &scratch);
 

@@ -588,67 +588,6 @@ struct Runtime {
         if (a.first == ref) return a.second;
       return -1;
     };
-    // GPU experts already resident (and the layer's shared chunks): one launch
-    std::vector<hm_group> batch;
-    for (const Event &ev : rec.plan.events) {
-      if (ev.device != HM_DEV_GPU || assign_of(ev.ref) != HM_ASSIGN_GPU_CACHED) continue;
-      const int e = ref_expert(ev.ref);
-      const int64_t slot = checked_slot(ev.ref, engine->cache.resident.at(ev.ref).slot);
-      wait_ready(slot, st);  // a prefetch may still be in flight
-      batch.push_back(hm_group{static_cast<int32_t>(slot), h_offsets[e], h_counts[e], 0});
-    }
-    s.n_gpu = static_cast<int32_t>(batch.size());
-    for (int c = 0; c < S; ++c)
-      if (c % W == R)
-        batch.push_back(hm_group{static_cast<int32_t>(shared_slot(layer, c)), h_offsets[N + c], h_counts[N + c], 0});
-    s.bytes_gpu = static_cast<int64_t>(batch.size()) * static_cast<int64_t>(slot_bytes);
-    if (!batch.empty()) {
-      ffn(batch.data(), static_cast<int>(batch.size()), rows_used, st);
-      mark_used(batch.data(), static_cast<int>(batch.size()), st);
-    }
-    // Copies in plan transfer order (== insert order), then prefetches; an
-    // expert the plan computes on the GPU is launched right after its copy so
-    // that a later copy into the same slot (same-layer eviction) waits for it.
-    auto copy_and_maybe_compute = [&](uint32_t ref, int64_t slot, bool demand) {
-      issue_copy(ref, slot, st);
-      s.bytes_h2d += static_cast<int64_t>(slot_bytes);
-      if (demand && assign_of(ref) == HM_ASSIGN_GPU_TRANSFER) {
-        const int e = ref_expert(ref);
-        wait_ready(slot, st);
-        hm_group g{static_cast<int32_t>(slot), h_offsets[e], h_counts[e], 0};
-        ffn(&g, 1, rows_used, st);
-        mark_used(&g, 1, st);
-        ++s.n_gpu;
-        s.bytes_gpu += static_cast<int64_t>(slot_bytes);
-      }
-    };
-    for (size_t i = 0; i < rec.demand.size(); ++i) {
-      copy_and_maybe_compute(rec.demand[i].first, checked_slot(rec.demand[i].first, rec.demand_slots[i]), true);
-      ++s.n_transfer;
-    }
-    // transfers that entered no cache slot (capacity 0: engine.py:318 inserts
-    // only when capacity > 0) still run where the plan put them: through the
-    // staging slot, one at a time (each copy waits for the previous reader)
-    if (rec.demand.size() < static_cast<size_t>(std::count_if(
-                                rec.plan.events.begin(), rec.plan.events.end(),
-                                [](const Event &e) { return e.kind == HM_KIND_TRANSFER; }))) {
-      std::vector<const Event *> xf;
-      for (const Event &e : rec.plan.events)
-        if (e.kind == HM_KIND_TRANSFER) xf.push_back(&e);
-      std::stable_sort(xf.begin(), xf.end(), [](const Event *a, const Event *b) { return a->start < b->start; });
-      for (const Event *e : xf) {
-        bool inserted = false;
-        for (auto &d : rec.demand) inserted = inserted || d.first == e->ref;
-        if (inserted) continue;
-        copy_and_maybe_compute(e->ref, staging_slot(), true);
-        ++s.n_transfer;
-      }
-    }
-    for (size_t i = 0; i < rec.chosen.size(); ++i) {
-      copy_and_maybe_compute(rec.chosen[i].first, checked_slot(rec.chosen[i].first, rec.chosen_slots[i]), false);
-      ++s.n_prefetch;
-    }
-
     // CPU experts in plan CPU order (scheduling.py:257-268)
     // CPU outputs reach the combine either zero-copy (positions < 256, the
     // combine reads the mapped host rows) or by H2D copies into `out`
@@ -679,12 +618,80 @@ struct Runtime {
       }
       ~TailGate() { open(); }
     } tail_gate{this, false};
-    if (pre_tail) {
-      ++tail_seq;
-      tail_gate.on = true;
-      ok(hm_combine_tail_gated(out, dv_h_out, host_mask, pos, w, T, Kp, H, cfg.residual ? x : nullptr, y, nullptr,
-                               scores_dev, layer, N, 0, 0.0, dv_flag + 4, tail_seq, vs));
-    }
+    // Everything the GPU gets for this layer (resident experts and shared
+    // chunks, transfers + their experts, prefetches, the gated combine tail).
+    // In decode it is issued while the host worker's threads already run:
+    // the caller joins the worker pass only after these launches (its share
+    // of the rows is stolen meanwhile), so ~20 µs of launch overhead per
+    // layer leaves the serial path.
+    auto issue_gpu = [&]() {
+      // GPU experts already resident (and the layer's shared chunks): one launch
+      std::vector<hm_group> batch;
+      for (const Event &ev : rec.plan.events) {
+        if (ev.device != HM_DEV_GPU || assign_of(ev.ref) != HM_ASSIGN_GPU_CACHED) continue;
+        const int e = ref_expert(ev.ref);
+        const int64_t slot = checked_slot(ev.ref, engine->cache.resident.at(ev.ref).slot);
+        wait_ready(slot, st);  // a prefetch may still be in flight
+        batch.push_back(hm_group{static_cast<int32_t>(slot), h_offsets[e], h_counts[e], 0});
+      }
+      s.n_gpu = static_cast<int32_t>(batch.size());
+      for (int c = 0; c < S; ++c)
+        if (c % W == R)
+          batch.push_back(hm_group{static_cast<int32_t>(shared_slot(layer, c)), h_offsets[N + c], h_counts[N + c], 0});
+      s.bytes_gpu = static_cast<int64_t>(batch.size()) * static_cast<int64_t>(slot_bytes);
+      if (!batch.empty()) {
+        ffn(batch.data(), static_cast<int>(batch.size()), rows_used, st);
+        mark_used(batch.data(), static_cast<int>(batch.size()), st);
+      }
+      // Copies in plan transfer order (== insert order), then prefetches; an
+      // expert the plan computes on the GPU is launched right after its copy so
+      // that a later copy into the same slot (same-layer eviction) waits for it.
+      auto copy_and_maybe_compute = [&](uint32_t ref, int64_t slot, bool demand) {
+        issue_copy(ref, slot, st);
+        s.bytes_h2d += static_cast<int64_t>(slot_bytes);
+        if (demand && assign_of(ref) == HM_ASSIGN_GPU_TRANSFER) {
+          const int e = ref_expert(ref);
+          wait_ready(slot, st);
+          hm_group g{static_cast<int32_t>(slot), h_offsets[e], h_counts[e], 0};
+          ffn(&g, 1, rows_used, st);
+          mark_used(&g, 1, st);
+          ++s.n_gpu;
+          s.bytes_gpu += static_cast<int64_t>(slot_bytes);
+        }
+      };
+      for (size_t i = 0; i < rec.demand.size(); ++i) {
+        copy_and_maybe_compute(rec.demand[i].first, checked_slot(rec.demand[i].first, rec.demand_slots[i]), true);
+        ++s.n_transfer;
+      }
+      // transfers that entered no cache slot (capacity 0: engine.py:318 inserts
+      // only when capacity > 0) still run where the plan put them: through the
+      // staging slot, one at a time (each copy waits for the previous reader)
+      if (rec.demand.size() < static_cast<size_t>(std::count_if(
+                                  rec.plan.events.begin(), rec.plan.events.end(),
+                                  [](const Event &e) { return e.kind == HM_KIND_TRANSFER; }))) {
+        std::vector<const Event *> xf;
+        for (const Event &e : rec.plan.events)
+          if (e.kind == HM_KIND_TRANSFER) xf.push_back(&e);
+        std::stable_sort(xf.begin(), xf.end(), [](const Event *a, const Event *b) { return a->start < b->start; });
+        for (const Event *e : xf) {
+          bool inserted = false;
+          for (auto &d : rec.demand) inserted = inserted || d.first == e->ref;
+          if (inserted) continue;
+          copy_and_maybe_compute(e->ref, staging_slot(), true);
+          ++s.n_transfer;
+        }
+      }
+      for (size_t i = 0; i < rec.chosen.size(); ++i) {
+        copy_and_maybe_compute(rec.chosen[i].first, checked_slot(rec.chosen[i].first, rec.chosen_slots[i]), false);
+        ++s.n_prefetch;
+      }
+      if (pre_tail) {
+        ++tail_seq;
+        tail_gate.on = true;
+        ok(hm_combine_tail_gated(out, dv_h_out, host_mask, pos, w, T, Kp, H, cfg.residual ? x : nullptr, y, nullptr,
+                                 scores_dev, layer, N, 0, 0.0, dv_flag + 4, tail_seq, vs));
+      }
+    };
     if (!cpu_refs.empty()) {
       if (!mirror_rows) RT_CUDA(cudaEventSynchronize(ev_rows));
       const double c0 = now_us();
@@ -700,16 +707,18 @@ struct Runtime {
           xs.push_back(h_x + (mirror_rows && T == 1 ? 0 : rb) * H);
           outs.push_back(h_out + rb * H);
         }
+        const std::function<void()> gpu_first = issue_gpu;
         if (q4) {
           std::vector<const uint8_t *> qimgs;
           for (auto *p : imgs) qimgs.push_back(reinterpret_cast<const uint8_t *>(p));
           cpu_experts_decode_q4(*workers, qimgs.data(), xs.data(), static_cast<int>(imgs.size()), H, I, outs.data(),
-                                hbuf);
+                                hbuf, &gpu_first);
         } else {
           cpu_experts_decode(*workers, imgs.data(), xs.data(), static_cast<int>(imgs.size()), H, I, outs.data(),
-                             hbuf);
+                             hbuf, &gpu_first);
         }
       } else {
+        issue_gpu();
         for (uint32_t r : cpu_refs) {  // plan CPU order
           const int e = ref_expert(r);
           const size_t rb = h_offsets[e];
@@ -730,6 +739,8 @@ struct Runtime {
           RT_CUDA(cudaMemcpyAsync(out + rb * H, h_out + rb * H, rc * H * 4, cudaMemcpyHostToDevice, st));
         }
       }
+    } else {
+      issue_gpu();
     }
     tail_gate.open();
     if (pre_tail) {
