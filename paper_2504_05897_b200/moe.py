@@ -221,9 +221,6 @@ class HybridMoE:
     def close(self) -> None:
         """Release the runtime now (HBM slot pool, pinned master store, host
         worker threads) whatever still references this object; idempotent."""
-        self.__del__()
-
-    def __del__(self) -> None:
         if getattr(self, "_rt", None):
             torch.cuda.synchronize()
             lib.hm_runtime_destroy(self._rt)
@@ -231,6 +228,9 @@ class HybridMoE:
         if getattr(self, "_ep", None) is not None:
             self._ep.close()
             self._ep = None
+
+    def __del__(self) -> None:
+        self.close()
 
     # -------------------------------------------------------------- weights
     def _encode(self, bf16_images: torch.Tensor) -> torch.Tensor:
@@ -400,6 +400,8 @@ class HybridMoE:
         logits: per-layer [T, ld] fp32 CUDA tensors (trace mode) or None (model
         mode: x_l . W_g,l).  predict(layer) -> list of predicted LayerRequests
         for the prefetch decision (prefetch.py:54-101).  Returns (y, info)."""
+        if not getattr(self, "_rt", None):
+            raise RuntimeError("this HybridMoE was closed")
         T = x.shape[0]
         if T > self.max_tokens:
             raise ValueError(f"T={T} exceeds max_tokens={self.max_tokens}")
