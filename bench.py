@@ -598,7 +598,7 @@ def run_ours(args) -> None:
                 "frac": achieved_gbs / hbm_peak, "traffic": tg.get("dram_bytes"),
                 "traffic_launch": tg.get("launch"), "traffic_algorithmic_bytes": tg.get("algorithmic_bytes"),
                 "traffic_source": traffic.get("source"),
-                "kernel": "decode expert FFN (fused GEMV, weights streamed once)" if args.bits == 16 else
+                "kernel": "decode expert FFN: ffn1_gemv + ffn2_gemv pair (PDL), weights streamed once" if args.bits == 16 else
                           "decode expert FFN on 4-bit images (ffn1_q4 + ffn2_q4)",
                 "launches": kn.value, "avg_launch_us": 1e3 * kms.value / max(1, kn.value),
                 "bytes_per_launch": kbytes.value / max(1, kn.value), "peak_kind": pk_kind,
@@ -666,6 +666,21 @@ def run_ours(args) -> None:
         dist.barrier()
     moe.close()
     del moe
+    # the same bytes per launch read by a pure 16-byte-load kernel as two
+    # dependent launches (the ffn1 / ffn2 split): the achievable floor at this
+    # launch size, next to the HBM peak
+    if rank == 0 and roofline["bytes_per_launch"] > 0:
+        nb = int(roofline["bytes_per_launch"]) // 256 * 256
+        n_buf = max(2, int(600e6 // nb) + 1)
+        rbuf = torch.empty(n_buf * nb, dtype=torch.uint8, device="cuda")
+        rms = C.c_float()
+        _lib.check(lib.hm_bench_stream_read(rbuf.data_ptr(), nb, n_buf, 1, 4, 20, st.cuda_stream, C.byref(rms)))
+        floor_gbs = nb / (rms.value * 1e-3) / 1e9
+        roofline["read_floor"] = {"gbs": floor_gbs, "frac_of_floor": roofline["achieved"] / floor_gbs,
+                                  "what": "bytes_per_launch read by a pure 16-byte-load kernel as two dependent "
+                                          "launches (2/3 + 1/3: the ffn1 / ffn2 split), back to back over "
+                                          "rotating buffers (hm_bench_stream_read)"}
+        del rbuf
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # rank 0 at N=1 only
         cpu = cpu_reference_decode(args.shape, args.cpu_baseline_steps, 1, prefill=0)
 
