@@ -55,10 +55,20 @@ def _run(rank: int, world: int, port: int, q, exchange: str = "p2p") -> None:
             lg = [torch.from_numpy(np.ascontiguousarray(logits[p][l], dtype=np.float32)).cuda()
                   for l in range(cfg.num_layers)]
             x = torch.randn((fwd.token_count, moe.H), generator=g, device="cuda").to(torch.bfloat16)
-            y, info = moe.forward_pass(x, lg, decision_log=True)
+            y, info = moe.forward_pass(x, lg, decision_log=True, keep_layers=world == 1)
             torch.cuda.synchronize()
             outs.append(y.float().cpu().numpy())
             loads.append([r[0].tolist() for r in info["requests"]])
+            if world == 1:  # the single-rank stack the ranks are compared with is itself checked against the oracle
+                from oracle import moe_ref as ref
+                from paper_2504_05897_b200.weights import unpack_expert
+                bf = lambda t: ref.bf16_to_f32(t.view(torch.int16).cpu().numpy().view(np.uint16))  # noqa: E731
+                for l, (xi, lgi, yo) in enumerate(info["layers"]):
+                    ex = [tuple(ref.bf16_to_f32(a) for a in unpack_expert(moe.expert_image(l, e), moe.H, moe.I))
+                          for e in range(moe.N)]
+                    want = ref.moe_layer(bf(xi), lgi.cpu().numpy(), ex, moe.N, moe.K, True, residual=True)
+                    err = float(np.abs(bf(yo) - want).max() / np.abs(want).max())
+                    assert err <= 1e-2, (p, l, err)
         native = []
         if world == 1 or exchange == "p2p":  # the one-call native pass (no Python per layer) on a fresh stack
             moe2 = HybridMoE(cfg, "tiny", EnginePolicy(), 0.5, prof, max_tokens=48, ep_rank=rank, ep_world=world,
