@@ -43,39 +43,60 @@ def peaks() -> tuple[dict, str]:
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks and throttle reasons sampled during the timed region:
+    ONE `nvidia-smi --query-gpu=... -lms 50` process (the profiling recipe's
+    looping form), started (and its first row read) before the region and
+    terminated after it, at least one row later.  (Spawning a
+    fresh nvidia-smi every 200 ms kept a host core busy with NVML start-up for
+    the whole region and delayed the host worker's threads.)"""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu: int = 0) -> None:
-        self.gpu, self.rows, self._stop = gpu, [], threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
+        self.gpu, self.rows, self._proc = gpu, [], None
+        self._t = threading.Thread(target=self._read, daemon=True)
 
-    def _run(self) -> None:
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                self.rows.append([v.strip() for v in out.stdout.strip().split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+    def _read(self) -> None:
+        try:
+            for line in self._proc.stdout:
+                self.rows.append([v.strip() for v in line.strip().split(",")])
+        except Exception:
+            pass
 
     def __enter__(self):
-        self._t.start()
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                           "--format=csv,noheader,nounits", "-lms", "50"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t.start()
+            t0 = time.time()  # NVML is up once the first row arrives: the region starts after it
+            while not self.rows and time.time() - t0 < 3.0 and self._proc.poll() is None:
+                time.sleep(0.005)
+            self._n0 = len(self.rows)
+        except Exception:
+            self._proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=6)
+        if self._proc is not None:
+            t0 = time.time()  # at least one row taken after the region started
+            while len(self.rows) <= getattr(self, "_n0", 0) and time.time() - t0 < 1.0:
+                time.sleep(0.005)
+            self._proc.terminate()  # our own child, by its handle
+            try:
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
+            self._t.join(timeout=5)
 
     def summary(self) -> dict:
-        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        rows = self.rows[getattr(self, "_n0", 0):] or self.rows  # rows taken inside the region
+        sm = [float(r[0]) for r in rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i - 3] for r in self.rows if len(r) >= 7 for i in range(3, 7)
+        reasons = sorted({names[i - 3] for r in rows if len(r) >= 7 for i in range(3, 7)
                           if r[i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(sm)}
@@ -498,6 +519,10 @@ def run_ours(args) -> None:
         moe.set_profile(prof)
     launches0 = lib.hm_launch_count()
     stats_all, predicted = [], []
+    worker_prof = os.environ.get("HM_BENCH_WORKER_PROF") == "1"  # diagnostics only, never in a reported run
+    if worker_prof:
+        _lib.check(lib.hm_cpu_decode_profile_accum(None, 1))
+        lib.hm_cpu_decode_profile(1, None, 0)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -523,6 +548,17 @@ def run_ours(args) -> None:
     launches = lib.hm_launch_count() - launches0
     predicted = [1e3 * info["pass"].latency for info in stats_all]
     stats_all = [s for info in stats_all for s in layer_stats(info)]
+    if worker_prof:  # per-call host-worker phase breakdown of the timed passes (diagnostics)
+        acc, hist, slow = (C.c_int64 * 7)(), (C.c_int64 * 5)(), (C.c_int64 * 64)()
+        _lib.check(lib.hm_cpu_decode_profile_hist(hist, slow, 64))
+        print("[worker profile] start-delay histogram (<=5, 20, 100, 1000, >1000 us):", list(hist),
+              "slowest starter per tid:", [v for v in slow][:threads], file=sys.stderr, flush=True)
+        _lib.check(lib.hm_cpu_decode_profile_accum(acc, 1))
+        lib.hm_cpu_decode_profile(0, None, 0)
+        n = max(1, acc[0])
+        print("[worker profile] calls %d, mean us: worker start %.1f, caller start %.1f, phase-1 end %.1f, "
+              "barrier %.1f, phase-2 end %.1f, wall %.1f" % (acc[0], *(acc[i] / n / 1e3 for i in range(1, 7))),
+              file=sys.stderr, flush=True)
     if os.environ.get("HM_BENCH_DUMP_DECODE"):  # per-layer timed-decode stats (diagnostics)
         Path(os.environ["HM_BENCH_DUMP_DECODE"]).write_text(json.dumps(
             [dataclasses.asdict(x) for x in stats_all]))

@@ -453,6 +453,13 @@ int hm_cpu_set_decode_steal(int on);
  * copy the last call's [thread][start, phase 1 done, barrier passed, phase 2
  * done] (ns since the call) into out. */
 int hm_cpu_decode_profile(int enable, int64_t *out, int n_threads);
+/* Tool hook: sums over the decode calls made while profiling is enabled --
+ * [calls, max worker start (tid >= 1), caller start, max phase-1 end, barrier
+ * passed, max phase-2 end, wall] in ns since each call; reset != 0 zeroes them. */
+int hm_cpu_decode_profile_accum(int64_t *out7, int reset);
+/* Tool hook: histogram of the per-call worker-start delay (<= 5, 20, 100, 1000,
+ * > 1000 us) and, per thread, how often it was the slowest to start. */
+int hm_cpu_decode_profile_hist(int64_t *out5, int64_t *slowest, int n_threads);
 int hm_host_read_bw(hm_cpu_pool *pool, const void *p, size_t bytes, int reps, double *gbs);
 
 typedef struct hm_runtime hm_runtime;

@@ -339,6 +339,8 @@ for _name, (_args, _res) in {
     "hm_q4_dequantize": ([vp, C.c_int, C.c_int, vp, vp], C.c_int),
     "hm_expert_ffn_q4": ([vp, C.c_size_t, C.c_int, C.c_int, C.c_int, P(HmGroup), C.c_int, vp, C.c_int, vp, vp, vp,
                           C.c_int, C.c_int, vp], C.c_int),
+    "hm_cpu_decode_profile_accum": ([P(C.c_int64), C.c_int], C.c_int),
+    "hm_cpu_decode_profile_hist": ([P(C.c_int64), P(C.c_int64), C.c_int], C.c_int),
     "hm_bench_stream_read": ([vp, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.POINTER(C.c_float)], C.c_int),
     "hm_bench_expert_ffn": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, C.c_int, C.c_int, vp,
                              P(C.c_float)], C.c_int),

@@ -397,6 +397,14 @@ int &decode_grain() {
 // [tid][0] start, [1] phase 1 done, [2] barrier passed, [3] phase 2 done (ns).
 static std::vector<int64_t> g_dec_prof;
 static bool g_dec_prof_on = false;
+// accumulated over decode calls while profiling (hm_cpu_decode_profile_accum):
+// calls, sum of [max worker start (tid >= 1), tid-0 start, max phase-1 end,
+// barrier passed, max phase-2 end, wall] in ns
+static int64_t g_dec_acc[7] = {0, 0, 0, 0, 0, 0, 0};
+// worker-start histogram (max over tid >= 1 per call: <= 5, 20, 100, 1000, > 1000 us)
+// and the slowest starter's tid
+static int64_t g_dec_hist[5] = {0, 0, 0, 0, 0};
+static std::vector<int64_t> g_dec_slowest;
 static inline int64_t ns_now() {
   return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
       .count();
@@ -1178,6 +1186,26 @@ void cpu_experts_decode(ThreadPool &pool, const uint16_t *const *imgs, const uin
     });
     if (tp) tp[3] = ns_now() - t_call;
   }, before_self);
+  if (g_dec_prof_on) {
+    int64_t mx[4] = {0, 0, 0, 0};
+    for (int t = 0; t < nt0; ++t)
+      for (int k = 0; k < 4; ++k)
+        if (t > 0 || k > 0) mx[k] = std::max(mx[k], g_dec_prof[static_cast<size_t>(t) * 4 + k]);
+    g_dec_acc[0] += 1;
+    g_dec_acc[1] += mx[0];
+    const int64_t us = mx[0] / 1000;
+    ++g_dec_hist[us <= 5 ? 0 : us <= 20 ? 1 : us <= 100 ? 2 : us <= 1000 ? 3 : 4];
+    if (static_cast<int>(g_dec_slowest.size()) < nt0) g_dec_slowest.assign(nt0, 0);
+    int slow = 1;
+    for (int t = 1; t < nt0; ++t)
+      if (g_dec_prof[static_cast<size_t>(t) * 4] > g_dec_prof[static_cast<size_t>(slow) * 4]) slow = t;
+    ++g_dec_slowest[slow];
+    g_dec_acc[2] += g_dec_prof[0];
+    g_dec_acc[3] += mx[1];
+    g_dec_acc[4] += mx[2];
+    g_dec_acc[5] += mx[3];
+    g_dec_acc[6] += ns_now() - t_call;
+  }
 }
 
 void cpu_expert(ThreadPool &pool, const uint16_t *img, int H, int I, const uint16_t *x, int M, float *out,
@@ -1282,6 +1310,27 @@ int hm_cpu_decode_profile(int enable, int64_t *out, int n_threads) {
   hm::g_dec_prof_on = enable != 0;
   if (out)
     for (int i = 0; i < n_threads * 4 && i < static_cast<int>(hm::g_dec_prof.size()); ++i) out[i] = hm::g_dec_prof[i];
+  HM_API_END
+}
+
+int hm_cpu_decode_profile_accum(int64_t *out7, int reset) {
+  HM_API_BEGIN
+  if (out7)
+    for (int i = 0; i < 7; ++i) out7[i] = hm::g_dec_acc[i];
+  if (reset) {
+    for (auto &v : hm::g_dec_acc) v = 0;
+    for (auto &v : hm::g_dec_hist) v = 0;
+    hm::g_dec_slowest.clear();
+  }
+  HM_API_END
+}
+
+int hm_cpu_decode_profile_hist(int64_t *out5, int64_t *slowest, int n_threads) {
+  HM_API_BEGIN
+  for (int i = 0; i < 5; ++i) out5[i] = hm::g_dec_hist[i];
+  if (slowest)
+    for (int t = 0; t < n_threads; ++t)
+      slowest[t] = t < static_cast<int>(hm::g_dec_slowest.size()) ? hm::g_dec_slowest[t] : 0;
   HM_API_END
 }
 
