@@ -295,18 +295,21 @@ __global__ void __launch_bounds__(256) router_fused_small_kernel(
       hm_.meta_i[E + e] = s_off[e];
     }
     if (threadIdx.x == 0) hm_.meta_i[2 * E] = s_off[E];
+    __shared__ double s_nrm[256];  // normalised scores, each divided once
     for (int e = threadIdx.x; e < N; e += blockDim.x) {
       const double tot = s_tot;
+      const double v = tot > 0.0 ? s_sum[e] / tot : 0.0;
+      s_nrm[e] = v;
       hm_.meta_d[e] = s_sum[e];
-      hm_.meta_d[N + e] = tot > 0.0 ? s_sum[e] / tot : 0.0;
+      hm_.meta_d[N + e] = v;
     }
+    __syncthreads();
     if (hm_.S && threadIdx.x < N) {  // this layer's new MRS row, a * TopP(s) + (1 - a) * S (caching.py:65-76)
-      const double tot = s_tot;
       const int i = threadIdx.x;
-      const double si = tot > 0.0 ? s_sum[i] / tot : 0.0;
+      const double si = s_nrm[i];
       int rank = 0;
       for (int j = 0; j < N; ++j) {
-        const double sj = tot > 0.0 ? s_sum[j] / tot : 0.0;
+        const double sj = s_nrm[j];
         rank += (sj > si || (sj == si && j < i)) ? 1 : 0;
       }
       const double t = rank < hm_.p ? si : 0.0;
