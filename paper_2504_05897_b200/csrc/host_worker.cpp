@@ -165,21 +165,25 @@ bool &decode_steal() {  // HM_DECODE_STEAL=0 / hm_cpu_set_decode_steal(0): stati
   return on;
 }
 
+// chunk: the owner's take from its front; steal_chunk (0 = chunk): what a
+// thief takes from another range's back -- small steals trim the tails finely
+// while the owner keeps long sequential runs.
 template <class F>
-void run_ranges(ThreadPool::Range *rs, int tid, int nt, uint32_t chunk, F &&process) {
+void run_ranges(ThreadPool::Range *rs, int tid, int nt, uint32_t chunk, F &&process, uint32_t steal_chunk = 0) {
+  if (steal_chunk == 0) steal_chunk = chunk;
   auto take = [&](ThreadPool::Range &r, bool front, uint32_t &a, uint32_t &b) {
     uint64_t v = r.fb.load(std::memory_order_relaxed);
     for (;;) {
       const uint32_t f = static_cast<uint32_t>(v >> 32), k = static_cast<uint32_t>(v);
       if (f >= k) return false;
-      if (!front && k - f < 2 * chunk) return false;  // leave the owner its last chunk
+      if (!front && k - f < 2 * steal_chunk) return false;  // leave the owner a last piece
       uint32_t nf = f, nk = k;
       if (front) {
         nf = std::min(k, f + chunk);
         a = f;
         b = nf;
       } else {
-        nk = k - chunk;
+        nk = k - steal_chunk;
         a = nk;
         b = k;
       }
@@ -380,6 +384,14 @@ void phase1_pairs(const uint16_t *img, int H, int I, const uint16_t *x, uint16_t
     for (int i = 0; i < n; ++i) h[i0 + i] = f2bf(silu(g[i]) * u[i]);
     i0 += n;
   }
+}
+
+long steal_kb() {
+  static const long v = [] {
+    const char *e = std::getenv("HM_STEAL_KB");
+    return e ? std::max(1L, std::atol(e)) : 64L;
+  }();
+  return v;
 }
 
 // Decode work split granularity (pairs in phase 1, rows in phase 2); 0 = the
@@ -1158,9 +1170,13 @@ void cpu_experts_decode(ThreadPool &pool, const uint16_t *const *imgs, const uin
       r2[t].fb.store((f2 << 32) | b2, std::memory_order_relaxed);
     }
   }
-  // steal units: ~64 KB of weights
+  // the owner takes grain-aligned runs of >= ~64 KB from its front; thieves take
+  // ~steal_kb() KB (HM_STEAL_KB, default 64) from the others' backs
+  const long skb = steal_kb();
   const uint32_t c1 = static_cast<uint32_t>(std::max<long>(g1, (64L << 10) / (4L * H) / g1 * g1));
+  const uint32_t s1 = static_cast<uint32_t>(std::max<long>(1, (skb << 10) / (4L * H)));
   const uint32_t c2 = static_cast<uint32_t>(std::max<long>(1, (64L << 10) / (2L * I)));
+  const uint32_t s2 = static_cast<uint32_t>(std::max<long>(1, (skb << 10) / (2L * I)));
   pool.run([&](int tid, int nt) {
     int64_t *tp = g_dec_prof_on ? &g_dec_prof[static_cast<size_t>(tid) * 4] : nullptr;
     if (tp) tp[0] = ns_now() - t_call;
@@ -1171,7 +1187,7 @@ void cpu_experts_decode(ThreadPool &pool, const uint16_t *const *imgs, const uin
         phase1_pairs(imgs[e], H, I, xs[e], h + static_cast<size_t>(e) * I, i0, i1);
         q += i1 - i0;
       }
-    });
+    }, s1);
     if (tp) tp[1] = ns_now() - t_call;
     pool.barrier();
     if (tp) tp[2] = ns_now() - t_call;
@@ -1183,7 +1199,7 @@ void cpu_experts_decode(ThreadPool &pool, const uint16_t *const *imgs, const uin
         stream_rows(w2 + static_cast<size_t>(j0) * I, j1 - j0, I, h + static_cast<size_t>(e) * I, outs[e] + j0);
         u += j1 - j0;
       }
-    });
+    }, s2);
     if (tp) tp[3] = ns_now() - t_call;
   }, before_self);
   if (g_dec_prof_on) {

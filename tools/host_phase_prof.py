@@ -21,7 +21,8 @@ NT = int(os.environ.get("NT", os.cpu_count()))
 pool = C.c_void_p()
 lib.hm_cpu_pool_create(NT, C.byref(pool))
 prof = np.zeros((NT, 4), np.int64)
-CASES = (("deepseek", 2048, 1408, 96, (1, 2, 3, 4), 300), ("mixtral", 4096, 14336, 8, (1,), 30))
+CASES = (("deepseek", 2048, 1408, 96, (1, 2, 3, 4), 300), ("mixtral", 4096, 14336, 8, (1,), 30),
+         ("qwen2", 3584, 2560, 48, (1, 2, 3, 4), 100))
 ONLY = os.environ.get("ONLY")  # e.g. deepseek:1,2
 if ONLY:
     nm, cs = ONLY.split(":")
