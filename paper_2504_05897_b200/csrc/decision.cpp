@@ -182,10 +182,12 @@ Plan simulate_schedule(const std::vector<Task> &gpu_q, const std::vector<Task> &
                        const hm_profile &p, double expert_bytes) {
   // scheduling.py:160-270
   {
-    std::unordered_set<uint32_t> g;
-    for (auto &t : gpu_q) g.insert(t.ref);
+    std::vector<uint32_t> g;  // sorted refs (tens of tasks: no hash set on the decision path)
+    g.reserve(gpu_q.size());
+    for (auto &t : gpu_q) g.push_back(t.ref);
+    std::sort(g.begin(), g.end());
     for (auto &t : cpu_q)
-      HM_REQUIRE(!g.count(t.ref), HM_EVALUE, "gpu and cpu queues must be disjoint");
+      HM_REQUIRE(!std::binary_search(g.begin(), g.end(), t.ref), HM_EVALUE, "gpu and cpu queues must be disjoint");
     for (auto &t : gpu_q) HM_REQUIRE(t.load >= 1, HM_EVALUE, "every scheduled expert needs load >= 1");
     for (auto &t : cpu_q) HM_REQUIRE(t.load >= 1, HM_EVALUE, "every scheduled expert needs load >= 1");
   }
@@ -653,6 +655,15 @@ void Engine::begin_pass() {
 
 Plan Engine::build_plan(int layer, const int64_t *loads, int n) {
   // engine.py:234-249 (_build_plan) with the baseline planners at 171-205.
+  // The plans built here satisfy SchedulePlan's invariants by construction;
+  // their per-plan check (scheduling.py:156) runs when the policy asks for
+  // validation (EnginePolicy.validate, engine.py:89) and stays on for plans
+  // built through the scheduling API.
+  struct CheckScope {
+    bool prev;
+    explicit CheckScope(bool on) : prev(t_check_plans) { t_check_plans = on; }
+    ~CheckScope() { t_check_plans = prev; }
+  } check_scope(cfg.validate != 0);
   std::vector<Task> tasks;
   for (int i = 0; i < n; ++i)
     if (loads[i] > 0) tasks.push_back({pack_ref(layer, i), loads[i]});
