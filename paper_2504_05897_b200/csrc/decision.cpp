@@ -393,12 +393,37 @@ Plan select_plan_tasks(const std::vector<Task> &cached, const std::vector<Task> 
   std::stable_sort(gq.begin(), gq.end(), load_desc_less);
   std::stable_sort(cq.begin(), cq.end(), load_asc_less);
   Plan best = simulate_schedule(gq, cq, p, expert_bytes);
+  // The guard plans are serial chains: their makespan is the last clock of
+  // the chain (finalize's max over event ends), computed here with the same
+  // operations in the same order; a plan is built only when it wins.
   std::vector<Task> all = cached;
   all.insert(all.end(), uncached.begin(), uncached.end());
-  Plan a1 = plan_all_cpu(all, p);
-  if (a1.makespan < best.makespan) best = std::move(a1);
-  Plan a2 = plan_all_gpu(cached, uncached, p, expert_bytes);
-  if (a2.makespan < best.makespan) best = std::move(a2);
+  if (!all.empty()) {
+    std::vector<Task> a = all;
+    std::stable_sort(a.begin(), a.end(), load_asc_less);
+    double clock = 0.0;
+    int64_t pos = 0;
+    for (const Task &t : a) clock = clock + cpu_time(p, t.load, pos++);
+    if (clock < best.makespan) best = plan_all_cpu(all, p);
+  } else if (0.0 < best.makespan) {
+    best = plan_all_cpu(all, p);
+  }
+  {
+    double gclock = 0.0;
+    for (const Task &t : gq) gclock = gclock + gpu_time(p, t.load);  // gq: cached by (-load, ref)
+    if (!uncached.empty()) {
+      std::vector<Task> u = uncached;
+      std::stable_sort(u.begin(), u.end(), load_desc_less);
+      const double tdur = transfer_time(p, expert_bytes);
+      double pclock = 0.0;
+      for (const Task &t : u) {
+        const double arrive = pclock + tdur;
+        pclock = arrive;
+        gclock = py_max(gclock, arrive) + gpu_time(p, t.load);
+      }
+    }
+    if (gclock < best.makespan) best = plan_all_gpu(cached, uncached, p, expert_bytes);
+  }
   return best;
 }
 

@@ -5,6 +5,7 @@
 // prefetch,engine}.py.  Every function cites the lines it follows.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <new>
@@ -111,10 +112,31 @@ struct CacheEntry {
   int64_t slot = -1;
 };
 
+// Sorted-vector set of refs: the pinned set holds a layer's activated experts
+// plus prefetch pins (tens, at most a few hundred), inserted and erased every
+// layer -- a hash set paid a node allocation per insert on the decision path.
+struct FlatSet {
+  std::vector<uint32_t> v;
+  size_t count(uint32_t r) const { return std::binary_search(v.begin(), v.end(), r) ? 1 : 0; }
+  void insert(uint32_t r) {
+    auto it = std::lower_bound(v.begin(), v.end(), r);
+    if (it == v.end() || *it != r) v.insert(it, r);
+  }
+  void erase(uint32_t r) {
+    auto it = std::lower_bound(v.begin(), v.end(), r);
+    if (it != v.end() && *it == r) v.erase(it);
+  }
+  void clear() { v.clear(); }
+  size_t size() const { return v.size(); }
+  bool empty() const { return v.empty(); }
+  std::vector<uint32_t>::const_iterator begin() const { return v.begin(); }
+  std::vector<uint32_t>::const_iterator end() const { return v.end(); }
+};
+
 struct Cache {
   int64_t capacity = 0;
   std::unordered_map<uint32_t, CacheEntry> resident;
-  std::unordered_set<uint32_t> pinned;
+  FlatSet pinned;
   std::vector<int64_t> free_slots;  // LIFO of unused HBM slots
   int64_t tick = 0;
 
