@@ -346,6 +346,13 @@ def run_ours(args) -> None:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # one process per GPU: this rank's host worker on its GPU's NUMA node, the
+    # node's cores split between the ranks that share it (before anything
+    # allocates pinned memory or starts host threads; hostplace.py)
+    bound_cpus = None
+    if world > 1 and not same_gpu:
+        from paper_2504_05897_b200.hostplace import bind_rank
+        bound_cpus = bind_rank(local, int(os.environ.get("LOCAL_WORLD_SIZE", world)))
 
     cfg = SHAPES[args.shape]
     if args.bits == 4:  # the paper's 4-bit experts: expert_bytes at 0.5 bytes per weight (core.py:55)
@@ -362,16 +369,19 @@ def run_ours(args) -> None:
     # expert at batch 1 -- so a host expert is rated at its streaming time, not
     # at a slope through loads 1-4 (which under-rated it 1.8x in round 1); the
     # prefill profile at prefill loads.  Each pass is planned with its stage's profile.
+    # host-worker threads of this rank (the calibration measures the same pool size)
+    threads = args.cpu_threads or (len(bound_cpus) if bound_cpus else max(1, (os.cpu_count() or 1) // world))
     if args.profile_file:  # e.g. for runs under a profiler, where warm-up timings are distorted
         base_profile = load_profile(args.profile_file)
         prefill_profile = load_profile(args.prefill_profile_file) if args.prefill_profile_file else base_profile
     else:
         base_profile = calibrate_shape(H, I, weight_bits=args.bits, gpu_loads=(1, 2, 3, 4), cpu_loads=(1,),
-                                       cpu_bursts=4)[0].profile
+                                       cpu_bursts=4, cpu_threads=threads)[0].profile
         prefill_profile = base_profile
         if args.stage_profiles and not args.live_fixture:  # a fixture replays with ONE profile
             prefill_profile = calibrate_shape(H, I, cpu_loads=(64, 128, 256), cpu_bursts=1,
-                                              gpu_loads=(64, 128, 256, 384, 512), weight_bits=args.bits)[0].profile
+                                              gpu_loads=(64, 128, 256, 384, 512), weight_bits=args.bits,
+                                              cpu_threads=threads)[0].profile
         if args.save_profile and rank == 0:
             save_profile(base_profile, args.save_profile)
             save_profile(prefill_profile, args.save_profile + ".prefill")
@@ -401,7 +411,6 @@ def run_ours(args) -> None:
         except Exception:
             avail = 0
         host_images = None if avail > 1.3 * total_bytes else max(16, int(0.5 * avail / image_bytes))
-    threads = args.cpu_threads or max(1, (os.cpu_count() or 1) // world)
     from paper_2504_05897_b200.ep import PeerMemoryUnavailable
     exchange_note = None
     try:
@@ -446,7 +455,7 @@ def run_ours(args) -> None:
     # host DRAM read bandwidth over (part of) the pinned master store: the host roofline
     import ctypes as C
     cp = C.c_void_p()
-    _lib.check(_lib.lib.hm_cpu_pool_create(args.cpu_threads, C.byref(cp)))
+    _lib.check(_lib.lib.hm_cpu_pool_create(threads, C.byref(cp)))
     hbw = C.c_double()
     nbytes = min(moe.store.nbytes, 16 << 30)
     _lib.check(_lib.lib.hm_host_read_bw(cp, moe.store.ctypes.data, nbytes, 3, C.byref(hbw)))
