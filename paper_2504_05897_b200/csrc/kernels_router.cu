@@ -267,29 +267,11 @@ __global__ void __launch_bounds__(256) router_fused_small_kernel(
     meta_d[N + e] = tot > 0.0 ? s_sum[e] / tot : 0.0;
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < R; j += blockDim.x) {  // stable rank inside the expert
-    const int e = s_sel[j];
-    int r = 0;
-    for (int q = 0; q < j; ++q) r += s_sel[q] == e;
-    const int p = s_off[e] + r;
-    sel[j] = e;
-    pos[j] = p;
-    row_src[p] = j;
-    s_rowtok[p] = j / Kp;  // token of the row at position p (shared: no global round trip)
-  }
-  __syncthreads();
-  const int H8 = H / 8;
-  // routed rows also go to the host worker's input; one token (decode): every
-  // routed row is that token, so one copy crosses PCIe (the host reads row 0)
-  const int n_host = hm_.xp ? (T == 1 ? min(1, s_off[N]) : s_off[N]) : 0;
-#pragma unroll 4
-  for (int v = threadIdx.x; v < R * H8; v += blockDim.x) {  // gather rows in permuted order
-    const int p = v / H8, c = v - p * H8;
-    const uint4 v4 = __ldg(reinterpret_cast<const uint4 *>(x + static_cast<size_t>(s_rowtok[p]) * H) + c);
-    reinterpret_cast<uint4 *>(xp + static_cast<size_t>(p) * H)[c] = v4;
-    if (p < n_host) reinterpret_cast<uint4 *>(hm_.xp + static_cast<size_t>(p) * H)[c] = v4;
-  }
-  if (hm_.flag) {  // LayerRequest straight into mapped host memory, then the flag
+  // The LayerRequest (and this layer's MRS row) go to mapped host memory and
+  // the request flag is raised BEFORE the permutation and the row gather: the
+  // host's decision core runs while the rows are gathered and mirrored; the
+  // host worker waits for the rows flag (flag[2]) before it reads them.
+  if (hm_.flag) {
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
       hm_.meta_i[e] = s_counts[e];
       hm_.meta_i[E + e] = s_off[e];
@@ -318,6 +300,34 @@ __global__ void __launch_bounds__(256) router_fused_small_kernel(
     __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) *reinterpret_cast<volatile uint32_t *>(hm_.flag) = hm_.seq;
+  }
+
+  for (int j = threadIdx.x; j < R; j += blockDim.x) {  // stable rank inside the expert
+    const int e = s_sel[j];
+    int r = 0;
+    for (int q = 0; q < j; ++q) r += s_sel[q] == e;
+    const int p = s_off[e] + r;
+    sel[j] = e;
+    pos[j] = p;
+    row_src[p] = j;
+    s_rowtok[p] = j / Kp;  // token of the row at position p (shared: no global round trip)
+  }
+  __syncthreads();
+  const int H8 = H / 8;
+  // routed rows also go to the host worker's input; one token (decode): every
+  // routed row is that token, so one copy crosses PCIe (the host reads row 0)
+  const int n_host = hm_.xp ? (T == 1 ? min(1, s_off[N]) : s_off[N]) : 0;
+#pragma unroll 4
+  for (int v = threadIdx.x; v < R * H8; v += blockDim.x) {  // gather rows in permuted order
+    const int p = v / H8, c = v - p * H8;
+    const uint4 v4 = __ldg(reinterpret_cast<const uint4 *>(x + static_cast<size_t>(s_rowtok[p]) * H) + c);
+    reinterpret_cast<uint4 *>(xp + static_cast<size_t>(p) * H)[c] = v4;
+    if (p < n_host) reinterpret_cast<uint4 *>(hm_.xp + static_cast<size_t>(p) * H)[c] = v4;
+  }
+  if (hm_.flag && hm_.xp) {  // the host worker's rows have landed
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) reinterpret_cast<volatile uint32_t *>(hm_.flag)[2] = hm_.seq;
   }
 }
 

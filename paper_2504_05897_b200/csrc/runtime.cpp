@@ -382,6 +382,22 @@ struct Runtime {
     std::atomic_thread_fence(std::memory_order_acquire);
   }
 
+  // The router raises its request flag before gathering the rows; the host
+  // worker reads the mirrored rows only after the rows flag (h_flag[2]).
+  void wait_rows_flag(cudaStream_t st) {
+    volatile uint32_t *f = h_flag + 2;
+    for (uint64_t i = 1;; ++i) {
+      if (*f == seq) break;
+      if ((i & 4095) == 0) {
+        const cudaError_t e = cudaStreamQuery(st);
+        if (e != cudaSuccess && e != cudaErrorNotReady) RT_CUDA(e);
+        if (e == cudaSuccess && *f != seq) raise(HM_ECUDA, "router finished without raising the rows flag");
+      }
+      __builtin_ia32_pause();
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+  }
+
   void issue_copy(uint32_t ref, int64_t slot, cudaStream_t /*compute*/) {
     const int64_t u = slot_use_seq[slot];
     if (u > copy_waited_seq) {  // wait for the last kernel that read this slot
@@ -693,7 +709,10 @@ struct Runtime {
       }
     };
     if (!cpu_refs.empty()) {
-      if (!mirror_rows) RT_CUDA(cudaEventSynchronize(ev_rows));
+      if (!mirror_rows)
+        RT_CUDA(cudaEventSynchronize(ev_rows));
+      else
+        wait_rows_flag(st);
       const double c0 = now_us();
       bool all_single = true;
       for (uint32_t r : cpu_refs) all_single = all_single && h_counts[ref_expert(r)] == 1;
