@@ -441,6 +441,10 @@ int hm_cpu_has_amx_bf16(void); /* AMX-BF16 present and XTILEDATA granted */
 /* Decode-stream tuning: software prefetch distance (elements) and hint (0 none, 1 T0, 2 T1, 3 NTA). */
 int hm_cpu_set_prefetch(int dist, int hint);
 /* n single-token experts in one worker pass (decode): outs[i][H] = expert(imgs[i])(xs[i][H]). */
+/* n multi-token experts (prefill groups, Ms[e] >= 1 tokens each) in one host-worker pass on AMX; outputs
+ * equal hm_cpu_expert's per expert (same per-unit arithmetic). */
+int hm_cpu_experts_amx(hm_cpu_pool *pool, const uint16_t *const *imgs, const uint16_t *const *xs, const int *Ms,
+                       int n, int H, int I, float *const *outs);
 int hm_cpu_experts_decode(hm_cpu_pool *pool, const uint16_t *const *imgs, const uint16_t *const *xs, int n,
                           int H, int I, float *const *outs);
 /* Best-of-reps host DRAM read bandwidth (GB/s) over `bytes` at p (64-byte aligned). */

@@ -321,6 +321,7 @@ for _name, (_args, _res) in {
     "hm_combine_f32": ([vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp], C.c_int),
     "hm_residual_add": ([vp, vp, C.c_int, C.c_int, vp, vp], C.c_int),
     "hm_runtime_preload": ([vp, P(u32), C.c_int], C.c_int),
+    "hm_cpu_experts_amx": ([vp, P(vp), P(vp), P(C.c_int), C.c_int, C.c_int, C.c_int, P(vp)], C.c_int),
     "hm_cpu_experts_decode": ([vp, P(vp), P(vp), C.c_int, C.c_int, C.c_int, P(vp)], C.c_int),
     "hm_cpu_set_prefetch": ([C.c_int, C.c_int], C.c_int),
     "hm_engine_set_profile": ([vp, P(Profile)], C.c_int),

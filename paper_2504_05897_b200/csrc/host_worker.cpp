@@ -1138,6 +1138,93 @@ void cpu_expert_amx(ThreadPool &pool, const uint16_t *img, int H, int I, const u
   });
 }
 
+// A layer's multi-token CPU experts (prefill) in ONE pool run: activations of
+// every expert VNNI-packed in parallel, then phase 1 over every (expert, 16-pair
+// unit) and phase 2 over every (expert, 32-row unit), claimed dynamically across
+// experts -- one wake-up and two barriers per layer instead of per expert, and
+// the units of all experts fill each other's tails.  Per unit the arithmetic is
+// cpu_expert_amx's (bit-identical outputs).
+void cpu_experts_amx(ThreadPool &pool, const uint16_t *const *imgs, const uint16_t *const *xs, const int *Ms, int n,
+                     int H, int I, float *const *outs, std::vector<uint16_t> &scratch,
+                     const std::function<void()> *before_self) {
+  HM_REQUIRE(H % 32 == 0 && I % kIlv == 0, HM_EVALUE, "host worker needs H % 32 == 0 and I % 128 == 0");
+  HM_REQUIRE(amx_enable(), HM_ERUNTIME, "multi-token host experts need AMX");
+  if (n <= 0) {
+    if (before_self) (*before_self)();
+    return;
+  }
+  std::vector<size_t> off_x(n), off_h(n);
+  std::vector<int> mpad(n);
+  size_t total = 0;
+  for (int e = 0; e < n; ++e) {
+    HM_REQUIRE(Ms[e] >= 1, HM_EVALUE, "every batched expert needs at least one token");
+    mpad[e] = (Ms[e] + 15) / 16 * 16;
+    off_x[e] = total;
+    total += static_cast<size_t>(H) * mpad[e];
+    off_h[e] = total;
+    total += static_cast<size_t>(I) * mpad[e];
+  }
+  scratch.resize(total);
+  uint16_t *base = scratch.data();
+  const int K2 = H / 2, pk = 64;              // pack units: 64 k-pairs of one expert
+  const int npk = (K2 + pk - 1) / pk;
+  const int ob = I / 16, pairs = (H / 16 + 1) / 2;
+  std::atomic<int> next0{0}, next1{0}, next2{0};
+  pool.run([&](int tid, int nt) {
+    amx_config();
+    for (int u; (u = next0.fetch_add(1, std::memory_order_relaxed)) < n * npk;) {
+      const int e = u / npk, k0 = (u % npk) * pk;
+      vnni_pack_rows(xs[e], Ms[e], H, mpad[e], base + off_x[e], k0, std::min(K2, k0 + pk));
+    }
+    pool.barrier();
+    float c[4][16][16];
+    for (int u; (u = next1.fetch_add(1, std::memory_order_relaxed)) < n * ob;) {
+      const int e = u / ob, o = u % ob, M = Ms[e], Mpad = mpad[e], nb = Mpad / 16;
+      const uint16_t *img = imgs[e], *xv = base + off_x[e];
+      uint16_t *hv = base + off_h[e];
+      const int i0 = o * 16;
+      const size_t grow = static_cast<size_t>((i0 / kIlv) * 2 * kIlv + i0 % kIlv);
+      const uint16_t *wg = img + grow * H, *wu = img + (grow + kIlv) * H;
+      for (int b = 0; b < nb; b += 2) {
+        const bool two = b + 1 < nb;
+        amx_block(wg, wu, static_cast<size_t>(H) * 2, xv, Mpad, b * 16, two, H, c);
+        for (int bb = 0; bb < (two ? 2 : 1); ++bb) {
+          const int tok0 = (b + bb) * 16;
+          const __mmask16 live = tok0 + 16 <= M ? 0xFFFF : static_cast<__mmask16>((1u << (M - tok0)) - 1u);
+          for (int r = 0; r < 16; r += 2) {
+            const __m512 h0 = _mm512_maskz_mov_ps(live, silu_mul16(c[bb][r], c[2 + bb][r]));
+            const __m512 h1 = _mm512_maskz_mov_ps(live, silu_mul16(c[bb][r + 1], c[2 + bb][r + 1]));
+            _mm512_storeu_si512(hv + (static_cast<size_t>((i0 + r) >> 1) * Mpad + tok0) * 2, interleave_bf16(h0, h1));
+          }
+        }
+      }
+    }
+    pool.barrier();
+    const __m512i col = _mm512_set_epi32(240, 224, 208, 192, 176, 160, 144, 128, 112, 96, 80, 64, 48, 32, 16, 0);
+    for (int u; (u = next2.fetch_add(1, std::memory_order_relaxed)) < n * pairs;) {
+      const int e = u / pairs, q = u % pairs, M = Ms[e], Mpad = mpad[e], nb = Mpad / 16;
+      const uint16_t *w2 = imgs[e] + static_cast<size_t>(2) * I * H, *hv = base + off_h[e];
+      float *out = outs[e];
+      const int j0 = q * 32;
+      const bool second = j0 + 16 < H;
+      const uint16_t *wa0 = w2 + static_cast<size_t>(j0) * I;
+      const uint16_t *wa1 = second ? wa0 + static_cast<size_t>(16) * I : wa0;
+      for (int b = 0; b < nb; b += 2) {
+        const bool two = b + 1 < nb;
+        amx_block(wa0, wa1, static_cast<size_t>(I) * 2, hv, Mpad, b * 16, two, I, c);
+        for (int a = 0; a < (second ? 2 : 1); ++a)
+          for (int bb = 0; bb < (two ? 2 : 1); ++bb)
+            for (int t = 0; t < 16; ++t) {
+              const int tok = (b + bb) * 16 + t;
+              if (tok >= M) break;
+              _mm512_storeu_ps(out + static_cast<size_t>(tok) * H + j0 + a * 16,
+                               _mm512_i32gather_ps(col, &c[a * 2 + bb][0][t], 4));
+            }
+      }
+    }
+  }, before_self);
+}
+
 void cpu_experts_decode(ThreadPool &pool, const uint16_t *const *imgs, const uint16_t *const *xs, int n, int H,
                         int I, float *const *outs, std::vector<uint16_t> &hbuf,
                         const std::function<void()> *before_self) {
@@ -1280,6 +1367,14 @@ int hm_cpu_expert(hm_cpu_pool *pool, const uint16_t *img, int H, int I, const ui
   HM_API_BEGIN
   std::vector<uint16_t> hbuf;
   hm::cpu_expert(*reinterpret_cast<hm::ThreadPool *>(pool), img, H, I, x, M, out, hbuf);
+  HM_API_END
+}
+
+int hm_cpu_experts_amx(hm_cpu_pool *pool, const uint16_t *const *imgs, const uint16_t *const *xs, const int *Ms,
+                       int n, int H, int I, float *const *outs) {
+  HM_API_BEGIN
+  std::vector<uint16_t> scratch;
+  hm::cpu_experts_amx(*reinterpret_cast<hm::ThreadPool *>(pool), imgs, xs, Ms, n, H, I, outs, scratch);
   HM_API_END
 }
 

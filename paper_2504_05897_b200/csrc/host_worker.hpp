@@ -70,6 +70,12 @@ void cpu_experts_decode(ThreadPool &pool, const uint16_t *const *imgs, const uin
                         int I, float *const *outs, std::vector<uint16_t> &hbuf,
                         const std::function<void()> *before_self = nullptr);
 
+// n multi-token experts (prefill) in one pool run on AMX (Ms[e] tokens each);
+// same per-unit arithmetic as cpu_expert_amx.  before_self: see ThreadPool::run.
+void cpu_experts_amx(ThreadPool &pool, const uint16_t *const *imgs, const uint16_t *const *xs, const int *Ms, int n,
+                     int H, int I, float *const *outs, std::vector<uint16_t> &scratch,
+                     const std::function<void()> *before_self = nullptr);
+
 // 4-bit expert images (include/hybrimoe.h, hm_q4_*): decode GEMV on the
 // nibbles; multi-token groups dequantize 32-row units and run on AMX.
 void cpu_experts_decode_q4(ThreadPool &pool, const uint8_t *const *imgs, const uint16_t *const *xs, int n, int H,

@@ -737,8 +737,37 @@ struct Runtime {
                              hbuf, &gpu_first);
         }
       } else {
-        issue_gpu();
-        for (uint32_t r : cpu_refs) {  // plan CPU order
+        // prefill: the layer's AMX-sized bf16 experts in one worker pass (GPU
+        // launches issued while it starts), the rest one by one in plan CPU order
+        std::vector<const uint16_t *> bimgs, bxs;
+        std::vector<float *> bouts;
+        std::vector<int> bms;
+        std::vector<uint32_t> rest;
+        static const bool batch = [] {  // HM_PREFILL_BATCH=0: one worker pass per expert (A/B)
+          const char *e = std::getenv("HM_PREFILL_BATCH");
+          return !e || std::atoi(e) != 0;
+        }();
+        const bool amx = batch && !q4 && amx_available();
+        for (uint32_t r : cpu_refs) {
+          const int e = ref_expert(r);
+          const size_t rb = h_offsets[e];
+          if (amx && h_counts[e] >= 8) {
+            bimgs.push_back(image_ptr(r));
+            bxs.push_back(h_x + rb * H);
+            bouts.push_back(h_out + rb * H);
+            bms.push_back(h_counts[e]);
+          } else {
+            rest.push_back(r);
+          }
+        }
+        if (!bimgs.empty()) {
+          const std::function<void()> gpu_first = issue_gpu;
+          cpu_experts_amx(*workers, bimgs.data(), bxs.data(), bms.data(), static_cast<int>(bimgs.size()), H, I,
+                          bouts.data(), hbuf, &gpu_first);
+        } else {
+          issue_gpu();
+        }
+        for (uint32_t r : rest) {  // plan CPU order
           const int e = ref_expert(r);
           const size_t rb = h_offsets[e];
           if (q4)

@@ -114,3 +114,27 @@ def test_cpu_experts_decode_q4_batch(pool):
     for (q, ex), x, o in zip(exps, xs, outs):
         want = ref.expert(ref.bf16_to_f32(x), *ex)
         assert np.abs(o - want).max() / np.abs(want).max() <= 1e-2
+
+
+@pytest.mark.skipif(not lib.hm_cpu_has_amx_bf16(), reason="host lacks AMX-BF16")
+@pytest.mark.parametrize("H,I,Ms", [(512, 384, [8, 33, 17]), (1024, 1408, [96, 9, 40, 128]), (256, 256, [300])])
+def test_batched_amx_experts_equal_one_by_one(pool, H, I, Ms):
+    """hm_cpu_experts_amx (a layer's prefill experts in one pass, units claimed
+    across experts) gives hm_cpu_expert's bits per expert, and the oracle's
+    values within 1e-2."""
+    rng = np.random.default_rng(H + len(Ms))
+    exps = [_expert(rng, H, I) for _ in Ms]
+    xs = [ref.f32_to_bf16(rng.standard_normal((m, H)).astype(np.float32)) for m in Ms]
+    one = []
+    for (img, _), x, m in zip(exps, xs, Ms):
+        o = np.empty((m, H), np.float32)
+        _lib.check(lib.hm_cpu_expert(pool, img.ctypes.data, H, I, x.ctypes.data, m, o.ctypes.data))
+        one.append(o)
+    outs = [np.full((m, H), np.nan, np.float32) for m in Ms]
+    P = C.c_void_p * len(Ms)
+    _lib.check(lib.hm_cpu_experts_amx(pool, P(*[e[0].ctypes.data for e in exps]), P(*[x.ctypes.data for x in xs]),
+                                      (C.c_int * len(Ms))(*Ms), len(Ms), H, I, P(*[o.ctypes.data for o in outs])))
+    for o, o1, (_, ex), x in zip(outs, one, exps, xs):
+        assert np.array_equal(o, o1)
+        want = ref.expert(ref.bf16_to_f32(x), *ex)
+        assert np.abs(o - want).max() / np.abs(want).max() <= 1e-2
