@@ -794,7 +794,9 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
-EXTRA_CONFIGS = {  # BASELINE.json configs 3-4: DeepSeek-V2-Lite at 25 %, Qwen2-57B-A14B budget sweep 10/25/50 %
+EXTRA_CONFIGS = {  # BASELINE.json configs 3-4: DeepSeek-V2-Lite at 25 %, Qwen2-57B-A14B budget sweep 10/25/50 %;
+    # plus the headline shape with the paper's 4-bit experts
+    "mixtral_25_q4": ["--shape", "mixtral", "--ratio", "0.25", "--bits", "4"],
     "deepseek_25": ["--shape", "deepseek", "--ratio", "0.25"],
     "qwen2_25": ["--shape", "qwen2", "--ratio", "0.25", "--host-images", "192"],
     "qwen2_10": ["--shape", "qwen2", "--ratio", "0.10", "--host-images", "192"],
@@ -945,7 +947,7 @@ def main() -> None:
     ap.add_argument("--profile-file", default=None, help="HardwareProfile key=value file instead of calibrating")
     ap.add_argument("--save-profile", default=None, help="write the calibrated HardwareProfile here")
     ap.add_argument("--prefill-profile-file", default=None)
-    ap.add_argument("--extra-configs", default="deepseek_25,qwen2_10,qwen2_25,qwen2_50",
+    ap.add_argument("--extra-configs", default="deepseek_25,qwen2_10,qwen2_25,qwen2_50,mixtral_25_q4",
                     help="comma list of other named configs run as child processes after the headline one "
                          "and summarised under 'configs' ('' = none)")
     ap.add_argument("--refit", action=argparse.BooleanOptionalAction, default=True,

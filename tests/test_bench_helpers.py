@@ -50,6 +50,6 @@ def test_refit_falls_back_to_mean_and_needs_samples(bench):
 
 
 def test_extra_configs_are_named_configs(bench):
-    assert set(bench.EXTRA_CONFIGS) == {"deepseek_25", "qwen2_10", "qwen2_25", "qwen2_50"}
+    assert set(bench.EXTRA_CONFIGS) == {"deepseek_25", "qwen2_10", "qwen2_25", "qwen2_50", "mixtral_25_q4"}
     for argv in bench.EXTRA_CONFIGS.values():
         assert "--shape" in argv and "--ratio" in argv
