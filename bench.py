@@ -342,6 +342,10 @@ def run_ours(args) -> None:
     dist = None
     if world > 1:
         import torch.distributed as dist
+        # NCCL's init log (communicator size and ranks) on stderr, also when
+        # torchrun launched us (the self-spawn path sets the same)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if same_gpu:
             dist.init_process_group("gloo")
         else:
