@@ -117,7 +117,8 @@ def test_cpu_experts_decode_q4_batch(pool):
 
 
 @pytest.mark.skipif(not lib.hm_cpu_has_amx_bf16(), reason="host lacks AMX-BF16")
-@pytest.mark.parametrize("H,I,Ms", [(512, 384, [8, 33, 17]), (1024, 1408, [96, 9, 40, 128]), (256, 256, [300])])
+@pytest.mark.parametrize("H,I,Ms", [(512, 384, [8, 33, 17]), (1024, 1408, [96, 9, 40, 128]), (256, 256, [300]),
+                                    (2048, 1408, [8, 96, 200])])   # the DeepSeek-V2-Lite expert shape
 def test_batched_amx_experts_equal_one_by_one(pool, H, I, Ms):
     """hm_cpu_experts_amx (a layer's prefill experts in one pass, units claimed
     across experts) gives hm_cpu_expert's bits per expert, and the oracle's
