@@ -48,7 +48,7 @@ def test_cpu_expert_matches_oracle(pool, H, I, M):
 
 
 @pytest.mark.parametrize("grain", [0, 5, 16, 64])
-@pytest.mark.parametrize("H,I,n", [(512, 384, 3), (256, 1408, 4)])
+@pytest.mark.parametrize("H,I,n", [(512, 384, 3), (256, 1408, 4), (2048, 1408, 3)])
 def test_cpu_experts_decode_batch(pool, grain, H, I, n):
     rng = np.random.default_rng(9 + grain)
     lib.hm_cpu_set_decode_grain.argtypes = [C.c_int]
